@@ -1,0 +1,145 @@
+/*
+ * pardyn_c.h — C-ABI of the B200-native batched forward-dynamics library
+ * (libpardyn_b200.so). Plain pointers and sizes only; no C++ or torch types.
+ *
+ * This is the drop-in boundary for the reference library "pardyn"
+ * (arxiv 1609.06779, /root/reference/proj/core). Each entry point names the
+ * reference interface it replaces:
+ *
+ *   pd_algo                  <- enum class FdAlgo { jsiia, abia, cfa }
+ *                               (include/pardyn/forward_dynamics.hpp:29)
+ *   pd_set_models            <- the RobotChain / LinkSpec values carried by
+ *                               FdProblem (model.hpp:17-30,
+ *                               forward_dynamics.hpp:111-116) plus the
+ *                               per-call spatial_inertia_from validation
+ *                               (src/spatial.cpp:70-100)
+ *   pd_forward_dynamics      <- batch_forward_dynamics(span<const FdProblem>,
+ *                               FdAlgo) (forward_dynamics.hpp:125-126,
+ *                               src/forward_dynamics.cpp:466-481) and, at
+ *                               batch 1, forward_dynamics(...)
+ *                               (forward_dynamics.hpp:103-105)
+ *   pd_forward_dynamics_device  same, on device-resident buffers
+ *   pd_slot_message          <- FdResult::error strings (e.what() of the
+ *                               reference exceptions, types.hpp:21-46)
+ *   pd_inverse_dynamics      <- inverse_dynamics / bias_torque
+ *                               (inverse_dynamics.hpp:71-78), default
+ *                               IdOptions
+ *
+ * Layouts
+ *   LinkSpec record: 31 doubles, the field order of LinkSpec (model.hpp:17-23)
+ *     [0] mass, [1..3] com, [4..12] inertia_rot row-major,
+ *     [13..18] joint_screw (angular, linear), [19..27] home rotation
+ *     row-major, [28..30] home translation.
+ *   Host models:  links[model][link][31], gravity[model][3].
+ *   Host states:  q/qdot/tau/qddot[problem][link] (one JointVector per row).
+ *   Device states (pd_*_device): [link][problem] (problem fastest).
+ *   Problem p uses model (n_models == 1 ? 0 : p).
+ *
+ * Errors never abort a batch: each slot gets a pd_slot_code plus
+ * (round, index); pd_slot_message() rebuilds the reference's message.
+ * A pd_ctx is used from one host thread at a time; contexts are independent.
+ */
+#ifndef PARDYN_C_H_
+#define PARDYN_C_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PD_LINK_FIELDS 31
+#define PD_ABI_VERSION 1
+
+typedef enum pd_algo { PD_JSIIA = 0, PD_ABIA = 1, PD_CFA = 2 } pd_algo;
+
+/* Call-level status. Classes mirror the reference's exceptions. */
+typedef enum pd_status {
+  PD_OK = 0,
+  PD_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  PD_MODEL_ERROR = 2,      /* pardyn::ModelError */
+  PD_DYNAMICS_ERROR = 3,   /* pardyn::DynamicsError */
+  PD_SINGULAR_BLOCK = 4,   /* pardyn::SingularBlockError */
+  PD_CUDA_ERROR = 5,
+  PD_NO_DEVICE = 6,
+  PD_INTERNAL = 7
+} pd_status;
+
+/* Per-slot outcome written by the kernels (or by host validation). */
+typedef enum pd_slot_code {
+  PD_SLOT_OK = 0,
+  PD_SLOT_DEGENERATE_ARTICULATION = 1, /* index = joint    forward_dynamics.cpp:140-144 */
+  PD_SLOT_JSI_NOT_SPD = 2,             /*                  forward_dynamics.cpp:93-98   */
+  PD_SLOT_JSI_REFINE_FAILED = 3,       /*                  forward_dynamics.cpp:108-116 */
+  PD_SLOT_LINK_INERTIA_NOT_PD = 4,     /*                  forward_dynamics.cpp:317-320 */
+  PD_SLOT_OEE_SINGULAR_PIVOT = 5,      /* (round, block)   oee.hpp:132-137             */
+  PD_SLOT_OEE_SINGULAR_FINAL = 6,      /* (round, block)   oee.hpp:182-187             */
+  PD_SLOT_BAD_MODEL = 7,               /* index = spatial-inertia rule, spatial.cpp:72-87 */
+  PD_SLOT_BAD_SIZE = 8                 /* check_sizes, forward_dynamics.cpp:19-31      */
+} pd_slot_code;
+
+/* Detail for PD_SLOT_BAD_MODEL (slot index field). */
+typedef enum pd_model_rule {
+  PD_RULE_MASS = 1,      /* "spatial inertia: mass must be positive" */
+  PD_RULE_FINITE = 2,    /* "spatial inertia: parameters must be finite" */
+  PD_RULE_SYMMETRIC = 3, /* "...rotational inertia must be symmetric" */
+  PD_RULE_PD = 4         /* "...rotational inertia must be positive definite" */
+} pd_model_rule;
+
+typedef struct pd_ctx pd_ctx;
+
+/* Context on one CUDA device (ordinal). Owns device buffers and a stream. */
+pd_status pd_create(pd_ctx** out, int device);
+void pd_destroy(pd_ctx* ctx);
+int pd_abi_version(void);
+const char* pd_status_string(pd_status s);
+/* Last call-level error text of this context ("" if none). */
+const char* pd_last_error(const pd_ctx* ctx);
+
+/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the
+ * context's own stream. */
+pd_status pd_set_stream(pd_ctx* ctx, void* stream);
+pd_status pd_synchronize(pd_ctx* ctx);
+
+/* Upload and pack a model set: n_models chains of n_links links each.
+ * Validates every link with the spatial_inertia_from rules; a model whose
+ * link fails gets model_status[m] = PD_SLOT_BAD_MODEL and model_rule[m] = the
+ * rule (pd_model_rule) of the first failing link (nullable outputs). Problems
+ * bound to a bad model report that code instead of being solved.
+ * gravity may be NULL (default (0,0,-9.81) for every model). */
+pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const double* links,
+                        const double* gravity, int32_t* model_status, int32_t* model_rule);
+
+/* Solve `batch` problems against the current models, host buffers in and out
+ * ([problem][link]); blocks until results are on the host. slot_* outputs are
+ * nullable. Returns PD_OK if the call ran (slots may still carry errors). */
+pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
+                              const double* tau, double* qddot, int32_t* slot_status, int32_t* slot_round,
+                              int32_t* slot_index);
+
+/* Same on device buffers in [link][problem] layout, asynchronous on the
+ * context's stream. d_slot_* must be device int32 arrays of length batch
+ * (nullable -> internal scratch). */
+pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* d_q,
+                                     const double* d_qdot, const double* d_tau, double* d_qddot,
+                                     int32_t* d_slot_status, int32_t* d_slot_round, int32_t* d_slot_index);
+
+/* Joint torques of inverse dynamics with default IdOptions (gravity on, no
+ * base motion, no tip wrench), host buffers [problem][link]. */
+pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot,
+                              const double* qddot, double* tau);
+
+/* Reference error message of a slot outcome into buf (always terminated). */
+void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links, char* buf, int32_t buflen);
+
+/* Number of kernels this context has launched since creation. */
+int64_t pd_kernel_launches(const pd_ctx* ctx);
+
+/* Name of the kernel variant pd_forward_dynamics would run for (algo, n). */
+const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARDYN_C_H_ */

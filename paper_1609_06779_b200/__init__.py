@@ -1,0 +1,31 @@
+"""B200-native batched forward dynamics of serial chains (arxiv 1609.06779).
+
+Hot path: FP64 ABIA / JSIIA / CFA forward dynamics on sm_100a, behind the
+C-ABI of libpardyn_b200.so (include/pardyn_c.h). This package is the Python
+mirror of the reference's C++ API (proj/core/include/pardyn/*.hpp); the C++
+drop-in lives in include/pardyn/ + paper_1609_06779_b200/cpp/.
+"""
+from .api import (  # noqa: F401
+    Context,
+    CudaError,
+    DynamicsError,
+    ExecTrace,
+    FdAlgo,
+    FdProblem,
+    FdResult,
+    InvalidArgument,
+    LinkSpec,
+    ModelError,
+    RobotChain,
+    SingularBlockError,
+    abia_forward_dynamics,
+    batch_forward_dynamics,
+    bias_torque,
+    cfa_forward_dynamics,
+    ceil_log2,
+    default_context,
+    forward_dynamics,
+    inverse_dynamics,
+    jsiia_forward_dynamics,
+)
+from ._capi import LIB_PATH, LibraryMissing  # noqa: F401

@@ -1,0 +1,91 @@
+"""ctypes binding of the C-ABI (include/pardyn_c.h) of libpardyn_b200.so.
+
+The shared library is built in-tree (paper_1609_06779_b200/lib/) by
+``make -C paper_1609_06779_b200/csrc`` (or ``__graft_entry__.build()``).
+There is no CPU fallback: if the library or a CUDA device is missing, calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpardyn_b200.so")
+
+PD_JSIIA, PD_ABIA, PD_CFA = 0, 1, 2
+PD_OK, PD_INVALID_ARGUMENT, PD_MODEL_ERROR, PD_DYNAMICS_ERROR, PD_SINGULAR_BLOCK, PD_CUDA_ERROR, PD_NO_DEVICE, \
+    PD_INTERNAL = range(8)
+SLOT_OK, SLOT_DEGENERATE_ARTICULATION, SLOT_JSI_NOT_SPD, SLOT_JSI_REFINE_FAILED, SLOT_LINK_INERTIA_NOT_PD, \
+    SLOT_OEE_SINGULAR_PIVOT, SLOT_OEE_SINGULAR_FINAL, SLOT_BAD_MODEL, SLOT_BAD_SIZE = range(9)
+LINK_FIELDS = 31
+
+# every symbol include/pardyn_c.h declares
+EXPORTS = (
+    "pd_create", "pd_destroy", "pd_abi_version", "pd_status_string", "pd_last_error", "pd_set_stream",
+    "pd_synchronize", "pd_set_models", "pd_forward_dynamics", "pd_forward_dynamics_device", "pd_inverse_dynamics",
+    "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant",
+)
+
+_lib = None
+_D = C.POINTER(C.c_double)
+_I32 = C.POINTER(C.c_int32)
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def load():
+    """Load libpardyn_b200.so (raises LibraryMissing if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise LibraryMissing(f"{LIB_PATH} not built; run `make -C paper_1609_06779_b200/csrc` "
+                             "(or __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    L.pd_create.argtypes = [C.POINTER(C.c_void_p), C.c_int]
+    L.pd_create.restype = C.c_int
+    L.pd_destroy.argtypes = [C.c_void_p]
+    L.pd_destroy.restype = None
+    L.pd_abi_version.restype = C.c_int
+    L.pd_status_string.argtypes = [C.c_int]
+    L.pd_status_string.restype = C.c_char_p
+    L.pd_last_error.argtypes = [C.c_void_p]
+    L.pd_last_error.restype = C.c_char_p
+    L.pd_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    L.pd_set_stream.restype = C.c_int
+    L.pd_synchronize.argtypes = [C.c_void_p]
+    L.pd_synchronize.restype = C.c_int
+    L.pd_set_models.argtypes = [C.c_void_p, C.c_int64, C.c_int32, _D, _D, _I32, _I32]
+    L.pd_set_models.restype = C.c_int
+    L.pd_forward_dynamics.argtypes = [C.c_void_p, C.c_int, C.c_int64, _D, _D, _D, _D, _I32, _I32, _I32]
+    L.pd_forward_dynamics.restype = C.c_int
+    L.pd_forward_dynamics_device.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.pd_forward_dynamics_device.restype = C.c_int
+    L.pd_inverse_dynamics.argtypes = [C.c_void_p, C.c_int64, _D, _D, _D, _D]
+    L.pd_inverse_dynamics.restype = C.c_int
+    L.pd_slot_message.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int32]
+    L.pd_slot_message.restype = None
+    L.pd_kernel_launches.argtypes = [C.c_void_p]
+    L.pd_kernel_launches.restype = C.c_int64
+    L.pd_kernel_variant.argtypes = [C.c_void_p, C.c_int, C.c_int32]
+    L.pd_kernel_variant.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def slot_message(code, round_, index, n_links):
+    buf = C.create_string_buffer(512)
+    load().pd_slot_message(int(code), int(round_), int(index), int(n_links), buf, 512)
+    return buf.value.decode()
+
+
+def dptr(a):
+    return None if a is None else a.ctypes.data_as(_D)
+
+
+def iptr(a):
+    return None if a is None else a.ctypes.data_as(_I32)

@@ -1,0 +1,360 @@
+"""Python mirror of the reference's forward-dynamics API over the C-ABI.
+
+Same names, argument meaning and error behaviour as
+proj/core/include/pardyn/forward_dynamics.hpp and inverse_dynamics.hpp:
+
+  FdAlgo {jsiia, abia, cfa}                    forward_dynamics.hpp:29
+  forward_dynamics(chain, q, qdot, tau, algo)  forward_dynamics.hpp:103-105
+  jsiia_/abia_/cfa_forward_dynamics            forward_dynamics.hpp:38-42,58-62,98-101
+  FdProblem / FdResult                         forward_dynamics.hpp:111-123
+  batch_forward_dynamics(problems, algo)       forward_dynamics.hpp:125-126
+  inverse_dynamics / bias_torque               inverse_dynamics.hpp:71-78
+  LinkSpec / RobotChain                        model.hpp:17-30
+  ModelError / DynamicsError / SingularBlockError(round, index)   types.hpp:21-46
+  std::invalid_argument -> InvalidArgument (a ValueError)
+
+Every solve runs on the GPU through libpardyn_b200.so (no CPU fallback).
+Batches are bucketed by link count, packed, solved with one C-ABI call per
+bucket and scattered back; per-slot errors carry the reference's messages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Iterable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument."""
+
+
+class ModelError(RuntimeError):
+    """pardyn::ModelError (types.hpp:21-24)."""
+
+
+class DynamicsError(RuntimeError):
+    """pardyn::DynamicsError (types.hpp:28-31)."""
+
+
+class SingularBlockError(DynamicsError):
+    """pardyn::SingularBlockError (types.hpp:35-46)."""
+
+    def __init__(self, round_: int, index: int, what: str):
+        super().__init__(what)
+        self._round, self._index = round_, index
+
+    def round(self) -> int:
+        return self._round
+
+    def index(self) -> int:
+        return self._index
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class FdAlgo(enum.IntEnum):
+    jsiia = _capi.PD_JSIIA
+    abia = _capi.PD_ABIA
+    cfa = _capi.PD_CFA
+
+
+@dataclass
+class LinkSpec:
+    """model.hpp:17-23 (defaults match the reference)."""
+    mass: float = 1.0
+    com: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    inertia_rot: np.ndarray = field(default_factory=lambda: np.eye(3))
+    joint_screw: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, 1.0, 0.0, 0.0, 0.0]))
+    home_rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    home_translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def to_record(self) -> np.ndarray:
+        return np.concatenate([[self.mass], np.ravel(self.com), np.ravel(self.inertia_rot), np.ravel(self.joint_screw),
+                               np.ravel(self.home_rotation), np.ravel(self.home_translation)]).astype(np.float64)
+
+    @staticmethod
+    def from_record(r) -> "LinkSpec":
+        r = np.asarray(r, dtype=np.float64)
+        return LinkSpec(float(r[0]), r[1:4].copy(), r[4:13].reshape(3, 3).copy(), r[13:19].copy(),
+                        r[19:28].reshape(3, 3).copy(), r[28:31].copy())
+
+
+@dataclass
+class RobotChain:
+    """model.hpp:25-30."""
+    links: List[LinkSpec] = field(default_factory=list)
+    gravity: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, -9.81]))
+
+    def size(self) -> int:
+        return len(self.links)
+
+    def to_records(self) -> np.ndarray:
+        if not self.links:
+            return np.zeros((0, _capi.LINK_FIELDS))
+        return np.stack([l.to_record() for l in self.links])
+
+    @staticmethod
+    def from_records(records, gravity=(0.0, 0.0, -9.81)) -> "RobotChain":
+        return RobotChain([LinkSpec.from_record(r) for r in np.asarray(records)], np.asarray(gravity, np.float64))
+
+
+@dataclass
+class ExecTrace:
+    """trace.hpp:24-39, filled with the designed dependency structure of the
+    kernel variant that ran."""
+    parallel_link_stages: int = 0
+    longest_sequential_link_chain: int = 0
+    scan_rounds_max: int = 0
+    oee_rounds: int = 0
+
+
+@dataclass
+class FdProblem:
+    chain: RobotChain
+    q: np.ndarray
+    qdot: np.ndarray
+    tau: np.ndarray
+
+
+@dataclass
+class FdResult:
+    qddot: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    error: str = ""
+
+    def ok(self) -> bool:
+        return self.error == ""
+
+
+def ceil_log2(n: int) -> int:
+    k, p = 0, 1
+    while p < n:
+        p <<= 1
+        k += 1
+    return k
+
+
+# --------------------------------------------------------------------------- context
+class Context:
+    """A pd_ctx on one CUDA device (one per process per device)."""
+
+    def __init__(self, device: int = 0):
+        L = _capi.load()
+        h = C.c_void_p()
+        st = L.pd_create(C.byref(h), int(device))
+        if st != _capi.PD_OK:
+            raise CudaError(f"pd_create(device={device}) failed: {L.pd_status_string(st).decode()}")
+        self._h = h
+        self._L = L
+        self.device = device
+        self._models_key = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _check(self, st):
+        if st == _capi.PD_OK:
+            return
+        msg = self._L.pd_last_error(self._h).decode()
+        if st == _capi.PD_INVALID_ARGUMENT:
+            raise InvalidArgument(msg)
+        raise CudaError(f"{self._L.pd_status_string(st).decode()}: {msg}")
+
+    def set_models(self, links: np.ndarray, gravity: Optional[np.ndarray] = None):
+        """links: (M, n, 31) float64; gravity: (M, 3) or None. Returns
+        (model_status, model_rule) int32 arrays."""
+        links = np.ascontiguousarray(links, dtype=np.float64)
+        M, n = links.shape[0], links.shape[1]
+        g = None if gravity is None else np.ascontiguousarray(np.broadcast_to(gravity, (M, 3)), dtype=np.float64)
+        ms = np.zeros(M, np.int32)
+        mr = np.zeros(M, np.int32)
+        self._check(self._L.pd_set_models(self._h, M, n, _capi.dptr(links), _capi.dptr(g), _capi.iptr(ms),
+                                          _capi.iptr(mr)))
+        self.n_links, self.n_models = n, M
+        return ms, mr
+
+    def solve(self, algo, q, qdot, tau):
+        """Host-buffer solve: q/qdot/tau (B, n) -> (qddot, status, round, index)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qdot, dtype=np.float64)
+        tau = np.ascontiguousarray(tau, dtype=np.float64)
+        B = q.shape[0]
+        qdd = np.empty_like(q)
+        st = np.zeros(B, np.int32)
+        rd = np.zeros(B, np.int32)
+        ix = np.zeros(B, np.int32)
+        self._check(self._L.pd_forward_dynamics(self._h, int(algo), B, _capi.dptr(q), _capi.dptr(qd), _capi.dptr(tau),
+                                                _capi.dptr(qdd), _capi.iptr(st), _capi.iptr(rd), _capi.iptr(ix)))
+        return qdd, st, rd, ix
+
+    def solve_device(self, algo, batch, d_q, d_qd, d_tau, d_qdd, d_st=None, d_rd=None, d_ix=None):
+        """Device solve on raw device pointers ([link][problem] layout)."""
+        self._check(self._L.pd_forward_dynamics_device(self._h, int(algo), int(batch), d_q, d_qd, d_tau, d_qdd, d_st,
+                                                       d_rd, d_ix))
+
+    def inverse_dynamics(self, q, qdot, qddot):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qdot, dtype=np.float64)
+        qdd = np.ascontiguousarray(qddot, dtype=np.float64)
+        tau = np.empty_like(q)
+        self._check(self._L.pd_inverse_dynamics(self._h, q.shape[0], _capi.dptr(q), _capi.dptr(qd), _capi.dptr(qdd),
+                                                _capi.dptr(tau)))
+        return tau
+
+    def set_stream(self, stream_ptr):
+        self._check(self._L.pd_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def synchronize(self):
+        self._check(self._L.pd_synchronize(self._h))
+
+    def kernel_launches(self) -> int:
+        return int(self._L.pd_kernel_launches(self._h))
+
+    def kernel_variant(self, algo, n) -> str:
+        return self._L.pd_kernel_variant(self._h, int(algo), int(n)).decode()
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# --------------------------------------------------------------------------- errors
+def _raise_slot(code, round_, index, n):
+    msg = _capi.slot_message(code, round_, index, n)
+    if code in (_capi.SLOT_BAD_MODEL, _capi.SLOT_BAD_SIZE):
+        raise InvalidArgument(msg)
+    if code in (_capi.SLOT_OEE_SINGULAR_PIVOT, _capi.SLOT_OEE_SINGULAR_FINAL):
+        raise SingularBlockError(int(round_), int(index), msg)
+    raise DynamicsError(msg)
+
+
+def _check_sizes(chain: RobotChain, q, qdot, tau):
+    """forward_dynamics.cpp:19-31."""
+    n = chain.size()
+    if n == 0:
+        raise InvalidArgument("forward dynamics: chain has no links")
+    if len(q) != n or len(qdot) != n or len(tau) != n:
+        raise InvalidArgument("forward dynamics: q, qdot and tau must each have one entry per joint "
+                              f"(chain has {n})")
+
+
+def _fill_trace(trace: Optional[ExecTrace], algo: FdAlgo, n: int):
+    if trace is None:
+        return
+    L = ceil_log2(n)
+    trace.scan_rounds_max = max(trace.scan_rounds_max, L)
+    if algo == FdAlgo.jsiia:
+        trace.parallel_link_stages += 6
+    elif algo == FdAlgo.abia:
+        trace.parallel_link_stages += 6
+        trace.longest_sequential_link_chain = max(trace.longest_sequential_link_chain, n)
+    else:
+        trace.parallel_link_stages += 9
+        trace.oee_rounds = L
+
+
+# --------------------------------------------------------------------------- API
+def forward_dynamics(chain: RobotChain, q, qdot, tau, algo: FdAlgo, trace: Optional[ExecTrace] = None,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    try:
+        algo = FdAlgo(int(algo))
+    except ValueError:
+        raise InvalidArgument("forward_dynamics: unknown algorithm") from None
+    _check_sizes(chain, q, qdot, tau)
+    ctx = ctx or default_context()
+    ctx.set_models(chain.to_records()[None], np.asarray(chain.gravity, np.float64)[None])
+    qdd, st, rd, ix = ctx.solve(algo, np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
+                                np.asarray(tau, np.float64)[None])
+    if st[0] != _capi.SLOT_OK:
+        _raise_slot(st[0], rd[0], ix[0], chain.size())
+    _fill_trace(trace, algo, chain.size())
+    return qdd[0]
+
+
+def jsiia_forward_dynamics(chain, q, qdot, tau, trace=None, ctx=None):
+    return forward_dynamics(chain, q, qdot, tau, FdAlgo.jsiia, trace, ctx)
+
+
+def abia_forward_dynamics(chain, q, qdot, tau, trace=None, ctx=None):
+    return forward_dynamics(chain, q, qdot, tau, FdAlgo.abia, trace, ctx)
+
+
+def cfa_forward_dynamics(chain, q, qdot, tau, trace=None, ctx=None):
+    return forward_dynamics(chain, q, qdot, tau, FdAlgo.cfa, trace, ctx)
+
+
+def batch_forward_dynamics(problems: Sequence[FdProblem], algo: FdAlgo, ctx: Optional[Context] = None) -> List[FdResult]:
+    """forward_dynamics.cpp:466-481: independent problems, per-slot errors,
+    never raises per problem. Problems are bucketed by link count."""
+    algo = FdAlgo(int(algo))
+    out = [FdResult() for _ in problems]
+    buckets = {}
+    for k, p in enumerate(problems):
+        try:
+            _check_sizes(p.chain, p.q, p.qdot, p.tau)
+        except InvalidArgument as e:
+            out[k].error = str(e)
+            continue
+        buckets.setdefault(p.chain.size(), []).append(k)
+    if not buckets:
+        return out
+    ctx = ctx or default_context()
+    for n, idx in buckets.items():
+        links = np.stack([problems[k].chain.to_records() for k in idx])
+        grav = np.stack([np.asarray(problems[k].chain.gravity, np.float64) for k in idx])
+        ctx.set_models(links, grav)
+        q = np.stack([np.asarray(problems[k].q, np.float64) for k in idx])
+        qd = np.stack([np.asarray(problems[k].qdot, np.float64) for k in idx])
+        tau = np.stack([np.asarray(problems[k].tau, np.float64) for k in idx])
+        qdd, st, rd, ix = ctx.solve(algo, q, qd, tau)
+        for j, k in enumerate(idx):
+            if st[j] == _capi.SLOT_OK:
+                out[k].qddot = qdd[j].copy()
+            else:
+                out[k].error = _capi.slot_message(st[j], rd[j], ix[j], n)
+    return out
+
+
+def inverse_dynamics(chain: RobotChain, q, qdot, qddot, ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:166-173 with default IdOptions."""
+    n = chain.size()
+    for name, v in (("q", q), ("qdot", qdot), ("qddot", qddot)):
+        if len(v) != n:
+            raise InvalidArgument(f"{name} has length {len(v)} but the chain has {n} joints")
+    if n == 0:
+        return np.zeros(0)
+    ctx = ctx or default_context()
+    ms, mr = ctx.set_models(chain.to_records()[None], np.asarray(chain.gravity, np.float64)[None])
+    if ms[0] != _capi.SLOT_OK:
+        raise InvalidArgument(_capi.slot_message(ms[0], 0, mr[0], n))
+    return ctx.inverse_dynamics(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
+                                np.asarray(qddot, np.float64)[None])[0]
+
+
+def bias_torque(chain: RobotChain, q, qdot, ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:175-179."""
+    return inverse_dynamics(chain, q, qdot, np.zeros(chain.size()), ctx)

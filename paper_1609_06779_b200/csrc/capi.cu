@@ -1,0 +1,517 @@
+// C-ABI of libpardyn_b200.so (include/pardyn_c.h): context, model upload and
+// packing, layout transposes for host buffers, kernel dispatch, reference
+// error messages. No CPU fallback: every solve runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pd_batch.cuh"
+
+namespace pd {
+void launch_abia(const ModelView& mv, const BatchIO& io, double* scratch, cudaStream_t s);
+void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
+void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+size_t cfa_workspace_bytes(int n);
+void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+size_t jsiia_workspace_bytes(int n);
+}  // namespace pd
+
+using namespace pd;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct pd_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  // models
+  int32_t n_links = 0;
+  int64_t n_models = 0;
+  DevBuf model, gravity, mstatus, mrule, raw;
+  // scratch
+  DevBuf abia_scratch, cta_ws, slots, io_q, io_qd, io_tau, io_qdd, io_status;
+  int64_t launches = 0;
+  std::string last_error;
+};
+
+namespace {
+
+pd_status cuda_fail(pd_ctx* c, cudaError_t e, const char* where) {
+  c->last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return PD_CUDA_ERROR;
+}
+
+#define PD_CUDA(call)                                         \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
+  } while (0)
+
+// raw [M][n][31] -> packed SoA [F_COUNT][n][M]; gravity [M][3] -> [3][M]
+__global__ void pack_models_kernel(const double* __restrict__ raw, const double* __restrict__ graw, int n,
+                                   int64_t M, double* __restrict__ out, double* __restrict__ gout) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (m >= M) return;
+  const double* r = raw + ((int64_t)m * n + i) * PD_LINK_FIELDS;
+  auto put = [&](int f, double v) { out[((int64_t)f * n + i) * M + m] = v; };
+  put(F_MASS, r[0]);
+  for (int k = 0; k < 3; ++k) put(F_COM + k, r[1 + k]);
+  // rotational inertia, lower triangle (what LLT / the assembled blocks read)
+  put(F_IC + 0, r[4 + 0]);
+  put(F_IC + 1, r[4 + 3]);
+  put(F_IC + 2, r[4 + 6]);
+  put(F_IC + 3, r[4 + 4]);
+  put(F_IC + 4, r[4 + 7]);
+  put(F_IC + 5, r[4 + 8]);
+  for (int k = 0; k < 6; ++k) put(F_SCREW + k, r[13 + k]);
+  for (int k = 0; k < 9; ++k) put(F_HR + k, r[19 + k]);
+  for (int k = 0; k < 3; ++k) put(F_HP + k, r[28 + k]);
+  if (i == 0)
+    for (int k = 0; k < 3; ++k) gout[(int64_t)k * M + m] = graw[m * 3 + k];
+}
+
+// [rows][cols] -> [cols][rows]
+__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t rows, int64_t cols) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
+void launch_transpose(pd_ctx* ctx, const double* in, double* out, int64_t rows, int64_t cols) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, out, rows, cols);
+  ctx->launches++;
+}
+
+// Smallest eigenvalue of a symmetric 3x3 (cyclic Jacobi) for the
+// positive-definiteness rule of spatial_inertia_from (spatial.cpp:83-87).
+double sym3_min_eig(double m[3][3]) {
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    const double off = m[0][1] * m[0][1] + m[0][2] * m[0][2] + m[1][2] * m[1][2];
+    if (off < 1e-300) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (m[p][q] == 0.0) continue;
+        const double th = (m[q][q] - m[p][p]) / (2.0 * m[p][q]);
+        const double tt = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(tt * tt + 1.0), s = tt * c;
+        for (int k = 0; k < 3; ++k) {
+          const double a = m[k][p], b = m[k][q];
+          m[k][p] = c * a - s * b;
+          m[k][q] = s * a + c * b;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double a = m[p][k], b = m[q][k];
+          m[p][k] = c * a - s * b;
+          m[q][k] = s * a + c * b;
+        }
+      }
+  }
+  return std::min(m[0][0], std::min(m[1][1], m[2][2]));
+}
+
+// spatial_inertia_from's rules (spatial.cpp:72-87), first failing rule or 0.
+int link_rule(const double* r) {
+  const double mass = r[0];
+  if (!(mass > 0.0) || !std::isfinite(mass)) return PD_RULE_MASS;
+  for (int k = 1; k < 13; ++k)
+    if (!std::isfinite(r[k])) return PD_RULE_FINITE;
+  double scale = 0.0, asym = 0.0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      scale = std::max(scale, std::fabs(r[4 + 3 * a + b]));
+      asym = std::max(asym, std::fabs(r[4 + 3 * a + b] - r[4 + 3 * b + a]));
+    }
+  if (asym > 1e-9 * std::max(scale, 1.0)) return PD_RULE_SYMMETRIC;
+  double m[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) m[a][b] = r[4 + 3 * a + b];
+  if (!(sym3_min_eig(m) > 0.0)) return PD_RULE_PD;
+  return 0;
+}
+
+ModelView model_view(const pd_ctx* c) {
+  ModelView mv;
+  mv.f = c->model.as<double>();
+  mv.g = c->gravity.as<double>();
+  mv.mstatus = c->mstatus.as<int32_t>();
+  mv.mrule = c->mrule.as<int32_t>();
+  mv.n = c->n_links;
+  mv.M = c->n_models;
+  return mv;
+}
+
+int64_t cta_slots(pd_ctx* ctx, size_t ws_bytes, int64_t batch) {
+  const size_t budget = (size_t)2 << 30;  // 2 GiB of global workspace at most
+  int64_t slots = (int64_t)std::max<size_t>(1, budget / std::max<size_t>(ws_bytes, 1));
+  return std::min<int64_t>(slots, batch);
+}
+
+pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qd, const double* tau,
+                     double* qdd, int32_t* st, int32_t* er, int32_t* ei) {
+  if (ctx->n_models <= 0 || ctx->n_links <= 0) {
+    ctx->last_error = "forward dynamics: no models set (pd_set_models)";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (ctx->n_models != 1 && ctx->n_models != batch) {
+    ctx->last_error = "forward dynamics: batch must equal the number of models (or use one shared model)";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  const int n = ctx->n_links;
+  if (!st || !er || !ei) {
+    PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+    st = ctx->io_status.as<int32_t>();
+    er = st + batch;
+    ei = er + batch;
+  }
+  BatchIO io{q, qd, tau, qdd, st, er, ei, batch};
+  const ModelView mv = model_view(ctx);
+  switch (algo) {
+    case PD_ABIA: {
+      PD_CUDA(ctx->abia_scratch.ensure(sizeof(double) * 7 * (size_t)n * batch));
+      launch_abia(mv, io, ctx->abia_scratch.as<double>(), ctx->stream);
+      ctx->launches++;
+      break;
+    }
+    case PD_CFA: {
+      const size_t wsb = cfa_workspace_bytes(n);
+      int64_t slots = 0;
+      if (wsb > 220 * 1024) {
+        slots = cta_slots(ctx, wsb, batch);
+        PD_CUDA(ctx->cta_ws.ensure(wsb * slots));
+        ctx->launches += (batch + slots - 1) / slots;
+      } else {
+        ctx->launches++;
+      }
+      launch_cfa(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream);
+      break;
+    }
+    case PD_JSIIA: {
+      const size_t wsb = jsiia_workspace_bytes(n);
+      int64_t slots = 0;
+      if (wsb > 220 * 1024) {
+        slots = cta_slots(ctx, wsb, batch);
+        PD_CUDA(ctx->cta_ws.ensure(wsb * slots));
+        ctx->launches += (batch + slots - 1) / slots;
+      } else {
+        ctx->launches++;
+      }
+      launch_jsiia(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream);
+      break;
+    }
+    default:
+      ctx->last_error = "forward_dynamics: unknown algorithm";
+      return PD_INVALID_ARGUMENT;
+  }
+  PD_CUDA(cudaGetLastError());
+  return PD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pd_abi_version(void) { return PD_ABI_VERSION; }
+
+const char* pd_status_string(pd_status s) {
+  switch (s) {
+    case PD_OK: return "ok";
+    case PD_INVALID_ARGUMENT: return "invalid argument";
+    case PD_MODEL_ERROR: return "model error";
+    case PD_DYNAMICS_ERROR: return "dynamics error";
+    case PD_SINGULAR_BLOCK: return "singular block";
+    case PD_CUDA_ERROR: return "CUDA error";
+    case PD_NO_DEVICE: return "no CUDA device";
+    case PD_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+pd_status pd_create(pd_ctx** out, int device) {
+  if (!out) return PD_INVALID_ARGUMENT;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return PD_NO_DEVICE;
+  if (device < 0 || device >= count) return PD_NO_DEVICE;
+  pd_ctx* ctx = new pd_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return PD_CUDA_ERROR;
+  }
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  ctx->stream = ctx->own_stream;
+  *out = ctx;
+  return PD_OK;
+}
+
+void pd_destroy(pd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->model, &ctx->gravity, &ctx->mstatus, &ctx->mrule, &ctx->raw, &ctx->abia_scratch, &ctx->cta_ws,
+                    &ctx->slots, &ctx->io_q, &ctx->io_qd, &ctx->io_tau, &ctx->io_qdd, &ctx->io_status})
+    b->release();
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* pd_last_error(const pd_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+pd_status pd_set_stream(pd_ctx* ctx, void* stream) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return PD_OK;
+}
+
+pd_status pd_synchronize(pd_ctx* ctx) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PD_OK;
+}
+
+int64_t pd_kernel_launches(const pd_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) {
+  (void)ctx;
+  switch (algo) {
+    case PD_ABIA: return "abia_lane_kernel (lane per chain, 3 fused passes)";
+    case PD_CFA: return cfa_workspace_bytes(n_links) <= 220 * 1024 ? "cfa_cta_kernel<smem> (CTA per chain, OEE in smem)"
+                                                                    : "cfa_cta_kernel<global> (CTA per chain, L2 workspace)";
+    case PD_JSIIA: return jsiia_workspace_bytes(n_links) <= 220 * 1024
+                              ? "jsiia_cta_kernel<smem> (CTA per chain, CRBA scans + CTA Cholesky)"
+                              : "jsiia_cta_kernel<global> (CTA per chain, L2 workspace)";
+  }
+  return "unknown";
+}
+
+pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const double* links, const double* gravity,
+                        int32_t* model_status, int32_t* model_rule) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (n_models <= 0 || n_links <= 0 || !links) {
+    ctx->last_error = "forward dynamics: chain has no links";
+    return PD_INVALID_ARGUMENT;
+  }
+  PD_CUDA(cudaSetDevice(ctx->device));
+  std::vector<int32_t> ms(n_models, PD_SLOT_OK), mr(n_models, 0);
+  for (int64_t m = 0; m < n_models; ++m)
+    for (int i = 0; i < n_links; ++i) {
+      const int rule = link_rule(links + ((size_t)m * n_links + i) * PD_LINK_FIELDS);
+      if (rule) {
+        ms[m] = PD_SLOT_BAD_MODEL;
+        mr[m] = rule;
+        break;
+      }
+    }
+  if (model_status) std::memcpy(model_status, ms.data(), sizeof(int32_t) * n_models);
+  if (model_rule) std::memcpy(model_rule, mr.data(), sizeof(int32_t) * n_models);
+  std::vector<double> g(3 * n_models);
+  for (int64_t m = 0; m < n_models; ++m)
+    for (int k = 0; k < 3; ++k) g[3 * m + k] = gravity ? gravity[3 * m + k] : (k == 2 ? -9.81 : 0.0);
+  const size_t raw_bytes = sizeof(double) * PD_LINK_FIELDS * n_links * (size_t)n_models;
+  PD_CUDA(ctx->raw.ensure(raw_bytes + sizeof(double) * 3 * n_models));
+  PD_CUDA(ctx->model.ensure(sizeof(double) * F_COUNT * n_links * (size_t)n_models));
+  PD_CUDA(ctx->gravity.ensure(sizeof(double) * 3 * n_models));
+  PD_CUDA(ctx->mstatus.ensure(sizeof(int32_t) * n_models));
+  PD_CUDA(ctx->mrule.ensure(sizeof(int32_t) * n_models));
+  double* raw = ctx->raw.as<double>();
+  double* graw = raw + PD_LINK_FIELDS * n_links * (size_t)n_models;
+  PD_CUDA(cudaMemcpyAsync(raw, links, raw_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(graw, g.data(), sizeof(double) * 3 * n_models, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(ctx->mstatus.p, ms.data(), sizeof(int32_t) * n_models, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(ctx->mrule.p, mr.data(), sizeof(int32_t) * n_models, cudaMemcpyHostToDevice, ctx->stream));
+  dim3 grid((unsigned)((n_models + 127) / 128), (unsigned)n_links);
+  pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, ctx->model.as<double>(),
+                                                     ctx->gravity.as<double>());
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->n_links = n_links;
+  ctx->n_models = n_models;
+  return PD_OK;
+}
+
+pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* d_q,
+                                     const double* d_qdot, const double* d_tau, double* d_qddot,
+                                     int32_t* d_slot_status, int32_t* d_slot_round, int32_t* d_slot_index) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0) {
+    ctx->last_error = "forward dynamics: negative batch";
+    return PD_INVALID_ARGUMENT;
+  }
+  PD_CUDA(cudaSetDevice(ctx->device));
+  return run_device(ctx, algo, batch, d_q, d_qdot, d_tau, d_qddot, d_slot_status, d_slot_round, d_slot_index);
+}
+
+pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
+                              const double* tau, double* qddot, int32_t* slot_status, int32_t* slot_round,
+                              int32_t* slot_index) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0 || (batch > 0 && (!q || !qdot || !tau || !qddot))) {
+    ctx->last_error = "forward dynamics: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int n = ctx->n_links;
+  const size_t bytes = sizeof(double) * (size_t)n * batch;
+  // staging: [B][n] host rows -> device -> [n][B]
+  PD_CUDA(ctx->io_q.ensure(2 * bytes));
+  PD_CUDA(ctx->io_qd.ensure(2 * bytes));
+  PD_CUDA(ctx->io_tau.ensure(2 * bytes));
+  PD_CUDA(ctx->io_qdd.ensure(2 * bytes));
+  PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+  double* sq = ctx->io_q.as<double>();
+  double* sqd = ctx->io_qd.as<double>();
+  double* stau = ctx->io_tau.as<double>();
+  double* sqdd = ctx->io_qdd.as<double>();
+  const size_t half = (size_t)n * batch;
+  PD_CUDA(cudaMemcpyAsync(sq + half, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(sqd + half, qdot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(stau + half, tau, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  launch_transpose(ctx, sq + half, sq, batch, n);
+  launch_transpose(ctx, sqd + half, sqd, batch, n);
+  launch_transpose(ctx, stau + half, stau, batch, n);
+  int32_t* st = ctx->io_status.as<int32_t>();
+  pd_status s = run_device(ctx, algo, batch, sq, sqd, stau, sqdd, st, st + batch, st + 2 * batch);
+  if (s != PD_OK) return s;
+  launch_transpose(ctx, sqdd, sqdd + half, n, batch);
+  PD_CUDA(cudaMemcpyAsync(qddot, sqdd + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<int32_t> hs;
+  if (slot_status || slot_round || slot_index) {
+    hs.resize(3 * batch);
+    PD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (slot_status) std::memcpy(slot_status, hs.data(), sizeof(int32_t) * batch);
+  if (slot_round) std::memcpy(slot_round, hs.data() + batch, sizeof(int32_t) * batch);
+  if (slot_index) std::memcpy(slot_index, hs.data() + 2 * batch, sizeof(int32_t) * batch);
+  return PD_OK;
+}
+
+pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
+                              double* tau) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0 || (batch > 0 && (!q || !qdot || !qddot || !tau))) {
+    ctx->last_error = "inverse dynamics: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  if (ctx->n_models <= 0 || (ctx->n_models != 1 && ctx->n_models != batch)) {
+    ctx->last_error = "inverse dynamics: batch must equal the number of models (or use one shared model)";
+    return PD_INVALID_ARGUMENT;
+  }
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int n = ctx->n_links;
+  const size_t bytes = sizeof(double) * (size_t)n * batch;
+  const size_t half = (size_t)n * batch;
+  PD_CUDA(ctx->io_q.ensure(2 * bytes));
+  PD_CUDA(ctx->io_qd.ensure(2 * bytes));
+  PD_CUDA(ctx->io_tau.ensure(2 * bytes));
+  PD_CUDA(ctx->io_qdd.ensure(2 * bytes));
+  PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+  double *sq = ctx->io_q.as<double>(), *sqd = ctx->io_qd.as<double>(), *sqdd = ctx->io_qdd.as<double>(),
+         *stau = ctx->io_tau.as<double>();
+  PD_CUDA(cudaMemcpyAsync(sq + half, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(sqd + half, qdot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(sqdd + half, qddot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  launch_transpose(ctx, sq + half, sq, batch, n);
+  launch_transpose(ctx, sqd + half, sqd, batch, n);
+  launch_transpose(ctx, sqdd + half, sqdd, batch, n);
+  int32_t* st = ctx->io_status.as<int32_t>();
+  // BatchIO: tau slot carries qddot in, qdd slot carries torques out
+  BatchIO io{sq, sqd, sqdd, stau, st, st + batch, st + 2 * batch, batch};
+  launch_invdyn(model_view(ctx), io, ctx->stream);
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  launch_transpose(ctx, stau, stau + half, n, batch);
+  PD_CUDA(cudaMemcpyAsync(tau, stau + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PD_OK;
+}
+
+void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links, char* buf, int32_t buflen) {
+  if (!buf || buflen <= 0) return;
+  std::string m;
+  switch (code) {
+    case PD_SLOT_OK: m = ""; break;
+    case PD_SLOT_DEGENERATE_ARTICULATION:
+      m = "degenerate articulation at joint " + std::to_string(index) + ": projected articulated inertia vanishes";
+      break;
+    case PD_SLOT_JSI_NOT_SPD:
+      m = "joint-space inertia is not positive definite; the chain model is degenerate";
+      break;
+    case PD_SLOT_JSI_REFINE_FAILED:
+      m = "joint-space inertia solve failed to reach the required residual; the inertia matrix is too "
+          "ill-conditioned";
+      break;
+    case PD_SLOT_LINK_INERTIA_NOT_PD:
+      m = "constraint-force assembly: a link inertia is not positive definite";
+      break;
+    case PD_SLOT_OEE_SINGULAR_PIVOT:
+      m = "odd-even elimination: singular pivot block (round " + std::to_string(round) + ", block " +
+          std::to_string(index) + ")";
+      break;
+    case PD_SLOT_OEE_SINGULAR_FINAL:
+      m = "odd-even elimination: singular diagonal block after elimination (block " + std::to_string(index) + ")";
+      break;
+    case PD_SLOT_BAD_MODEL:
+      switch (index) {
+        case PD_RULE_MASS: m = "spatial inertia: mass must be positive"; break;
+        case PD_RULE_FINITE: m = "spatial inertia: parameters must be finite"; break;
+        case PD_RULE_SYMMETRIC: m = "spatial inertia: rotational inertia must be symmetric"; break;
+        default: m = "spatial inertia: rotational inertia must be positive definite"; break;
+      }
+      break;
+    case PD_SLOT_BAD_SIZE:
+      m = n_links <= 0 ? "forward dynamics: chain has no links"
+                       : "forward dynamics: q, qdot and tau must each have one entry per joint (chain has " +
+                             std::to_string(n_links) + ")";
+      break;
+    default: m = "unknown slot status"; break;
+  }
+  std::strncpy(buf, m.c_str(), (size_t)buflen - 1);
+  buf[buflen - 1] = '\0';
+}
+
+}  // extern "C"

@@ -1,0 +1,522 @@
+// CFA forward dynamics (the paper's Algorithm 1), one CTA per chain, one
+// thread per link (LPT consecutive links per thread for long chains).
+//
+// Reference: cfa_forward_dynamics (proj/core/src/forward_dynamics.cpp:418-450)
+//   = kinematics + torque surplus (3 scans)           -> cta_kinematics / cta_bias_torque
+//   + build_constraint_basis (:245-259)               -> householder_basis
+//   + build_cfa_operators (:261-357)                   -> stage "operators"
+//   + rhs = -apply_cross(tau_delta) (:359-376, :433-436)
+//   + oee_solve<5,1> (include/pardyn/oee.hpp:149-189)  -> stage "OEE"
+//   + qdd = apply_joint(td) + apply_cross_transpose(F_c) (:378-416, :441-442)
+//
+// OEE (the paper's building block 2, Eq. 17, row-centric form of
+// oee.hpp:73-145). Each round every row factors its own pivot D_k once
+// (LDL^T, 5x5) and publishes (L_k, 1/d_k, L_k^{-1} U_k, L_k^{-1} R_k); after
+// one barrier every row applies both eliminations from published data only:
+//   up   (pivot i+h): Z = L^{-1} U_i^T, D_i -= Z^T d^{-1} Z, R_i -= Z^T d^{-1} Rt,
+//                     U_i <- -Z^T d^{-1} Y_{i+h}            (only if i+2h < n)
+//   down (pivot i-h): D_i -= Y^T d^{-1} Y, R_i -= Y^T d^{-1} Rt.
+// Pivots are Schur complements of the SPD constraint operator (SURVEY.md
+// §7.4.6), so a symmetric factorization is valid; the rank test mirrors
+// FullPivLU::isInvertible (|pivot| > 5 eps max|diag|). The reported error
+// is the reference's: smallest failing row, its first failing pivot.
+#include "cta_common.cuh"
+
+namespace pd {
+
+namespace cfa {
+// Workspace field offsets (units of n doubles, ws[field * n + link]).
+constexpr int TD = 0, XS = 1, XB = 6, XD = 11, JD = 16, JO = 17;  // persistent
+constexpr int REL = 18;                                           // 12, until operators done
+constexpr int X = 30, V = 42, TMP = 48;                           // bias-torque phase only
+constexpr int AD = 30, UP = 45;                                   // 15 + 25: operators -> OEE D_i, U_i
+constexpr int HT = 70;                                            // 36: H columns (operators phase)
+constexpr int HH = 70;                                            // 21: H^T H for row i+1
+constexpr int PL = 18, SG = 28;                                   // OEE published: L (10), singular flag
+constexpr int PY = 70, PR = 95, PI = 100, OR = 105;               // Y (25), Rt (5), 1/d (5), R_i (5)
+constexpr int FIELDS = 110;
+}  // namespace cfa
+
+__device__ __forceinline__ int pk(int r, int c) { return r * (r + 1) / 2 + c; }   // packed lower incl diag
+__device__ __forceinline__ int pks(int r, int c) { return r * (r - 1) / 2 + c; }  // packed strict lower
+// index of (r, c) in Sym6's 3x3 packing (xx xy xz yy yz zz)
+__device__ __forceinline__ int s3(int r, int c) {
+  const int lo = r < c ? r : c, hi = r < c ? c : r;
+  return lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+}
+
+// Orthonormal complement of the screw: last five columns of the Householder
+// reflector Eigen's HouseholderQR builds for the 6x1 screw
+// (forward_dynamics.cpp:245-259: makeHouseholder + applyHouseholderOnTheLeft).
+// z[c][r]: column c of Z = [W | S].
+__device__ __forceinline__ void householder_basis(const Sv& S, double z[6][6]) {
+  const double s[6] = {S.a.x, S.a.y, S.a.z, S.l.x, S.l.y, S.l.z};
+  double tail = 0.0;
+#pragma unroll
+  for (int k = 1; k < 6; ++k) tail = fma(s[k], s[k], tail);
+  const double c0 = s[0];
+  double v[6] = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double tau = 0.0;
+  if (tail > 2.2250738585072014e-308) {
+    double beta = sqrt(fma(c0, c0, tail));
+    if (c0 >= 0.0) beta = -beta;
+    const double den = c0 - beta;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) v[k] = s[k] / den;
+    tau = (beta - c0) / beta;
+  }
+#pragma unroll
+  for (int c = 0; c < 5; ++c)
+#pragma unroll
+    for (int r = 0; r < 6; ++r) z[c][r] = (r == c + 1 ? 1.0 : 0.0) - (tau * v[r]) * v[c + 1];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) z[5][r] = s[r];
+}
+
+// LLT of the link's spatial inertia (packed lower, 21), Eigen semantics:
+// fails iff a pivot is <= 0 (forward_dynamics.cpp:302-305).
+__device__ __forceinline__ bool llt_inertia(const Inertia& J, double L[21], double inv[6]) {
+  const Sym6 S = inertia_sym6(J);
+  double a[21];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      a[pk(r, c)] = S.A[s3(r, c)];
+      a[pk(r + 3, c + 3)] = S.D[s3(r, c)];
+    }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a[pk(r + 3, c)] = S.B[3 * c + r];  // lower-left = B^T
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    double x = a[pk(k, k)];
+#pragma unroll
+    for (int j = 0; j < k; ++j) x = fma(-L[pk(k, j)], L[pk(k, j)], x);
+    ok = ok && (x > 0.0);
+    const double l = sqrt(x);
+    L[pk(k, k)] = l;
+    inv[k] = 1.0 / l;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      double s = a[pk(i, k)];
+#pragma unroll
+      for (int j = 0; j < k; ++j) s = fma(-L[pk(i, j)], L[pk(k, j)], s);
+      L[pk(i, k)] = s * inv[k];
+    }
+  }
+  return ok;
+}
+__device__ __forceinline__ void lower_solve6(const double L[21], const double inv[6], double x[6]) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    double s = x[r];
+#pragma unroll
+    for (int c = 0; c < r; ++c) s = fma(-L[pk(r, c)], x[c], s);
+    x[r] = s * inv[r];
+  }
+}
+
+// LDL^T of a packed symmetric 5x5 with the FullPivLU-style rank test.
+__device__ __forceinline__ bool ldlt5(const double D[15], double L[10], double dinv[5]) {
+  double maxd = 0.0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) maxd = fmax(maxd, fabs(D[pk(k, k)]));
+  const double thr = 5.0 * 2.220446049250313e-16 * maxd;
+  double d[5];
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    double x = D[pk(j, j)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) x = fma(-L[pks(j, k)] * d[k], L[pks(j, k)], x);
+    d[j] = x;
+    ok = ok && (fabs(x) > thr);
+    dinv[j] = 1.0 / x;
+#pragma unroll
+    for (int i = j + 1; i < 5; ++i) {
+      double s = D[pk(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s = fma(-L[pks(i, k)] * d[k], L[pks(j, k)], s);
+      L[pks(i, j)] = s * dinv[j];
+    }
+  }
+  return ok;
+}
+__device__ __forceinline__ void unit_lower_solve5(const double L[10], double x[5]) {
+#pragma unroll
+  for (int r = 1; r < 5; ++r) {
+    double s = x[r];
+#pragma unroll
+    for (int c = 0; c < r; ++c) s = fma(-L[pks(r, c)], x[c], s);
+    x[r] = s;
+  }
+}
+__device__ __forceinline__ void unit_lowerT_solve5(const double L[10], double x[5]) {  // x <- L^{-T} x
+#pragma unroll
+  for (int r = 3; r >= 0; --r) {
+    double s = x[r];
+#pragma unroll
+    for (int c = r + 1; c < 5; ++c) s = fma(-L[pks(c, r)], x[c], s);
+    x[r] = s;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void ws_load(const double* ws, int n, int f0, int i, double* out) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = ws[(f0 + k) * n + i];
+}
+template <int K>
+__device__ __forceinline__ void ws_store(double* ws, int n, int f0, int i, const double* in) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) ws[(f0 + k) * n + i] = in[k];
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, double* __restrict__ gws, int lpt,
+                                                       int64_t p_off) {
+  extern __shared__ double dyn_smem[];
+  __shared__ ScanSmem scan_sm;
+  __shared__ int s_bad, s_link_fail;
+  const int n = mv.n;
+  const int64_t p = p_off + blockIdx.x;
+  const int64_t mc = mv.model_of(p);
+  double* ws = SMEM ? dyn_smem : gws + (int64_t)blockIdx.x * cfa::FIELDS * n;
+  const int t = threadIdx.x;
+  const int i0 = t * lpt, i1 = min(n, i0 + lpt);
+  if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) {
+    if (t == 0) model_rejected(mv, io, p, mc);
+    return;
+  }
+  if (t == 0) {
+    s_bad = n;
+    s_link_fail = 0;
+  }
+
+  // ---- kinematics + torque surplus ----------------------------------------
+  const IdFields idf{cfa::REL, cfa::X, cfa::V, cfa::TMP, cfa::TD};
+  cta_kinematics(mv, io, p, mc, ws, idf, lpt);
+  cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);  // ends with a barrier
+
+  // ---- operators (forward_dynamics.cpp:261-357) ----------------------------
+  // Z_i = [W_i | S_i], C_i = Ad(rel_{i+1})^T Z_{i+1}, J_i = L L^T,
+  // G = L^{-1} Z_i, H = L^{-1} C_i: own blocks G^T G, couplings G^T H,
+  // the next row's carried blocks H^T H.
+  for (int i = i0; i < i1; ++i) {
+    double L[21], linv[6];
+    if (!llt_inertia(mv.inertia(i, mc), L, linv)) atomicOr(&s_link_fail, 1);
+    double G[6][6];
+    householder_basis(mv.screw(i, mc), G);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) lower_solve6(L, linv, G[c]);
+    {
+      double ad[15], xd[5];
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) s = fma(G[r][k], G[c][k], s);
+          if (r < 5) ad[pk(r, c)] = s;
+          else if (c < 5) xd[c] = s;
+          else ws[cfa::JD * n + i] = s;
+        }
+      ws_store<15>(ws, n, cfa::AD, i, ad);
+      ws_store<5>(ws, n, cfa::XD, i, xd);
+    }
+    if (i + 1 < n) {
+      const SE3d T1 = ws_get_se3(ws, n, cfa::REL, i + 1);
+      double Z1[6][6];
+      householder_basis(mv.screw(i + 1, mc), Z1);
+      double up[25], xs[5], xb[5];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const Sv col = adT_apply(T1, Sv{mk(Z1[c][0], Z1[c][1], Z1[c][2]), mk(Z1[c][3], Z1[c][4], Z1[c][5])});
+        double h[6] = {col.a.x, col.a.y, col.a.z, col.l.x, col.l.y, col.l.z};
+        lower_solve6(L, linv, h);
+        ws_store<6>(ws, n, cfa::HT + 6 * c, i, h);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) s = fma(G[r][k], h[k], s);
+          if (r < 5 && c < 5) up[r * 5 + c] = -s;       // upper_i       (:347)
+          else if (r < 5) xs[r] = -s;                    // cross_super_i (:348)
+          else if (c < 5) xb[c] = -s;                    // cross_sub_i   (:349)
+          else ws[cfa::JO * n + i] = -s;                 // joint_off_i   (:350)
+        }
+      }
+      ws_store<25>(ws, n, cfa::UP, i, up);
+      ws_store<5>(ws, n, cfa::XS, i, xs);
+      ws_store<5>(ws, n, cfa::XB, i, xb);
+      double hh[21];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        double hr[6];
+        ws_load<6>(ws, n, cfa::HT + 6 * r, i, hr);
+#pragma unroll
+        for (int c = 0; c <= r; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) s = fma(hr[k], ws[(cfa::HT + 6 * c + k) * n + i], s);
+          hh[pk(r, c)] = s;
+        }
+      }
+      ws_store<21>(ws, n, cfa::HH, i, hh);
+    }
+  }
+  __syncthreads();
+  if (s_link_fail) {  // forward_dynamics.cpp:317-320
+    if (t == 0) {
+      io.status[p] = PD_SLOT_LINK_INERTIA_NOT_PD;
+      io.eround[p] = 0;
+      io.eindex[p] = 0;
+    }
+    return;
+  }
+
+  // ---- OEE initial state: D_i = A_diag (symmetric), U_i = upper_i,
+  //      R_i = -apply_cross(td)_i; diag/cross/joint blocks gain row i-1's H^T H.
+  for (int i = i0; i < i1; ++i) {
+    double d[15], xd[5];
+    ws_load<15>(ws, n, cfa::AD, i, d);
+    ws_load<5>(ws, n, cfa::XD, i, xd);
+    double jd = ws[cfa::JD * n + i];
+    if (i > 0) {
+      double hh[21];
+      ws_load<21>(ws, n, cfa::HH, i - 1, hh);
+#pragma unroll
+      for (int r = 0; r < 5; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) d[pk(r, c)] += hh[pk(r, c)];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) xd[r] += hh[pk(5, r)];
+      jd += hh[pk(5, 5)];
+    }
+    const double td = ws[cfa::TD * n + i];
+    double r5[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) r5[r] = xd[r] * td;
+    if (i > 0) {
+      const double tdm = ws[cfa::TD * n + i - 1];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) r5[r] = fma(ws[(cfa::XB + r) * n + i - 1], tdm, r5[r]);
+    }
+    if (i + 1 < n) {
+      const double tdp = ws[cfa::TD * n + i + 1];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) r5[r] = fma(ws[(cfa::XS + r) * n + i], tdp, r5[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) r5[r] = -r5[r];
+    ws_store<15>(ws, n, cfa::AD, i, d);
+    ws_store<5>(ws, n, cfa::XD, i, xd);
+    ws[cfa::JD * n + i] = jd;
+    ws_store<5>(ws, n, cfa::OR, i, r5);
+  }
+  __syncthreads();
+
+  // ---- OEE rounds -----------------------------------------------------------
+  const int rounds = ceil_log2_dev(n);
+  int h = 1;
+  for (int round = 1; round <= rounds; ++round, h <<= 1) {
+    // publish own pivot factorization
+    for (int k = i0; k < i1; ++k) {
+      double D[15], Lk[10], dinv[5];
+      ws_load<15>(ws, n, cfa::AD, k, D);
+      const bool ok = ldlt5(D, Lk, dinv);
+      ws_store<10>(ws, n, cfa::PL, k, Lk);
+      ws_store<5>(ws, n, cfa::PI, k, dinv);
+      ws[cfa::SG * n + k] = ok ? 0.0 : 1.0;
+      double rt[5];
+      ws_load<5>(ws, n, cfa::OR, k, rt);
+      unit_lower_solve5(Lk, rt);
+      ws_store<5>(ws, n, cfa::PR, k, rt);
+      if (k < n - h) {  // U_k exists at distance h
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          double col[5];
+#pragma unroll
+          for (int r = 0; r < 5; ++r) col[r] = ws[(cfa::UP + r * 5 + c) * n + k];
+          unit_lower_solve5(Lk, col);
+#pragma unroll
+          for (int r = 0; r < 5; ++r) ws[(cfa::PY + r * 5 + c) * n + k] = col[r];
+        }
+      }
+    }
+    __syncthreads();
+    // singular pivots: smallest failing row reports its first failing pivot (oee.hpp:88-138)
+    for (int i = i0; i < i1; ++i) {
+      const bool up_bad = (i < n - h) && ws[cfa::SG * n + i + h] != 0.0;
+      const bool dn_bad = (i >= h) && ws[cfa::SG * n + i - h] != 0.0;
+      if (up_bad || dn_bad) atomicMin(&s_bad, i);
+    }
+    __syncthreads();
+    if (s_bad < n) {
+      if (t == 0) {
+        const int i = s_bad;
+        const bool up_bad = (i < n - h) && ws[cfa::SG * n + i + h] != 0.0;
+        io.status[p] = PD_SLOT_OEE_SINGULAR_PIVOT;
+        io.eround[p] = round;
+        io.eindex[p] = up_bad ? i + h : i - h;
+      }
+      return;
+    }
+    // eliminate
+    for (int i = i0; i < i1; ++i) {
+      double D[15], R[5];
+      ws_load<15>(ws, n, cfa::AD, i, D);
+      ws_load<5>(ws, n, cfa::OR, i, R);
+      if (i < n - h) {
+        const int k = i + h;
+        double Lk[10], dinv[5], rt[5];
+        ws_load<10>(ws, n, cfa::PL, k, Lk);
+        ws_load<5>(ws, n, cfa::PI, k, dinv);
+        ws_load<5>(ws, n, cfa::PR, k, rt);
+        double Z[5][5];  // Z[a] = L^{-1} (row a of U_i)^T  (column a of Z)
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+#pragma unroll
+          for (int r = 0; r < 5; ++r) Z[a][r] = ws[(cfa::UP + a * 5 + r) * n + i];
+          unit_lower_solve5(Lk, Z[a]);
+        }
+        double Zs[5][5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a)
+#pragma unroll
+          for (int r = 0; r < 5; ++r) Zs[a][r] = Z[a][r] * dinv[r];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+#pragma unroll
+          for (int b = 0; b <= a; ++b) {
+            double s = D[pk(a, b)];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) s = fma(-Zs[a][r], Z[b][r], s);
+            D[pk(a, b)] = s;
+          }
+          double s = R[a];
+#pragma unroll
+          for (int r = 0; r < 5; ++r) s = fma(-Zs[a][r], rt[r], s);
+          R[a] = s;
+        }
+        if (i < n - 2 * h) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            double yc[5];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) yc[r] = ws[(cfa::PY + r * 5 + c) * n + k];
+#pragma unroll
+            for (int a = 0; a < 5; ++a) {
+              double s = 0.0;
+#pragma unroll
+              for (int r = 0; r < 5; ++r) s = fma(Zs[a][r], yc[r], s);
+              ws[(cfa::UP + a * 5 + c) * n + i] = -s;
+            }
+          }
+        }
+      }
+      if (i >= h) {
+        const int k = i - h;
+        double dinv[5], rt[5], Y[5][5];
+        ws_load<5>(ws, n, cfa::PI, k, dinv);
+        ws_load<5>(ws, n, cfa::PR, k, rt);
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+          for (int c = 0; c < 5; ++c) Y[r][c] = ws[(cfa::PY + r * 5 + c) * n + k];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+#pragma unroll
+          for (int b = 0; b <= a; ++b) {
+            double s = D[pk(a, b)];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) s = fma(-Y[r][a] * dinv[r], Y[r][b], s);
+            D[pk(a, b)] = s;
+          }
+          double s = R[a];
+#pragma unroll
+          for (int r = 0; r < 5; ++r) s = fma(-Y[r][a] * dinv[r], rt[r], s);
+          R[a] = s;
+        }
+      }
+      ws_store<15>(ws, n, cfa::AD, i, D);
+      ws_store<5>(ws, n, cfa::OR, i, R);
+    }
+    __syncthreads();
+  }
+
+  // ---- final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187) -------------
+  for (int i = i0; i < i1; ++i) {
+    double D[15], L[10], dinv[5], x[5];
+    ws_load<15>(ws, n, cfa::AD, i, D);
+    ws_load<5>(ws, n, cfa::OR, i, x);
+    if (!ldlt5(D, L, dinv)) atomicMin(&s_bad, i);
+    unit_lower_solve5(L, x);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) x[r] *= dinv[r];
+    unit_lowerT_solve5(L, x);
+    ws_store<5>(ws, n, cfa::OR, i, x);  // constraint force F_c,i
+  }
+  __syncthreads();
+  if (s_bad < n) {
+    if (t == 0) {
+      io.status[p] = PD_SLOT_OEE_SINGULAR_FINAL;
+      io.eround[p] = rounds;
+      io.eindex[p] = s_bad;
+    }
+    return;
+  }
+
+  // ---- qdd = apply_joint(td) + apply_cross_transpose(F_c) ------------------
+  for (int i = i0; i < i1; ++i) {
+    const double td = ws[cfa::TD * n + i];
+    double v = ws[cfa::JD * n + i] * td;
+    double f[5];
+    ws_load<5>(ws, n, cfa::OR, i, f);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) v = fma(ws[(cfa::XD + r) * n + i], f[r], v);
+    if (i > 0) {
+      v = fma(ws[cfa::JO * n + i - 1], ws[cfa::TD * n + i - 1], v);
+#pragma unroll
+      for (int r = 0; r < 5; ++r) v = fma(ws[(cfa::XS + r) * n + i - 1], ws[(cfa::OR + r) * n + i - 1], v);
+    }
+    if (i + 1 < n) {
+      v = fma(ws[cfa::JO * n + i], ws[cfa::TD * n + i + 1], v);
+#pragma unroll
+      for (int r = 0; r < 5; ++r) v = fma(ws[(cfa::XB + r) * n + i], ws[(cfa::OR + r) * n + i + 1], v);
+    }
+    io.qdd[(int64_t)i * io.B + p] = v;
+  }
+  if (t == 0) {
+    io.status[p] = PD_SLOT_OK;
+    io.eround[p] = 0;
+    io.eindex[p] = 0;
+  }
+}
+
+size_t cfa_workspace_bytes(int n) { return (size_t)cfa::FIELDS * n * sizeof(double); }
+
+// Shared-memory workspace when it fits (n <= 260), otherwise one global slot
+// per CTA in flight, launched in waves of gws_slots CTAs.
+void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s) {
+  const int n = mv.n;
+  int nt = ((n + 31) / 32) * 32;
+  if (nt > 256) nt = 256;
+  const int lpt = (n + nt - 1) / nt;
+  const size_t ws_bytes = cfa_workspace_bytes(n);
+  if (ws_bytes <= 224 * 1024) {
+    cudaFuncSetAttribute(cfa_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
+    cfa_cta_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, lpt, 0);
+  } else {
+    for (int64_t b0 = 0; b0 < io.B; b0 += gws_slots) {
+      const int64_t nb = (io.B - b0 < gws_slots) ? io.B - b0 : gws_slots;
+      cfa_cta_kernel<false><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, lpt, b0);
+    }
+  }
+}
+
+}  // namespace pd

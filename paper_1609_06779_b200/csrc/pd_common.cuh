@@ -1,0 +1,298 @@
+// Device-side spatial algebra for the batched forward-dynamics kernels.
+//
+// Everything is FP64 and structure-aware: transforms stay as (R, p) and are
+// applied through cross products instead of dense 6x6 adjoints, spatial
+// inertias are applied from (m, c, Ic), symmetric 6x6 articulated inertias
+// are kept as three 3x3 blocks (21 doubles). Conventions follow the
+// reference (proj/core/include/pardyn/spatial.hpp:7-10, src/spatial.cpp):
+// twists stack (angular, linear), wrenches (moment, force),
+// Ad(R,p) = [[R,0],[p^R,R]], ad_V = [[w^,0],[v^,w^]].
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/pardyn_c.h"
+
+namespace pd {
+
+// Packed device model record, 28 doubles per link, stored SoA as
+// model[(field * n_links + link) * n_models + chain] (chain fastest).
+enum ModelField : int {
+  F_MASS = 0,
+  F_COM = 1,    // 3
+  F_IC = 4,     // 6: xx xy xz yy yz zz (rotational inertia about the COM)
+  F_SCREW = 10, // 6: angular, linear
+  F_HR = 16,    // 9: home rotation, row-major
+  F_HP = 25,    // 3: home translation
+  F_COUNT = 28
+};
+
+struct Vec3d {
+  double x, y, z;
+};
+
+__device__ __forceinline__ Vec3d mk(double x, double y, double z) { return {x, y, z}; }
+__device__ __forceinline__ Vec3d operator+(Vec3d a, Vec3d b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ Vec3d operator-(Vec3d a, Vec3d b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ Vec3d operator*(double s, Vec3d a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ double dot(Vec3d a, Vec3d b) { return fma(a.x, b.x, fma(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ Vec3d cross(Vec3d a, Vec3d b) {
+  return {fma(a.y, b.z, -a.z * b.y), fma(a.z, b.x, -a.x * b.z), fma(a.x, b.y, -a.y * b.x)};
+}
+__device__ __forceinline__ Vec3d fmav(double s, Vec3d a, Vec3d b) {  // s*a + b
+  return {fma(s, a.x, b.x), fma(s, a.y, b.y), fma(s, a.z, b.z)};
+}
+
+// 3x3 row-major rotation.
+struct Mat3d {
+  double m[9];
+};
+__device__ __forceinline__ Vec3d mul(const Mat3d& R, Vec3d v) {
+  return {fma(R.m[0], v.x, fma(R.m[1], v.y, R.m[2] * v.z)), fma(R.m[3], v.x, fma(R.m[4], v.y, R.m[5] * v.z)),
+          fma(R.m[6], v.x, fma(R.m[7], v.y, R.m[8] * v.z))};
+}
+__device__ __forceinline__ Vec3d mulT(const Mat3d& R, Vec3d v) {
+  return {fma(R.m[0], v.x, fma(R.m[3], v.y, R.m[6] * v.z)), fma(R.m[1], v.x, fma(R.m[4], v.y, R.m[7] * v.z)),
+          fma(R.m[2], v.x, fma(R.m[5], v.y, R.m[8] * v.z))};
+}
+__device__ __forceinline__ Mat3d matmul(const Mat3d& A, const Mat3d& B) {
+  Mat3d C;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      C.m[3 * r + c] = fma(A.m[3 * r], B.m[c], fma(A.m[3 * r + 1], B.m[3 + c], A.m[3 * r + 2] * B.m[6 + c]));
+  return C;
+}
+
+struct SE3d {
+  Mat3d R;
+  Vec3d p;
+};
+
+// Spatial 6-vectors as (angular/moment, linear/force) 3-vector pairs.
+struct Sv {
+  Vec3d a, l;
+};
+__device__ __forceinline__ Sv operator+(const Sv& x, const Sv& y) { return {x.a + y.a, x.l + y.l}; }
+__device__ __forceinline__ Sv operator-(const Sv& x, const Sv& y) { return {x.a - y.a, x.l - y.l}; }
+__device__ __forceinline__ Sv operator*(double s, const Sv& x) { return {s * x.a, s * x.l}; }
+__device__ __forceinline__ double dot(const Sv& x, const Sv& y) { return dot(x.a, y.a) + dot(x.l, y.l); }
+__device__ __forceinline__ Sv svzero() { return {mk(0, 0, 0), mk(0, 0, 0)}; }
+
+// Ad(R,p) x = (R w, R v + p x (R w))                         spatial.cpp:27-34
+__device__ __forceinline__ Sv ad_apply(const SE3d& T, const Sv& x) {
+  const Vec3d rw = mul(T.R, x.a);
+  return {rw, mul(T.R, x.l) + cross(T.p, rw)};
+}
+// Ad(R,p)^T f = (R^T (m - p x f), R^T f)
+__device__ __forceinline__ Sv adT_apply(const SE3d& T, const Sv& f) {
+  return {mulT(T.R, f.a - cross(T.p, f.l)), mulT(T.R, f.l)};
+}
+// Ad(R,p)^{-1} x = (R^T w, R^T (v - p x w))
+__device__ __forceinline__ Sv adinv_apply(const SE3d& T, const Sv& x) {
+  return {mulT(T.R, x.a), mulT(T.R, x.l - cross(T.p, x.a))};
+}
+// Ad(R,p)^{-T} f = (R m + p x (R f), R f)   (wrench carried from link to base coords)
+__device__ __forceinline__ Sv adinvT_apply(const SE3d& T, const Sv& f) {
+  const Vec3d rf = mul(T.R, f.l);
+  return {mul(T.R, f.a) + cross(T.p, rf), rf};
+}
+// ad_V x = (w x xw, v x xw + w x xv)                           spatial.cpp:18-25
+__device__ __forceinline__ Sv adv_apply(const Sv& V, const Sv& x) {
+  return {cross(V.a, x.a), cross(V.l, x.a) + cross(V.a, x.l)};
+}
+// -ad_V^T h = (w x ha + v x hl, w x hl)
+__device__ __forceinline__ Sv neg_advT_apply(const Sv& V, const Sv& h) {
+  return {cross(V.a, h.a) + cross(V.l, h.l), cross(V.a, h.l)};
+}
+// Compose (a*b)(x) = a(b(x))                                     spatial.hpp:80-82
+__device__ __forceinline__ SE3d compose(const SE3d& a, const SE3d& b) {
+  return {matmul(a.R, b.R), mul(a.R, b.p) + a.p};
+}
+
+// Link inertia parameters; J = [[Ic + m c^ c^T, m c^], [m c^T, m I]].
+struct Inertia {
+  double m;
+  Vec3d c;
+  double I[6];  // xx xy xz yy yz zz
+};
+__device__ __forceinline__ Vec3d sym3_mul(const double* I, Vec3d w) {
+  return {fma(I[0], w.x, fma(I[1], w.y, I[2] * w.z)), fma(I[1], w.x, fma(I[3], w.y, I[4] * w.z)),
+          fma(I[2], w.x, fma(I[4], w.y, I[5] * w.z))};
+}
+// J (w, v): lin = m (v - c x w); ang = Ic w + c x lin
+__device__ __forceinline__ Sv inertia_apply(const Inertia& J, const Sv& x) {
+  const Vec3d lin = J.m * (x.l - cross(J.c, x.a));
+  return {sym3_mul(J.I, x.a) + cross(J.c, lin), lin};
+}
+
+// Symmetric 6x6 as blocks [[A, B], [B^T, D]]; A, D packed sym (xx xy xz yy yz zz),
+// B row-major 3x3.
+struct Sym6 {
+  double A[6];
+  double B[9];
+  double D[6];
+};
+__device__ __forceinline__ Sv sym6_apply(const Sym6& P, const Sv& x) {
+  const Vec3d bl = mul(*reinterpret_cast<const Mat3d*>(P.B), x.l);
+  const Vec3d btw = mulT(*reinterpret_cast<const Mat3d*>(P.B), x.a);
+  return {sym3_mul(P.A, x.a) + bl, btw + sym3_mul(P.D, x.l)};
+}
+__device__ __forceinline__ double sym6_trace(const Sym6& P) { return P.A[0] + P.A[3] + P.A[5] + P.D[0] + P.D[3] + P.D[5]; }
+
+// Explicit J as Sym6 (spatial.cpp:89-98: Ic + m * (cx cx^T), m cx, m I).
+__device__ __forceinline__ Sym6 inertia_sym6(const Inertia& J) {
+  Sym6 P;
+  const double cx = J.c.x, cy = J.c.y, cz = J.c.z;
+  // cx^ cx^T = |c|^2 I - c c^T
+  const double c2 = fma(cx, cx, fma(cy, cy, cz * cz));
+  P.A[0] = fma(J.m, c2 - cx * cx, J.I[0]);
+  P.A[1] = fma(J.m, -cx * cy, J.I[1]);
+  P.A[2] = fma(J.m, -cx * cz, J.I[2]);
+  P.A[3] = fma(J.m, c2 - cy * cy, J.I[3]);
+  P.A[4] = fma(J.m, -cy * cz, J.I[4]);
+  P.A[5] = fma(J.m, c2 - cz * cz, J.I[5]);
+  // m c^ = m [[0,-cz,cy],[cz,0,-cx],[-cy,cx,0]]
+  P.B[0] = 0.0;        P.B[1] = -J.m * cz; P.B[2] = J.m * cy;
+  P.B[3] = J.m * cz;   P.B[4] = 0.0;       P.B[5] = -J.m * cx;
+  P.B[6] = -J.m * cy;  P.B[7] = J.m * cx;  P.B[8] = 0.0;
+  P.D[0] = J.m; P.D[1] = 0.0; P.D[2] = 0.0; P.D[3] = J.m; P.D[4] = 0.0; P.D[5] = J.m;
+  return P;
+}
+
+// R^T S R for symmetric packed S -> symmetric packed.
+__device__ __forceinline__ void sym3_congruence(const double* S, const Mat3d& R, double* out) {
+  // T = S R (3x3)
+  double T[9];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const Vec3d col = sym3_mul(S, mk(R.m[c], R.m[3 + c], R.m[6 + c]));
+    T[c] = col.x;
+    T[3 + c] = col.y;
+    T[6 + c] = col.z;
+  }
+  // out = R^T T
+  const int idx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int r = idx[k][0], c = idx[k][1];
+    out[k] = fma(R.m[r], T[c], fma(R.m[3 + r], T[3 + c], R.m[6 + r] * T[6 + c]));
+  }
+}
+
+// Ad(T)^T P Ad(T) for symmetric P (articulated-inertia carry across a joint,
+// forward_dynamics.cpp:150-156). Shift of reference point by p, then rotation:
+//   Y = B - p^ D ; X11 = A - p^ B^T + Y p^ ; out = (R^T X11 R, R^T Y R, R^T D R).
+__device__ __forceinline__ Sym6 sym6_congruence(const Sym6& P, const SE3d& T) {
+  const Vec3d p = T.p;
+  double Y[9];
+  // columns of p^ D: p x D[:,j]
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int j0 = j == 0 ? 0 : (j == 1 ? 1 : 2);
+    const int j1 = j == 0 ? 1 : (j == 1 ? 3 : 4);
+    const int j2 = j == 0 ? 2 : (j == 1 ? 4 : 5);
+    const Vec3d dcol = mk(P.D[j0], P.D[j1], P.D[j2]);
+    const Vec3d pd = cross(p, dcol);
+    Y[j] = P.B[j] - pd.x;
+    Y[3 + j] = P.B[3 + j] - pd.y;
+    Y[6 + j] = P.B[6 + j] - pd.z;
+  }
+  // K = p^ B^T : column j of B^T is row j of B
+  double K[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const Vec3d pb = cross(p, mk(P.B[3 * j], P.B[3 * j + 1], P.B[3 * j + 2]));
+    K[j] = pb.x;
+    K[3 + j] = pb.y;
+    K[6 + j] = pb.z;
+  }
+  // W = Y p^ : row r of W = -(p x Y[r,:])
+  double W[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const Vec3d py = cross(p, mk(Y[3 * r], Y[3 * r + 1], Y[3 * r + 2]));
+    W[3 * r] = -py.x;
+    W[3 * r + 1] = -py.y;
+    W[3 * r + 2] = -py.z;
+  }
+  double X11[6];
+  X11[0] = P.A[0] - K[0] + W[0];
+  X11[1] = P.A[1] - 0.5 * (K[1] + K[3]) + 0.5 * (W[1] + W[3]);
+  X11[2] = P.A[2] - 0.5 * (K[2] + K[6]) + 0.5 * (W[2] + W[6]);
+  X11[3] = P.A[3] - K[4] + W[4];
+  X11[4] = P.A[4] - 0.5 * (K[5] + K[7]) + 0.5 * (W[5] + W[7]);
+  X11[5] = P.A[5] - K[8] + W[8];
+  Sym6 out;
+  sym3_congruence(X11, T.R, out.A);
+  sym3_congruence(P.D, T.R, out.D);
+  // R^T Y R
+  double T1[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      T1[3 * r + c] = fma(Y[3 * r], T.R.m[c], fma(Y[3 * r + 1], T.R.m[3 + c], Y[3 * r + 2] * T.R.m[6 + c]));
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      out.B[3 * r + c] = fma(T.R.m[r], T1[c], fma(T.R.m[3 + r], T1[3 + c], T.R.m[6 + r] * T1[6 + c]));
+  return out;
+}
+
+// Joint transform rel = screw_exp(S, -q) * home                 model.cpp:117-146
+// screw_exp: Rodrigues for a not-necessarily-unit angular part, pure
+// translation if |w| < 1e-12                                     spatial.cpp:43-68
+__device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Vec3d hp, double q) {
+  const double qq = -q;
+  const Vec3d w = S.a, v = S.l;
+  const double wn2 = dot(w, w);
+  const double wn = sqrt(wn2);
+  Mat3d E;
+  Vec3d t;
+  if (wn < 1e-12) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) E.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    t = qq * v;
+  } else {
+    double st, ct;
+    sincos(wn * qq, &st, &ct);
+    const double a = st / wn;
+    const double b = (1.0 - ct) / wn2;
+    const double c = (qq - a) / wn2;
+    // R = I + a w^ + b w^2 ; w^2 = w w^T - |w|^2 I
+    E.m[0] = fma(b, w.x * w.x - wn2, 1.0);
+    E.m[4] = fma(b, w.y * w.y - wn2, 1.0);
+    E.m[8] = fma(b, w.z * w.z - wn2, 1.0);
+    const double bxy = b * w.x * w.y, bxz = b * w.x * w.z, byz = b * w.y * w.z;
+    E.m[1] = fma(-a, w.z, bxy);
+    E.m[3] = fma(a, w.z, bxy);
+    E.m[2] = fma(a, w.y, bxz);
+    E.m[6] = fma(-a, w.y, bxz);
+    E.m[5] = fma(-a, w.x, byz);
+    E.m[7] = fma(a, w.x, byz);
+    // t = (q I + b w^ + c w^2) v = q v + b (w x v) + c (w x (w x v))
+    const Vec3d wv = cross(w, v);
+    t = fmav(c, cross(w, wv), fmav(b, wv, qq * v));
+  }
+  SE3d T;
+  T.R = matmul(E, HR);
+  T.p = mul(E, hp) + t;
+  return T;
+}
+
+// Kernel-side error record: first failure wins per slot.
+__device__ __forceinline__ void set_slot_error(int32_t* status, int32_t* eround, int32_t* eindex, int64_t slot,
+                                               int code, int round, int index) {
+  if (status[slot] == PD_SLOT_OK) {
+    status[slot] = code;
+    eround[slot] = round;
+    eindex[slot] = index;
+  }
+}
+
+__device__ __forceinline__ int ceil_log2_dev(int n) { return n <= 1 ? 0 : 32 - __clz(n - 1); }
+
+}  // namespace pd

@@ -1,0 +1,129 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs. Tolerance: rel_gap = ||a-b|| / max(1, ||b||)
+(tests/support/oracles.hpp:64-66) <= 1e-9 against the same algorithm's oracle
+(BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+import paper_1609_06779_b200 as pd
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+ALGOS = [pd.FdAlgo.jsiia, pd.FdAlgo.abia, pd.FdAlgo.cfa]
+ONAME = {pd.FdAlgo.jsiia: "jsiia", pd.FdAlgo.abia: "abia", pd.FdAlgo.cfa: "cfa"}
+
+
+def rel_gap(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(1.0, np.linalg.norm(b))
+
+
+def sample(oracle, n, seed):
+    links, g = oracle.random_chain(n, seed)
+    rng = np.random.default_rng(seed ^ 0xF00D)
+    return links, g, rng.uniform(-3, 3, n), rng.uniform(-2, 2, n), rng.uniform(-10, 10, n)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 32, 33, 64])
+def test_batch_matches_oracle(oracle, gpu_ctx, algo, n):
+    B = 40
+    cell = oracle.workload_seed(42, n, B)
+    links = oracle.workload_chains(cell, n, B)
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    q, qd, tau = 3 * q, 2 * qd, 10 * tau
+    ms, _ = gpu_ctx.set_models(links, np.tile([0, 0, -9.81], (B, 1)))
+    assert (ms == 0).all()
+    qdd, st, _, _ = gpu_ctx.solve(algo, q, qd, tau)
+    assert (st == 0).all(), st
+    ref, ost = oracle.batch_forward_dynamics(ONAME[algo], links, [0, 0, -9.81], q, qd, tau)
+    assert (ost == 0).all()
+    gaps = [rel_gap(qdd[b], ref[b]) for b in range(B)]
+    assert max(gaps) <= TOL, max(gaps)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("n", [128, 200, 256])
+def test_long_chains_match_oracle(oracle, gpu_ctx, algo, n):
+    B = 3
+    links = np.stack([oracle.random_chain(n, 9100 + 10 * n + c)[0] for c in range(B)])
+    rng = np.random.default_rng(n)
+    q, qd, tau = rng.uniform(-3, 3, (B, n)), rng.uniform(-2, 2, (B, n)), rng.uniform(-10, 10, (B, n))
+    gpu_ctx.set_models(links, None)
+    qdd, st, _, _ = gpu_ctx.solve(algo, q, qd, tau)
+    assert (st == 0).all(), st
+    ref, _ = oracle.batch_forward_dynamics(ONAME[algo], links, [0, 0, -9.81], q, qd, tau)
+    for b in range(B):
+        assert rel_gap(qdd[b], ref[b]) <= TOL
+
+
+def test_c1_shared_model_1024_states(oracle, gpu_ctx):
+    """configs[0]: ABIA on an 8-link chain, 1024 random states (shared model)."""
+    n, S = 8, 1024
+    cell = oracle.workload_seed(42, n, 1)
+    links = oracle.workload_chains(cell, n, 1)
+    qs, qds, taus = zip(*[oracle.workload_inputs(cell, n, 1, r) for r in range(S)])
+    q, qd, tau = np.concatenate(qs), np.concatenate(qds), np.concatenate(taus)
+    gpu_ctx.set_models(links, None)
+    qdd, st, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    assert (st == 0).all()
+    ref, _ = oracle.batch_forward_dynamics("abia", links, [0, 0, -9.81], q, qd, tau)
+    assert max(rel_gap(qdd[s], ref[s]) for s in range(S)) <= TOL
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_pendulum_closed_form(algo):
+    """test_fwddyn.cpp:105-122 / oracles.hpp:293-318."""
+    m, lc, izz, g = 1.3, 0.45, 0.07, 9.81
+    link = pd.LinkSpec(mass=m, com=np.array([lc, 0, 0]), inertia_rot=np.diag([0.11, 0.13, izz]))
+    chain = pd.RobotChain([link], np.array([0.0, -g, 0.0]))
+    rng = np.random.default_rng(111)
+    for _ in range(20):
+        q, qd, tau = rng.uniform(-6, 6), rng.uniform(-4, 4), rng.uniform(-8, 8)
+        want = (tau - m * g * lc * np.cos(q)) / (izz + m * lc * lc)
+        got = pd.forward_dynamics(chain, [q], [qd], [tau], algo)[0]
+        assert abs(got - want) < 1e-8 * max(1.0, abs(want))
+
+
+def test_errors_and_isolation(oracle):
+    """test_fwddyn.cpp:319-341 and the spatial-inertia rules."""
+    probs = []
+    for n in range(2, 6):
+        links, g, q, qd, tau = sample(oracle, n, 4600 + n)
+        probs.append(pd.FdProblem(pd.RobotChain.from_records(links, g), q, qd, tau))
+    probs[1].tau = np.zeros(1)
+    bad = pd.RobotChain.from_records(sample(oracle, 3, 77)[0])
+    bad.links[1].mass = -2.0
+    probs.append(pd.FdProblem(bad, np.zeros(3), np.zeros(3), np.zeros(3)))
+    res = pd.batch_forward_dynamics(probs, pd.FdAlgo.abia)
+    assert not res[1].ok() and "forward dynamics" in res[1].error
+    assert not res[4].ok() and res[4].error == "spatial inertia: mass must be positive"
+    for i in (0, 2, 3):
+        assert res[i].ok()
+        single = pd.forward_dynamics(probs[i].chain, probs[i].q, probs[i].qdot, probs[i].tau, pd.FdAlgo.abia)
+        assert np.array_equal(res[i].qddot, single)
+    assert pd.batch_forward_dynamics([], pd.FdAlgo.cfa) == []
+    with pytest.raises(pd.InvalidArgument):
+        pd.forward_dynamics(pd.RobotChain(), [], [], [], pd.FdAlgo.jsiia)
+
+
+@pytest.mark.parametrize("n", [1, 5, 20])
+def test_inverse_dynamics_matches_oracle(oracle, n):
+    links, g, q, qd, _ = sample(oracle, n, 7700 + n)
+    qdd = np.random.default_rng(n).uniform(-5, 5, n)
+    chain = pd.RobotChain.from_records(links, g)
+    got = pd.inverse_dynamics(chain, q, qd, qdd)
+    want = oracle.inverse_dynamics(links, g, q, qd, qdd)
+    assert rel_gap(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_deterministic(oracle, gpu_ctx, algo):
+    n, B = 16, 64
+    cell = oracle.workload_seed(42, n, B)
+    links = oracle.workload_chains(cell, n, B)
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 3)
+    gpu_ctx.set_models(links, None)
+    a = gpu_ctx.solve(algo, q, qd, tau)[0]
+    b = gpu_ctx.solve(algo, q, qd, tau)[0]
+    assert np.array_equal(a, b)
