@@ -96,8 +96,9 @@ const char* pd_status_string(pd_status s);
 /* Last call-level error text of this context ("" if none). */
 const char* pd_last_error(const pd_ctx* ctx);
 
-/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the
- * context's own stream. */
+/* Use an external CUDA stream (cudaStream_t as void*; cudaStreamLegacy
+ * ((void*)1) selects the legacy default stream); NULL restores the context's
+ * own non-blocking stream. */
 pd_status pd_set_stream(pd_ctx* ctx, void* stream);
 pd_status pd_synchronize(pd_ctx* ctx);
 
@@ -131,6 +132,25 @@ pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const
 
 /* Reference error message of a slot outcome into buf (always terminated). */
 void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links, char* buf, int32_t buflen);
+
+/* Seeded synthetic workloads of the reference benchmark (product side,
+ * host threads):
+ *   pd_mix             <- mix (bench.cpp:42-47, splitmix64 finalizer)
+ *   pd_workload_seed   <- workload_seed (bench.cpp:350-355)
+ *   pd_random_chain    <- random_chain(n, seed) (model.cpp:157-185)
+ *   pd_workload_chains <- workload_chains (bench.cpp:357-366), chains
+ *                         [g0, g0+count) of the cell, links[chain][link][31]
+ *   pd_workload_inputs <- workload_inputs (bench.cpp:368-383), [group][link] */
+uint64_t pd_mix(uint64_t x);
+uint64_t pd_workload_seed(uint64_t seed, int32_t n_links, int64_t n_groups);
+void pd_random_chain(int32_t n_links, uint64_t seed, double* links);
+void pd_workload_chains(uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count, double* links);
+void pd_workload_inputs(uint64_t cell_seed, int32_t n_links, int64_t n_groups, int64_t repeat, double* q,
+                        double* qdot, double* drive);
+
+/* Diagnostic: measured dense FP64 FMA throughput of this device (TFLOP/s),
+ * the FP64 roofline denominator (no FP64 figure in MEASURED_PEAKS.json). */
+pd_status pd_probe_fp64_peak(pd_ctx* ctx, double* tflops, double* elapsed_ms);
 
 /* Number of kernels this context has launched since creation. */
 int64_t pd_kernel_launches(const pd_ctx* ctx);

@@ -24,7 +24,8 @@ LINK_FIELDS = 31
 EXPORTS = (
     "pd_create", "pd_destroy", "pd_abi_version", "pd_status_string", "pd_last_error", "pd_set_stream",
     "pd_synchronize", "pd_set_models", "pd_forward_dynamics", "pd_forward_dynamics_device", "pd_inverse_dynamics",
-    "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant",
+    "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant", "pd_mix", "pd_workload_seed", "pd_random_chain",
+    "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak",
 )
 
 _lib = None
@@ -73,6 +74,18 @@ def load():
     L.pd_kernel_launches.restype = C.c_int64
     L.pd_kernel_variant.argtypes = [C.c_void_p, C.c_int, C.c_int32]
     L.pd_kernel_variant.restype = C.c_char_p
+    L.pd_mix.argtypes = [C.c_uint64]
+    L.pd_mix.restype = C.c_uint64
+    L.pd_workload_seed.argtypes = [C.c_uint64, C.c_int32, C.c_int64]
+    L.pd_workload_seed.restype = C.c_uint64
+    L.pd_random_chain.argtypes = [C.c_int32, C.c_uint64, _D]
+    L.pd_random_chain.restype = None
+    L.pd_workload_chains.argtypes = [C.c_uint64, C.c_int32, C.c_int64, C.c_int64, _D]
+    L.pd_workload_chains.restype = None
+    L.pd_workload_inputs.argtypes = [C.c_uint64, C.c_int32, C.c_int64, C.c_int64, _D, _D, _D]
+    L.pd_workload_inputs.restype = None
+    L.pd_probe_fp64_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.pd_probe_fp64_peak.restype = C.c_int
     _lib = L
     return L
 

@@ -191,13 +191,14 @@ class Context:
         self.n_links, self.n_models = n, M
         return ms, mr
 
-    def solve(self, algo, q, qdot, tau):
-        """Host-buffer solve: q/qdot/tau (B, n) -> (qddot, status, round, index)."""
+    def solve(self, algo, q, qdot, tau, out=None):
+        """Host-buffer solve: q/qdot/tau (B, n) -> (qddot, status, round, index).
+        `out` may be a preallocated (pinned) (B, n) float64 array."""
         q = np.ascontiguousarray(q, dtype=np.float64)
         qd = np.ascontiguousarray(qdot, dtype=np.float64)
         tau = np.ascontiguousarray(tau, dtype=np.float64)
         B = q.shape[0]
-        qdd = np.empty_like(q)
+        qdd = np.empty_like(q) if out is None else out
         st = np.zeros(B, np.int32)
         rd = np.zeros(B, np.int32)
         ix = np.zeros(B, np.int32)
@@ -220,10 +221,22 @@ class Context:
         return tau
 
     def set_stream(self, stream_ptr):
-        self._check(self._L.pd_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+        """Run on a CUDA stream (cudaStream_t as int). 0 = the legacy default
+        stream (what torch.cuda.current_stream() is unless a stream is set);
+        None restores the context's own stream."""
+        if stream_ptr is None:
+            self._check(self._L.pd_set_stream(self._h, None))
+        else:
+            self._check(self._L.pd_set_stream(self._h, C.c_void_p(stream_ptr if stream_ptr else 1)))
 
     def synchronize(self):
         self._check(self._L.pd_synchronize(self._h))
+
+    def probe_fp64_peak(self):
+        """Measured dense FP64 FMA throughput (TFLOP/s) of this device."""
+        tf, ms = C.c_double(0), C.c_double(0)
+        self._check(self._L.pd_probe_fp64_peak(self._h, C.byref(tf), C.byref(ms)))
+        return tf.value
 
     def kernel_launches(self) -> int:
         return int(self._L.pd_kernel_launches(self._h))

@@ -1,0 +1,169 @@
+// ABIA per-link steps in base coordinates, shared by the TMA-pipelined kernel
+// (abia_tma.cu) and the plain lane kernel (abia.cu) so both execute the same
+// arithmetic. See abia.cu for the derivation and the reference mapping.
+#pragma once
+
+#include "pd_batch.cuh"
+
+namespace pd {
+
+// Spatial inertia of link i expressed in base coordinates, J0 = Ad(X)^T J Ad(X)
+// for X = (R, p) mapping base to link coordinates: same mass, com at
+// X^{-1}(c) = R^T (c - p), rotational inertia R^T Ic R about the com.
+__device__ __forceinline__ Inertia inertia_to_base(const Inertia& J, const SE3d& X) {
+  Inertia o;
+  o.m = J.m;
+  o.c = mulT(X.R, J.c - X.p);
+  double T[9];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const Vec3d col = sym3_mul(J.I, mk(X.R.m[c], X.R.m[3 + c], X.R.m[6 + c]));
+    T[c] = col.x;
+    T[3 + c] = col.y;
+    T[6 + c] = col.z;
+  }
+  const int idx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int r = idx[k][0], c = idx[k][1];
+    o.I[k] = fma(X.R.m[r], T[c], fma(X.R.m[3 + r], T[3 + c], X.R.m[6 + r] * T[6 + c]));
+  }
+  return o;
+}
+
+// trace of Ad(Y)^T P Ad(Y) for Y = X^{-1} = (R^T, -R^T p): the link-frame
+// trace the reference's degeneracy test uses (forward_dynamics.cpp:140).
+// Rotations keep traces; the shift by q = -R^T p adds 2 tr(B q^) - q^T D q + |q|^2 tr(D).
+__device__ __forceinline__ double link_frame_trace(const Sym6& P, const SE3d& X) {
+  const Vec3d q = -1.0 * mulT(X.R, X.p);
+  const double trD = P.D[0] + P.D[3] + P.D[5];
+  const double trBq = q.x * (P.B[5] - P.B[7]) + q.y * (P.B[6] - P.B[2]) + q.z * (P.B[1] - P.B[3]);
+  const Vec3d Dq = sym3_mul(P.D, q);
+  return P.A[0] + P.A[3] + P.A[5] + 2.0 * trBq - dot(q, Dq) + dot(q, q) * trD + trD;
+}
+
+// X_{i-1} = rel_i^{-1} * X_i
+__device__ __forceinline__ SE3d step_back(const SE3d& rel, const SE3d& X) {
+  SE3d o;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      o.R.m[3 * r + c] = fma(rel.R.m[r], X.R.m[c], fma(rel.R.m[3 + r], X.R.m[3 + c], rel.R.m[6 + r] * X.R.m[6 + c]));
+  o.p = mulT(rel.R, X.p - rel.p);
+  return o;
+}
+
+// Per-link record between pass B and pass C: base-frame gain g0 = U0/lambda
+// (6), base-frame screw S0 (6), free joint rate u (1).
+constexpr int kRec = 13;
+
+struct AbiaState {
+  SE3d X;       // base -> current link
+  Sv V0, A0;    // base-frame twist / bias acceleration of the current link
+  Sv F0, Z0;    // sums of base-frame wrenches / z-sweep terms (tip side)
+  Sym6 P0;      // projected articulated inertia of the child link
+  Sv a0;        // pass C acceleration
+  int code, eidx;
+};
+
+__device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) st.X.R.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  st.X.p = mk(0, 0, 0);
+  st.V0 = svzero();
+  st.A0 = {mk(0, 0, 0), mk(-g.x, -g.y, -g.z)};  // gravity as base acceleration (inverse_dynamics.cpp:135-140)
+  st.F0 = svzero();
+  st.Z0 = svzero();
+  st.a0 = svzero();
+  st.code = PD_SLOT_OK;
+  st.eidx = 0;
+}
+
+// pass A, link i (base -> tip): X_i = rel_i X_{i-1}, V0 and A0 (qddot = 0)
+//   inverse_dynamics.cpp:43-48 (velocity source), :72-80 (acceleration source)
+// rel = joint_transform(S, HR, hp, q) is history independent; callers may
+// compute it ahead (software pipelining across links).
+__device__ __forceinline__ void abia_pass_a(AbiaState& st, const SE3d& rel, const Sv& S, double qd) {
+  st.X = compose(rel, st.X);
+  const Sv rate0 = qd * adinv_apply(st.X, S);
+  st.V0 = st.V0 + rate0;
+  st.A0 = st.A0 + adv_apply(st.V0, rate0);
+}
+
+// pass B, link i (tip -> base): link wrench and tau_delta, articulated
+// inertia, z sweep and u; writes the 13-double record; steps back to link i-1.
+__device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const SE3d& rel, const Sv& S, double qd,
+                                            const Inertia& Jl, double tau, double rec[kRec]) {
+  const Sv S0 = adinv_apply(st.X, S);
+  const Inertia J0 = inertia_to_base(Jl, st.X);
+  // link wrench, bias torque                      inverse_dynamics.cpp:103-112,146-150
+  const Sv h = inertia_apply(J0, st.V0);
+  st.F0 = st.F0 + inertia_apply(J0, st.A0) + neg_advT_apply(st.V0, h);
+  const double tau_delta = tau - dot(S0, st.F0);
+  // articulated inertia                            forward_dynamics.cpp:136-156
+  Sym6 Ia = inertia_sym6(J0);
+  if (i < n - 1) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      Ia.A[k] += st.P0.A[k];
+      Ia.D[k] += st.P0.D[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Ia.B[k] += st.P0.B[k];
+  }
+  const Sv U = sym6_apply(Ia, S0);
+  const double lambda = dot(S0, U);
+  if (!(lambda > 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
+    st.code = PD_SLOT_DEGENERATE_ARTICULATION;
+    st.eidx = i;
+  }
+  const double inv_l = 1.0 / lambda;
+  const double u = (tau_delta - dot(S0, st.Z0)) * inv_l;  // forward_dynamics.cpp:202-212
+  rec[0] = U.a.x * inv_l;
+  rec[1] = U.a.y * inv_l;
+  rec[2] = U.a.z * inv_l;
+  rec[3] = U.l.x * inv_l;
+  rec[4] = U.l.y * inv_l;
+  rec[5] = U.l.z * inv_l;
+  rec[6] = S0.a.x;
+  rec[7] = S0.a.y;
+  rec[8] = S0.a.z;
+  rec[9] = S0.l.x;
+  rec[10] = S0.l.y;
+  rec[11] = S0.l.z;
+  rec[12] = u;
+  if (i > 0) {
+    st.Z0 = st.Z0 + u * U;  // forward_dynamics.cpp:186-197
+    // projected = I^A - U U^T / lambda             (:150-156)
+    st.P0 = Ia;
+    const double ua[3] = {U.a.x, U.a.y, U.a.z}, ul[3] = {U.l.x, U.l.y, U.l.z};
+    const int sidx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      st.P0.A[k] = fma(-ua[sidx[k][0]] * inv_l, ua[sidx[k][1]], st.P0.A[k]);
+      st.P0.D[k] = fma(-ul[sidx[k][0]] * inv_l, ul[sidx[k][1]], st.P0.D[k]);
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) st.P0.B[3 * r + c] = fma(-ua[r] * inv_l, ul[c], st.P0.B[3 * r + c]);
+    // parent's link states and frame
+    const Sv rate0 = qd * S0;
+    st.A0 = st.A0 - adv_apply(st.V0, rate0);
+    st.V0 = st.V0 - rate0;
+    st.X = step_back(rel, st.X);
+  }
+}
+
+// pass C, link i (base -> tip): qdd_i = u_i - g0_i . a0_{i-1}; a0_i = a0_{i-1} + S0_i qdd_i
+//   forward_dynamics.cpp:199-235
+__device__ __forceinline__ double abia_pass_c(AbiaState& st, const double rec[kRec]) {
+  const Sv g0 = {mk(rec[0], rec[1], rec[2]), mk(rec[3], rec[4], rec[5])};
+  const Sv S0 = {mk(rec[6], rec[7], rec[8]), mk(rec[9], rec[10], rec[11])};
+  const double qdd = rec[12] - dot(g0, st.a0);
+  st.a0 = st.a0 + qdd * S0;
+  return qdd;
+}
+
+}  // namespace pd

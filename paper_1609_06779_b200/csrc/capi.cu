@@ -14,6 +14,8 @@
 
 namespace pd {
 void launch_abia(const ModelView& mv, const BatchIO& io, double* scratch, cudaStream_t s);
+bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, cudaStream_t s);
+int abia_scratch_doubles_per_link();
 void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
@@ -54,6 +56,7 @@ struct pd_ctx {
   // models
   int32_t n_links = 0;
   int64_t n_models = 0;
+  int64_t model_ld = 0;
   DevBuf model, gravity, mstatus, mrule, raw;
   // scratch
   DevBuf abia_scratch, cta_ws, slots, io_q, io_qd, io_tau, io_qdd, io_status;
@@ -76,12 +79,12 @@ pd_status cuda_fail(pd_ctx* c, cudaError_t e, const char* where) {
 
 // raw [M][n][31] -> packed SoA [F_COUNT][n][M]; gravity [M][3] -> [3][M]
 __global__ void pack_models_kernel(const double* __restrict__ raw, const double* __restrict__ graw, int n,
-                                   int64_t M, double* __restrict__ out, double* __restrict__ gout) {
+                                   int64_t M, int64_t ld, double* __restrict__ out, double* __restrict__ gout) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (m >= M) return;
   const double* r = raw + ((int64_t)m * n + i) * PD_LINK_FIELDS;
-  auto put = [&](int f, double v) { out[((int64_t)f * n + i) * M + m] = v; };
+  auto put = [&](int f, double v) { out[((int64_t)f * n + i) * ld + m] = v; };
   put(F_MASS, r[0]);
   for (int k = 0; k < 3; ++k) put(F_COM + k, r[1 + k]);
   // rotational inertia, lower triangle (what LLT / the assembled blocks read)
@@ -98,24 +101,26 @@ __global__ void pack_models_kernel(const double* __restrict__ raw, const double*
     for (int k = 0; k < 3; ++k) gout[(int64_t)k * M + m] = graw[m * 3 + k];
 }
 
-// [rows][cols] -> [cols][rows]
-__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t rows, int64_t cols) {
+// [rows][cols] (row stride ld_in) -> [cols][rows] (row stride ld_out)
+__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t rows, int64_t cols,
+                                 int64_t ld_in, int64_t ld_out) {
   __shared__ double tile[32][33];
   const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t r = r0 + k, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * ld_in + c];
   }
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t c = c0 + k, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+    if (r < rows && c < cols) out[c * ld_out + r] = tile[threadIdx.x][k];
   }
 }
 
-void launch_transpose(pd_ctx* ctx, const double* in, double* out, int64_t rows, int64_t cols) {
+void launch_transpose(pd_ctx* ctx, const double* in, double* out, int64_t rows, int64_t cols, int64_t ld_in,
+                      int64_t ld_out) {
   dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
-  transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, out, rows, cols);
+  transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, out, rows, cols, ld_in, ld_out);
   ctx->launches++;
 }
 
@@ -174,6 +179,7 @@ ModelView model_view(const pd_ctx* c) {
   mv.mrule = c->mrule.as<int32_t>();
   mv.n = c->n_links;
   mv.M = c->n_models;
+  mv.ld = c->model_ld;
   return mv;
 }
 
@@ -183,8 +189,8 @@ int64_t cta_slots(pd_ctx* ctx, size_t ws_bytes, int64_t batch) {
   return std::min<int64_t>(slots, batch);
 }
 
-pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qd, const double* tau,
-                     double* qdd, int32_t* st, int32_t* er, int32_t* ei) {
+pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, const double* q, const double* qd,
+                     const double* tau, double* qdd, int32_t* st, int32_t* er, int32_t* ei) {
   if (ctx->n_models <= 0 || ctx->n_links <= 0) {
     ctx->last_error = "forward dynamics: no models set (pd_set_models)";
     return PD_INVALID_ARGUMENT;
@@ -201,12 +207,14 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, 
     er = st + batch;
     ei = er + batch;
   }
-  BatchIO io{q, qd, tau, qdd, st, er, ei, batch};
+  BatchIO io{q, qd, tau, qdd, st, er, ei, batch, lds};
   const ModelView mv = model_view(ctx);
   switch (algo) {
     case PD_ABIA: {
-      PD_CUDA(ctx->abia_scratch.ensure(sizeof(double) * 7 * (size_t)n * batch));
-      launch_abia(mv, io, ctx->abia_scratch.as<double>(), ctx->stream);
+      const int64_t scr_ld = (batch + 31) / 32 * 32;
+      PD_CUDA(ctx->abia_scratch.ensure(sizeof(double) * abia_scratch_doubles_per_link() * (size_t)n * scr_ld));
+      if (!launch_abia_tma(mv, io, ctx->abia_scratch.as<double>(), scr_ld, ctx->stream))
+        launch_abia(mv, io, ctx->abia_scratch.as<double>(), ctx->stream);
       ctx->launches++;
       break;
     }
@@ -244,9 +252,53 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, 
   return PD_OK;
 }
 
+// 8 independent DFMA chains per thread; nothing but FP64 FMAs in the loop.
+__global__ void fp64_probe_kernel(double* out, int iters, double seed) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-7 + k;
+  const double b = 0.999999999, c = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the chain alive
+}
+
 }  // namespace
 
 extern "C" {
+
+pd_status pd_probe_fp64_peak(pd_ctx* ctx, double* tflops, double* elapsed_ms) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  PD_CUDA(ctx->slots.ensure(64));
+  const int threads = 256, blocks = ctx->sm_count * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  PD_CUDA(cudaEventCreate(&e0));
+  PD_CUDA(cudaEventCreate(&e1));
+  fp64_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(ctx->slots.as<double>(), iters, 1.0);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    PD_CUDA(cudaEventRecord(e0, ctx->stream));
+    fp64_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(ctx->slots.as<double>(), iters, 1.0 + r);
+    PD_CUDA(cudaEventRecord(e1, ctx->stream));
+    PD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  ctx->launches += 6;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = 2.0 * 8.0 * iters * (double)threads * blocks;
+  if (tflops) *tflops = flops / (best * 1e-3) / 1e12;
+  if (elapsed_ms) *elapsed_ms = best;
+  return PD_OK;
+}
 
 int pd_abi_version(void) { return PD_ABI_VERSION; }
 
@@ -350,7 +402,8 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
     for (int k = 0; k < 3; ++k) g[3 * m + k] = gravity ? gravity[3 * m + k] : (k == 2 ? -9.81 : 0.0);
   const size_t raw_bytes = sizeof(double) * PD_LINK_FIELDS * n_links * (size_t)n_models;
   PD_CUDA(ctx->raw.ensure(raw_bytes + sizeof(double) * 3 * n_models));
-  PD_CUDA(ctx->model.ensure(sizeof(double) * F_COUNT * n_links * (size_t)n_models));
+  const int64_t model_ld = (n_models + 31) / 32 * 32;
+  PD_CUDA(ctx->model.ensure(sizeof(double) * F_COUNT * n_links * (size_t)model_ld));
   PD_CUDA(ctx->gravity.ensure(sizeof(double) * 3 * n_models));
   PD_CUDA(ctx->mstatus.ensure(sizeof(int32_t) * n_models));
   PD_CUDA(ctx->mrule.ensure(sizeof(int32_t) * n_models));
@@ -361,13 +414,14 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   PD_CUDA(cudaMemcpyAsync(ctx->mstatus.p, ms.data(), sizeof(int32_t) * n_models, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(ctx->mrule.p, mr.data(), sizeof(int32_t) * n_models, cudaMemcpyHostToDevice, ctx->stream));
   dim3 grid((unsigned)((n_models + 127) / 128), (unsigned)n_links);
-  pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, ctx->model.as<double>(),
-                                                     ctx->gravity.as<double>());
+  pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, model_ld,
+                                                     ctx->model.as<double>(), ctx->gravity.as<double>());
   ctx->launches++;
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->n_links = n_links;
   ctx->n_models = n_models;
+  ctx->model_ld = model_ld;
   return PD_OK;
 }
 
@@ -380,7 +434,8 @@ pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, c
     return PD_INVALID_ARGUMENT;
   }
   PD_CUDA(cudaSetDevice(ctx->device));
-  return run_device(ctx, algo, batch, d_q, d_qdot, d_tau, d_qddot, d_slot_status, d_slot_round, d_slot_index);
+  return run_device(ctx, algo, batch, batch, d_q, d_qdot, d_tau, d_qddot, d_slot_status, d_slot_round,
+                    d_slot_index);
 }
 
 pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
@@ -394,28 +449,29 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   if (batch == 0) return PD_OK;
   PD_CUDA(cudaSetDevice(ctx->device));
   const int n = ctx->n_links;
+  const int64_t lds = (batch + 31) / 32 * 32;  // padded link stride (TMA-friendly)
   const size_t bytes = sizeof(double) * (size_t)n * batch;
-  // staging: [B][n] host rows -> device -> [n][B]
-  PD_CUDA(ctx->io_q.ensure(2 * bytes));
-  PD_CUDA(ctx->io_qd.ensure(2 * bytes));
-  PD_CUDA(ctx->io_tau.ensure(2 * bytes));
-  PD_CUDA(ctx->io_qdd.ensure(2 * bytes));
+  const size_t half = (size_t)n * lds;
+  // staging: [B][n] host rows -> device -> [n][lds]
+  PD_CUDA(ctx->io_q.ensure(2 * sizeof(double) * half));
+  PD_CUDA(ctx->io_qd.ensure(2 * sizeof(double) * half));
+  PD_CUDA(ctx->io_tau.ensure(2 * sizeof(double) * half));
+  PD_CUDA(ctx->io_qdd.ensure(2 * sizeof(double) * half));
   PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
   double* sq = ctx->io_q.as<double>();
   double* sqd = ctx->io_qd.as<double>();
   double* stau = ctx->io_tau.as<double>();
   double* sqdd = ctx->io_qdd.as<double>();
-  const size_t half = (size_t)n * batch;
   PD_CUDA(cudaMemcpyAsync(sq + half, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(sqd + half, qdot, bytes, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(stau + half, tau, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  launch_transpose(ctx, sq + half, sq, batch, n);
-  launch_transpose(ctx, sqd + half, sqd, batch, n);
-  launch_transpose(ctx, stau + half, stau, batch, n);
+  launch_transpose(ctx, sq + half, sq, batch, n, n, lds);
+  launch_transpose(ctx, sqd + half, sqd, batch, n, n, lds);
+  launch_transpose(ctx, stau + half, stau, batch, n, n, lds);
   int32_t* st = ctx->io_status.as<int32_t>();
-  pd_status s = run_device(ctx, algo, batch, sq, sqd, stau, sqdd, st, st + batch, st + 2 * batch);
+  pd_status s = run_device(ctx, algo, batch, lds, sq, sqd, stau, sqdd, st, st + batch, st + 2 * batch);
   if (s != PD_OK) return s;
-  launch_transpose(ctx, sqdd, sqdd + half, n, batch);
+  launch_transpose(ctx, sqdd, sqdd + half, n, batch, lds, n);
   PD_CUDA(cudaMemcpyAsync(qddot, sqdd + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   std::vector<int32_t> hs;
   if (slot_status || slot_round || slot_index) {
@@ -455,16 +511,16 @@ pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const
   PD_CUDA(cudaMemcpyAsync(sq + half, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(sqd + half, qdot, bytes, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(sqdd + half, qddot, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  launch_transpose(ctx, sq + half, sq, batch, n);
-  launch_transpose(ctx, sqd + half, sqd, batch, n);
-  launch_transpose(ctx, sqdd + half, sqdd, batch, n);
+  launch_transpose(ctx, sq + half, sq, batch, n, n, batch);
+  launch_transpose(ctx, sqd + half, sqd, batch, n, n, batch);
+  launch_transpose(ctx, sqdd + half, sqdd, batch, n, n, batch);
   int32_t* st = ctx->io_status.as<int32_t>();
   // BatchIO: tau slot carries qddot in, qdd slot carries torques out
-  BatchIO io{sq, sqd, sqdd, stau, st, st + batch, st + 2 * batch, batch};
+  BatchIO io{sq, sqd, sqdd, stau, st, st + batch, st + 2 * batch, batch, batch};
   launch_invdyn(model_view(ctx), io, ctx->stream);
   ctx->launches++;
   PD_CUDA(cudaGetLastError());
-  launch_transpose(ctx, stau, stau + half, n, batch);
+  launch_transpose(ctx, stau, stau + half, n, batch, batch, n);
   PD_CUDA(cudaMemcpyAsync(tau, stau + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
   return PD_OK;

@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
 #pragma unroll
       for (int r = 0; r < 5; ++r) v = fma(ws[(cfa::XB + r) * n + i], ws[(cfa::OR + r) * n + i + 1], v);
     }
-    io.qdd[(int64_t)i * io.B + p] = v;
+    io.put_qdd(i, p, v);
   }
   if (t == 0) {
     io.status[p] = PD_SLOT_OK;

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) jsiia_cta_kernel(ModelView mv, BatchIO io
     for (int i = t; i < n; i += nt) xv[i] += dv[i];
     __syncthreads();
   }
-  for (int i = t; i < n; i += nt) io.qdd[(int64_t)i * io.B + p] = xv[i];
+  for (int i = t; i < n; i += nt) io.put_qdd(i, p, xv[i]);
   if (t == 0) {
     io.status[p] = code;
     io.eround[p] = 0;

@@ -14,8 +14,9 @@ struct ModelView {
   const int32_t* __restrict__ mrule;    // [M]
   int n;
   int64_t M;
+  int64_t ld;  // stride between links of one field (>= M, even: TMA needs 16-byte strides)
   __device__ __forceinline__ double at(int field, int link, int64_t mc) const {
-    return __ldg(f + ((int64_t)field * n + link) * M + mc);
+    return __ldg(f + ((int64_t)field * n + link) * ld + mc);
   }
   __device__ __forceinline__ int64_t model_of(int64_t p) const { return M == 1 ? 0 : p; }
   __device__ __forceinline__ Vec3d gravity(int64_t mc) const {
@@ -53,7 +54,9 @@ struct BatchIO {
   int32_t* __restrict__ eround;    // [B]
   int32_t* __restrict__ eindex;    // [B]
   int64_t B;
-  __device__ __forceinline__ double ld(const double* a, int i, int64_t p) const { return __ldg(a + (int64_t)i * B + p); }
+  int64_t lds;  // stride between links of the state arrays (>= B)
+  __device__ __forceinline__ double ld(const double* a, int i, int64_t p) const { return __ldg(a + (int64_t)i * lds + p); }
+  __device__ __forceinline__ void put_qdd(int i, int64_t p, double v) const { qdd[(int64_t)i * lds + p] = v; }
 };
 
 // Host-validated model problems short-circuit with the model's rule.

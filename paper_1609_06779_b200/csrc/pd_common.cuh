@@ -249,19 +249,20 @@ __device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Ve
   const double qq = -q;
   const Vec3d w = S.a, v = S.l;
   const double wn2 = dot(w, w);
-  const double wn = sqrt(wn2);
   Mat3d E;
   Vec3d t;
-  if (wn < 1e-12) {
+  if (wn2 < 1e-24) {  // |w| < 1e-12: pure translation
 #pragma unroll
     for (int k = 0; k < 9; ++k) E.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
     t = qq * v;
   } else {
+    const double iwn = rsqrt(wn2);        // 1/|w|
+    const double iwn2 = iwn * iwn;        // 1/|w|^2
     double st, ct;
-    sincos(wn * qq, &st, &ct);
-    const double a = st / wn;
-    const double b = (1.0 - ct) / wn2;
-    const double c = (qq - a) / wn2;
+    sincos(wn2 * iwn * qq, &st, &ct);     // theta = |w| q
+    const double a = st * iwn;
+    const double b = (1.0 - ct) * iwn2;
+    const double c = (qq - a) * iwn2;
     // R = I + a w^ + b w^2 ; w^2 = w w^T - |w|^2 I
     E.m[0] = fma(b, w.x * w.x - wn2, 1.0);
     E.m[4] = fma(b, w.y * w.y - wn2, 1.0);
