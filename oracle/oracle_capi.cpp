@@ -258,15 +258,16 @@ int orc_joint_space_inertia(int n, const double* links, const double* gravity, c
       err, errlen);
 }
 
-int orc_forward_dynamics(int algo, int n, const double* links, const double* gravity, const double* q,
-                         const double* qd, const double* tau, double* qdd, int* trace4, int* err_round,
-                         int* err_index, char* err, int errlen) {
+// nq / nqd / ntau are the vector lengths (check_sizes sees the true lengths).
+int orc_forward_dynamics(int algo, int n, const double* links, const double* gravity, const double* q, int nq,
+                         const double* qd, int nqd, const double* tau, int ntau, double* qdd, int* trace4,
+                         int* err_round, int* err_index, char* err, int errlen) {
   return guarded(
       [&] {
         if (algo < 0 || algo > 2) throw std::invalid_argument("forward_dynamics: unknown algorithm");
         const RobotChain c = chain_from_flat(n, links, gravity);
         ExecTrace tr;
-        const VecX out = forward_dynamics(c, vec(q, n), vec(qd, n), vec(tau, n), static_cast<FdAlgo>(algo),
+        const VecX out = forward_dynamics(c, vec(q, nq), vec(qd, nqd), vec(tau, ntau), static_cast<FdAlgo>(algo),
                                           trace4 ? &tr : nullptr);
         out_vec(out, qdd);
         if (trace4) {

@@ -57,8 +57,8 @@ def lib():
                                       C.c_char_p, C.c_int]
         L.orc_newton_euler.argtypes = [C.c_int, _D, _D, _D, _D, _D, C.c_int, _D, _D, _D, _D, C.c_char_p, C.c_int]
         L.orc_joint_space_inertia.argtypes = [C.c_int, _D, _D, _D, _D, C.c_char_p, C.c_int]
-        L.orc_forward_dynamics.argtypes = [C.c_int, C.c_int, _D, _D, _D, _D, _D, _D, _I, _I, _I,
-                                           C.c_char_p, C.c_int]
+        L.orc_forward_dynamics.argtypes = [C.c_int, C.c_int, _D, _D, _D, C.c_int, _D, C.c_int, _D, C.c_int, _D, _I,
+                                           _I, _I, C.c_char_p, C.c_int]
         L.orc_batch_forward_dynamics.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int64, _D, _D, _D, _D, _D,
                                                  _D, _I, C.c_int]
         L.orc_articulated_body_inertias.argtypes = [C.c_int, _D, _D, _D, _D, _D, C.c_char_p, C.c_int]
@@ -255,16 +255,18 @@ def dense_forward_dynamics(links, gravity, q, qd, tau):
 
 
 def forward_dynamics(algo, links, gravity, q, qd, tau, trace=False):
-    links = _f(links)
+    links = _f(links).reshape(-1, 31)
     n = links.shape[0]
-    qdd = np.zeros(n)
+    q, qd, tau = _f(q), _f(qd), _f(tau)
+    qdd = np.zeros(max(n, 1))
     tr = (C.c_int * 4)()
     r, i = C.c_int(-1), C.c_int(-1)
     e = _err()
     algo = ALGOS.get(algo, algo)
-    _check(lib().orc_forward_dynamics(algo, n, _p(links) if n else None, _p(_f(gravity)), _p(_f(q)),
-                                      _p(_f(qd)), _p(_f(tau)), _p(qdd), tr if trace else None, C.byref(r),
+    _check(lib().orc_forward_dynamics(algo, n, _p(links) if n else None, _p(_f(gravity)), _p(q), len(q), _p(qd),
+                                      len(qd), _p(tau), len(tau), _p(qdd), tr if trace else None, C.byref(r),
                                       C.byref(i), e, 512), e, r, i)
+    qdd = qdd[:n]
     return (qdd, list(tr)) if trace else qdd
 
 
