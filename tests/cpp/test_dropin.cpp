@@ -1,0 +1,166 @@
+// The reference's test_fwddyn.cpp cases, written against the pardyn drop-in
+// C++ API (include/pardyn/pardyn.hpp -> C-ABI -> sm_100a kernels), checked
+// against the CPU oracle (oracle/oracle.hpp, test infrastructure only).
+// Prints one PASS/FAIL line per case; exit status = number of failures.
+#include <pardyn/pardyn.hpp>
+
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../oracle/oracle.hpp"
+
+using pardyn::FdAlgo;
+using pardyn::JointVector;
+
+namespace {
+
+int failures = 0;
+
+void check(bool ok, const std::string& what) {
+  std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+  if (!ok) ++failures;
+}
+
+double rel_gap(const JointVector& a, const std::vector<double>& b) {
+  double num = 0.0, den = 0.0;
+  for (std::size_t i = 0; i < b.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return std::sqrt(num) / std::max(1.0, std::sqrt(den));
+}
+
+oracle::RobotChain to_oracle(const pardyn::RobotChain& c) {
+  oracle::RobotChain o;
+  o.gravity = oracle::v3(c.gravity[0], c.gravity[1], c.gravity[2]);
+  for (const auto& l : c.links) {
+    double f[31];
+    f[0] = l.mass;
+    for (int k = 0; k < 3; ++k) f[1 + k] = l.com[k];
+    for (int k = 0; k < 9; ++k) f[4 + k] = l.inertia_rot[k];
+    for (int k = 0; k < 6; ++k) f[13 + k] = l.joint_screw[k];
+    for (int k = 0; k < 9; ++k) f[19 + k] = l.home_rotation[k];
+    for (int k = 0; k < 3; ++k) f[28 + k] = l.home_translation[k];
+    o.links.push_back(oracle::link_from_flat(f));
+  }
+  return o;
+}
+
+JointVector uniform(std::mt19937_64& e, int n, double lo, double hi) {
+  JointVector v(n);
+  for (int i = 0; i < n; ++i) v[i] = lo + (hi - lo) * (static_cast<double>(e() >> 11) * 0x1.0p-53);
+  return v;
+}
+
+std::vector<double> as_vec(const JointVector& v) { return std::vector<double>(v.data(), v.data() + v.size()); }
+
+}  // namespace
+
+int main() {
+  // all three algorithms vs the same algorithm's oracle (north star: 1e-9)
+  for (int n : {1, 2, 5, 10, 30}) {
+    for (std::uint64_t trial = 0; trial < 3; ++trial) {
+      const pardyn::RobotChain chain = pardyn::random_chain(n, 400 + 10 * n + trial);
+      std::mt19937_64 e((400 + 10 * n + trial) ^ 0xF00D);
+      const JointVector q = uniform(e, n, -3, 3), qd = uniform(e, n, -2, 2), tau = uniform(e, n, -10, 10);
+      const oracle::RobotChain oc = to_oracle(chain);
+      for (FdAlgo a : {FdAlgo::jsiia, FdAlgo::abia, FdAlgo::cfa}) {
+        const JointVector got = pardyn::forward_dynamics(chain, q, qd, tau, a);
+        const auto want = oracle::forward_dynamics(oc, as_vec(q), as_vec(qd), as_vec(tau),
+                                                   static_cast<oracle::FdAlgo>(static_cast<int>(a)));
+        check(rel_gap(got, want) < 1e-9, "algo " + std::to_string(static_cast<int>(a)) + " n=" + std::to_string(n) +
+                                             " trial " + std::to_string(trial) + " vs oracle");
+      }
+    }
+  }
+
+  // closed-form pendulum (test_fwddyn.cpp:105-122)
+  {
+    pardyn::RobotChain c;
+    c.gravity = {0.0, -9.81, 0.0};
+    pardyn::LinkSpec l;
+    l.mass = 1.3;
+    l.com = {0.45, 0, 0};
+    l.inertia_rot = {0.11, 0, 0, 0, 0.13, 0, 0, 0, 0.07};
+    c.links.push_back(l);
+    std::mt19937_64 e(111);
+    bool ok = true;
+    for (int t = 0; t < 20; ++t) {
+      const JointVector q = uniform(e, 1, -6, 6), qd = uniform(e, 1, -4, 4), tau = uniform(e, 1, -8, 8);
+      const double want = (tau[0] - 1.3 * 9.81 * 0.45 * std::cos(q[0])) / (0.07 + 1.3 * 0.45 * 0.45);
+      for (FdAlgo a : {FdAlgo::jsiia, FdAlgo::abia, FdAlgo::cfa}) {
+        const double got = pardyn::forward_dynamics(c, q, qd, tau, a)[0];
+        ok = ok && std::abs(got - want) < 1e-8 * std::max(1.0, std::abs(want));
+      }
+    }
+    check(ok, "closed-form pendulum, every algorithm");
+  }
+
+  // dispatcher reaches the algorithm it names (test_fwddyn.cpp:285-296)
+  {
+    const pardyn::RobotChain chain = pardyn::random_chain(4, 9100);
+    const JointVector q{0.1, -0.2, 0.3, 0.4}, qd{0.5, 0.1, -0.3, 0.2}, tau{1, -1, 2, 0.5};
+    check(pardyn::forward_dynamics(chain, q, qd, tau, FdAlgo::cfa) ==
+              pardyn::cfa_forward_dynamics(chain, q, qd, tau),
+          "dispatcher == cfa_forward_dynamics");
+  }
+
+  // batch: slot identity, per-slot errors, empty batch (test_fwddyn.cpp:298-341)
+  {
+    std::vector<pardyn::FdProblem> probs;
+    for (int n = 1; n <= 8; ++n) {
+      std::mt19937_64 e(600 + n);
+      probs.push_back({pardyn::random_chain(n, 600 + n), uniform(e, n, -3, 3), uniform(e, n, -2, 2),
+                       uniform(e, n, -10, 10)});
+    }
+    probs[2].tau = JointVector::Zero(1);
+    const auto res = pardyn::batch_forward_dynamics(probs, FdAlgo::abia);
+    bool ok = !res[2].ok() && res[2].error.find("forward dynamics") != std::string::npos;
+    for (std::size_t i = 0; i < probs.size(); ++i) {
+      if (i == 2) continue;
+      const auto& p = probs[i];
+      ok = ok && res[i].ok() && res[i].qddot == pardyn::forward_dynamics(p.chain, p.q, p.qdot, p.tau, FdAlgo::abia);
+    }
+    check(ok, "batch slot identity and error isolation");
+    check(pardyn::batch_forward_dynamics({}, FdAlgo::cfa).empty(), "empty batch");
+  }
+
+  // validation and error classes (test_fwddyn.cpp:343-361, spatial.cpp:72-87)
+  {
+    const pardyn::RobotChain chain = pardyn::random_chain(3, 77);
+    const JointVector good = JointVector::Zero(3), bad = JointVector::Zero(2);
+    bool threw = false;
+    try {
+      pardyn::forward_dynamics(chain, bad, good, good, FdAlgo::jsiia);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    check(threw, "size mismatch -> std::invalid_argument");
+    pardyn::RobotChain neg = chain;
+    neg.links[1].mass = -2.0;
+    std::string msg;
+    try {
+      pardyn::forward_dynamics(neg, good, good, good, FdAlgo::abia);
+    } catch (const std::invalid_argument& e) {
+      msg = e.what();
+    }
+    check(msg == "spatial inertia: mass must be positive", "negative mass -> spatial inertia message");
+  }
+
+  // inverse dynamics and bias torque vs the oracle
+  {
+    const pardyn::RobotChain chain = pardyn::random_chain(9, 2222);
+    std::mt19937_64 e(2222);
+    const JointVector q = uniform(e, 9, -3, 3), qd = uniform(e, 9, -2, 2), qdd = uniform(e, 9, -5, 5);
+    const auto want = oracle::inverse_dynamics(to_oracle(chain), as_vec(q), as_vec(qd), as_vec(qdd));
+    check(rel_gap(pardyn::inverse_dynamics(chain, q, qd, qdd), want) < 1e-12, "inverse dynamics vs oracle");
+    check(pardyn::bias_torque(chain, q, qd) == pardyn::inverse_dynamics(chain, q, qd, JointVector::Zero(9)),
+          "bias torque = ID(qdd = 0)");
+  }
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}
