@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(128) abia_lane_kernel(ModelView mv, BatchIO io
   io.eindex[p] = st.eidx;
 }
 
-int abia_scratch_doubles_per_link() { return kRec; }
+int abia_scratch_doubles_per_link() { return kRec + 2; }  // records + (sin, cos)
 
 void launch_abia(const ModelView& mv, const BatchIO& io, double* scratch, cudaStream_t s) {
   const int threads = 128;

@@ -86,9 +86,9 @@ __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
 // compute it ahead (software pipelining across links).
 __device__ __forceinline__ void abia_pass_a(AbiaState& st, const SE3d& rel, const Sv& S, double qd) {
   st.X = compose(rel, st.X);
-  const Sv rate0 = qd * adinv_apply(st.X, S);
-  st.V0 = st.V0 + rate0;
-  st.A0 = st.A0 + adv_apply(st.V0, rate0);
+  const Sv S0 = adinv_apply(st.X, S);
+  st.V0 = svfma(qd, S0, st.V0);
+  st.A0 = adv_acc(st.V0, qd * S0, st.A0);
 }
 
 // pass B, link i (tip -> base): link wrench and tau_delta, articulated
@@ -99,7 +99,7 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   const Inertia J0 = inertia_to_base(Jl, st.X);
   // link wrench, bias torque                      inverse_dynamics.cpp:103-112,146-150
   const Sv h = inertia_apply(J0, st.V0);
-  st.F0 = st.F0 + inertia_apply(J0, st.A0) + neg_advT_apply(st.V0, h);
+  st.F0 = neg_advT_acc(st.V0, h, inertia_apply_acc(J0, st.A0, st.F0));
   const double tau_delta = tau - dot(S0, st.F0);
   // articulated inertia                            forward_dynamics.cpp:136-156
   Sym6 Ia = inertia_sym6(J0);
@@ -120,12 +120,13 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   }
   const double inv_l = 1.0 / lambda;
   const double u = (tau_delta - dot(S0, st.Z0)) * inv_l;  // forward_dynamics.cpp:202-212
-  rec[0] = U.a.x * inv_l;
-  rec[1] = U.a.y * inv_l;
-  rec[2] = U.a.z * inv_l;
-  rec[3] = U.l.x * inv_l;
-  rec[4] = U.l.y * inv_l;
-  rec[5] = U.l.z * inv_l;
+  const Sv g0 = inv_l * U;                                 // gain (base frame)
+  rec[0] = g0.a.x;
+  rec[1] = g0.a.y;
+  rec[2] = g0.a.z;
+  rec[3] = g0.l.x;
+  rec[4] = g0.l.y;
+  rec[5] = g0.l.z;
   rec[6] = S0.a.x;
   rec[7] = S0.a.y;
   rec[8] = S0.a.z;
@@ -134,24 +135,25 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   rec[11] = S0.l.z;
   rec[12] = u;
   if (i > 0) {
-    st.Z0 = st.Z0 + u * U;  // forward_dynamics.cpp:186-197
-    // projected = I^A - U U^T / lambda             (:150-156)
+    st.Z0 = svfma(u, U, st.Z0);  // forward_dynamics.cpp:186-197
+    // projected = I^A - U U^T / lambda = I^A - U g0^T   (:150-156)
     st.P0 = Ia;
     const double ua[3] = {U.a.x, U.a.y, U.a.z}, ul[3] = {U.l.x, U.l.y, U.l.z};
+    const double ga[3] = {g0.a.x, g0.a.y, g0.a.z}, gl[3] = {g0.l.x, g0.l.y, g0.l.z};
     const int sidx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-      st.P0.A[k] = fma(-ua[sidx[k][0]] * inv_l, ua[sidx[k][1]], st.P0.A[k]);
-      st.P0.D[k] = fma(-ul[sidx[k][0]] * inv_l, ul[sidx[k][1]], st.P0.D[k]);
+      st.P0.A[k] = fma(-ua[sidx[k][0]], ga[sidx[k][1]], st.P0.A[k]);
+      st.P0.D[k] = fma(-ul[sidx[k][0]], gl[sidx[k][1]], st.P0.D[k]);
     }
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) st.P0.B[3 * r + c] = fma(-ua[r] * inv_l, ul[c], st.P0.B[3 * r + c]);
+      for (int c = 0; c < 3; ++c) st.P0.B[3 * r + c] = fma(-ua[r], gl[c], st.P0.B[3 * r + c]);
     // parent's link states and frame
     const Sv rate0 = qd * S0;
-    st.A0 = st.A0 - adv_apply(st.V0, rate0);
-    st.V0 = st.V0 - rate0;
+    st.A0 = adv_acc(st.V0, -1.0 * rate0, st.A0);
+    st.V0 = svfma(-qd, S0, st.V0);
     st.X = step_back(rel, st.X);
   }
 }
@@ -162,7 +164,7 @@ __device__ __forceinline__ double abia_pass_c(AbiaState& st, const double rec[kR
   const Sv g0 = {mk(rec[0], rec[1], rec[2]), mk(rec[3], rec[4], rec[5])};
   const Sv S0 = {mk(rec[6], rec[7], rec[8]), mk(rec[9], rec[10], rec[11])};
   const double qdd = rec[12] - dot(g0, st.a0);
-  st.a0 = st.a0 + qdd * S0;
+  st.a0 = svfma(qdd, S0, st.a0);
   return qdd;
 }
 

@@ -14,6 +14,8 @@
 //   pass C loads the 13-double records pass B wrote (after a proxy fence)
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "abia_common.cuh"
 
 namespace pd {
@@ -21,9 +23,9 @@ namespace pd {
 namespace {
 
 constexpr int kT = 128;          // chains per CTA
-constexpr int kStages = 3;       // ring depth
-constexpr int kStageFields = 32; // 28 model + q, qd, tau (+1 pad); pass C uses 13
-constexpr int kQ = 28, kQD = 29, kTAU = 30;
+constexpr int kStageFields = 33; // 28 model + q, qd, tau, sin, cos; pass C uses 13
+constexpr int kQ = 28, kQD = 29, kTAU = 30, kSIN = 31, kCOS = 32;
+constexpr int kSC0 = kRec;       // scratch rows n*kRec + 2*i + {0,1}: (sin, cos) of link i's joint angle
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -60,11 +62,45 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       : "memory");
 }
 
+__device__ __forceinline__ void tma_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(saddr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double* addr, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(addr), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void discard_l2(const void* addr) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(addr) : "memory");
+}
+
 struct Maps {
   CUtensorMap model_all;  // box {T, 1, 28}
   CUtensorMap model_kin;  // box {T, 1, 18} from field 10
   CUtensorMap q, qd, tau; // box {T, 1}
   CUtensorMap scr;        // box {T, 13}
+  CUtensorMap sc;         // box {T, 2}: (sin, cos) rows written by pass A
 };
 
 }  // namespace
@@ -73,97 +109,186 @@ __device__ __forceinline__ Sv stage_screw(const double* f) {
   return {mk(f[F_SCREW * kT], f[(F_SCREW + 1) * kT], f[(F_SCREW + 2) * kT]),
           mk(f[(F_SCREW + 3) * kT], f[(F_SCREW + 4) * kT], f[(F_SCREW + 5) * kT])};
 }
-__device__ __forceinline__ SE3d stage_rel(const double* f) {
+__device__ __forceinline__ SE3d stage_rel(const double* f, double st, double ct) {
   Mat3d HR;
 #pragma unroll
   for (int j = 0; j < 9; ++j) HR.m[j] = f[(F_HR + j) * kT];
-  return joint_transform(stage_screw(f), HR, mk(f[F_HP * kT], f[(F_HP + 1) * kT], f[(F_HP + 2) * kT]), f[kQ * kT]);
+  return joint_transform_sc(stage_screw(f), HR, mk(f[F_HP * kT], f[(F_HP + 1) * kT], f[(F_HP + 2) * kT]), f[kQ * kT],
+                            st, ct);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
 }
 
-__global__ void __launch_bounds__(kT, 2)
+// KSTAGES-deep ring; MINB CTAs per SM; HINTS = L2 policy (records evict_last
+// + discard after use, last-use streams evict_first).
+//
+// Synchronisation: full[s] (TMA transaction count) tells consumers a stage
+// landed; empty[s] (one arrival per warp) tells the producer (thread 0) that
+// every warp is done with it. There is no CTA-wide barrier per link: warps
+// drift freely within the ring and only the producer waits for the slowest.
+// Pass A stores sin/cos of each joint angle for pass B (one sincos per link);
+// the last KSTAGES links of pass A, whose pass-B loads are issued before pass A
+// reaches them, keep theirs in registers.
+template <int KSTAGES, int MINB, bool HINTS>
+__global__ void __launch_bounds__(kT, MINB)
     abia_tma_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
                     int64_t scr_ld) {
-  extern __shared__ __align__(128) double ring[];  // [kStages][kStageFields][kT]
-  __shared__ __align__(8) uint64_t full[kStages];
-  const int t = threadIdx.x;
+  static_assert(KSTAGES == 3, "the register hand-off of the last pass-A links assumes 3 stages");
+  extern __shared__ __align__(128) double ring[];  // [KSTAGES][kStageFields][kT]
+  __shared__ __align__(8) uint64_t full[KSTAGES];
+  __shared__ __align__(8) uint64_t empty[KSTAGES];
+  const int t = threadIdx.x, lane = t & 31;
   const int n = mv.n;
   const int c0 = blockIdx.x * kT;
   const int64_t p = (int64_t)c0 + t;
   const bool live = p < io.B;
   const int total = 3 * n;
   if (t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < KSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  uint64_t pol_first = 0, pol_last = 0;
+  if (HINTS) {
+    pol_first = policy_evict_first();
+    pol_last = policy_evict_last();
+  }
 
   // step k: pass A link k (k < n), pass B link 2n-1-k, pass C link k-2n
   auto issue = [&](int k) {
-    const int s = k % kStages;
+    const int s = k % KSTAGES;
     double* dst = ring + (size_t)s * kStageFields * kT;
     uint64_t* bar = &full[s];
-    if (k < n) {
+    if (k < n) {  // re-read in pass B: default policy
       mbar_expect_tx(bar, (18 + 2) * kT * 8);
       tma_3d(dst + 10 * kT, &maps.model_kin, c0, k, 10, bar);
       tma_2d(dst + kQ * kT, &maps.q, c0, k, bar);
       tma_2d(dst + kQD * kT, &maps.qd, c0, k, bar);
-    } else if (k < 2 * n) {
+    } else if (k < 2 * n) {  // last use of the model
       const int i = 2 * n - 1 - k;
-      mbar_expect_tx(bar, (28 + 3) * kT * 8);
-      tma_3d(dst, &maps.model_all, c0, i, 0, bar);
+      mbar_expect_tx(bar, (28 + 5) * kT * 8);
+      if (HINTS) {
+        tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
+        tma_2d_hint(dst + kTAU * kT, &maps.tau, c0, i, bar, pol_first);
+        tma_2d_hint(dst + kSIN * kT, &maps.sc, c0, 2 * i, bar, pol_first);
+      } else {
+        tma_3d(dst, &maps.model_all, c0, i, 0, bar);
+        tma_2d(dst + kTAU * kT, &maps.tau, c0, i, bar);
+        tma_2d(dst + kSIN * kT, &maps.sc, c0, 2 * i, bar);
+      }
       tma_2d(dst + kQ * kT, &maps.q, c0, i, bar);
       tma_2d(dst + kQD * kT, &maps.qd, c0, i, bar);
-      tma_2d(dst + kTAU * kT, &maps.tau, c0, i, bar);
     } else {
       const int i = k - 2 * n;
       mbar_expect_tx(bar, kRec * kT * 8);
-      tma_2d(dst, &maps.scr, c0, i * kRec, bar);
+      if (HINTS)
+        tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
+      else
+        tma_2d(dst, &maps.scr, c0, i * kRec, bar);
     }
   };
-  // Producer = thread 0. Steps [0, kStages) are issued up front; at the end
-  // of step k (after the CTA barrier freed stage k % kStages) it issues step
-  // k + kStages into that stage, so each link's data is requested kStages
-  // steps before it is used. Pass-C steps read the records pass B wrote and
-  // are only issued once the barrier after the last pass-B step has passed.
+  // Producer = thread 0: steps [0, KSTAGES) up front; at the end of step k it
+  // waits until every warp released step k's stage, then issues step
+  // k + KSTAGES into it. Pass-C steps read pass B's records, so they are
+  // issued only once every warp released the last pass-B step (2n - 1).
   int next = 0;
-  auto produce_until = [&](int target) {
-    for (; next < target; ++next) issue(next);
+  if (t == 0)
+    for (; next < min(KSTAGES, min(total, 2 * n)); ++next) issue(next);
+  auto after_step = [&](int k) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[k % KSTAGES]);
+    if (t == 0) {
+      const int target = k < 2 * n - 1 ? min(2 * n, k + 1 + KSTAGES) : min(total, k + 1 + KSTAGES);
+      for (; next < target; ++next) {
+        const int prev = next - KSTAGES;  // previous user of the stage
+        if (prev >= 0) mbar_wait(&empty[prev % KSTAGES], (uint32_t)((prev / KSTAGES) & 1));
+        if (next == 2 * n && prev != 2 * n - 1)
+          mbar_wait(&empty[(2 * n - 1) % KSTAGES], (uint32_t)(((2 * n - 1) / KSTAGES) & 1));
+        issue(next);
+      }
+    }
   };
-  if (t == 0) produce_until(min(kStages, min(total, 2 * n)));
 
   const int64_t mc = live ? mv.model_of(p) : 0;
   AbiaState st;
   abia_init(st, live ? mv.gravity(mc) : mk(0, 0, 0));
-  for (int k = 0; k < total; ++k) {
-    const int s = k % kStages;
-    mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+  double s0 = 0, c0r = 1, s1 = 0, c1r = 1, s2 = 0, c2r = 1;  // (sin, cos) of links n-1, n-2, n-3
+  int k = 0;
+  for (; k < n; ++k) {  // pass A
+    const int s = k % KSTAGES;
+    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
     const double* f = ring + (size_t)s * kStageFields * kT + t;
-    if (k < n) {
-      abia_pass_a(st, stage_rel(f), stage_screw(f), f[kQD * kT]);
-    } else if (k < 2 * n) {
-      const int i = 2 * n - 1 - k;
-      Inertia J;
-      J.m = f[F_MASS * kT];
-      J.c = mk(f[F_COM * kT], f[(F_COM + 1) * kT], f[(F_COM + 2) * kT]);
-#pragma unroll
-      for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * kT];
-      double rec[kRec];
-      abia_pass_b(st, i, n, stage_rel(f), stage_screw(f), f[kQD * kT], J, f[kTAU * kT], rec);
+    const Sv S = stage_screw(f);
+    double sn, cs;
+    joint_angle_sincos(S, f[kQ * kT], &sn, &cs);
+    abia_pass_a(st, stage_rel(f, sn, cs), S, f[kQD * kT]);
+    if (k < n - KSTAGES) {
       if (live) {
-#pragma unroll
-        for (int j = 0; j < kRec; ++j) scratch[((int64_t)i * kRec + j) * scr_ld + p] = rec[j];
+        double* a = scratch + ((int64_t)n * kSC0 + 2 * k) * scr_ld + p;
+        if (HINTS) {
+          st_hint(a, sn, pol_last);
+          st_hint(a + scr_ld, cs, pol_last);
+        } else {
+          a[0] = sn;
+          a[scr_ld] = cs;
+        }
       }
-      if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
     } else {
-      const int i = k - 2 * n;
-      double rec[kRec];
-#pragma unroll
-      for (int j = 0; j < kRec; ++j) rec[j] = f[j * kT];
-      const double qdd = abia_pass_c(st, rec);
-      if (live) io.put_qdd(i, p, qdd);
+      s2 = s1; c2r = c1r; s1 = s0; c1r = c0r; s0 = sn; c0r = cs;
     }
-    __syncthreads();  // stage s consumed; at k = 2n-1 also: every record written
-    if (t == 0) produce_until(k < 2 * n - 1 ? min(2 * n, k + 1 + kStages) : min(total, k + 1 + kStages));
+    if (k == n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // sin/cos rows -> TMA reads
+    after_step(k);
+  }
+  for (; k < 2 * n; ++k) {  // pass B
+    const int s = k % KSTAGES;
+    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
+    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const int i = 2 * n - 1 - k;
+    double sn = f[kSIN * kT], cs = f[kCOS * kT];
+    if (i == n - 1) { sn = s0; cs = c0r; }
+    if (i == n - 2) { sn = s1; cs = c1r; }
+    if (i == n - 3) { sn = s2; cs = c2r; }
+    Inertia J;
+    J.m = f[F_MASS * kT];
+    J.c = mk(f[F_COM * kT], f[(F_COM + 1) * kT], f[(F_COM + 2) * kT]);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * kT];
+    double rec[kRec];
+    abia_pass_b(st, i, n, stage_rel(f, sn, cs), stage_screw(f), f[kQD * kT], J, f[kTAU * kT], rec);
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < kRec; ++j) {
+        double* a = scratch + ((int64_t)i * kRec + j) * scr_ld + p;
+        if (HINTS)
+          st_hint(a, rec[j], pol_last);
+        else
+          *a = rec[j];
+      }
+    }
+    if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
+    after_step(k);
+  }
+  for (; k < total; ++k) {  // pass C
+    const int s = k % KSTAGES;
+    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
+    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const int i = k - 2 * n;
+    double rec[kRec];
+#pragma unroll
+    for (int j = 0; j < kRec; ++j) rec[j] = f[j * kT];
+    const double qdd = abia_pass_c(st, rec);
+    if (live) io.put_qdd(i, p, qdd);
+    if (HINTS && t < kRec * (kT * 8 / 128)) {
+      // the records of link i are dead: drop their L2 lines without write-back
+      const int row = t / (kT * 8 / 128), seg = t % (kT * 8 / 128);
+      const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
+      if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
+    }
+    after_step(k);
   }
   if (live) {
     const int32_t ms = __ldg(mv.mstatus + mc);
@@ -206,6 +331,17 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Kernel variant (tuning experiments): PD_ABIA_VARIANT selects
+// 0 = L2 policy hints (default), 2 = no hints.
+int abia_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PD_ABIA_VARIANT");
+    v = e ? std::atoi(e) : 0;
+  }
+  return v;
+}
+
 }  // namespace
 
 // Returns false (caller falls back to the plain kernel) when the batch does
@@ -239,15 +375,20 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
     const cuuint64_t str[1] = {(cuuint64_t)scr_ld * 8};
     const cuuint32_t box[2] = {kT, kRec};
     if (!encode(&maps.scr, scratch, 2, dims, str, box)) return false;
-  }
-  const size_t smem = (size_t)kStages * kStageFields * kT * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(abia_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    const cuuint64_t dims_sc[2] = {(cuuint64_t)io.B, (cuuint64_t)n * 2};
+    const cuuint32_t box_sc[2] = {kT, 2};
+    if (!encode(&maps.sc, scratch + (size_t)n * kSC0 * scr_ld, 2, dims_sc, str, box_sc)) return false;
   }
   const unsigned blocks = (unsigned)((io.B + kT - 1) / kT);
-  abia_tma_kernel<<<blocks, kT, smem, s>>>(maps, mv, io, scratch, scr_ld);
+  auto go = [&](auto kernel, int stages) {
+    const size_t smem = (size_t)stages * kStageFields * kT * sizeof(double);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel<<<blocks, kT, smem, s>>>(maps, mv, io, scratch, scr_ld);
+  };
+  switch (abia_variant()) {
+    case 2: go(abia_tma_kernel<3, 2, false>, 3); break;
+    default: go(abia_tma_kernel<3, 2, true>, 3); break;  // measured best (profiles/README.md)
+  }
   return true;
 }
 

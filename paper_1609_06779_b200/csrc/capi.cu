@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -20,6 +21,7 @@ void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
 void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+bool launch_jsiia_warp(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
 size_t jsiia_workspace_bytes(int n);
 }  // namespace pd
 
@@ -58,6 +60,8 @@ struct pd_ctx {
   int64_t n_models = 0;
   int64_t model_ld = 0;
   DevBuf model, gravity, mstatus, mrule, raw;
+  DevBuf model_cl;        // link-fastest copy [chain][field][link] for warp-per-chain kernels
+  bool model_cl_valid = false;
   // scratch
   DevBuf abia_scratch, cta_ws, slots, io_q, io_qd, io_tau, io_qdd, io_status;
   int64_t launches = 0;
@@ -99,6 +103,18 @@ __global__ void pack_models_kernel(const double* __restrict__ raw, const double*
   for (int k = 0; k < 3; ++k) put(F_HP + k, r[28 + k]);
   if (i == 0)
     for (int k = 0; k < 3; ++k) gout[(int64_t)k * M + m] = graw[m * 3 + k];
+}
+
+// [field][link][chain] (stride ld) -> [chain][field][link]
+__global__ void repack_link_fastest_kernel(const double* __restrict__ in, int n, int64_t M, int64_t ld,
+                                           double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)M * F_COUNT * n;
+  if (idx >= total) return;
+  const int i = (int)(idx % n);
+  const int f = (int)((idx / n) % F_COUNT);
+  const int64_t m = idx / ((int64_t)n * F_COUNT);
+  out[idx] = in[((int64_t)f * n + i) * ld + m];
 }
 
 // [rows][cols] (row stride ld_in) -> [cols][rows] (row stride ld_out)
@@ -232,6 +248,20 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       break;
     }
     case PD_JSIIA: {
+      static const bool force_cta = std::getenv("PD_JSIIA_CTA") != nullptr;
+      if (n <= 32 && !force_cta) {
+        if (!ctx->model_cl_valid) {
+          const int64_t total = ctx->n_models * F_COUNT * (int64_t)n;
+          PD_CUDA(ctx->model_cl.ensure(sizeof(double) * total));
+          repack_link_fastest_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+              ctx->model.as<double>(), n, ctx->n_models, ctx->model_ld, ctx->model_cl.as<double>());
+          ctx->launches++;
+          ctx->model_cl_valid = true;
+        }
+        launch_jsiia_warp(mv, ctx->model_cl.as<double>(), io, ctx->stream);
+        ctx->launches++;
+        break;
+      }
       const size_t wsb = jsiia_workspace_bytes(n);
       int64_t slots = 0;
       if (wsb > 220 * 1024) {
@@ -367,10 +397,11 @@ int64_t pd_kernel_launches(const pd_ctx* ctx) { return ctx ? ctx->launches : 0; 
 const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) {
   (void)ctx;
   switch (algo) {
-    case PD_ABIA: return "abia_lane_kernel (lane per chain, 3 fused passes)";
+    case PD_ABIA: return "abia_tma_kernel (lane per chain, 3 fused base-frame passes, TMA ring)";
     case PD_CFA: return cfa_workspace_bytes(n_links) <= 220 * 1024 ? "cfa_cta_kernel<smem> (CTA per chain, OEE in smem)"
                                                                     : "cfa_cta_kernel<global> (CTA per chain, L2 workspace)";
-    case PD_JSIIA: return jsiia_workspace_bytes(n_links) <= 220 * 1024
+    case PD_JSIIA: return n_links <= 32 ? "jsiia_warp_kernel (warp per chain, register-resident M rows + row Cholesky)"
+                          : jsiia_workspace_bytes(n_links) <= 220 * 1024
                               ? "jsiia_cta_kernel<smem> (CTA per chain, CRBA scans + CTA Cholesky)"
                               : "jsiia_cta_kernel<global> (CTA per chain, L2 workspace)";
   }
@@ -422,6 +453,7 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   ctx->n_links = n_links;
   ctx->n_models = n_models;
   ctx->model_ld = model_ld;
+  ctx->model_cl_valid = false;
   return PD_OK;
 }
 

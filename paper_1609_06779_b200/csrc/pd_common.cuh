@@ -43,6 +43,12 @@ __device__ __forceinline__ Vec3d fmav(double s, Vec3d a, Vec3d b) {  // s*a + b
   return {fma(s, a.x, b.x), fma(s, a.y, b.y), fma(s, a.z, b.z)};
 }
 
+// acc + a x b, fused (2 FMA per component, no separate multiply / add)
+__device__ __forceinline__ Vec3d cross_acc(Vec3d a, Vec3d b, Vec3d acc) {
+  return {fma(a.y, b.z, fma(-a.z, b.y, acc.x)), fma(a.z, b.x, fma(-a.x, b.z, acc.y)),
+          fma(a.x, b.y, fma(-a.y, b.x, acc.z))};
+}
+
 // 3x3 row-major rotation.
 struct Mat3d {
   double m[9];
@@ -54,6 +60,11 @@ __device__ __forceinline__ Vec3d mul(const Mat3d& R, Vec3d v) {
 __device__ __forceinline__ Vec3d mulT(const Mat3d& R, Vec3d v) {
   return {fma(R.m[0], v.x, fma(R.m[3], v.y, R.m[6] * v.z)), fma(R.m[1], v.x, fma(R.m[4], v.y, R.m[7] * v.z)),
           fma(R.m[2], v.x, fma(R.m[5], v.y, R.m[8] * v.z))};
+}
+__device__ __forceinline__ Vec3d mul_acc(const Mat3d& R, Vec3d v, Vec3d acc) {
+  return {fma(R.m[0], v.x, fma(R.m[1], v.y, fma(R.m[2], v.z, acc.x))),
+          fma(R.m[3], v.x, fma(R.m[4], v.y, fma(R.m[5], v.z, acc.y))),
+          fma(R.m[6], v.x, fma(R.m[7], v.y, fma(R.m[8], v.z, acc.z)))};
 }
 __device__ __forceinline__ Mat3d matmul(const Mat3d& A, const Mat3d& B) {
   Mat3d C;
@@ -102,6 +113,14 @@ __device__ __forceinline__ Sv adinvT_apply(const SE3d& T, const Sv& f) {
 __device__ __forceinline__ Sv adv_apply(const Sv& V, const Sv& x) {
   return {cross(V.a, x.a), cross(V.l, x.a) + cross(V.a, x.l)};
 }
+// acc + ad_V x
+__device__ __forceinline__ Sv adv_acc(const Sv& V, const Sv& x, const Sv& acc) {
+  return {cross_acc(V.a, x.a, acc.a), cross_acc(V.a, x.l, cross_acc(V.l, x.a, acc.l))};
+}
+// acc + s x
+__device__ __forceinline__ Sv svfma(double s, const Sv& x, const Sv& acc) {
+  return {fmav(s, x.a, acc.a), fmav(s, x.l, acc.l)};
+}
 // -ad_V^T h = (w x ha + v x hl, w x hl)
 __device__ __forceinline__ Sv neg_advT_apply(const Sv& V, const Sv& h) {
   return {cross(V.a, h.a) + cross(V.l, h.l), cross(V.a, h.l)};
@@ -121,10 +140,23 @@ __device__ __forceinline__ Vec3d sym3_mul(const double* I, Vec3d w) {
   return {fma(I[0], w.x, fma(I[1], w.y, I[2] * w.z)), fma(I[1], w.x, fma(I[3], w.y, I[4] * w.z)),
           fma(I[2], w.x, fma(I[4], w.y, I[5] * w.z))};
 }
+__device__ __forceinline__ Vec3d sym3_mul_acc(const double* I, Vec3d w, Vec3d acc) {
+  return {fma(I[0], w.x, fma(I[1], w.y, fma(I[2], w.z, acc.x))), fma(I[1], w.x, fma(I[3], w.y, fma(I[4], w.z, acc.y))),
+          fma(I[2], w.x, fma(I[4], w.y, fma(I[5], w.z, acc.z)))};
+}
 // J (w, v): lin = m (v - c x w); ang = Ic w + c x lin
 __device__ __forceinline__ Sv inertia_apply(const Inertia& J, const Sv& x) {
   const Vec3d lin = J.m * (x.l - cross(J.c, x.a));
   return {sym3_mul(J.I, x.a) + cross(J.c, lin), lin};
+}
+// acc + J x, fused
+__device__ __forceinline__ Sv inertia_apply_acc(const Inertia& J, const Sv& x, const Sv& acc) {
+  const Vec3d lin = J.m * cross_acc(x.a, J.c, x.l);  // m (v - c x w) = m (v + w x c)
+  return {cross_acc(J.c, lin, sym3_mul_acc(J.I, x.a, acc.a)), acc.l + lin};
+}
+// acc - ad_V^T h = acc + (w x ha + v x hl, w x hl), fused
+__device__ __forceinline__ Sv neg_advT_acc(const Sv& V, const Sv& h, const Sv& acc) {
+  return {cross_acc(V.a, h.a, cross_acc(V.l, h.l, acc.a)), cross_acc(V.a, h.l, acc.l)};
 }
 
 // Symmetric 6x6 as blocks [[A, B], [B^T, D]]; A, D packed sym (xx xy xz yy yz zz),
@@ -245,24 +277,36 @@ __device__ __forceinline__ Sym6 sym6_congruence(const Sym6& P, const SE3d& T) {
 // Joint transform rel = screw_exp(S, -q) * home                 model.cpp:117-146
 // screw_exp: Rodrigues for a not-necessarily-unit angular part, pure
 // translation if |w| < 1e-12                                     spatial.cpp:43-68
-__device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Vec3d hp, double q) {
+// joint_angle_sincos gives (sin, cos) of theta = -|w| q (the expensive,
+// history-independent part); joint_transform_sc assembles rel from it.
+__device__ __forceinline__ void joint_angle_sincos(const Sv& S, double q, double* st, double* ct) {
+  const double wn2 = dot(S.a, S.a);
+  if (wn2 < 1e-24) {
+    *st = 0.0;
+    *ct = 1.0;
+    return;
+  }
+  const double iwn = rsqrt(wn2);
+  sincos(wn2 * iwn * (-q), st, ct);
+}
+
+__device__ __forceinline__ SE3d joint_transform_sc(const Sv& S, const Mat3d& HR, Vec3d hp, double q, double st,
+                                                   double ct) {
   const double qq = -q;
   const Vec3d w = S.a, v = S.l;
   const double wn2 = dot(w, w);
   Mat3d E;
   Vec3d t;
+  const bool has_v = (v.x != 0.0) | (v.y != 0.0) | (v.z != 0.0);
   if (wn2 < 1e-24) {  // |w| < 1e-12: pure translation
 #pragma unroll
     for (int k = 0; k < 9; ++k) E.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
     t = qq * v;
   } else {
-    const double iwn = rsqrt(wn2);        // 1/|w|
-    const double iwn2 = iwn * iwn;        // 1/|w|^2
-    double st, ct;
-    sincos(wn2 * iwn * qq, &st, &ct);     // theta = |w| q
+    const double iwn = rsqrt(wn2);
+    const double iwn2 = iwn * iwn;
     const double a = st * iwn;
     const double b = (1.0 - ct) * iwn2;
-    const double c = (qq - a) * iwn2;
     // R = I + a w^ + b w^2 ; w^2 = w w^T - |w|^2 I
     E.m[0] = fma(b, w.x * w.x - wn2, 1.0);
     E.m[4] = fma(b, w.y * w.y - wn2, 1.0);
@@ -274,14 +318,25 @@ __device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Ve
     E.m[6] = fma(-a, w.y, bxz);
     E.m[5] = fma(-a, w.x, byz);
     E.m[7] = fma(a, w.x, byz);
-    // t = (q I + b w^ + c w^2) v = q v + b (w x v) + c (w x (w x v))
-    const Vec3d wv = cross(w, v);
-    t = fmav(c, cross(w, wv), fmav(b, wv, qq * v));
+    if (has_v) {
+      // t = (q I + b w^ + c w^2) v = q v + b (w x v) + c (w x (w x v))
+      const double c = (qq - a) * iwn2;
+      const Vec3d wv = cross(w, v);
+      t = fmav(c, cross(w, wv), fmav(b, wv, qq * v));
+    } else {
+      t = mk(0.0, 0.0, 0.0);  // revolute screw through the link origin
+    }
   }
   SE3d T;
   T.R = matmul(E, HR);
-  T.p = mul(E, hp) + t;
+  T.p = mul_acc(E, hp, t);
   return T;
+}
+
+__device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Vec3d hp, double q) {
+  double st, ct;
+  joint_angle_sincos(S, q, &st, &ct);
+  return joint_transform_sc(S, HR, hp, q, st, ct);
 }
 
 // Kernel-side error record: first failure wins per slot.
