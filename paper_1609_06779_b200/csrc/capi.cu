@@ -193,6 +193,7 @@ ModelView model_view(const pd_ctx* c) {
   mv.g = c->gravity.as<double>();
   mv.mstatus = c->mstatus.as<int32_t>();
   mv.mrule = c->mrule.as<int32_t>();
+  mv.fcl = nullptr;
   mv.n = c->n_links;
   mv.M = c->n_models;
   mv.ld = c->model_ld;
@@ -203,6 +204,20 @@ int64_t cta_slots(pd_ctx* ctx, size_t ws_bytes, int64_t batch) {
   const size_t budget = (size_t)2 << 30;  // 2 GiB of global workspace at most
   int64_t slots = (int64_t)std::max<size_t>(1, budget / std::max<size_t>(ws_bytes, 1));
   return std::min<int64_t>(slots, batch);
+}
+
+// Builds the link-fastest model copy once per model set (CTA/warp-per-chain kernels).
+cudaError_t ensure_model_cl(pd_ctx* ctx) {
+  if (ctx->model_cl_valid) return cudaSuccess;
+  const int n = ctx->n_links;
+  const int64_t total = ctx->n_models * F_COUNT * (int64_t)n;
+  cudaError_t e = ctx->model_cl.ensure(sizeof(double) * total);
+  if (e != cudaSuccess) return e;
+  repack_link_fastest_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->model.as<double>(), n, ctx->n_models, ctx->model_ld, ctx->model_cl.as<double>());
+  ctx->launches++;
+  ctx->model_cl_valid = true;
+  return cudaGetLastError();
 }
 
 pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, const double* q, const double* qd,
@@ -224,7 +239,7 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
     ei = er + batch;
   }
   BatchIO io{q, qd, tau, qdd, st, er, ei, batch, lds};
-  const ModelView mv = model_view(ctx);
+  ModelView mv = model_view(ctx);
   switch (algo) {
     case PD_ABIA: {
       const int64_t scr_ld = (batch + 31) / 32 * 32;
@@ -235,6 +250,8 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       break;
     }
     case PD_CFA: {
+      PD_CUDA(ensure_model_cl(ctx));
+      mv.fcl = ctx->model_cl.as<double>();
       const size_t wsb = cfa_workspace_bytes(n);
       int64_t slots = 0;
       if (wsb > 220 * 1024) {
@@ -249,15 +266,9 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
     }
     case PD_JSIIA: {
       static const bool force_cta = std::getenv("PD_JSIIA_CTA") != nullptr;
+      PD_CUDA(ensure_model_cl(ctx));
+      mv.fcl = ctx->model_cl.as<double>();
       if (n <= 32 && !force_cta) {
-        if (!ctx->model_cl_valid) {
-          const int64_t total = ctx->n_models * F_COUNT * (int64_t)n;
-          PD_CUDA(ctx->model_cl.ensure(sizeof(double) * total));
-          repack_link_fastest_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
-              ctx->model.as<double>(), n, ctx->n_models, ctx->model_ld, ctx->model_cl.as<double>());
-          ctx->launches++;
-          ctx->model_cl_valid = true;
-        }
         launch_jsiia_warp(mv, ctx->model_cl.as<double>(), io, ctx->stream);
         ctx->launches++;
         break;

@@ -320,8 +320,146 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
   }
   __syncthreads();
 
-  // ---- OEE rounds -----------------------------------------------------------
   const int rounds = ceil_log2_dev(n);
+  if (lpt == 1) {
+    // ---- OEE with the row's own state (D, U, R) in registers ---------------------
+    const int i = t;
+    const bool own = i < n;
+    double D[15], U[25], R[5];
+    if (own) {
+      ws_load<15>(ws, n, cfa::AD, i, D);
+      ws_load<5>(ws, n, cfa::OR, i, R);
+      if (i + 1 < n) ws_load<25>(ws, n, cfa::UP, i, U);
+    }
+    __syncthreads();  // AD/UP/OR are overwritten by the published fields below
+    int h = 1;
+    for (int round = 1; round <= rounds; ++round, h <<= 1) {
+      if (own) {  // publish own pivot factorization
+        double Lk[10], dinv[5], rt[5];
+        const bool ok = ldlt5(D, Lk, dinv);
+        ws_store<10>(ws, n, cfa::PL, i, Lk);
+        ws_store<5>(ws, n, cfa::PI, i, dinv);
+        ws[cfa::SG * n + i] = ok ? 0.0 : 1.0;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) rt[r] = R[r];
+        unit_lower_solve5(Lk, rt);
+        ws_store<5>(ws, n, cfa::PR, i, rt);
+        if (i < n - h) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            double col[5];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) col[r] = U[r * 5 + c];
+            unit_lower_solve5(Lk, col);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) ws[(cfa::PY + r * 5 + c) * n + i] = col[r];
+          }
+        }
+      }
+      __syncthreads();
+      if (own) {
+        // singular pivots: smallest failing row, its first failing pivot (oee.hpp:88-138)
+        const bool up_bad = (i < n - h) && ws[cfa::SG * n + i + h] != 0.0;
+        const bool dn_bad = (i >= h) && ws[cfa::SG * n + i - h] != 0.0;
+        if (up_bad || dn_bad) atomicMin(&s_bad, i);
+        if (i < n - h) {
+          const int k = i + h;
+          double Lk[10], dinv[5], rt[5];
+          ws_load<10>(ws, n, cfa::PL, k, Lk);
+          ws_load<5>(ws, n, cfa::PI, k, dinv);
+          ws_load<5>(ws, n, cfa::PR, k, rt);
+          double Z[5][5], Zs[5][5];
+#pragma unroll
+          for (int a2 = 0; a2 < 5; ++a2) {
+#pragma unroll
+            for (int r = 0; r < 5; ++r) Z[a2][r] = U[a2 * 5 + r];
+            unit_lower_solve5(Lk, Z[a2]);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) Zs[a2][r] = Z[a2][r] * dinv[r];
+          }
+#pragma unroll
+          for (int a2 = 0; a2 < 5; ++a2) {
+#pragma unroll
+            for (int b2 = 0; b2 <= a2; ++b2) {
+              double sacc = D[pk(a2, b2)];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], Z[b2][r], sacc);
+              D[pk(a2, b2)] = sacc;
+            }
+            double sacc = R[a2];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], rt[r], sacc);
+            R[a2] = sacc;
+          }
+          if (i < n - 2 * h) {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+              double yc[5];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) yc[r] = ws[(cfa::PY + r * 5 + c) * n + k];
+#pragma unroll
+              for (int a2 = 0; a2 < 5; ++a2) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int r = 0; r < 5; ++r) sacc = fma(Zs[a2][r], yc[r], sacc);
+                U[a2 * 5 + c] = -sacc;
+              }
+            }
+          }
+        }
+        if (i >= h) {
+          const int k = i - h;
+          double dinv[5], rt[5], Ys[5][5], Y[5][5];
+          ws_load<5>(ws, n, cfa::PI, k, dinv);
+          ws_load<5>(ws, n, cfa::PR, k, rt);
+#pragma unroll
+          for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+              Y[r][c] = ws[(cfa::PY + r * 5 + c) * n + k];
+              Ys[r][c] = Y[r][c] * dinv[r];
+            }
+#pragma unroll
+          for (int a2 = 0; a2 < 5; ++a2) {
+#pragma unroll
+            for (int b2 = 0; b2 <= a2; ++b2) {
+              double sacc = D[pk(a2, b2)];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], Y[r][b2], sacc);
+              D[pk(a2, b2)] = sacc;
+            }
+            double sacc = R[a2];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], rt[r], sacc);
+            R[a2] = sacc;
+          }
+        }
+      }
+      __syncthreads();
+      if (s_bad < n) {
+        if (t == 0) {
+          const int ib = s_bad;
+          const bool up_bad = (ib < n - h) && ws[cfa::SG * n + ib + h] != 0.0;
+          io.status[p] = PD_SLOT_OEE_SINGULAR_PIVOT;
+          io.eround[p] = round;
+          io.eindex[p] = up_bad ? ib + h : ib - h;
+        }
+        return;
+      }
+    }
+    // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
+    if (own) {
+      double Lf[10], dinv[5];
+      if (!ldlt5(D, Lf, dinv)) atomicMin(&s_bad, i);
+      unit_lower_solve5(Lf, R);
+#pragma unroll
+      for (int r = 0; r < 5; ++r) R[r] *= dinv[r];
+      unit_lowerT_solve5(Lf, R);
+      ws_store<5>(ws, n, cfa::OR, i, R);  // constraint force F_c,i
+    }
+    __syncthreads();
+  } else {
+  // ---- OEE rounds -----------------------------------------------------------
   int h = 1;
   for (int round = 1; round <= rounds; ++round, h <<= 1) {
     // publish own pivot factorization
@@ -462,6 +600,7 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     ws_store<5>(ws, n, cfa::OR, i, x);  // constraint force F_c,i
   }
   __syncthreads();
+  }  // smem-row OEE path
   if (s_bad < n) {
     if (t == 0) {
       io.status[p] = PD_SLOT_OEE_SINGULAR_FINAL;

@@ -204,9 +204,11 @@ __global__ void __launch_bounds__(32 * kWarps) jsiia_warp_kernel(ModelView mv, c
   bool spd = true;
 #pragma unroll
   for (int mm = 0; mm < 32; ++mm) {
-    double acc = L[mm];
+    // four independent partial sums: the inner product is the critical path
+    double a4[4] = {L[mm], 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int pp = 0; pp < mm; ++pp) acc = fma(-L[pp], sm.L[mm][pp], acc);
+    for (int pp = 0; pp < mm; ++pp) a4[pp & 3] = fma(-L[pp], sm.L[mm][pp], a4[pp & 3]);
+    const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     const bool real = mm < n;
     const double dmm = __shfl_sync(0xffffffffu, acc, mm);  // M[mm][mm] - sum_p L[mm][p]^2
     spd = spd && (!real || dmm > 0.0);                      // Eigen LLT: fails iff a pivot <= 0

@@ -12,11 +12,16 @@ struct ModelView {
   const double* __restrict__ g;  // gravity [3][M]
   const int32_t* __restrict__ mstatus;  // [M] PD_SLOT_OK or PD_SLOT_BAD_MODEL
   const int32_t* __restrict__ mrule;    // [M]
+  // Optional link-fastest copy [chain][field][link] (nullptr if absent). Lane-per-
+  // chain kernels read the chain-fastest SoA above (coalesced across chains);
+  // CTA/warp-per-chain kernels read this copy (coalesced across links).
+  const double* __restrict__ fcl;
   int n;
   int64_t M;
   int64_t ld;  // stride between links of one field (>= M, even: TMA needs 16-byte strides)
   __device__ __forceinline__ double at(int field, int link, int64_t mc) const {
-    return __ldg(f + ((int64_t)field * n + link) * ld + mc);
+    return fcl ? __ldg(fcl + ((int64_t)mc * F_COUNT + field) * n + link)
+               : __ldg(f + ((int64_t)field * n + link) * ld + mc);
   }
   __device__ __forceinline__ int64_t model_of(int64_t p) const { return M == 1 ? 0 : p; }
   __device__ __forceinline__ Vec3d gravity(int64_t mc) const {
