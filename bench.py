@@ -71,6 +71,8 @@ WORKLOADS = {
                 shared=False),
     "c4c": dict(desc="configs[3]: single chain, 1,024 links (CFA, latency)", algo="cfa", n=1024, batch=1,
                 shared=False),
+    "c4j": dict(desc="configs[3]: single chain, 1,024 links (JSIIA, latency)", algo="jsiia", n=1024, batch=1,
+                shared=False),
 }
 
 
@@ -398,11 +400,11 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_extra:
         extra = {}
-        for name in ("c2j", "c3", "c1", "c4a", "c4c"):
+        for name in ("c2j", "c3", "c1", "c4a", "c4c", "c4j"):
             if name == args.workload:
                 continue
             w = WORKLOADS[name]
-            steps = 20 if w["batch"] > 1 else 10
+            steps = 20 if w["batch"] > 1 else 3
             r = measure_workload(ctx, name, w, steps, 3, 0, local, stream, False, 0)
             mps = r["ms_total"] / steps
             h, f, b, wk = roofline_entry(w, mps / max(r["launches"] / steps, 1), bw, fp64_peak)

@@ -14,9 +14,11 @@
 //   pass C loads the 13-double records pass B wrote (after a proxy fence)
 #include <cuda.h>
 
+#include <cmath>
 #include <cstdlib>
 
 #include "abia_common.cuh"
+#include "tmem_util.cuh"
 
 namespace pd {
 
@@ -105,16 +107,18 @@ struct Maps {
 
 }  // namespace
 
+template <int KT = kT>
 __device__ __forceinline__ Sv stage_screw(const double* f) {
-  return {mk(f[F_SCREW * kT], f[(F_SCREW + 1) * kT], f[(F_SCREW + 2) * kT]),
-          mk(f[(F_SCREW + 3) * kT], f[(F_SCREW + 4) * kT], f[(F_SCREW + 5) * kT])};
+  return {mk(f[F_SCREW * KT], f[(F_SCREW + 1) * KT], f[(F_SCREW + 2) * KT]),
+          mk(f[(F_SCREW + 3) * KT], f[(F_SCREW + 4) * KT], f[(F_SCREW + 5) * KT])};
 }
+template <int KT = kT>
 __device__ __forceinline__ SE3d stage_rel(const double* f, double st, double ct) {
   Mat3d HR;
 #pragma unroll
-  for (int j = 0; j < 9; ++j) HR.m[j] = f[(F_HR + j) * kT];
-  return joint_transform_sc(stage_screw(f), HR, mk(f[F_HP * kT], f[(F_HP + 1) * kT], f[(F_HP + 2) * kT]), f[kQ * kT],
-                            st, ct);
+  for (int j = 0; j < 9; ++j) HR.m[j] = f[(F_HR + j) * KT];
+  return joint_transform_sc(stage_screw<KT>(f), HR, mk(f[F_HP * KT], f[(F_HP + 1) * KT], f[(F_HP + 2) * KT]),
+                            f[kQ * KT], st, ct);
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
@@ -130,24 +134,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Pass A stores sin/cos of each joint angle for pass B (one sincos per link);
 // the last KSTAGES links of pass A, whose pass-B loads are issued before pass A
 // reaches them, keep theirs in registers.
-template <int KSTAGES, int MINB, bool HINTS>
-__global__ void __launch_bounds__(kT, MINB)
+template <int KSTAGES, int MINB, bool HINTS, int KT>
+__global__ void __launch_bounds__(KT, MINB)
     abia_tma_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
                     int64_t scr_ld) {
-  static_assert(KSTAGES == 3, "the register hand-off of the last pass-A links assumes 3 stages");
-  extern __shared__ __align__(128) double ring[];  // [KSTAGES][kStageFields][kT]
+  static_assert(KSTAGES == 2 || KSTAGES == 3, "the register hand-off of the last pass-A links covers <= 3 stages");
+  extern __shared__ __align__(128) double ring[];  // [KSTAGES][kStageFields][KT]
   __shared__ __align__(8) uint64_t full[KSTAGES];
   __shared__ __align__(8) uint64_t empty[KSTAGES];
   const int t = threadIdx.x, lane = t & 31;
   const int n = mv.n;
-  const int c0 = blockIdx.x * kT;
+  const int c0 = blockIdx.x * KT;
   const int64_t p = (int64_t)c0 + t;
   const bool live = p < io.B;
   const int total = 3 * n;
   if (t == 0) {
     for (int s = 0; s < KSTAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kT / 32);
+      mbar_init(&empty[s], KT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -161,30 +165,30 @@ __global__ void __launch_bounds__(kT, MINB)
   // step k: pass A link k (k < n), pass B link 2n-1-k, pass C link k-2n
   auto issue = [&](int k) {
     const int s = k % KSTAGES;
-    double* dst = ring + (size_t)s * kStageFields * kT;
+    double* dst = ring + (size_t)s * kStageFields * KT;
     uint64_t* bar = &full[s];
     if (k < n) {  // re-read in pass B: default policy
-      mbar_expect_tx(bar, (18 + 2) * kT * 8);
-      tma_3d(dst + 10 * kT, &maps.model_kin, c0, k, 10, bar);
-      tma_2d(dst + kQ * kT, &maps.q, c0, k, bar);
-      tma_2d(dst + kQD * kT, &maps.qd, c0, k, bar);
+      mbar_expect_tx(bar, (18 + 2) * KT * 8);
+      tma_3d(dst + 10 * KT, &maps.model_kin, c0, k, 10, bar);
+      tma_2d(dst + kQ * KT, &maps.q, c0, k, bar);
+      tma_2d(dst + kQD * KT, &maps.qd, c0, k, bar);
     } else if (k < 2 * n) {  // last use of the model
       const int i = 2 * n - 1 - k;
-      mbar_expect_tx(bar, (28 + 5) * kT * 8);
+      mbar_expect_tx(bar, (28 + 5) * KT * 8);
       if (HINTS) {
         tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
-        tma_2d_hint(dst + kTAU * kT, &maps.tau, c0, i, bar, pol_first);
-        tma_2d_hint(dst + kSIN * kT, &maps.sc, c0, 2 * i, bar, pol_first);
+        tma_2d_hint(dst + kTAU * KT, &maps.tau, c0, i, bar, pol_first);
+        tma_2d_hint(dst + kSIN * KT, &maps.sc, c0, 2 * i, bar, pol_first);
       } else {
         tma_3d(dst, &maps.model_all, c0, i, 0, bar);
-        tma_2d(dst + kTAU * kT, &maps.tau, c0, i, bar);
-        tma_2d(dst + kSIN * kT, &maps.sc, c0, 2 * i, bar);
+        tma_2d(dst + kTAU * KT, &maps.tau, c0, i, bar);
+        tma_2d(dst + kSIN * KT, &maps.sc, c0, 2 * i, bar);
       }
-      tma_2d(dst + kQ * kT, &maps.q, c0, i, bar);
-      tma_2d(dst + kQD * kT, &maps.qd, c0, i, bar);
+      tma_2d(dst + kQ * KT, &maps.q, c0, i, bar);
+      tma_2d(dst + kQD * KT, &maps.qd, c0, i, bar);
     } else {
       const int i = k - 2 * n;
-      mbar_expect_tx(bar, kRec * kT * 8);
+      mbar_expect_tx(bar, kRec * KT * 8);
       if (HINTS)
         tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
       else
@@ -221,11 +225,11 @@ __global__ void __launch_bounds__(kT, MINB)
   for (; k < n; ++k) {  // pass A
     const int s = k % KSTAGES;
     mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * kT + t;
-    const Sv S = stage_screw(f);
+    const double* f = ring + (size_t)s * kStageFields * KT + t;
+    const Sv S = stage_screw<KT>(f);
     double sn, cs;
-    joint_angle_sincos(S, f[kQ * kT], &sn, &cs);
-    abia_pass_a(st, stage_rel(f, sn, cs), S, f[kQD * kT]);
+    joint_angle_sincos(S, f[kQ * KT], &sn, &cs);
+    abia_pass_a(st, stage_rel<KT>(f, sn, cs), S, f[kQD * KT]);
     if (k < n - KSTAGES) {
       if (live) {
         double* a = scratch + ((int64_t)n * kSC0 + 2 * k) * scr_ld + p;
@@ -246,19 +250,19 @@ __global__ void __launch_bounds__(kT, MINB)
   for (; k < 2 * n; ++k) {  // pass B
     const int s = k % KSTAGES;
     mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const double* f = ring + (size_t)s * kStageFields * KT + t;
     const int i = 2 * n - 1 - k;
-    double sn = f[kSIN * kT], cs = f[kCOS * kT];
+    double sn = f[kSIN * KT], cs = f[kCOS * KT];
     if (i == n - 1) { sn = s0; cs = c0r; }
     if (i == n - 2) { sn = s1; cs = c1r; }
     if (i == n - 3) { sn = s2; cs = c2r; }
     Inertia J;
-    J.m = f[F_MASS * kT];
-    J.c = mk(f[F_COM * kT], f[(F_COM + 1) * kT], f[(F_COM + 2) * kT]);
+    J.m = f[F_MASS * KT];
+    J.c = mk(f[F_COM * KT], f[(F_COM + 1) * KT], f[(F_COM + 2) * KT]);
 #pragma unroll
-    for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * kT];
+    for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
     double rec[kRec];
-    abia_pass_b(st, i, n, stage_rel(f, sn, cs), stage_screw(f), f[kQD * kT], J, f[kTAU * kT], rec);
+    abia_pass_b(st, i, n, stage_rel<KT>(f, sn, cs), stage_screw<KT>(f), f[kQD * KT], J, f[kTAU * KT], rec);
     if (live) {
 #pragma unroll
       for (int j = 0; j < kRec; ++j) {
@@ -275,16 +279,16 @@ __global__ void __launch_bounds__(kT, MINB)
   for (; k < total; ++k) {  // pass C
     const int s = k % KSTAGES;
     mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const double* f = ring + (size_t)s * kStageFields * KT + t;
     const int i = k - 2 * n;
     double rec[kRec];
 #pragma unroll
-    for (int j = 0; j < kRec; ++j) rec[j] = f[j * kT];
+    for (int j = 0; j < kRec; ++j) rec[j] = f[j * KT];
     const double qdd = abia_pass_c(st, rec);
     if (live) io.put_qdd(i, p, qdd);
-    if (HINTS && t < kRec * (kT * 8 / 128)) {
+    if (HINTS && t < kRec * (KT * 8 / 128)) {
       // the records of link i are dead: drop their L2 lines without write-back
-      const int row = t / (kT * 8 / 128), seg = t % (kT * 8 / 128);
+      const int row = t / (KT * 8 / 128), seg = t % (KT * 8 / 128);
       const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
       if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
     }
@@ -296,6 +300,295 @@ __global__ void __launch_bounds__(kT, MINB)
     io.eround[p] = 0;
     io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : st.eidx;
   }
+}
+
+// Variant with the per-chain recursion state in TMEM: P0 (21 doubles), Z0 and
+// F0 (6 each) live in the thread's own TMEM lane between links and are loaded
+// only around the few instructions that use them; the last pass-A sin/cos
+// pairs too. That frees ~80 registers of live state, so 3 CTAs (12 warps) fit
+// per SM with a 2-stage ring. TMEM columns per thread:
+//   [0,42) P0   [42,54) Z0   [54,66) F0   [66,74) (sin, cos) of links n-1, n-2
+constexpr int kTmemCols = 128;
+__global__ void __launch_bounds__(kT, 3)
+    abia_tma_tmem_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
+                         int64_t scr_ld) {
+  constexpr int KSTAGES = 2;
+  extern __shared__ __align__(128) double ring[];  // [KSTAGES][kStageFields][kT]
+  __shared__ __align__(8) uint64_t full[KSTAGES];
+  __shared__ __align__(8) uint64_t empty[KSTAGES];
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int n = mv.n;
+  const int c0 = blockIdx.x * kT;
+  const int64_t p = (int64_t)c0 + t;
+  const bool live = p < io.B;
+  const int total = 3 * n;
+  if (warp == 0) tmem_alloc(&tmem_base, kTmemCols);
+  if (t == 0) {
+    for (int s = 0; s < KSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tm = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+
+  auto issue = [&](int k) {
+    const int s = k % KSTAGES;
+    double* dst = ring + (size_t)s * kStageFields * kT;
+    uint64_t* bar = &full[s];
+    if (k < n) {
+      mbar_expect_tx(bar, (18 + 2) * kT * 8);
+      tma_3d(dst + 10 * kT, &maps.model_kin, c0, k, 10, bar);
+      tma_2d(dst + kQ * kT, &maps.q, c0, k, bar);
+      tma_2d(dst + kQD * kT, &maps.qd, c0, k, bar);
+    } else if (k < 2 * n) {
+      const int i = 2 * n - 1 - k;
+      mbar_expect_tx(bar, (28 + 5) * kT * 8);
+      tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
+      tma_2d_hint(dst + kTAU * kT, &maps.tau, c0, i, bar, pol_first);
+      tma_2d_hint(dst + kSIN * kT, &maps.sc, c0, 2 * i, bar, pol_first);
+      tma_2d(dst + kQ * kT, &maps.q, c0, i, bar);
+      tma_2d(dst + kQD * kT, &maps.qd, c0, i, bar);
+    } else {
+      const int i = k - 2 * n;
+      mbar_expect_tx(bar, kRec * kT * 8);
+      tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
+    }
+  };
+  int next = 0;
+  if (t == 0)
+    for (; next < min(KSTAGES, min(total, 2 * n)); ++next) issue(next);
+  auto after_step = [&](int k) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[k % KSTAGES]);
+    if (t == 0) {
+      const int target = k < 2 * n - 1 ? min(2 * n, k + 1 + KSTAGES) : min(total, k + 1 + KSTAGES);
+      for (; next < target; ++next) {
+        const int prev = next - KSTAGES;
+        if (prev >= 0) mbar_wait(&empty[prev % KSTAGES], (uint32_t)((prev / KSTAGES) & 1));
+        if (next == 2 * n && prev != 2 * n - 1)
+          mbar_wait(&empty[(2 * n - 1) % KSTAGES], (uint32_t)(((2 * n - 1) / KSTAGES) & 1));
+        issue(next);
+      }
+    }
+  };
+
+  const int64_t mc = live ? mv.model_of(p) : 0;
+  const Vec3d grav = live ? mv.gravity(mc) : mk(0, 0, 0);
+  SE3d X;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) X.R.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  X.p = mk(0, 0, 0);
+  Sv V0 = svzero();
+  Sv A0 = {mk(0, 0, 0), mk(-grav.x, -grav.y, -grav.z)};
+  {  // F0 = 0 in TMEM
+    double z[6] = {0, 0, 0, 0, 0, 0};
+    uint32_t r[12];
+    pack_doubles<6>(z, r);
+    uint32_t r8[8], r4[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r8[j] = r[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r4[j] = r[8 + j];
+    tmem_st8(tm + 54, r8);
+    tmem_st4(tm + 62, r4);
+    tmem_st8(tm + 42, r8);  // Z0 = 0
+    tmem_st4(tm + 50, r4);
+  }
+  int k = 0;
+  for (; k < n; ++k) {  // pass A (base -> tip)
+    const int s = k % KSTAGES;
+    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
+    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const Sv S = stage_screw(f);
+    double sn, cs;
+    joint_angle_sincos(S, f[kQ * kT], &sn, &cs);
+    const SE3d rel = stage_rel(f, sn, cs);
+    X = compose(rel, X);
+    const Sv S0 = adinv_apply(X, S);
+    const double qd = f[kQD * kT];
+    V0 = svfma(qd, S0, V0);
+    A0 = adv_acc(V0, qd * S0, A0);
+    if (k < n - KSTAGES) {
+      if (live) {
+        double* a = scratch + ((int64_t)n * kSC0 + 2 * k) * scr_ld + p;
+        st_hint(a, sn, pol_last);
+        st_hint(a + scr_ld, cs, pol_last);
+      }
+    } else {  // links n-1, n-2: TMEM slots 66 + 4*(n-1-k)
+      const double sc[2] = {sn, cs};
+      uint32_t r[4];
+      pack_doubles<2>(sc, r);
+      tmem_st4(tm + 66 + 4 * (n - 1 - k), r);
+    }
+    if (k == n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");
+    after_step(k);
+  }
+  int code = PD_SLOT_OK, eidx = 0;
+  for (; k < 2 * n; ++k) {  // pass B (tip -> base)
+    const int s = k % KSTAGES;
+    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
+    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const int i = 2 * n - 1 - k;
+    double sn = f[kSIN * kT], cs = f[kCOS * kT];
+    if (i >= n - KSTAGES) {
+      uint32_t r[4];
+      tmem_ld_wait4(tm + 66 + 4 * (n - 1 - i), r);
+      double sc[2];
+      unpack_doubles<2>(r, sc);
+      sn = sc[0];
+      cs = sc[1];
+    }
+    const Sv S = stage_screw(f);
+    const double qd = f[kQD * kT];
+    const SE3d rel = stage_rel(f, sn, cs);
+    const Sv S0 = adinv_apply(X, S);
+    Inertia Jl;
+    Jl.m = f[F_MASS * kT];
+    Jl.c = mk(f[F_COM * kT], f[(F_COM + 1) * kT], f[(F_COM + 2) * kT]);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) Jl.I[j] = f[(F_IC + j) * kT];
+    const Inertia J0 = inertia_to_base(Jl, X);
+    const Vec3d qshift = -1.0 * mulT(X.R, X.p);  // for the link-frame trace
+    X = step_back(rel, X);                        // X_{i-1}
+    // wrench sum and bias torque           inverse_dynamics.cpp:103-112,146-150
+    double tau_delta;
+    {
+      uint32_t r[12];
+      tmem_ld_wait12(tm + 54, r);
+      double fv[6];
+      unpack_doubles<6>(r, fv);
+      Sv F0 = {mk(fv[0], fv[1], fv[2]), mk(fv[3], fv[4], fv[5])};
+      const Sv h = inertia_apply(J0, V0);
+      F0 = neg_advT_acc(V0, h, inertia_apply_acc(J0, A0, F0));
+      tau_delta = f[kTAU * kT] - dot(S0, F0);
+      const double fo[6] = {F0.a.x, F0.a.y, F0.a.z, F0.l.x, F0.l.y, F0.l.z};
+      pack_doubles<6>(fo, r);
+      uint32_t r8[8], r4[4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r8[j] = r[j];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r4[j] = r[8 + j];
+      tmem_st8(tm + 54, r8);
+      tmem_st4(tm + 62, r4);
+    }
+    // parent's link states
+    const Sv rate0 = qd * S0;
+    A0 = adv_acc(V0, -1.0 * rate0, A0);
+    V0 = svfma(-qd, S0, V0);
+    // articulated inertia, z sweep, u            forward_dynamics.cpp:136-212
+    {
+      Sym6 Ia = inertia_sym6(J0);
+      double zv[6] = {0, 0, 0, 0, 0, 0};
+      uint32_t r[54];
+      tmem_ld_wait54(tm + 0, r);
+      double pz[27];
+      unpack_doubles<27>(r, pz);
+      if (i < n - 1) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) Ia.A[j] += pz[j];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) Ia.B[j] += pz[6 + j];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) Ia.D[j] += pz[15 + j];
+      }
+#pragma unroll
+      for (int j = 0; j < 6; ++j) zv[j] = pz[21 + j];
+      const Sv Z0 = {mk(zv[0], zv[1], zv[2]), mk(zv[3], zv[4], zv[5])};
+      const Sv U = sym6_apply(Ia, S0);
+      const double lambda = dot(S0, U);
+      // link-frame trace of Ia (shift q = -R^T p of X_i)
+      const double trD = Ia.D[0] + Ia.D[3] + Ia.D[5];
+      const double trBq = qshift.x * (Ia.B[5] - Ia.B[7]) + qshift.y * (Ia.B[6] - Ia.B[2]) +
+                          qshift.z * (Ia.B[1] - Ia.B[3]);
+      const double trI = Ia.A[0] + Ia.A[3] + Ia.A[5] + 2.0 * trBq - dot(qshift, sym3_mul(Ia.D, qshift)) +
+                         dot(qshift, qshift) * trD + trD;
+      if (!(lambda > 1e-14 * trI) && code == PD_SLOT_OK) {
+        code = PD_SLOT_DEGENERATE_ARTICULATION;
+        eidx = i;
+      }
+      const double inv_l = 1.0 / lambda;
+      const double u = (tau_delta - dot(S0, Z0)) * inv_l;
+      const Sv g0 = inv_l * U;
+      if (live) {
+        const double rec[kRec] = {g0.a.x, g0.a.y, g0.a.z, g0.l.x, g0.l.y, g0.l.z,
+                                  S0.a.x, S0.a.y, S0.a.z, S0.l.x, S0.l.y, S0.l.z, u};
+#pragma unroll
+        for (int j = 0; j < kRec; ++j) st_hint(scratch + ((int64_t)i * kRec + j) * scr_ld + p, rec[j], pol_last);
+      }
+      if (i > 0) {
+        const Sv Zn = svfma(u, U, Z0);
+        const double ua[3] = {U.a.x, U.a.y, U.a.z}, ul[3] = {U.l.x, U.l.y, U.l.z};
+        const double ga[3] = {g0.a.x, g0.a.y, g0.a.z}, gl[3] = {g0.l.x, g0.l.y, g0.l.z};
+        const int sidx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          pz[j] = fma(-ua[sidx[j][0]], ga[sidx[j][1]], Ia.A[j]);
+          pz[15 + j] = fma(-ul[sidx[j][0]], gl[sidx[j][1]], Ia.D[j]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) pz[6 + 3 * rr + cc] = fma(-ua[rr], gl[cc], Ia.B[3 * rr + cc]);
+        pz[21] = Zn.a.x;
+        pz[22] = Zn.a.y;
+        pz[23] = Zn.a.z;
+        pz[24] = Zn.l.x;
+        pz[25] = Zn.l.y;
+        pz[26] = Zn.l.z;
+        pack_doubles<27>(pz, r);
+        uint32_t r32[32], r16[16], r4[4], r2[2];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r32[j] = r[j];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r16[j] = r[32 + j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r4[j] = r[48 + j];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) r2[j] = r[52 + j];
+        tmem_st16(tm + 0, *reinterpret_cast<uint32_t(*)[16]>(r32));
+        tmem_st16(tm + 16, *reinterpret_cast<uint32_t(*)[16]>(r32 + 16));
+        tmem_st16(tm + 32, r16);
+        tmem_st4(tm + 48, r4);
+        tmem_st2(tm + 52, r2);
+      }
+    }
+    if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");
+    after_step(k);
+  }
+  Sv a0 = svzero();
+  for (; k < total; ++k) {  // pass C (base -> tip)
+    const int s = k % KSTAGES;
+    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
+    const double* f = ring + (size_t)s * kStageFields * kT + t;
+    const int i = k - 2 * n;
+    const Sv g0 = {mk(f[0], f[kT], f[2 * kT]), mk(f[3 * kT], f[4 * kT], f[5 * kT])};
+    const Sv S0 = {mk(f[6 * kT], f[7 * kT], f[8 * kT]), mk(f[9 * kT], f[10 * kT], f[11 * kT])};
+    const double qdd = f[12 * kT] - dot(g0, a0);
+    a0 = svfma(qdd, S0, a0);
+    if (live) io.put_qdd(i, p, qdd);
+    if (t < kRec * (kT * 8 / 128)) {
+      const int row = t / (kT * 8 / 128), seg = t % (kT * 8 / 128);
+      const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
+      if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
+    }
+    after_step(k);
+  }
+  if (live) {
+    const int32_t ms = __ldg(mv.mstatus + mc);
+    io.status[p] = ms != PD_SLOT_OK ? ms : code;
+    io.eround[p] = 0;
+    io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : eidx;
+  }
+  tmem_wait_st();
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem_base, kTmemCols);
 }
 
 // ---------------------------------------------------------------- host side
@@ -331,18 +624,59 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Kernel variant (tuning experiments): PD_ABIA_VARIANT selects
-// 0 = L2 policy hints (default), 2 = no hints.
+// Kernel variant: PD_ABIA_VARIANT forces one (tuning experiments); by
+// default the tile size is chosen for wave balance (0 or 4).
+// 0 = 128-chain tiles, 3 stages, 2 CTAs/SM, L2 hints; 1 = 2 stages, 3 CTAs/SM;
+// 2 = no L2 hints; 3 = TMEM-state kernel; 4 = 224-chain tiles, 1 CTA/SM.
 int abia_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("PD_ABIA_VARIANT");
-    v = e ? std::atoi(e) : 0;
+    v = e ? std::atoi(e) : -1;
   }
   return v;
 }
 
 }  // namespace
+
+bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, uint32_t kt) {
+  const int n = mv.n;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)mv.M, (cuuint64_t)n, (cuuint64_t)F_COUNT};
+    const cuuint64_t str[2] = {(cuuint64_t)mv.ld * 8, (cuuint64_t)mv.ld * n * 8};
+    const cuuint32_t box_all[3] = {kt, 1, 28}, box_kin[3] = {kt, 1, 18};
+    if (!encode(&maps.model_all, mv.f, 3, dims, str, box_all)) return false;
+    if (!encode(&maps.model_kin, mv.f, 3, dims, str, box_kin)) return false;
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)io.B, (cuuint64_t)n};
+    const cuuint64_t str[1] = {(cuuint64_t)io.lds * 8};
+    const cuuint32_t box[2] = {kt, 1};
+    if (!encode(&maps.q, io.q, 2, dims, str, box)) return false;
+    if (!encode(&maps.qd, io.qd, 2, dims, str, box)) return false;
+    if (!encode(&maps.tau, io.tau, 2, dims, str, box)) return false;
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)io.B, (cuuint64_t)n * kRec};
+    const cuuint64_t str[1] = {(cuuint64_t)scr_ld * 8};
+    const cuuint32_t box[2] = {kt, kRec};
+    if (!encode(&maps.scr, scratch, 2, dims, str, box)) return false;
+    const cuuint64_t dims_sc[2] = {(cuuint64_t)io.B, (cuuint64_t)n * 2};
+    const cuuint32_t box_sc[2] = {kt, 2};
+    if (!encode(&maps.sc, scratch + (size_t)n * kSC0 * scr_ld, 2, dims_sc, str, box_sc)) return false;
+  }
+  return true;
+}
+
+int sm_count() {
+  static int c = 0;
+  if (!c) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0) c = 148;
+  }
+  return c;
+}
 
 // Returns false (caller falls back to the plain kernel) when the batch does
 // not meet TMA's layout rules: one model per chain, 16-byte aligned bases,
@@ -353,41 +687,31 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
   if (!aligned16(mv.f) || !aligned16(io.q) || !aligned16(io.qd) || !aligned16(io.tau) || !aligned16(scratch))
     return false;
   if (io.B >= (1ll << 31) || (int64_t)mv.n * kRec >= (1ll << 31)) return false;
-  const int n = mv.n;
+  int v = abia_variant();
+  if (v < 0) {
+    // Tile choice by wave balance. One CTA = one chain tile; an SM holds 256
+    // resident chains with 128-chain tiles (2 CTAs) or 224 with one 224-chain
+    // CTA. Pick the tiling whose last wave is fullest.
+    auto waste = [&](int per_sm) {
+      const double waves = (double)io.B / ((double)sm_count() * per_sm);
+      return std::ceil(waves) - waves;
+    };
+    v = waste(224) < waste(256) ? 4 : 0;
+  }
+  const uint32_t kt = (v == 4) ? 224u : 128u;
   Maps maps;
-  {
-    const cuuint64_t dims[3] = {(cuuint64_t)mv.M, (cuuint64_t)n, (cuuint64_t)F_COUNT};
-    const cuuint64_t str[2] = {(cuuint64_t)mv.ld * 8, (cuuint64_t)mv.ld * n * 8};
-    const cuuint32_t box_all[3] = {kT, 1, 28}, box_kin[3] = {kT, 1, 18};
-    if (!encode(&maps.model_all, mv.f, 3, dims, str, box_all)) return false;
-    if (!encode(&maps.model_kin, mv.f, 3, dims, str, box_kin)) return false;
-  }
-  {
-    const cuuint64_t dims[2] = {(cuuint64_t)io.B, (cuuint64_t)n};
-    const cuuint64_t str[1] = {(cuuint64_t)io.lds * 8};
-    const cuuint32_t box[2] = {kT, 1};
-    if (!encode(&maps.q, io.q, 2, dims, str, box)) return false;
-    if (!encode(&maps.qd, io.qd, 2, dims, str, box)) return false;
-    if (!encode(&maps.tau, io.tau, 2, dims, str, box)) return false;
-  }
-  {
-    const cuuint64_t dims[2] = {(cuuint64_t)io.B, (cuuint64_t)n * kRec};
-    const cuuint64_t str[1] = {(cuuint64_t)scr_ld * 8};
-    const cuuint32_t box[2] = {kT, kRec};
-    if (!encode(&maps.scr, scratch, 2, dims, str, box)) return false;
-    const cuuint64_t dims_sc[2] = {(cuuint64_t)io.B, (cuuint64_t)n * 2};
-    const cuuint32_t box_sc[2] = {kT, 2};
-    if (!encode(&maps.sc, scratch + (size_t)n * kSC0 * scr_ld, 2, dims_sc, str, box_sc)) return false;
-  }
-  const unsigned blocks = (unsigned)((io.B + kT - 1) / kT);
+  if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
   auto go = [&](auto kernel, int stages) {
-    const size_t smem = (size_t)stages * kStageFields * kT * sizeof(double);
+    const size_t smem = (size_t)stages * kStageFields * kt * sizeof(double);
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kernel<<<blocks, kT, smem, s>>>(maps, mv, io, scratch, scr_ld);
+    kernel<<<(unsigned)((io.B + kt - 1) / kt), kt, smem, s>>>(maps, mv, io, scratch, scr_ld);
   };
-  switch (abia_variant()) {
-    case 2: go(abia_tma_kernel<3, 2, false>, 3); break;
-    default: go(abia_tma_kernel<3, 2, true>, 3); break;  // measured best (profiles/README.md)
+  switch (v) {
+    case 1: go(abia_tma_kernel<2, 3, true, 128>, 2); break;
+    case 2: go(abia_tma_kernel<3, 2, false, 128>, 3); break;
+    case 3: go(abia_tma_tmem_kernel, 2); break;
+    case 4: go(abia_tma_kernel<3, 1, true, 224>, 3); break;
+    default: go(abia_tma_kernel<3, 2, true, 128>, 3); break;
   }
   return true;
 }
