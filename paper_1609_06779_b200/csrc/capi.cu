@@ -16,6 +16,8 @@
 namespace pd {
 void launch_abia(const ModelView& mv, const BatchIO& io, double* scratch, cudaStream_t s);
 bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, cudaStream_t s);
+void launch_abia_cta(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+size_t abia_cta_workspace_bytes(int n);
 int abia_scratch_doubles_per_link();
 void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
@@ -242,6 +244,22 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
   ModelView mv = model_view(ctx);
   switch (algo) {
     case PD_ABIA: {
+      // long chains in small batches: CTA per chain (parallel kinematics and
+      // bias torque, sequential articulated recursion); otherwise lane per chain
+      static const bool force_cta = std::getenv("PD_ABIA_CTA") != nullptr;
+      if (force_cta || (n >= 64 && batch <= 2 * ctx->sm_count)) {
+        PD_CUDA(ensure_model_cl(ctx));
+        mv.fcl = ctx->model_cl.as<double>();
+        const size_t wsb = abia_cta_workspace_bytes(n);
+        int64_t slots = 0;
+        if (wsb > 200 * 1024) {
+          slots = cta_slots(ctx, wsb, batch);
+          PD_CUDA(ctx->cta_ws.ensure(wsb * slots));
+        }
+        launch_abia_cta(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream);
+        ctx->launches += slots ? (batch + slots - 1) / slots : 1;
+        break;
+      }
       const int64_t scr_ld = (batch + 31) / 32 * 32;
       PD_CUDA(ctx->abia_scratch.ensure(sizeof(double) * abia_scratch_doubles_per_link() * (size_t)n * scr_ld));
       if (!launch_abia_tma(mv, io, ctx->abia_scratch.as<double>(), scr_ld, ctx->stream))

@@ -127,3 +127,30 @@ def test_deterministic(oracle, gpu_ctx, algo):
     a = gpu_ctx.solve(algo, q, qd, tau)[0]
     b = gpu_ctx.solve(algo, q, qd, tau)[0]
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("algo", [pd.FdAlgo.abia, pd.FdAlgo.cfa])
+def test_c4_single_1024_link_chain(oracle, gpu_ctx, algo):
+    """configs[3]: one 1,024-link chain (CTA-parallel variants, L2 workspace)."""
+    n = 1024
+    cell = oracle.workload_seed(42, n, 1)
+    links = oracle.workload_chains(cell, n, 1)
+    q, qd, tau = oracle.workload_inputs(cell, n, 1, 0)
+    gpu_ctx.set_models(links, None)
+    qdd, st, _, _ = gpu_ctx.solve(algo, q, qd, tau)
+    assert (st == 0).all()
+    ref, _ = oracle.batch_forward_dynamics(ONAME[algo], links, [0, 0, -9.81], q, qd, tau)
+    assert rel_gap(qdd[0], ref[0]) <= TOL
+
+
+@pytest.mark.parametrize("n,B", [(64, 5), (100, 7), (48, 300)])
+def test_abia_cta_path(oracle, gpu_ctx, n, B):
+    """Small batches of longer chains take the CTA-per-chain ABIA kernel."""
+    cell = oracle.workload_seed(42, n, B)
+    links = oracle.workload_chains(cell, n, B)
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    gpu_ctx.set_models(links, None)
+    qdd, st, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    assert (st == 0).all()
+    ref, _ = oracle.batch_forward_dynamics("abia", links, [0, 0, -9.81], q, qd, tau)
+    assert max(rel_gap(qdd[b], ref[b]) for b in range(B)) <= TOL
