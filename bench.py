@@ -73,7 +73,25 @@ WORKLOADS = {
                 shared=False),
     "c4j": dict(desc="configs[3]: single chain, 1,024 links (JSIIA, latency)", algo="jsiia", n=1024, batch=1,
                 shared=False),
+    # configs[4]: the global batch is fixed and sharded over the ranks (strong scaling)
+    "c5a": dict(desc="configs[4]: ABIA, 1M chains x 64 links, batch-sharded", algo="abia", n=64, batch=1 << 20,
+                shared=False, sharded=True),
+    "c5j": dict(desc="configs[4]: JSIIA, 1M chains x 64 links, batch-sharded", algo="jsiia", n=64, batch=1 << 20,
+                shared=False, sharded=True),
+    "c5c": dict(desc="configs[4]: CFA, 1M chains x 64 links, batch-sharded", algo="cfa", n=64, batch=1 << 20,
+                shared=False, sharded=True),
 }
+
+
+def local_batch(wl: dict, world: int, rank: int):
+    """(first problem, count) this rank solves: sharded configs split the
+    global batch (sharding.shard_bounds), the others give every rank a full
+    batch of its own chains (weak scaling)."""
+    if wl.get("sharded"):
+        from paper_1609_06779_b200.sharding import shard_bounds
+        lo, hi = shard_bounds(wl["batch"], world, rank)
+        return lo, hi - lo
+    return rank * wl["batch"], wl["batch"]
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -180,10 +198,15 @@ def cpu_reference(algo: str, n: int, links, q, qd, tau, budget_s: float, reps: i
     return S * reps / dt, S, cores
 
 
-def gen_workload(wl: dict, rank: int):
+def gen_workload(wl: dict, rank: int, world: int = 1):
     from paper_1609_06779_b200 import workload as W
     n, B = wl["n"], wl["batch"]
     cell = W.workload_seed(42, n, B)
+    if wl.get("sharded"):
+        lo, cnt = local_batch(wl, world, rank)
+        links = W.workload_chains(cell, n, cnt, g0=lo)
+        inputs = tuple(np.ascontiguousarray(a[lo:lo + cnt]) for a in W.workload_inputs(cell, n, B, 0))
+        return links, inputs, None
     if wl["shared"]:
         links = W.workload_chains(cell, n, 1)
         qs = [W.workload_inputs(cell, n, 1, r) for r in range(B)]
@@ -264,10 +287,11 @@ def time_device(ctx, algo, B, n, dev_inputs, steps, warmup, stream):
     return e0.elapsed_time(e1), ctx.kernel_launches() - l0, qdd
 
 
-def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e, e2e_steps):
+def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e, e2e_steps, world=1):
     import torch
-    n, B, algo = wl["n"], wl["batch"], wl["algo"]
-    links, inp, inp2 = gen_workload(wl, rank)
+    n, algo = wl["n"], wl["algo"]
+    links, inp, inp2 = gen_workload(wl, rank, world)
+    B = len(inp[0])
     ms, mr = ctx.set_models(links, None)
     assert (ms == 0).all()
     dev = torch.device("cuda", local)
@@ -279,7 +303,7 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
     if inp2 is not None:
         dev_inputs.append(tuple(to_dev(a) for a in inp2))
     ms_total, launches, qdd = time_device(ctx, algo, B, n, dev_inputs, steps, warmup, stream)
-    res = {"ms_total": ms_total, "launches": launches, "links": links, "inputs": inp}
+    res = {"ms_total": ms_total, "launches": launches, "links": links, "inputs": inp, "B": B}
     if want_e2e:
         pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in inp]
         out = torch.empty((B, n), dtype=torch.float64).pin_memory()
@@ -357,25 +381,29 @@ def main():
     dist_barrier(world, local)
     torch.cuda.synchronize()
     res = measure_workload(ctx, args.workload, wl, args.steps, args.warmup, rank, local, stream, not args.no_e2e,
-                           e2e_steps=max(3, min(args.steps, 30)))
+                           e2e_steps=max(3, min(args.steps, 30)), world=world)
     clocks = sampler.stop()
     ms_max = dist_max(res["ms_total"], world, local)
     e2e_max = dist_max(res.get("e2e_s", 0.0), world, local)
 
-    n, B = wl["n"], wl["batch"]
-    total = B * world * args.steps
+    n, B = wl["n"], res["B"]
+    sharded = bool(wl.get("sharded"))
+    global_batch = wl["batch"] if sharded else B * world
+    total = global_batch * args.steps
     value = total / (ms_max * 1e-3)
     ms_per_step = ms_max / args.steps
     launches_per_step = res["launches"] / args.steps
-    hbm, fp, binding, work = roofline_entry(wl, ms_per_step / max(launches_per_step, 1), bw, fp64_peak)
+    # roofline of this rank's kernel on its own (local) batch
+    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B), res["ms_total"] / args.steps / max(launches_per_step, 1),
+                                            bw, fp64_peak)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference generators workload_chains/workload_inputs (seed 42), random-init chains",
         "config": {"workload": f"{args.workload}: {wl['desc']}", "algo": wl["algo"], "n_links": n,
-                   "batch_per_gpu": B, "global_batch": B * world, "parallelism": f"batch-sharded x{world}",
+                   "batch_per_gpu": B, "global_batch": global_batch, "parallelism": f"batch-sharded x{world}",
                    "l2": "inputs larger than L2 (%.0f MB streamed per step)" % (work["bytes_per_launch"] / 1e6)
                    if work["bytes_per_launch"] > 126e6 else "L2 not flushed (small workload)"},
         "roofline": hbm,
@@ -387,7 +415,7 @@ def main():
         "clocks": clocks,
     }
     if "e2e_s" in res:
-        line["e2e"] = {"value": B * world * res["e2e_steps"] / e2e_max, "unit": UNIT,
+        line["e2e"] = {"value": global_batch * res["e2e_steps"] / e2e_max, "unit": UNIT,
                        "h2d_bytes_per_step": res["h2d"] * world, "d2h_bytes_per_step": res["d2h"] * world,
                        "timing": "wall clock around pd_forward_dynamics (pinned host buffers), max over ranks"}
 

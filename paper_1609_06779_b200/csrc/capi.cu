@@ -22,7 +22,9 @@ int abia_scratch_doubles_per_link();
 void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
-void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count,
+                  cudaStream_t s);
+bool jsiia_smem_path(int n);
 bool launch_jsiia_warp(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
 size_t jsiia_workspace_bytes(int n);
 }  // namespace pd
@@ -293,14 +295,14 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       }
       const size_t wsb = jsiia_workspace_bytes(n);
       int64_t slots = 0;
-      if (wsb > 220 * 1024) {
+      if (!jsiia_smem_path(n)) {
         slots = cta_slots(ctx, wsb, batch);
         PD_CUDA(ctx->cta_ws.ensure(wsb * slots));
         ctx->launches += (batch + slots - 1) / slots;
       } else {
         ctx->launches++;
       }
-      launch_jsiia(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream);
+      launch_jsiia(mv, io, ctx->cta_ws.as<double>(), slots, ctx->sm_count, ctx->stream);
       break;
     }
     default:
@@ -426,13 +428,14 @@ int64_t pd_kernel_launches(const pd_ctx* ctx) { return ctx ? ctx->launches : 0; 
 const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) {
   (void)ctx;
   switch (algo) {
-    case PD_ABIA: return "abia_tma_kernel (lane per chain, 3 fused base-frame passes, TMA ring)";
+    case PD_ABIA: return "abia_tma_kernel (lane per chain, 3 fused base-frame passes, TMA ring); "
+                         "abia_cta_kernel for n >= 64 in batches <= 2 x SMs (CTA per chain)";
     case PD_CFA: return cfa_workspace_bytes(n_links) <= 220 * 1024 ? "cfa_cta_kernel<smem> (CTA per chain, OEE in smem)"
                                                                     : "cfa_cta_kernel<global> (CTA per chain, L2 workspace)";
     case PD_JSIIA: return n_links <= 32 ? "jsiia_warp_kernel (warp per chain, register-resident M rows + row Cholesky)"
-                          : jsiia_workspace_bytes(n_links) <= 220 * 1024
-                              ? "jsiia_cta_kernel<smem> (CTA per chain, CRBA scans + CTA Cholesky)"
-                              : "jsiia_cta_kernel<global> (CTA per chain, L2 workspace)";
+                          : jsiia_smem_path(n_links)
+                              ? "jsiia_tiled_kernel<smem> (CTA per chain, CRBA scans + 32x32-tile Cholesky in smem)"
+                              : "jsiia_tiled_kernel<global> (CTA per chain, 32x32-tile Cholesky, L2 workspace)";
   }
   return "unknown";
 }

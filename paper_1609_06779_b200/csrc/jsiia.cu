@@ -1,4 +1,5 @@
-// JSIIA forward dynamics, one CTA per chain.
+// JSIIA forward dynamics for chains longer than one warp (n > 32): one CTA per
+// chain, M factored by a blocked (32x32-tile) right-looking Cholesky.
 //
 // Reference: jsiia_forward_dynamics (proj/core/src/forward_dynamics.cpp:82-118)
 //   = kinematics + torque surplus (3 scans)                 -> cta_bias_torque
@@ -8,35 +9,67 @@
 //     one refinement step if ||td - M qdd|| > 1e-9 ||td||, error if still
 //     above (:105-116).
 //
-// B200 mapping. The n column probes of the reference (n inverse-dynamics
-// solves, 3 scans each) are replaced by the closed form they evaluate: in base
-// coordinates the probe of column j accumulates Ic_j = sum_{k>=j} J_k^b, so
-// M_ij = S_i^b . (Ic_{max(i,j)}^b S_{max(i,j)}^b)... = S^b_min . F^b_max with
-// F^b_k = Ic^b_k S^b_k, S^b_k = Ad(X_k)^{-1} S_k, J^b_k = Ad(X_k)^T J_k Ad(X_k).
-// That is one SE(3) prefix scan (shared with the bias stage) and one 21-wide
-// suffix sum instead of 3n scans; M comes out exactly symmetric (same
-// expression for (i,j) and (j,i)). Cholesky, triangular solves and the
-// refinement run CTA-parallel with M in shared memory (column-major, odd
-// leading dimension).
+// B200 mapping.
+//  * The n column probes of the reference (n inverse-dynamics solves) are
+//    replaced by the closed form they evaluate: in base coordinates
+//    M_ij = S0_min(i,j) . (Ic0_max S0_max), Ic0_k = sum_{l>=k} J0_l -- one SE(3)
+//    prefix scan (shared with the bias stage) and one 21-wide suffix sum. The
+//    expression is the same for (i,j) and (j,i), so M is exactly symmetric.
+//  * M is stored row-major, padded to npad = 32*ceil(n/32) with an identity
+//    block (so the padding needs no special cases anywhere), leading
+//    dimension npad+2 (16-byte rows for double2 loads; 4-way banked columns).
+//    It lives in shared memory when the chain's workspace fits (n <= ~150),
+//    else in a per-CTA global slot (L2-resident).
+//  * Cholesky by 32x32 tiles, one warp per tile task, lane = tile row with the
+//    row in registers: POTRF (left-looking by rows, broadcast of row m),
+//    TRSM (same recurrence against the factored diagonal tile) and the
+//    trailing update C -= A B^T (double2 broadcasts of B rows, 2 FMA per
+//    load). Tasks of one panel step are spread over the CTA's warps.
+//    L overwrites the lower triangle; the strict upper triangle keeps M and
+//    the diagonal of M is saved, so the residual uses M itself, as the
+//    reference does.
+#include "abia_common.cuh"
 #include "cta_common.cuh"
 
 namespace pd {
 
-namespace jsi {
-constexpr int REL = 0, X = 12, V = 24, TMP = 30, TD = 36, SB = 37, FB = 43, IC = 49;
+namespace jst {
+// workspace fields, units of n doubles. TD, S0, FB stay live while M is built
+// (M starts right after them and overwrites the dead kinematics fields).
+constexpr int TD = 0, S0 = 1, FB = 7, REL = 13, X = 25, V = 37, TMP = 43, IC = 49;
 constexpr int FIELDS = 70;
-constexpr int VEC_Y = 0, VEC_X = 1, VEC_R = 2, VEC_DG = 3, VEC_D = 4;  // n-vectors after the fields
-constexpr int NVEC = 5;
-}  // namespace jsi
+constexpr int KEEP = 13;
+constexpr int NVEC = 4;  // after M: x, work vector, diag(M), 1/diag(L)
+}  // namespace jst
 
-__host__ __device__ __forceinline__ int jsi_ld(int n) { return n | 1; }
-__host__ __device__ __forceinline__ size_t jsi_workspace_doubles(int n) {
-  return (size_t)(jsi::FIELDS + jsi::NVEC) * n + (size_t)jsi_ld(n) * n;
+struct JstLayout {
+  int n, np, npad, ld;
+  size_t m_off, v_off, total;  // doubles
+};
+
+__host__ __device__ inline JstLayout jst_layout(int n) {
+  JstLayout L;
+  L.n = n;
+  L.np = (n + 31) / 32;
+  L.npad = 32 * L.np;
+  L.ld = L.npad + 2;
+  L.m_off = ((size_t)jst::KEEP * n + 1) & ~(size_t)1;  // 16-byte aligned
+  L.v_off = L.m_off + (size_t)L.npad * L.ld;
+  size_t end = L.v_off + (size_t)jst::NVEC * L.npad;
+  const size_t phase_a = (size_t)jst::FIELDS * n;
+  if (end < phase_a) end = phase_a;
+  L.total = (end + 1) & ~(size_t)1;
+  return L;
 }
+
+size_t jsiia_workspace_bytes(int n) { return jst_layout(n).total * sizeof(double); }
+
+namespace {
 
 struct BlockReduce {
   double part[kMaxWarps];
 };
+
 // Deterministic CTA sum (fixed order), result broadcast to all threads.
 __device__ double block_sum(double v, BlockReduce& br) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -50,113 +83,246 @@ __device__ double block_sum(double v, BlockReduce& br) {
   return s;
 }
 
-// Solve (L L^T) v = v in place (vec field f of the workspace); L in the lower
-// triangle of column-major M.
-__device__ void cta_llt_solve(double* ws, int n, const double* M, int ld, double* v) {
-  const int t = threadIdx.x, nt = blockDim.x;
-  for (int k = 0; k < n; ++k) {  // forward: L y = v
-    const double yk = v[k] / M[k * ld + k];
-    __syncthreads();
-    for (int i = k + 1 + t; i < n; i += nt) v[i] = fma(-M[k * ld + i], yk, v[i]);
-    if (t == 0) v[k] = yk;
-    __syncthreads();
-  }
-  for (int k = n - 1; k >= 0; --k) {  // backward: L^T x = y
-    const double xk = v[k] / M[k * ld + k];
-    __syncthreads();
-    for (int i = t; i < k; i += nt) v[i] = fma(-M[i * ld + k], xk, v[i]);
-    if (t == 0) v[k] = xk;
-    __syncthreads();
+__device__ __forceinline__ void load_row(double (&r)[32], const double* row) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(row + j);
+    r[j] = v.x;
+    r[j + 1] = v.y;
   }
 }
 
+// Cholesky of a diagonal tile in place (lower triangle; the strict upper
+// triangle is read back unchanged). invd[i] = 1 / L_ii. Returns false iff a
+// pivot is <= 0 (Eigen LLT's failure condition). Warp-uniform result.
+__device__ bool tile_potrf(double* A, int ld, double* invd, int lane) {
+  double r[32];
+  load_row(r, A + lane * ld);
+  bool spd = true;
+  double inv_d = 0.0;
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    double a4[4] = {r[m], 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], A[m * ld + p], a4[p & 3]);
+    const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    const double dmm = __shfl_sync(0xffffffffu, acc, m);
+    spd = spd && dmm > 0.0;
+    const double lmm = sqrt(dmm > 0.0 ? dmm : 1.0);
+    const double inv = 1.0 / lmm;
+    inv_d = (lane == m) ? inv : inv_d;
+    r[m] = (lane == m) ? lmm : ((lane > m) ? acc * inv : r[m]);
+    A[lane * ld + m] = r[m];
+    __syncwarp();
+  }
+  invd[lane] = inv_d;
+  return spd;
+}
+
+// B := B L^{-T} for an off-diagonal tile B of the panel of the factored L.
+__device__ void tile_trsm(const double* Lkk, int ld, const double* invd, double* B, int lane) {
+  double r[32];
+  load_row(r, B + lane * ld);
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    double a4[4] = {r[m], 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], Lkk[m * ld + p], a4[p & 3]);
+    r[m] = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * invd[m];
+  }
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(B + lane * ld + j) = make_double2(r[j], r[j + 1]);
+}
+
+// C -= A B^T (32x32 tiles). On a diagonal tile only the lower triangle is
+// written back (the strict upper triangle holds M).
+__device__ void tile_gemm(double* C, const double* A, const double* Bt, int ld, bool diag, int lane) {
+  double r[32];
+  load_row(r, C + lane * ld);
+#pragma unroll 1
+  for (int p = 0; p < 32; p += 2) {
+    const double2 a = *reinterpret_cast<const double2*>(A + lane * ld + p);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 b = *reinterpret_cast<const double2*>(Bt + j * ld + p);
+      r[j] = fma(-a.x, b.x, r[j]);
+      r[j] = fma(-a.y, b.y, r[j]);
+    }
+  }
+  double* row = C + lane * ld;
+  if (diag) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j <= lane) row[j] = r[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(row + j) = make_double2(r[j], r[j + 1]);
+  }
+}
+
+// (L L^T) v = v in place, one warp. L: lower triangle of the padded matrix.
+__device__ void warp_llt_solve(const double* Mb, int ld, int np, const double* invd, double* v, int lane) {
+  double r[32];
+  // forward: L y = v
+  for (int I = 0; I < np; ++I) {
+    double acc = v[32 * I + lane];
+    for (int K = 0; K < I; ++K) {
+      const double* a = Mb + (size_t)(32 * I + lane) * ld + 32 * K;
+      const double* y = v + 32 * K;
+#pragma unroll 8
+      for (int p = 0; p < 32; p += 2) {
+        const double2 av = *reinterpret_cast<const double2*>(a + p);
+        const double2 yv = *reinterpret_cast<const double2*>(y + p);
+        acc = fma(-av.x, yv.x, acc);
+        acc = fma(-av.y, yv.y, acc);
+      }
+    }
+    load_row(r, Mb + (size_t)(32 * I + lane) * ld + 32 * I);
+    const double id = invd[32 * I + lane];
+    double yo = 0.0;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      const double ym = __shfl_sync(0xffffffffu, acc * id, m);
+      yo = (lane == m) ? ym : yo;
+      acc = (lane > m) ? fma(-r[m], ym, acc) : acc;
+    }
+    v[32 * I + lane] = yo;
+    __syncwarp();
+  }
+  // backward: L^T x = y
+  for (int I = np - 1; I >= 0; --I) {
+    double acc = v[32 * I + lane];
+    for (int J = I + 1; J < np; ++J) {
+      const double* col = Mb + (size_t)(32 * J) * ld + 32 * I + lane;
+      const double* x = v + 32 * J;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) acc = fma(-col[(size_t)j * ld], x[j], acc);
+    }
+    const double* dt = Mb + (size_t)(32 * I) * ld + 32 * I + lane;
+    const double id = invd[32 * I + lane];
+    double xo = 0.0;
+#pragma unroll
+    for (int m = 31; m >= 0; --m) {
+      const double xm = __shfl_sync(0xffffffffu, acc * id, m);
+      xo = (lane == m) ? xm : xo;
+      acc = (lane < m) ? fma(-dt[(size_t)m * ld], xm, acc) : acc;
+    }
+    v[32 * I + lane] = xo;
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
 template <bool SMEM>
-__global__ void __launch_bounds__(256) jsiia_cta_kernel(ModelView mv, BatchIO io, double* __restrict__ gws, int lpt,
-                                                         int64_t p_off) {
-  extern __shared__ double dyn_smem[];
+__global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO io, double* __restrict__ gws,
+                                                           int64_t p_off) {
+  extern __shared__ __align__(16) double dyn_smem[];
   __shared__ ScanSmem scan_sm;
   __shared__ BlockReduce br;
   __shared__ int s_fail;
   const int n = mv.n;
+  const JstLayout L = jst_layout(n);
   const int64_t p = p_off + blockIdx.x;
   const int64_t mc = mv.model_of(p);
-  double* ws = SMEM ? dyn_smem : gws + (int64_t)blockIdx.x * jsi_workspace_doubles(n);
-  const int t = threadIdx.x, nt = blockDim.x;
+  double* ws = SMEM ? dyn_smem : gws + (int64_t)blockIdx.x * L.total;
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5, nw = nt >> 5;
+  const int lpt = (n + nt - 1) / nt;
   const int i0 = t * lpt, i1 = min(n, i0 + lpt);
   if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) {
     if (t == 0) model_rejected(mv, io, p, mc);
     return;
   }
   if (t == 0) s_fail = 0;
-  const int ld = jsi_ld(n);
-  double* vec = ws + jsi::FIELDS * n;
-  double* M = ws + (jsi::FIELDS + jsi::NVEC) * n;  // column-major, M[j*ld + i] = M_ij
+  const int np = L.np, npad = L.npad, ld = L.ld;
+  double* Mb = ws + L.m_off;
+  double* vx = ws + L.v_off;
+  double* vw = vx + npad;
+  double* dg = vw + npad;
+  double* invd = dg + npad;
+  auto tile = [&](int I, int J) { return Mb + (size_t)(32 * I) * ld + 32 * J; };
 
-  // ---- kinematics + torque surplus ----------------------------------------
-  const IdFields idf{jsi::REL, jsi::X, jsi::V, jsi::TMP, jsi::TD};
+  // ---- kinematics + torque surplus ------------------------------------------
+  const IdFields idf{jst::REL, jst::X, jst::V, jst::TMP, jst::TD};
   cta_kinematics(mv, io, p, mc, ws, idf, lpt);
   cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);
 
-  // ---- composite inertias in base coordinates -------------------------------
+  // ---- composite inertias in base coordinates ---------------------------------
   for (int i = i0; i < i1; ++i) {
-    const SE3d X = ws_get_se3(ws, n, jsi::X, i);
-    const Sym6 Jb = sym6_congruence(inertia_sym6(mv.inertia(i, mc)), X);
+    const SE3d X = ws_get_se3(ws, n, jst::X, i);
+    const Sym6 Jb = inertia_sym6(inertia_to_base(mv.inertia(i, mc), X));
 #pragma unroll
-    for (int k = 0; k < 6; ++k) ws[(jsi::IC + k) * n + i] = Jb.A[k];
+    for (int k = 0; k < 6; ++k) ws[(jst::IC + k) * n + i] = Jb.A[k];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) ws[(jsi::IC + 6 + k) * n + i] = Jb.B[k];
+    for (int k = 0; k < 9; ++k) ws[(jst::IC + 6 + k) * n + i] = Jb.B[k];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) ws[(jsi::IC + 15 + k) * n + i] = Jb.D[k];
-    ws_put_sv(ws, n, jsi::SB, i, adinv_apply(X, mv.screw(i, mc)));
+    for (int k = 0; k < 6; ++k) ws[(jst::IC + 15 + k) * n + i] = Jb.D[k];
+    ws_put_sv(ws, n, jst::S0, i, adinv_apply(X, mv.screw(i, mc)));
   }
   __syncthreads();
-  ws_scan<12, true>(ws, n, jsi::IC, lpt, AddOp{}, scan_sm);
+  ws_scan<12, true>(ws, n, jst::IC, lpt, AddOp{}, scan_sm);
   __syncthreads();
-  ws_scan<9, true>(ws, n, jsi::IC + 12, lpt, AddOp{}, scan_sm);
+  ws_scan<9, true>(ws, n, jst::IC + 12, lpt, AddOp{}, scan_sm);
   __syncthreads();
   for (int i = i0; i < i1; ++i) {
     Sym6 Ic;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) Ic.A[k] = ws[(jsi::IC + k) * n + i];
+    for (int k = 0; k < 6; ++k) Ic.A[k] = ws[(jst::IC + k) * n + i];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Ic.B[k] = ws[(jsi::IC + 6 + k) * n + i];
+    for (int k = 0; k < 9; ++k) Ic.B[k] = ws[(jst::IC + 6 + k) * n + i];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) Ic.D[k] = ws[(jsi::IC + 15 + k) * n + i];
-    ws_put_sv(ws, n, jsi::FB, i, sym6_apply(Ic, ws_get_sv(ws, n, jsi::SB, i)));
+    for (int k = 0; k < 6; ++k) Ic.D[k] = ws[(jst::IC + 15 + k) * n + i];
+    ws_put_sv(ws, n, jst::FB, i, sym6_apply(Ic, ws_get_sv(ws, n, jst::S0, i)));
   }
   __syncthreads();
 
-  // ---- M_ij = S^b_min(i,j) . F^b_max(i,j) ------------------------------------
-  for (int j = t; j < n; j += nt) {
-    const Sv Sj = ws_get_sv(ws, n, jsi::SB, j);
-    const Sv Fj = ws_get_sv(ws, n, jsi::FB, j);
-    for (int i = 0; i < n; ++i) {
-      const double mij = (i <= j) ? dot(ws_get_sv(ws, n, jsi::SB, i), Fj) : dot(Sj, ws_get_sv(ws, n, jsi::FB, i));
-      M[j * ld + i] = mij;
+  // ---- M_ij = S0_min(i,j) . FB_max(i,j), identity padding ---------------------
+  for (int J = 0; J < np; ++J) {
+    const int j = 32 * J + lane;
+    const bool jr = j < n;
+    const Sv Sj = jr ? ws_get_sv(ws, n, jst::S0, j) : svzero();
+    const Sv Fj = jr ? ws_get_sv(ws, n, jst::FB, j) : svzero();
+    for (int i = warp; i < npad; i += nw) {
+      double mij;
+      if (i < n && jr) {
+        const bool low = j <= i;  // lower: S0_j . FB_i, upper: S0_i . FB_j
+        const Sv c = low ? Sj : Fj;
+        const Sv rv = ws_get_sv(ws, n, low ? jst::FB : jst::S0, i);
+        mij = dot(c, rv);
+      } else {
+        mij = (i == j) ? 1.0 : 0.0;
+      }
+      Mb[(size_t)i * ld + j] = mij;
+      if (i == j) dg[i] = mij;
     }
-    vec[jsi::VEC_DG * n + j] = M[j * ld + j];
-    vec[jsi::VEC_X * n + j] = ws[jsi::TD * n + j];  // rhs
   }
+  for (int i = t; i < npad; i += nt) vx[i] = (i < n) ? ws[jst::TD * n + i] : 0.0;
   __syncthreads();
 
-  // ---- Cholesky (right-looking, lower triangle) -----------------------------
-  for (int k = 0; k < n; ++k) {
-    const double piv = M[k * ld + k];
-    if (!(piv > 0.0)) {
-      if (t == 0) s_fail = 1;
+  // ---- blocked Cholesky, right-looking by 32-column panels -------------------
+  for (int K = 0; K < np; ++K) {
+    if (warp == 0) {
+      const bool ok = tile_potrf(tile(K, K), ld, invd + 32 * K, lane);
+      if (!ok && lane == 0) s_fail = 1;
     }
-    const double lkk = sqrt(piv);
-    const double inv = 1.0 / lkk;
-    for (int i = k + 1 + t; i < n; i += nt) M[k * ld + i] *= inv;
     __syncthreads();
-    if (t == 0) M[k * ld + k] = lkk;
-    for (int j = k + 1 + t; j < n; j += nt) {
-      const double ljk = M[k * ld + j];
-      for (int i = j; i < n; ++i) M[j * ld + i] = fma(-M[k * ld + i], ljk, M[j * ld + i]);
+    if (s_fail) break;  // forward_dynamics.cpp:93-98 (CTA-uniform)
+    for (int I = K + 1 + warp; I < np; I += nw) tile_trsm(tile(K, K), ld, invd + 32 * K, tile(I, K), lane);
+    __syncthreads();
+    const int m = np - 1 - K;  // trailing tiles (I, J), K < J <= I
+    const int tasks = m * (m + 1) / 2;
+    for (int q = warp; q < tasks; q += nw) {
+      // row-major enumeration of the lower triangle: q -> (a, b), b <= a
+      int a = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+      while ((a + 1) * (a + 2) / 2 <= q) ++a;
+      while (a * (a + 1) / 2 > q) --a;
+      const int b = q - a * (a + 1) / 2;
+      const int I = K + 1 + a, J = K + 1 + b;
+      tile_gemm(tile(I, J), tile(I, K), tile(J, K), ld, I == J, lane);
     }
     __syncthreads();
   }
-  if (s_fail) {  // forward_dynamics.cpp:93-98
+  if (s_fail) {
     if (t == 0) {
       io.status[p] = PD_SLOT_JSI_NOT_SPD;
       io.eround[p] = 0;
@@ -166,25 +332,20 @@ __global__ void __launch_bounds__(256) jsiia_cta_kernel(ModelView mv, BatchIO io
   }
 
   // ---- solve + residual contract (forward_dynamics.cpp:99-116) --------------
-  double* xv = vec + jsi::VEC_X * n;
-  double* rv = vec + jsi::VEC_R * n;
-  double* dg = vec + jsi::VEC_DG * n;
-  double* dv = vec + jsi::VEC_D * n;
-  cta_llt_solve(ws, n, M, ld, xv);
+  if (warp == 0) warp_llt_solve(Mb, ld, np, invd, vx, lane);
   double sq = 0.0;
-  for (int i = t; i < n; i += nt) sq = fma(ws[jsi::TD * n + i], ws[jsi::TD * n + i], sq);
-  const double scale = fmax(sqrt(block_sum(sq, br)), 2.2250738585072014e-308);
+  for (int i = t; i < n; i += nt) sq = fma(ws[jst::TD * n + i], ws[jst::TD * n + i], sq);
+  const double scale = fmax(sqrt(block_sum(sq, br)), 2.2250738585072014e-308);  // block_sum syncs
   int code = PD_SLOT_OK;
   for (int pass = 0; pass < 2; ++pass) {
     double rr = 0.0;
-    for (int i = t; i < n; i += nt) {
-      double s = ws[jsi::TD * n + i];
-      for (int j = 0; j < n; ++j) {
-        const double mij = (i < j) ? M[j * ld + i] : ((i > j) ? M[i * ld + j] : dg[i]);
-        s = fma(-mij, xv[j], s);
-      }
-      rv[i] = s;
-      dv[i] = s;
+    for (int i = t; i < npad; i += nt) {
+      // (M x)_i from the saved diagonal and the untouched strict upper triangle
+      double s = (i < n) ? ws[jst::TD * n + i] : 0.0;
+      s = fma(-dg[i], vx[i], s);
+      for (int j = 0; j < i; ++j) s = fma(-Mb[(size_t)j * ld + i], vx[j], s);
+      for (int j = i + 1; j < npad; ++j) s = fma(-Mb[(size_t)i * ld + j], vx[j], s);
+      vw[i] = s;
       rr = fma(s, s, rr);
     }
     const double rn = sqrt(block_sum(rr, br));
@@ -193,11 +354,12 @@ __global__ void __launch_bounds__(256) jsiia_cta_kernel(ModelView mv, BatchIO io
       code = PD_SLOT_JSI_REFINE_FAILED;
       break;
     }
-    cta_llt_solve(ws, n, M, ld, dv);
-    for (int i = t; i < n; i += nt) xv[i] += dv[i];
+    if (warp == 0) warp_llt_solve(Mb, ld, np, invd, vw, lane);
+    __syncthreads();
+    for (int i = t; i < npad; i += nt) vx[i] += vw[i];
     __syncthreads();
   }
-  for (int i = t; i < n; i += nt) io.put_qdd(i, p, xv[i]);
+  for (int i = t; i < n; i += nt) io.put_qdd(i, p, vx[i]);
   if (t == 0) {
     io.status[p] = code;
     io.eround[p] = 0;
@@ -205,21 +367,31 @@ __global__ void __launch_bounds__(256) jsiia_cta_kernel(ModelView mv, BatchIO io
   }
 }
 
-size_t jsiia_workspace_bytes(int n) { return jsi_workspace_doubles(n) * sizeof(double); }
+// Warps per CTA: one for two panels or fewer (the tile tasks of a step are
+// serial there); otherwise enough to cover a panel step's trailing update,
+// fewer when the batch alone fills the GPU.
+int jsiia_warps(int n, int64_t batch, int sm_count) {
+  const int np = (n + 31) / 32;
+  if (np <= 2) return 1;
+  const int tiles = np * (np - 1) / 2;
+  if (batch >= 4 * (int64_t)sm_count) return np <= 4 ? 2 : 4;
+  return tiles < 8 ? tiles : 8;
+}
 
-void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s) {
+bool jsiia_smem_path(int n) { return jsiia_workspace_bytes(n) <= 200 * 1024; }
+
+void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count,
+                  cudaStream_t s) {
   const int n = mv.n;
-  int nt = ((n + 31) / 32) * 32;
-  if (nt > 256) nt = 256;
-  const int lpt = (n + nt - 1) / nt;
+  const int nt = 32 * jsiia_warps(n, io.B, sm_count);
   const size_t ws_bytes = jsiia_workspace_bytes(n);
-  if (ws_bytes <= 220 * 1024) {
-    cudaFuncSetAttribute(jsiia_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
-    jsiia_cta_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, lpt, 0);
+  if (jsiia_smem_path(n)) {
+    cudaFuncSetAttribute(jsiia_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
+    jsiia_tiled_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, 0);
   } else {
     for (int64_t b0 = 0; b0 < io.B; b0 += gws_slots) {
       const int64_t nb = (io.B - b0 < gws_slots) ? io.B - b0 : gws_slots;
-      jsiia_cta_kernel<false><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, lpt, b0);
+      jsiia_tiled_kernel<false><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, b0);
     }
   }
 }

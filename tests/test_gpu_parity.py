@@ -129,7 +129,7 @@ def test_deterministic(oracle, gpu_ctx, algo):
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("algo", [pd.FdAlgo.abia, pd.FdAlgo.cfa])
+@pytest.mark.parametrize("algo", ALGOS)
 def test_c4_single_1024_link_chain(oracle, gpu_ctx, algo):
     """configs[3]: one 1,024-link chain (CTA-parallel variants, L2 workspace)."""
     n = 1024
@@ -153,4 +153,18 @@ def test_abia_cta_path(oracle, gpu_ctx, n, B):
     qdd, st, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
     assert (st == 0).all()
     ref, _ = oracle.batch_forward_dynamics("abia", links, [0, 0, -9.81], q, qd, tau)
+    assert max(rel_gap(qdd[b], ref[b]) for b in range(B)) <= TOL
+
+
+@pytest.mark.parametrize("n,B", [(33, 5), (64, 600), (96, 600), (130, 2), (160, 1)])
+def test_jsiia_tiled_paths(oracle, gpu_ctx, n, B):
+    """n > 32: CTA-per-chain blocked Cholesky (1, 2 or more warps per CTA; M in
+    shared memory up to n ~ 150, in a global slot above)."""
+    cell = oracle.workload_seed(7, n, B)
+    links = oracle.workload_chains(cell, n, B)
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    gpu_ctx.set_models(links, None)
+    qdd, st, _, _ = gpu_ctx.solve(pd.FdAlgo.jsiia, q, qd, tau)
+    assert (st == 0).all()
+    ref, _ = oracle.batch_forward_dynamics("jsiia", links, [0, 0, -9.81], q, qd, tau)
     assert max(rel_gap(qdd[b], ref[b]) for b in range(B)) <= TOL
