@@ -86,7 +86,7 @@ __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
 // compute it ahead (software pipelining across links).
 __device__ __forceinline__ void abia_pass_a(AbiaState& st, const SE3d& rel, const Sv& S, double qd) {
   st.X = compose(rel, st.X);
-  const Sv S0 = adinv_apply(st.X, S);
+  const Sv S0 = adinv_screw(st.X, S);
   st.V0 = svfma(qd, S0, st.V0);
   st.A0 = adv_acc(st.V0, qd * S0, st.A0);
 }
@@ -95,7 +95,7 @@ __device__ __forceinline__ void abia_pass_a(AbiaState& st, const SE3d& rel, cons
 // inertia, z sweep and u; writes the 13-double record; steps back to link i-1.
 __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const SE3d& rel, const Sv& S, double qd,
                                             const Inertia& Jl, double tau, double rec[kRec]) {
-  const Sv S0 = adinv_apply(st.X, S);
+  const Sv S0 = adinv_screw(st.X, S);
   const Inertia J0 = inertia_to_base(Jl, st.X);
   // link wrench, bias torque                      inverse_dynamics.cpp:103-112,146-150
   const Sv h = inertia_apply(J0, st.V0);

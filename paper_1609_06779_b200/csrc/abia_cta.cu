@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) abia_cta_kernel(ModelView mv, BatchIO io,
 
   for (int i = i0; i < i1; ++i) {
     const SE3d Xi = ws_get_se3(ws, n, abc::X, i);
-    ws_put_sv(ws, n, abc::S0, i, adinv_apply(Xi, mv.screw(i, mc)));
+    ws_put_sv(ws, n, abc::S0, i, adinv_screw(Xi, mv.screw(i, mc)));
     const Sym6 J = inertia_sym6(inertia_to_base(mv.inertia(i, mc), Xi));
 #pragma unroll
     for (int k = 0; k < 6; ++k) ws[(abc::J0 + k) * n + i] = J.A[k];

@@ -134,7 +134,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Pass A stores sin/cos of each joint angle for pass B (one sincos per link);
 // the last KSTAGES links of pass A, whose pass-B loads are issued before pass A
 // reaches them, keep theirs in registers.
-template <int KSTAGES, int MINB, bool HINTS, int KT>
+template <int KSTAGES, int MINB, int HINTS, int KT>
 __global__ void __launch_bounds__(KT, MINB)
     abia_tma_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
                     int64_t scr_ld) {
@@ -167,11 +167,17 @@ __global__ void __launch_bounds__(KT, MINB)
     const int s = k % KSTAGES;
     double* dst = ring + (size_t)s * kStageFields * KT;
     uint64_t* bar = &full[s];
-    if (k < n) {  // re-read in pass B: default policy
+    if (k < n) {  // re-read in pass B: default policy, or evict_last (HINTS & 2)
       mbar_expect_tx(bar, (18 + 2) * KT * 8);
-      tma_3d(dst + 10 * KT, &maps.model_kin, c0, k, 10, bar);
-      tma_2d(dst + kQ * KT, &maps.q, c0, k, bar);
-      tma_2d(dst + kQD * KT, &maps.qd, c0, k, bar);
+      if (HINTS & 2) {
+        tma_3d_hint(dst + 10 * KT, &maps.model_kin, c0, k, 10, bar, pol_last);
+        tma_2d_hint(dst + kQ * KT, &maps.q, c0, k, bar, pol_last);
+        tma_2d_hint(dst + kQD * KT, &maps.qd, c0, k, bar, pol_last);
+      } else {
+        tma_3d(dst + 10 * KT, &maps.model_kin, c0, k, 10, bar);
+        tma_2d(dst + kQ * KT, &maps.q, c0, k, bar);
+        tma_2d(dst + kQD * KT, &maps.qd, c0, k, bar);
+      }
     } else if (k < 2 * n) {  // last use of the model
       const int i = 2 * n - 1 - k;
       mbar_expect_tx(bar, (28 + 5) * KT * 8);
@@ -184,8 +190,13 @@ __global__ void __launch_bounds__(KT, MINB)
         tma_2d(dst + kTAU * KT, &maps.tau, c0, i, bar);
         tma_2d(dst + kSIN * KT, &maps.sc, c0, 2 * i, bar);
       }
-      tma_2d(dst + kQ * KT, &maps.q, c0, i, bar);
-      tma_2d(dst + kQD * KT, &maps.qd, c0, i, bar);
+      if (HINTS & 2) {  // last use of q, qd: demote
+        tma_2d_hint(dst + kQ * KT, &maps.q, c0, i, bar, pol_first);
+        tma_2d_hint(dst + kQD * KT, &maps.qd, c0, i, bar, pol_first);
+      } else {
+        tma_2d(dst + kQ * KT, &maps.q, c0, i, bar);
+        tma_2d(dst + kQD * KT, &maps.qd, c0, i, bar);
+      }
     } else {
       const int i = k - 2 * n;
       mbar_expect_tx(bar, kRec * KT * 8);
@@ -293,6 +304,187 @@ __global__ void __launch_bounds__(KT, MINB)
       if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
     }
     after_step(k);
+  }
+  if (live) {
+    const int32_t ms = __ldg(mv.mstatus + mc);
+    io.status[p] = ms != PD_SLOT_OK ? ms : st.code;
+    io.eround[p] = 0;
+    io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : st.eidx;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ring-buffer variant: same three passes and arithmetic, but the stages are
+// sized per pass (pass A 20 rows, pass B 31, pass C 13; a row = one field of
+// the KT-chain tile) in one shared-memory byte ring, so the cheap passes run
+// many links ahead (up to kSlots steps in flight) instead of a fixed
+// 3-stage depth. Pass B recomputes the joint sin/cos instead of reading them
+// back (no scratch round trip, no register hand-off of the last links).
+// Thread 0 is the producer; it never blocks on a stage it does not need yet:
+// before consuming step k it issues up to k (blocking reclaims), after each
+// step it issues further ahead only while slots are free (non-blocking).
+constexpr int kSlots = 16;
+constexpr int kRowsA = 20, kRowsB = 31, kRowsC = kRec;
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(saddr(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
+template <int KT>
+__device__ __forceinline__ Sv row_screw(const double* f, int r0) {
+  return {mk(f[r0 * KT], f[(r0 + 1) * KT], f[(r0 + 2) * KT]), mk(f[(r0 + 3) * KT], f[(r0 + 4) * KT], f[(r0 + 5) * KT])};
+}
+// rows r0.. = screw (6), home R (9), home p (3): the F_SCREW..F_HP block
+template <int KT>
+__device__ __forceinline__ SE3d row_rel(const double* f, int r0, const Sv& S, double q, double st, double ct) {
+  Mat3d HR;
+#pragma unroll
+  for (int j = 0; j < 9; ++j) HR.m[j] = f[(r0 + 6 + j) * KT];
+  return joint_transform_sc(S, HR, mk(f[(r0 + 15) * KT], f[(r0 + 16) * KT], f[(r0 + 17) * KT]), q, st, ct);
+}
+
+template <int KT, int MINB, bool KEEP_A>
+__global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32, MINB)
+    abia_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
+                     int64_t scr_ld, uint32_t cap_rows) {
+  static_assert(KT % 16 == 0, "ring rows must stay 128-byte aligned for TMA");
+  extern __shared__ __align__(128) double ring[];  // cap_rows x KT doubles
+  __shared__ __align__(8) uint64_t full[kSlots];
+  __shared__ __align__(8) uint64_t empty[kSlots];
+  constexpr int NW = (KT + 31) / 32;  // consumer warps; warp NW is the producer
+  const int t = threadIdx.x, lane = t & 31;
+  const int n = mv.n;
+  const int c0 = blockIdx.x * KT;
+  const int total = 3 * n;
+  if (t == 0) {
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  auto rows_of = [&](int k) -> uint32_t { return k < n ? kRowsA : (k < 2 * n ? kRowsB : kRowsC); };
+  auto start_of = [&](uint32_t v, uint32_t rows) -> uint32_t {
+    const uint32_t o = v % cap_rows;
+    return o + rows > cap_rows ? v + (cap_rows - o) : v;
+  };
+  if (t >= NW * 32) {  // ---- producer warp: one elected lane issues every step in order
+    if (lane == 0) {
+      uint32_t vst[kSlots];
+      uint32_t pv = 0;
+      int old = 0;
+      for (int k = 0; k < total; ++k) {
+        const uint32_t rows = rows_of(k);
+        const uint32_t st = start_of(pv, rows);
+        // free the slot, the ring bytes, and (pass C) every pass-B step
+        while (k - old >= kSlots || (old < k && st + rows - vst[old % kSlots] > cap_rows) ||
+               (k >= 2 * n && old < 2 * n)) {
+          mbar_wait(&empty[old % kSlots], (uint32_t)((old / kSlots) & 1));
+          ++old;
+        }
+        double* dst = ring + (size_t)(st % cap_rows) * KT;
+        uint64_t* bar = &full[k % kSlots];
+        if (k < n) {  // pass A: kin rows 0..17, q 18, qd 19
+          mbar_expect_tx(bar, kRowsA * KT * 8);
+          if (KEEP_A) {
+            tma_3d_hint(dst, &maps.model_kin, c0, k, F_SCREW, bar, pol_last);
+            tma_2d_hint(dst + 18 * KT, &maps.q, c0, k, bar, pol_last);
+            tma_2d_hint(dst + 19 * KT, &maps.qd, c0, k, bar, pol_last);
+          } else {
+            tma_3d(dst, &maps.model_kin, c0, k, F_SCREW, bar);
+            tma_2d(dst + 18 * KT, &maps.q, c0, k, bar);
+            tma_2d(dst + 19 * KT, &maps.qd, c0, k, bar);
+          }
+        } else if (k < 2 * n) {  // pass B: model rows 0..27, q 28, qd 29, tau 30 (last use)
+          const int i = 2 * n - 1 - k;
+          mbar_expect_tx(bar, kRowsB * KT * 8);
+          tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
+          tma_2d_hint(dst + 28 * KT, &maps.q, c0, i, bar, pol_first);
+          tma_2d_hint(dst + 29 * KT, &maps.qd, c0, i, bar, pol_first);
+          tma_2d_hint(dst + 30 * KT, &maps.tau, c0, i, bar, pol_first);
+        } else {  // pass C: records of link i
+          const int i = k - 2 * n;
+          mbar_expect_tx(bar, kRowsC * KT * 8);
+          tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
+        }
+        vst[k % kSlots] = st;
+        pv = st + rows;
+      }
+    }
+    return;
+  }
+  const int64_t p = (int64_t)c0 + t;
+  const bool live = t < KT && p < io.B;  // lanes past KT (partial last warp) only keep the warp convergent
+  uint32_t cv = 0;  // consumer's virtual ring position (mirrors the producer's)
+  auto acquire = [&](int k) -> const double* {
+    const uint32_t st = start_of(cv, rows_of(k));
+    cv = st + rows_of(k);
+    mbar_wait(&full[k % kSlots], (uint32_t)((k / kSlots) & 1));
+    return ring + (size_t)(st % cap_rows) * KT + (t < KT ? t : 0);
+  };
+  auto release = [&](int k) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[k % kSlots]);
+  };
+
+  const int64_t mc = live ? mv.model_of(p) : 0;
+  AbiaState st;
+  abia_init(st, live ? mv.gravity(mc) : mk(0, 0, 0));
+  int k = 0;
+  for (; k < n; ++k) {  // pass A
+    const double* f = acquire(k);
+    const Sv S = row_screw<KT>(f, 0);
+    const double q = f[18 * KT];
+    double sn, cs;
+    joint_angle_sincos(S, q, &sn, &cs);
+    abia_pass_a(st, row_rel<KT>(f, 0, S, q, sn, cs), S, f[19 * KT]);
+    release(k);
+  }
+  for (; k < 2 * n; ++k) {  // pass B
+    const double* f = acquire(k);
+    const int i = 2 * n - 1 - k;
+    const Sv S = row_screw<KT>(f, F_SCREW);
+    const double q = f[28 * KT];
+    double sn, cs;
+    joint_angle_sincos(S, q, &sn, &cs);
+    Inertia J;
+    J.m = f[F_MASS * KT];
+    J.c = mk(f[F_COM * KT], f[(F_COM + 1) * KT], f[(F_COM + 2) * KT]);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
+    double rec[kRec];
+    abia_pass_b(st, i, n, row_rel<KT>(f, F_SCREW, S, q, sn, cs), S, f[29 * KT], J, f[30 * KT], rec);
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < kRec; ++j) st_hint(scratch + ((int64_t)i * kRec + j) * scr_ld + p, rec[j], pol_last);
+    }
+    if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
+    release(k);
+  }
+  for (; k < total; ++k) {  // pass C
+    const double* f = acquire(k);
+    const int i = k - 2 * n;
+    double rec[kRec];
+#pragma unroll
+    for (int j = 0; j < kRec; ++j) rec[j] = f[j * KT];
+    const double qdd = abia_pass_c(st, rec);
+    if (live) io.put_qdd(i, p, qdd);
+    if (KT % 16 == 0 && t < kRec * (KT / 16)) {  // drop the dead records' L2 lines without write-back
+      const int row = t / (KT / 16), seg = t % (KT / 16);
+      const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
+      if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
+    }
+    release(k);
   }
   if (live) {
     const int32_t ms = __ldg(mv.mstatus + mc);
@@ -410,7 +602,7 @@ __global__ void __launch_bounds__(kT, 3)
     joint_angle_sincos(S, f[kQ * kT], &sn, &cs);
     const SE3d rel = stage_rel(f, sn, cs);
     X = compose(rel, X);
-    const Sv S0 = adinv_apply(X, S);
+    const Sv S0 = adinv_screw(X, S);
     const double qd = f[kQD * kT];
     V0 = svfma(qd, S0, V0);
     A0 = adv_acc(V0, qd * S0, A0);
@@ -447,7 +639,7 @@ __global__ void __launch_bounds__(kT, 3)
     const Sv S = stage_screw(f);
     const double qd = f[kQD * kT];
     const SE3d rel = stage_rel(f, sn, cs);
-    const Sv S0 = adinv_apply(X, S);
+    const Sv S0 = adinv_screw(X, S);
     Inertia Jl;
     Jl.m = f[F_MASS * kT];
     Jl.c = mk(f[F_COM * kT], f[(F_COM + 1) * kT], f[(F_COM + 2) * kT]);
@@ -698,7 +890,29 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
     };
     v = waste(224) < waste(256) ? 4 : 0;
   }
-  const uint32_t kt = (v == 4) ? 224u : 128u;
+  if (v >= 10) {
+    // ring kernels: (tile, CTAs per SM) per variant; the ring takes the SM's shared memory
+    const uint32_t kt = v == 12 ? 224u : (v == 13 ? 112u : (v == 14 ? 96u : (v == 15 ? 64u : 128u)));
+    const int ctas = v == 13 ? 2 : (v == 14 ? 2 : (v == 15 ? 3 : 1));
+    Maps maps;
+    if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
+    const size_t smem = (size_t)(220 * 1024 / ctas) / (kt * 8) * (kt * 8);
+    const uint32_t cap_rows = (uint32_t)(smem / (kt * 8));
+    auto go = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kernel<<<(unsigned)((io.B + kt - 1) / kt), (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
+    };
+    switch (v) {
+      case 11: go(abia_ring_kernel<128, 1, true>); break;
+      case 12: go(abia_ring_kernel<224, 1, false>); break;
+      case 13: go(abia_ring_kernel<112, 2, false>); break;
+      case 14: go(abia_ring_kernel<96, 2, false>); break;
+      case 15: go(abia_ring_kernel<64, 3, false>); break;
+      default: go(abia_ring_kernel<128, 1, false>); break;
+    }
+    return true;
+  }
+  const uint32_t kt = (v == 4 || v == 5) ? 224u : (v == 9 ? 96u : 128u);
   Maps maps;
   if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
   auto go = [&](auto kernel, int stages) {
@@ -707,11 +921,17 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
     kernel<<<(unsigned)((io.B + kt - 1) / kt), kt, smem, s>>>(maps, mv, io, scratch, scr_ld);
   };
   switch (v) {
-    case 1: go(abia_tma_kernel<2, 3, true, 128>, 2); break;
-    case 2: go(abia_tma_kernel<3, 2, false, 128>, 3); break;
+    case 1: go(abia_tma_kernel<2, 3, 1, 128>, 2); break;
+    case 2: go(abia_tma_kernel<3, 2, 0, 128>, 3); break;
     case 3: go(abia_tma_tmem_kernel, 2); break;
-    case 4: go(abia_tma_kernel<3, 1, true, 224>, 3); break;
-    default: go(abia_tma_kernel<3, 2, true, 128>, 3); break;
+    case 4: go(abia_tma_kernel<3, 1, 1, 224>, 3); break;
+    // L2-retention experiments: pass-A model loads evict_last, demoted by pass B
+    case 5: go(abia_tma_kernel<3, 1, 3, 224>, 3); break;
+    case 6: go(abia_tma_kernel<3, 1, 3, 128>, 3); break;
+    case 7: go(abia_tma_kernel<3, 2, 3, 128>, 3); break;
+    case 8: go(abia_tma_kernel<3, 1, 1, 128>, 3); break;
+    case 9: go(abia_tma_kernel<3, 1, 3, 96>, 3); break;
+    default: go(abia_tma_kernel<3, 2, 1, 128>, 3); break;
   }
   return true;
 }

@@ -26,6 +26,7 @@ void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t g
                   cudaStream_t s);
 bool jsiia_smem_path(int n);
 bool launch_jsiia_warp(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
+bool launch_jsiia_dmma(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
 size_t jsiia_workspace_bytes(int n);
 }  // namespace pd
 
@@ -68,6 +69,10 @@ struct pd_ctx {
   bool model_cl_valid = false;
   // scratch
   DevBuf abia_scratch, cta_ws, slots, io_q, io_qd, io_tau, io_qdd, io_status;
+  // host-buffer path: copy-in / copy-out streams and per-chunk events
+  static constexpr int kMaxChunks = 8;
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
   int64_t launches = 0;
   std::string last_error;
 };
@@ -85,7 +90,62 @@ pd_status cuda_fail(pd_ctx* c, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
   } while (0)
 
-// raw [M][n][31] -> packed SoA [F_COUNT][n][M]; gravity [M][3] -> [3][M]
+// Joint-aligned link frames. Link i's coordinates are re-expressed in a
+// rotated frame F'_i = Q_i F_i (same origin) chosen so that its screw reads
+// S' = Ad(Q_i) S = (0, 0, |w|, v'x, 0, v'z): z' along the rotation axis (or
+// along v for a pure prismatic screw) and x' along the part of v normal to
+// it. The chain is physically unchanged: rel'_i = Q_i rel_i Q_{i-1}^T with
+// home' = (Q_i R_h Q_{i-1}^T, Q_i p_h), com' = Q_i c, Ic' = Q_i Ic Q_i^T, and
+// the base frame (Q_{-1} = I, gravity) untouched. Joint-space results (qdd,
+// tau, M, lambda, traces about the link origin) are frame invariant; the
+// kernels exploit the zeros: exp(-q S') is a rotation about z plus a
+// translation in the x-z plane (pd_common.cuh joint_transform_sc).
+__device__ void joint_frame(const double* s, double Q[9], double sz[3]) {
+  const double w2 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+  const double v2 = s[3] * s[3] + s[4] * s[4] + s[5] * s[5];
+  double z[3] = {0.0, 0.0, 1.0};
+  if (w2 > 0.0) {
+    const double iw = 1.0 / sqrt(w2);
+    z[0] = s[0] * iw; z[1] = s[1] * iw; z[2] = s[2] * iw;
+  } else if (v2 > 0.0) {
+    const double iv = 1.0 / sqrt(v2);
+    z[0] = s[3] * iv; z[1] = s[4] * iv; z[2] = s[5] * iv;
+  }
+  // x': component u of v normal to z' (Gram-Schmidt twice, so x' is normal to
+  // z' to rounding even when u is small), else the world axis least aligned
+  // with z'. Either way |v'y| = |y'.u| is at rounding level and is stored as 0.
+  const double vz = z[0] * s[3] + z[1] * s[4] + z[2] * s[5];
+  double x[3] = {s[3] - vz * z[0], s[4] - vz * z[1], s[5] - vz * z[2]};
+  double x2 = x[0] * x[0] + x[1] * x[1] + x[2] * x[2];
+  if (!(x2 > 1e-280)) {
+    const int a = (fabs(z[0]) <= fabs(z[1]) && fabs(z[0]) <= fabs(z[2])) ? 0 : (fabs(z[1]) <= fabs(z[2]) ? 1 : 2);
+    x[0] = (a == 0) - z[a] * z[0]; x[1] = (a == 1) - z[a] * z[1]; x[2] = (a == 2) - z[a] * z[2];
+    x2 = x[0] * x[0] + x[1] * x[1] + x[2] * x[2];
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const double ix = 1.0 / sqrt(x2);
+    x[0] *= ix; x[1] *= ix; x[2] *= ix;
+    const double xz = x[0] * z[0] + x[1] * z[1] + x[2] * z[2];
+    x[0] -= xz * z[0]; x[1] -= xz * z[1]; x[2] -= xz * z[2];
+    x2 = x[0] * x[0] + x[1] * x[1] + x[2] * x[2];
+  }
+  {
+    const double ix = 1.0 / sqrt(x2);
+    x[0] *= ix; x[1] *= ix; x[2] *= ix;
+  }
+  const double y[3] = {z[1] * x[2] - z[2] * x[1], z[2] * x[0] - z[0] * x[2], z[0] * x[1] - z[1] * x[0]};
+  for (int k = 0; k < 3; ++k) {
+    Q[k] = x[k];
+    Q[3 + k] = y[k];
+    Q[6 + k] = z[k];
+  }
+  sz[0] = sqrt(w2);                                  // |w| (the reference's w_n)
+  sz[1] = x[0] * s[3] + x[1] * s[4] + x[2] * s[5];   // v'x
+  sz[2] = vz;                                        // v'z
+}
+
+// raw [M][n][31] -> packed SoA [F_COUNT][n][M] in joint-aligned frames;
+// gravity [M][3] -> [3][M]
 __global__ void pack_models_kernel(const double* __restrict__ raw, const double* __restrict__ graw, int n,
                                    int64_t M, int64_t ld, double* __restrict__ out, double* __restrict__ gout) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -93,18 +153,40 @@ __global__ void pack_models_kernel(const double* __restrict__ raw, const double*
   if (m >= M) return;
   const double* r = raw + ((int64_t)m * n + i) * PD_LINK_FIELDS;
   auto put = [&](int f, double v) { out[((int64_t)f * n + i) * ld + m] = v; };
+  double Q[9], Qp[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, sz[3], dummy[3];
+  joint_frame(r + 13, Q, sz);
+  if (i > 0) joint_frame(r - PD_LINK_FIELDS + 13, Qp, dummy);
   put(F_MASS, r[0]);
-  for (int k = 0; k < 3; ++k) put(F_COM + k, r[1 + k]);
-  // rotational inertia, lower triangle (what LLT / the assembled blocks read)
-  put(F_IC + 0, r[4 + 0]);
-  put(F_IC + 1, r[4 + 3]);
-  put(F_IC + 2, r[4 + 6]);
-  put(F_IC + 3, r[4 + 4]);
-  put(F_IC + 4, r[4 + 7]);
-  put(F_IC + 5, r[4 + 8]);
-  for (int k = 0; k < 6; ++k) put(F_SCREW + k, r[13 + k]);
-  for (int k = 0; k < 9; ++k) put(F_HR + k, r[19 + k]);
-  for (int k = 0; k < 3; ++k) put(F_HP + k, r[28 + k]);
+  // com' = Q c
+  for (int k = 0; k < 3; ++k) put(F_COM + k, Q[3 * k] * r[1] + Q[3 * k + 1] * r[2] + Q[3 * k + 2] * r[3]);
+  // Ic' = Q Ic Q^T from the lower triangle of Ic (what LLT / the assembled blocks read)
+  double I[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) I[3 * a + b] = a >= b ? r[4 + 3 * a + b] : r[4 + 3 * b + a];
+  double T[9];  // Q Ic
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) T[3 * a + b] = Q[3 * a] * I[b] + Q[3 * a + 1] * I[3 + b] + Q[3 * a + 2] * I[6 + b];
+  const int sidx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  for (int k = 0; k < 6; ++k) {
+    const int a = sidx[k][0], b = sidx[k][1];
+    put(F_IC + k, T[3 * a] * Q[3 * b] + T[3 * a + 1] * Q[3 * b + 1] + T[3 * a + 2] * Q[3 * b + 2]);
+  }
+  // S' = (0, 0, |w|, v'x, 0, v'z)
+  put(F_SCREW + 0, 0.0);
+  put(F_SCREW + 1, 0.0);
+  put(F_SCREW + 2, sz[0]);
+  put(F_SCREW + 3, sz[1]);
+  put(F_SCREW + 4, 0.0);
+  put(F_SCREW + 5, sz[2]);
+  // home' = (Q R_h Qp^T, Q p_h)
+  const double* Rh = r + 19;
+  double U[9];  // Q R_h
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) U[3 * a + b] = Q[3 * a] * Rh[b] + Q[3 * a + 1] * Rh[3 + b] + Q[3 * a + 2] * Rh[6 + b];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b)
+      put(F_HR + 3 * a + b, U[3 * a] * Qp[3 * b] + U[3 * a + 1] * Qp[3 * b + 1] + U[3 * a + 2] * Qp[3 * b + 2]);
+  for (int k = 0; k < 3; ++k) put(F_HP + k, Q[3 * k] * r[28] + Q[3 * k + 1] * r[29] + Q[3 * k + 2] * r[30]);
   if (i == 0)
     for (int k = 0; k < 3; ++k) gout[(int64_t)k * M + m] = graw[m * 3 + k];
 }
@@ -191,16 +273,21 @@ int link_rule(const double* r) {
   return 0;
 }
 
-ModelView model_view(const pd_ctx* c) {
+// View of models [m0, m0 + count) (count = batch of a sub-range; a shared
+// model is never offset).
+ModelView model_view(const pd_ctx* c, int64_t m0 = 0, int64_t count = -1) {
   ModelView mv;
-  mv.f = c->model.as<double>();
-  mv.g = c->gravity.as<double>();
-  mv.mstatus = c->mstatus.as<int32_t>();
-  mv.mrule = c->mrule.as<int32_t>();
+  const bool shared = c->n_models == 1;
+  if (shared) m0 = 0;
+  mv.f = c->model.as<double>() + m0;
+  mv.g = c->gravity.as<double>() + m0;
+  mv.mstatus = c->mstatus.as<int32_t>() + m0;
+  mv.mrule = c->mrule.as<int32_t>() + m0;
   mv.fcl = nullptr;
   mv.n = c->n_links;
-  mv.M = c->n_models;
+  mv.M = shared ? 1 : (count >= 0 ? count : c->n_models - m0);
   mv.ld = c->model_ld;
+  mv.gld = c->n_models;
   return mv;
 }
 
@@ -224,13 +311,15 @@ cudaError_t ensure_model_cl(pd_ctx* ctx) {
   return cudaGetLastError();
 }
 
+// Problems [m0, m0 + batch) of the model set (m0 > 0: one chunk of a larger
+// host-buffer call; the caller checked the full batch against the models).
 pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, const double* q, const double* qd,
-                     const double* tau, double* qdd, int32_t* st, int32_t* er, int32_t* ei) {
+                     const double* tau, double* qdd, int32_t* st, int32_t* er, int32_t* ei, int64_t m0 = 0) {
   if (ctx->n_models <= 0 || ctx->n_links <= 0) {
     ctx->last_error = "forward dynamics: no models set (pd_set_models)";
     return PD_INVALID_ARGUMENT;
   }
-  if (ctx->n_models != 1 && ctx->n_models != batch) {
+  if (ctx->n_models != 1 && m0 + batch > ctx->n_models) {
     ctx->last_error = "forward dynamics: batch must equal the number of models (or use one shared model)";
     return PD_INVALID_ARGUMENT;
   }
@@ -243,7 +332,8 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
     ei = er + batch;
   }
   BatchIO io{q, qd, tau, qdd, st, er, ei, batch, lds};
-  ModelView mv = model_view(ctx);
+  ModelView mv = model_view(ctx, m0, batch);
+  const size_t cl_off = ctx->n_models == 1 ? 0 : (size_t)m0 * F_COUNT * n;  // link-fastest copy offset
   switch (algo) {
     case PD_ABIA: {
       // long chains in small batches: CTA per chain (parallel kinematics and
@@ -251,7 +341,7 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       static const bool force_cta = std::getenv("PD_ABIA_CTA") != nullptr;
       if (force_cta || (n >= 64 && batch <= 2 * ctx->sm_count)) {
         PD_CUDA(ensure_model_cl(ctx));
-        mv.fcl = ctx->model_cl.as<double>();
+        mv.fcl = ctx->model_cl.as<double>() + cl_off;
         const size_t wsb = abia_cta_workspace_bytes(n);
         int64_t slots = 0;
         if (wsb > 200 * 1024) {
@@ -271,7 +361,7 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
     }
     case PD_CFA: {
       PD_CUDA(ensure_model_cl(ctx));
-      mv.fcl = ctx->model_cl.as<double>();
+      mv.fcl = ctx->model_cl.as<double>() + cl_off;
       const size_t wsb = cfa_workspace_bytes(n);
       int64_t slots = 0;
       if (wsb > 220 * 1024) {
@@ -287,9 +377,17 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
     case PD_JSIIA: {
       static const bool force_cta = std::getenv("PD_JSIIA_CTA") != nullptr;
       PD_CUDA(ensure_model_cl(ctx));
-      mv.fcl = ctx->model_cl.as<double>();
-      if (n <= 32 && !force_cta) {
-        launch_jsiia_warp(mv, ctx->model_cl.as<double>(), io, ctx->stream);
+      mv.fcl = ctx->model_cl.as<double>() + cl_off;
+      // n <= 64: warp per chain, M and its Cholesky on the FP64 tensor cores
+      // (PD_JSIIA_WARP selects the earlier register-row kernel for n <= 32)
+      static const bool use_warp = std::getenv("PD_JSIIA_WARP") != nullptr;
+      if (n <= 32 && use_warp && !force_cta) {
+        launch_jsiia_warp(mv, mv.fcl, io, ctx->stream);
+        ctx->launches++;
+        break;
+      }
+      if (n <= 64 && !force_cta) {
+        launch_jsiia_dmma(mv, mv.fcl, io, ctx->stream);
         ctx->launches++;
         break;
       }
@@ -392,6 +490,16 @@ pd_status pd_create(pd_ctx** out, int device) {
     return PD_CUDA_ERROR;
   }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = std::getenv("PD_L2_PERSIST_MB")) {  // experiment: L2 set-aside for evict_last lines
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+    size_t want = (size_t)std::atoi(e) << 20;
+    if (want > (size_t)maxp) want = (size_t)maxp;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    std::fprintf(stderr, "pd: persisting L2 set-aside %zu MB (max %d MB)\n", got >> 20, maxp >> 20);
+  }
   ctx->stream = ctx->own_stream;
   *out = ctx;
   return PD_OK;
@@ -404,6 +512,17 @@ void pd_destroy(pd_ctx* ctx) {
   for (DevBuf* b : {&ctx->model, &ctx->gravity, &ctx->mstatus, &ctx->mrule, &ctx->raw, &ctx->abia_scratch, &ctx->cta_ws,
                     &ctx->slots, &ctx->io_q, &ctx->io_qd, &ctx->io_tau, &ctx->io_qdd, &ctx->io_status})
     b->release();
+  if (ctx->cp_in) {
+    cudaStreamSynchronize(ctx->cp_in);
+    cudaStreamSynchronize(ctx->cp_out);
+    cudaStreamDestroy(ctx->cp_in);
+    cudaStreamDestroy(ctx->cp_out);
+    cudaEventDestroy(ctx->ev_entry);
+    for (int c = 0; c < pd_ctx::kMaxChunks; ++c) {
+      cudaEventDestroy(ctx->ev_in[c]);
+      cudaEventDestroy(ctx->ev_out[c]);
+    }
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -432,7 +551,7 @@ const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) 
                          "abia_cta_kernel for n >= 64 in batches <= 2 x SMs (CTA per chain)";
     case PD_CFA: return cfa_workspace_bytes(n_links) <= 220 * 1024 ? "cfa_cta_kernel<smem> (CTA per chain, OEE in smem)"
                                                                     : "cfa_cta_kernel<global> (CTA per chain, L2 workspace)";
-    case PD_JSIIA: return n_links <= 32 ? "jsiia_warp_kernel (warp per chain, register-resident M rows + row Cholesky)"
+    case PD_JSIIA: return n_links <= 64 ? "jsiia_dmma_kernel (warp per chain, M and blocked Cholesky on FP64 tensor cores, DMMA 8x8x4)"
                           : jsiia_smem_path(n_links)
                               ? "jsiia_tiled_kernel<smem> (CTA per chain, CRBA scans + 32x32-tile Cholesky in smem)"
                               : "jsiia_tiled_kernel<global> (CTA per chain, 32x32-tile Cholesky, L2 workspace)";
@@ -498,6 +617,10 @@ pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, c
     return PD_INVALID_ARGUMENT;
   }
   PD_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->n_models > 1 && ctx->n_models != batch) {
+    ctx->last_error = "forward dynamics: batch must equal the number of models (or use one shared model)";
+    return PD_INVALID_ARGUMENT;
+  }
   return run_device(ctx, algo, batch, batch, d_q, d_qdot, d_tau, d_qddot, d_slot_status, d_slot_round,
                     d_slot_index);
 }
@@ -512,37 +635,71 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   }
   if (batch == 0) return PD_OK;
   PD_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->n_models <= 0 || ctx->n_links <= 0) {
+    ctx->last_error = "forward dynamics: no models set (pd_set_models)";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (ctx->n_models != 1 && ctx->n_models != batch) {
+    ctx->last_error = "forward dynamics: batch must equal the number of models (or use one shared model)";
+    return PD_INVALID_ARGUMENT;
+  }
   const int n = ctx->n_links;
   const int64_t lds = (batch + 31) / 32 * 32;  // padded link stride (TMA-friendly)
-  const size_t bytes = sizeof(double) * (size_t)n * batch;
   const size_t half = (size_t)n * lds;
-  // staging: [B][n] host rows -> device -> [n][lds]
+  // staging: [B][n] host rows -> device rows (upper half) -> [n][lds] (lower half)
   PD_CUDA(ctx->io_q.ensure(2 * sizeof(double) * half));
   PD_CUDA(ctx->io_qd.ensure(2 * sizeof(double) * half));
   PD_CUDA(ctx->io_tau.ensure(2 * sizeof(double) * half));
   PD_CUDA(ctx->io_qdd.ensure(2 * sizeof(double) * half));
   PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+  if (!ctx->cp_in) {
+    PD_CUDA(cudaStreamCreateWithFlags(&ctx->cp_in, cudaStreamNonBlocking));
+    PD_CUDA(cudaStreamCreateWithFlags(&ctx->cp_out, cudaStreamNonBlocking));
+    PD_CUDA(cudaEventCreateWithFlags(&ctx->ev_entry, cudaEventDisableTiming));
+    for (int c = 0; c < pd_ctx::kMaxChunks; ++c) {
+      PD_CUDA(cudaEventCreateWithFlags(&ctx->ev_in[c], cudaEventDisableTiming));
+      PD_CUDA(cudaEventCreateWithFlags(&ctx->ev_out[c], cudaEventDisableTiming));
+    }
+  }
   double* sq = ctx->io_q.as<double>();
   double* sqd = ctx->io_qd.as<double>();
   double* stau = ctx->io_tau.as<double>();
   double* sqdd = ctx->io_qdd.as<double>();
-  PD_CUDA(cudaMemcpyAsync(sq + half, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  PD_CUDA(cudaMemcpyAsync(sqd + half, qdot, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  PD_CUDA(cudaMemcpyAsync(stau + half, tau, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  launch_transpose(ctx, sq + half, sq, batch, n, n, lds);
-  launch_transpose(ctx, sqd + half, sqd, batch, n, n, lds);
-  launch_transpose(ctx, stau + half, stau, batch, n, n, lds);
   int32_t* st = ctx->io_status.as<int32_t>();
-  pd_status s = run_device(ctx, algo, batch, lds, sq, sqd, stau, sqdd, st, st + batch, st + 2 * batch);
-  if (s != PD_OK) return s;
-  launch_transpose(ctx, sqdd, sqdd + half, n, batch, lds, n);
-  PD_CUDA(cudaMemcpyAsync(qddot, sqdd + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  // Chunked pipeline: the copy-in stream streams chunk c+1 over PCIe while the
+  // compute stream transposes and solves chunk c and the copy-out stream
+  // returns chunk c-1. Chunks are 32-aligned (TMA bases stay 16-byte aligned).
+  const int nch = (int)std::min<int64_t>(pd_ctx::kMaxChunks, std::max<int64_t>(1, batch / 4096));
+  const int64_t csz = ((batch + nch - 1) / nch + 31) / 32 * 32;
+  PD_CUDA(cudaEventRecord(ctx->ev_entry, ctx->stream));  // earlier work on the staging buffers
+  PD_CUDA(cudaStreamWaitEvent(ctx->cp_in, ctx->ev_entry, 0));
+  PD_CUDA(cudaStreamWaitEvent(ctx->cp_out, ctx->ev_entry, 0));
+  for (int c = 0; c < nch; ++c) {
+    const int64_t b0 = c * csz, nb = std::min<int64_t>(csz, batch - b0);
+    if (nb <= 0) break;
+    const size_t off = (size_t)b0 * n, bytes = sizeof(double) * (size_t)n * nb;
+    PD_CUDA(cudaMemcpyAsync(sq + half + off, q + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
+    PD_CUDA(cudaMemcpyAsync(sqd + half + off, qdot + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
+    PD_CUDA(cudaMemcpyAsync(stau + half + off, tau + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
+    PD_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->cp_in));
+    PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[c], 0));
+    launch_transpose(ctx, sq + half + off, sq + b0, nb, n, n, lds);
+    launch_transpose(ctx, sqd + half + off, sqd + b0, nb, n, n, lds);
+    launch_transpose(ctx, stau + half + off, stau + b0, nb, n, n, lds);
+    pd_status s = run_device(ctx, algo, nb, lds, sq + b0, sqd + b0, stau + b0, sqdd + b0, st + b0, st + batch + b0,
+                             st + 2 * batch + b0, b0);
+    if (s != PD_OK) return s;
+    launch_transpose(ctx, sqdd + b0, sqdd + half + off, n, nb, lds, n);
+    PD_CUDA(cudaEventRecord(ctx->ev_out[c], ctx->stream));
+    PD_CUDA(cudaStreamWaitEvent(ctx->cp_out, ctx->ev_out[c], 0));
+    PD_CUDA(cudaMemcpyAsync(qddot + off, sqdd + half + off, bytes, cudaMemcpyDeviceToHost, ctx->cp_out));
+  }
   std::vector<int32_t> hs;
   if (slot_status || slot_round || slot_index) {
     hs.resize(3 * batch);
-    PD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->cp_out));
   }
-  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  PD_CUDA(cudaStreamSynchronize(ctx->cp_out));
   if (slot_status) std::memcpy(slot_status, hs.data(), sizeof(int32_t) * batch);
   if (slot_round) std::memcpy(slot_round, hs.data() + batch, sizeof(int32_t) * batch);
   if (slot_index) std::memcpy(slot_index, hs.data() + 2 * batch, sizeof(int32_t) * batch);

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO 
     for (int k = 0; k < 9; ++k) ws[(jst::IC + 6 + k) * n + i] = Jb.B[k];
 #pragma unroll
     for (int k = 0; k < 6; ++k) ws[(jst::IC + 15 + k) * n + i] = Jb.D[k];
-    ws_put_sv(ws, n, jst::S0, i, adinv_apply(X, mv.screw(i, mc)));
+    ws_put_sv(ws, n, jst::S0, i, adinv_screw(X, mv.screw(i, mc)));
   }
   __syncthreads();
   ws_scan<12, true>(ws, n, jst::IC, lpt, AddOp{}, scan_sm);

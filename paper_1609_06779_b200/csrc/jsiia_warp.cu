@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(32 * kWarps) jsiia_warp_kernel(ModelView mv, c
   const SE3d X = warp_se3_prefix(rel, lane);
 
   // ---- bias torque (base frame) ------------------------------------------------
-  const Sv S0 = adinv_apply(X, S);
+  const Sv S0 = adinv_screw(X, S);
   const Sv rate0 = qd * S0;
   const Sv V0 = sv_unpack(warp_sum_scan<6, false>(sv_pack(rate0), lane));
   const Vec3d g = mv.gravity(mc);

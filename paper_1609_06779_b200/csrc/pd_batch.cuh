@@ -17,15 +17,16 @@ struct ModelView {
   // CTA/warp-per-chain kernels read this copy (coalesced across links).
   const double* __restrict__ fcl;
   int n;
-  int64_t M;
-  int64_t ld;  // stride between links of one field (>= M, even: TMA needs 16-byte strides)
+  int64_t M;    // models in this view (1 = one model shared by every problem)
+  int64_t ld;   // stride between links of one field (>= M, even: TMA needs 16-byte strides)
+  int64_t gld;  // stride between gravity components
   __device__ __forceinline__ double at(int field, int link, int64_t mc) const {
     return fcl ? __ldg(fcl + ((int64_t)mc * F_COUNT + field) * n + link)
                : __ldg(f + ((int64_t)field * n + link) * ld + mc);
   }
   __device__ __forceinline__ int64_t model_of(int64_t p) const { return M == 1 ? 0 : p; }
   __device__ __forceinline__ Vec3d gravity(int64_t mc) const {
-    return mk(__ldg(g + mc), __ldg(g + M + mc), __ldg(g + 2 * M + mc));
+    return mk(__ldg(g + mc), __ldg(g + gld + mc), __ldg(g + 2 * gld + mc));
   }
   __device__ __forceinline__ Sv screw(int i, int64_t mc) const {
     return {mk(at(F_SCREW, i, mc), at(F_SCREW + 1, i, mc), at(F_SCREW + 2, i, mc)),

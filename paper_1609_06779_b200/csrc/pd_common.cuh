@@ -277,59 +277,44 @@ __device__ __forceinline__ Sym6 sym6_congruence(const Sym6& P, const SE3d& T) {
 // Joint transform rel = screw_exp(S, -q) * home                 model.cpp:117-146
 // screw_exp: Rodrigues for a not-necessarily-unit angular part, pure
 // translation if |w| < 1e-12                                     spatial.cpp:43-68
-// joint_angle_sincos gives (sin, cos) of theta = -|w| q (the expensive,
+// Packed models live in joint-aligned frames (capi.cu pack_models_kernel):
+// S = (0, 0, w, vx, 0, vz) with w = |w| >= 0, so exp(-q S) is a rotation by
+// theta = -w q about z plus t = (vx sin(theta)/w, vx (1 - cos(theta))/w, -q vz)
+// (the reference's R = I + a w^ + b w^2, t = (q I + b w^ + c w^2) v with the
+// zeros of S substituted), and rel = (E H, E h + t) mixes only two rows.
+// joint_angle_sincos gives (sin, cos) of theta (the expensive,
 // history-independent part); joint_transform_sc assembles rel from it.
 __device__ __forceinline__ void joint_angle_sincos(const Sv& S, double q, double* st, double* ct) {
-  const double wn2 = dot(S.a, S.a);
-  if (wn2 < 1e-24) {
+  const double w = S.a.z;
+  if (w * w < 1e-24) {
     *st = 0.0;
     *ct = 1.0;
     return;
   }
-  const double iwn = rsqrt(wn2);
-  sincos(wn2 * iwn * (-q), st, ct);
+  sincos(w * (-q), st, ct);
 }
 
 __device__ __forceinline__ SE3d joint_transform_sc(const Sv& S, const Mat3d& HR, Vec3d hp, double q, double st,
                                                    double ct) {
-  const double qq = -q;
-  const Vec3d w = S.a, v = S.l;
-  const double wn2 = dot(w, w);
-  Mat3d E;
+  const double w = S.a.z, vx = S.l.x, vz = S.l.z;
   Vec3d t;
-  const bool has_v = (v.x != 0.0) | (v.y != 0.0) | (v.z != 0.0);
-  if (wn2 < 1e-24) {  // |w| < 1e-12: pure translation
-#pragma unroll
-    for (int k = 0; k < 9; ++k) E.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
-    t = qq * v;
+  double c = ct, s = st;
+  if (w * w < 1e-24) {  // |w| < 1e-12: pure translation
+    c = 1.0;
+    s = 0.0;
+    t = mk(-q * vx, 0.0, -q * vz);
   } else {
-    const double iwn = rsqrt(wn2);
-    const double iwn2 = iwn * iwn;
-    const double a = st * iwn;
-    const double b = (1.0 - ct) * iwn2;
-    // R = I + a w^ + b w^2 ; w^2 = w w^T - |w|^2 I
-    E.m[0] = fma(b, w.x * w.x - wn2, 1.0);
-    E.m[4] = fma(b, w.y * w.y - wn2, 1.0);
-    E.m[8] = fma(b, w.z * w.z - wn2, 1.0);
-    const double bxy = b * w.x * w.y, bxz = b * w.x * w.z, byz = b * w.y * w.z;
-    E.m[1] = fma(-a, w.z, bxy);
-    E.m[3] = fma(a, w.z, bxy);
-    E.m[2] = fma(a, w.y, bxz);
-    E.m[6] = fma(-a, w.y, bxz);
-    E.m[5] = fma(-a, w.x, byz);
-    E.m[7] = fma(a, w.x, byz);
-    if (has_v) {
-      // t = (q I + b w^ + c w^2) v = q v + b (w x v) + c (w x (w x v))
-      const double c = (qq - a) * iwn2;
-      const Vec3d wv = cross(w, v);
-      t = fmav(c, cross(w, wv), fmav(b, wv, qq * v));
-    } else {
-      t = mk(0.0, 0.0, 0.0);  // revolute screw through the link origin
-    }
+    const double iw = 1.0 / w;
+    t = mk(vx * (st * iw), vx * ((1.0 - ct) * iw), -q * vz);
   }
   SE3d T;
-  T.R = matmul(E, HR);
-  T.p = mul_acc(E, hp, t);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    T.R.m[k] = fma(c, HR.m[k], -s * HR.m[3 + k]);
+    T.R.m[3 + k] = fma(s, HR.m[k], c * HR.m[3 + k]);
+    T.R.m[6 + k] = HR.m[6 + k];
+  }
+  T.p = mk(fma(c, hp.x, fma(-s, hp.y, t.x)), fma(s, hp.x, fma(c, hp.y, t.y)), hp.z + t.z);
   return T;
 }
 
@@ -337,6 +322,14 @@ __device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Ve
   double st, ct;
   joint_angle_sincos(S, q, &st, &ct);
   return joint_transform_sc(S, HR, hp, q, st, ct);
+}
+
+// Ad(R,p)^{-1} S for a joint-aligned screw S = (0, 0, w, vx, 0, vz):
+// (w R^T e_z, R^T (v - p x w e_z)), p x (w e_z) = w (py, -px, 0)
+__device__ __forceinline__ Sv adinv_screw(const SE3d& T, const Sv& S) {
+  const double w = S.a.z;
+  const Vec3d u = mk(fma(-w, T.p.y, S.l.x), w * T.p.x, S.l.z);
+  return {mk(w * T.R.m[6], w * T.R.m[7], w * T.R.m[8]), mulT(T.R, u)};
 }
 
 // Kernel-side error record: first failure wins per slot.
