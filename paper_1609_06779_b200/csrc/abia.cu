@@ -28,12 +28,13 @@ namespace pd {
 
 struct LinkKinParams {
   Sv S;
+  double iw;
   Mat3d HR;
   Vec3d hp;
 };
 
 __device__ __forceinline__ LinkKinParams load_kin(const ModelView& mv, int i, int64_t mc) {
-  return {mv.screw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc)};
+  return {mv.screw(i, mc), mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc)};
 }
 
 // The whole solve runs in base coordinates. With X_i = rel_i * ... * rel_0
@@ -58,12 +59,13 @@ __global__ void __launch_bounds__(128) abia_lane_kernel(ModelView mv, BatchIO io
   abia_init(st, mv.gravity(mc));
   for (int i = 0; i < n; ++i) {
     const Sv S = mv.screw(i, mc);
-    abia_pass_a(st, joint_transform(S, mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p)), S, io.ld(io.qd, i, p));
+    abia_pass_a(st, joint_transform(S, mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p)), S,
+                io.ld(io.qd, i, p));
   }
   for (int i = n - 1; i >= 0; --i) {
     double rec[kRec];
     const Sv S = mv.screw(i, mc);
-    abia_pass_b(st, i, n, joint_transform(S, mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p)), S,
+    abia_pass_b(st, i, n, joint_transform(S, mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p)), S,
                 io.ld(io.qd, i, p), mv.inertia(i, mc), io.ld(io.tau, i, p), rec);
 #pragma unroll
     for (int k = 0; k < kRec; ++k) scratch[((int64_t)i * kRec + k) * B + p] = rec[k];
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(128) invdyn_lane_kernel(ModelView mv, BatchIO 
   Sv A = {mk(0, 0, 0), mk(-g.x, -g.y, -g.z)};
   for (int i = 0; i < n; ++i) {
     const LinkKinParams L = load_kin(mv, i, mc);
-    const SE3d T = joint_transform(L.S, L.HR, L.hp, io.ld(io.q, i, p));
+    const SE3d T = joint_transform(L.S, L.iw, L.HR, L.hp, io.ld(io.q, i, p));
     const Sv rate = io.ld(io.qd, i, p) * L.S;
     V = ad_apply(T, V) + rate;
     A = ad_apply(T, A) + io.ld(io.tau, i, p) * L.S + adv_apply(V, rate);
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(128) invdyn_lane_kernel(ModelView mv, BatchIO 
   Sv carryF = svzero();
   for (int i = n - 1; i >= 0; --i) {
     const LinkKinParams L = load_kin(mv, i, mc);
-    const SE3d T = joint_transform(L.S, L.HR, L.hp, io.ld(io.q, i, p));
+    const SE3d T = joint_transform(L.S, L.iw, L.HR, L.hp, io.ld(io.q, i, p));
     const Inertia J = mv.inertia(i, mc);
     const Sv h = inertia_apply(J, V);
     const Sv F = inertia_apply(J, A) + neg_advT_apply(V, h) + carryF;

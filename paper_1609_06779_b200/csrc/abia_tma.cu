@@ -1,32 +1,35 @@
-// ABIA, TMA-pipelined lane-per-chain kernel for batches of independent chains.
+// ABIA for batches of independent chains, lane per chain, TMA-fed.
 //
-// Same arithmetic as abia_lane_kernel (abia_common.cuh); what changes is the
-// memory path. A CTA owns a tile of 128 consecutive chains (one per thread).
-// For every link step of the three passes one elected thread issues TMA tile
-// loads (cp.async.bulk.tensor) of that link's model fields for the whole tile
-// -- a {128 chains x 1 link x F fields} box of the [field][link][chain] SoA
-// model -- plus the tile's q / qdot / tau rows into a 3-stage shared-memory
-// ring, completion tracked by mbarrier transaction counts. Threads read their
-// chain's values from shared memory while the next two links are in flight,
-// so the FP64 pipes are not left waiting on global-memory latency.
-//   pass A loads model fields 10..27 (screw, home R, home p) + q, qd
-//   pass B loads all 28 model fields + q, qd, tau
-//   pass C loads the 13-double records pass B wrote (after a proxy fence)
+// Same arithmetic as abia_lane_kernel (abia_common.cuh: three fused passes in
+// base coordinates); what differs is the memory path. A CTA owns tiles of KT
+// consecutive chains (one per consumer thread). For every link step of the
+// three passes TMA tile loads (cp.async.bulk.tensor) bring that link's fields
+// for the whole tile -- a {KT chains x 1 link x F fields} box of the
+// [field][link][chain] SoA model -- plus the tile's q / qdot / tau rows into
+// shared memory, completion tracked by mbarrier transaction counts:
+//   pass A: the F_NKIN kinematic fields + q, qd
+//   pass B: all F_COUNT model fields + q, qd, tau
+//   pass C: the 13-double records pass B wrote (after a proxy fence)
+// abia_ring_kernel (default): a dedicated producer warp streams the steps of
+// all the CTA's tiles (persistent CTAs) through one byte ring with per-pass
+// stage sizes, so cheap passes run many links ahead and the next tile's pass
+// A streams in during this tile's pass C. abia_tma_kernel: the earlier fixed
+// 3-stage ring with the producer inside warp 0 (PD_ABIA_VARIANT 0..9).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
 #include "abia_common.cuh"
-#include "tmem_util.cuh"
 
 namespace pd {
 
 namespace {
 
 constexpr int kT = 128;          // chains per CTA
-constexpr int kStageFields = 33; // 28 model + q, qd, tau, sin, cos; pass C uses 13
-constexpr int kQ = 28, kQD = 29, kTAU = 30, kSIN = 31, kCOS = 32;
+constexpr int kStageFields = F_COUNT + 5;  // model + q, qd, tau, sin, cos; pass C uses 13
+constexpr int kQ = F_COUNT, kQD = F_COUNT + 1, kTAU = F_COUNT + 2, kSIN = F_COUNT + 3, kCOS = F_COUNT + 4;
 constexpr int kSC0 = kRec;       // scratch rows n*kRec + 2*i + {0,1}: (sin, cos) of link i's joint angle
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -98,8 +101,8 @@ __device__ __forceinline__ void discard_l2(const void* addr) {
 }
 
 struct Maps {
-  CUtensorMap model_all;  // box {T, 1, 28}
-  CUtensorMap model_kin;  // box {T, 1, 18} from field 10
+  CUtensorMap model_all;  // box {T, 1, F_COUNT}
+  CUtensorMap model_kin;  // box {T, 1, F_NKIN} from field F_KIN
   CUtensorMap q, qd, tau; // box {T, 1}
   CUtensorMap scr;        // box {T, 13}
   CUtensorMap sc;         // box {T, 2}: (sin, cos) rows written by pass A
@@ -109,15 +112,14 @@ struct Maps {
 
 template <int KT = kT>
 __device__ __forceinline__ Sv stage_screw(const double* f) {
-  return {mk(f[F_SCREW * KT], f[(F_SCREW + 1) * KT], f[(F_SCREW + 2) * KT]),
-          mk(f[(F_SCREW + 3) * KT], f[(F_SCREW + 4) * KT], f[(F_SCREW + 5) * KT])};
+  return joint_screw(f[F_SW * KT], f[F_SVX * KT], f[F_SVZ * KT]);
 }
 template <int KT = kT>
 __device__ __forceinline__ SE3d stage_rel(const double* f, double st, double ct) {
   Mat3d HR;
 #pragma unroll
   for (int j = 0; j < 9; ++j) HR.m[j] = f[(F_HR + j) * KT];
-  return joint_transform_sc(stage_screw<KT>(f), HR, mk(f[F_HP * KT], f[(F_HP + 1) * KT], f[(F_HP + 2) * KT]),
+  return joint_transform_sc(stage_screw<KT>(f), f[F_SIW * KT], HR, mk(f[F_HP * KT], f[(F_HP + 1) * KT], f[(F_HP + 2) * KT]),
                             f[kQ * KT], st, ct);
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -168,19 +170,19 @@ __global__ void __launch_bounds__(KT, MINB)
     double* dst = ring + (size_t)s * kStageFields * KT;
     uint64_t* bar = &full[s];
     if (k < n) {  // re-read in pass B: default policy, or evict_last (HINTS & 2)
-      mbar_expect_tx(bar, (18 + 2) * KT * 8);
+      mbar_expect_tx(bar, (F_NKIN + 2) * KT * 8);
       if (HINTS & 2) {
-        tma_3d_hint(dst + 10 * KT, &maps.model_kin, c0, k, 10, bar, pol_last);
+        tma_3d_hint(dst + F_KIN * KT, &maps.model_kin, c0, k, F_KIN, bar, pol_last);
         tma_2d_hint(dst + kQ * KT, &maps.q, c0, k, bar, pol_last);
         tma_2d_hint(dst + kQD * KT, &maps.qd, c0, k, bar, pol_last);
       } else {
-        tma_3d(dst + 10 * KT, &maps.model_kin, c0, k, 10, bar);
+        tma_3d(dst + F_KIN * KT, &maps.model_kin, c0, k, F_KIN, bar);
         tma_2d(dst + kQ * KT, &maps.q, c0, k, bar);
         tma_2d(dst + kQD * KT, &maps.qd, c0, k, bar);
       }
     } else if (k < 2 * n) {  // last use of the model
       const int i = 2 * n - 1 - k;
-      mbar_expect_tx(bar, (28 + 5) * KT * 8);
+      mbar_expect_tx(bar, (F_COUNT + 5) * KT * 8);
       if (HINTS) {
         tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
         tma_2d_hint(dst + kTAU * KT, &maps.tau, c0, i, bar, pol_first);
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(KT, MINB)
 // before consuming step k it issues up to k (blocking reclaims), after each
 // step it issues further ahead only while slots are free (non-blocking).
 constexpr int kSlots = 16;
-constexpr int kRowsA = 20, kRowsB = 31, kRowsC = kRec;
+constexpr int kRowsA = F_NKIN + 2, kRowsB = F_COUNT + 3, kRowsC = kRec;
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t done;
@@ -338,17 +340,18 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return done != 0;
 }
 
+// rows r0.. = the kinematic block F_SW..F_HP: w, vx, vz, 1/w, home R (9), home p (3)
 template <int KT>
 __device__ __forceinline__ Sv row_screw(const double* f, int r0) {
-  return {mk(f[r0 * KT], f[(r0 + 1) * KT], f[(r0 + 2) * KT]), mk(f[(r0 + 3) * KT], f[(r0 + 4) * KT], f[(r0 + 5) * KT])};
+  return joint_screw(f[r0 * KT], f[(r0 + 1) * KT], f[(r0 + 2) * KT]);
 }
-// rows r0.. = screw (6), home R (9), home p (3): the F_SCREW..F_HP block
 template <int KT>
 __device__ __forceinline__ SE3d row_rel(const double* f, int r0, const Sv& S, double q, double st, double ct) {
   Mat3d HR;
 #pragma unroll
-  for (int j = 0; j < 9; ++j) HR.m[j] = f[(r0 + 6 + j) * KT];
-  return joint_transform_sc(S, HR, mk(f[(r0 + 15) * KT], f[(r0 + 16) * KT], f[(r0 + 17) * KT]), q, st, ct);
+  for (int j = 0; j < 9; ++j) HR.m[j] = f[(r0 + 4 + j) * KT];
+  return joint_transform_sc(S, f[(r0 + 3) * KT], HR, mk(f[(r0 + 13) * KT], f[(r0 + 14) * KT], f[(r0 + 15) * KT]), q,
+                            st, ct);
 }
 
 template <int KT, int MINB, bool KEEP_A>
@@ -359,11 +362,12 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32, MINB)
   extern __shared__ __align__(128) double ring[];  // cap_rows x KT doubles
   __shared__ __align__(8) uint64_t full[kSlots];
   __shared__ __align__(8) uint64_t empty[kSlots];
-  constexpr int NW = (KT + 31) / 32;  // consumer warps; warp NW is the producer
+  __shared__ uint32_t vstart[kSlots];  // producer only: virtual ring row of each step in flight
+  constexpr int NW = (KT + 31) / 32;   // consumer warps; warp NW is the producer
   const int t = threadIdx.x, lane = t & 31;
   const int n = mv.n;
-  const int c0 = blockIdx.x * KT;
-  const int total = 3 * n;
+  const uint32_t total = 3u * (uint32_t)n;
+  const int ntiles = (int)((io.B + KT - 1) / KT);
   if (t == 0) {
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&full[s], 1);
@@ -373,414 +377,138 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32, MINB)
   }
   __syncthreads();
   const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-  auto rows_of = [&](int k) -> uint32_t { return k < n ? kRowsA : (k < 2 * n ? kRowsB : kRowsC); };
-  auto start_of = [&](uint32_t v, uint32_t rows) -> uint32_t {
-    const uint32_t o = v % cap_rows;
-    return o + rows > cap_rows ? v + (cap_rows - o) : v;
-  };
+  auto rows_of = [&](uint32_t k) -> uint32_t { return k < (uint32_t)n ? kRowsA : (k < 2u * n ? kRowsB : kRowsC); };
+  // Persistent CTA: tiles blockIdx.x, blockIdx.x + gridDim.x, ... flow through
+  // one ring, so the next tile's pass-A loads stream in during this tile's
+  // (memory-light) pass C. Steps are numbered gk across the CTA's tiles.
   if (t >= NW * 32) {  // ---- producer warp: one elected lane issues every step in order
     if (lane == 0) {
-      uint32_t vst[kSlots];
-      uint32_t pv = 0;
-      int old = 0;
-      for (int k = 0; k < total; ++k) {
-        const uint32_t rows = rows_of(k);
-        const uint32_t st = start_of(pv, rows);
-        // free the slot, the ring bytes, and (pass C) every pass-B step
-        while (k - old >= kSlots || (old < k && st + rows - vst[old % kSlots] > cap_rows) ||
-               (k >= 2 * n && old < 2 * n)) {
-          mbar_wait(&empty[old % kSlots], (uint32_t)((old / kSlots) & 1));
-          ++old;
-        }
-        double* dst = ring + (size_t)(st % cap_rows) * KT;
-        uint64_t* bar = &full[k % kSlots];
-        if (k < n) {  // pass A: kin rows 0..17, q 18, qd 19
-          mbar_expect_tx(bar, kRowsA * KT * 8);
-          if (KEEP_A) {
-            tma_3d_hint(dst, &maps.model_kin, c0, k, F_SCREW, bar, pol_last);
-            tma_2d_hint(dst + 18 * KT, &maps.q, c0, k, bar, pol_last);
-            tma_2d_hint(dst + 19 * KT, &maps.qd, c0, k, bar, pol_last);
-          } else {
-            tma_3d(dst, &maps.model_kin, c0, k, F_SCREW, bar);
-            tma_2d(dst + 18 * KT, &maps.q, c0, k, bar);
-            tma_2d(dst + 19 * KT, &maps.qd, c0, k, bar);
+      uint32_t vpos = 0, phys = 0, old = 0, gk = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int c0 = tile * KT;
+        const uint32_t base = gk;
+        for (uint32_t k = 0; k < total; ++k, ++gk) {
+          const uint32_t rows = rows_of(k);
+          if (phys + rows > cap_rows) {  // wrap: skip the ring's tail
+            vpos += cap_rows - phys;
+            phys = 0;
           }
-        } else if (k < 2 * n) {  // pass B: model rows 0..27, q 28, qd 29, tau 30 (last use)
-          const int i = 2 * n - 1 - k;
-          mbar_expect_tx(bar, kRowsB * KT * 8);
-          tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
-          tma_2d_hint(dst + 28 * KT, &maps.q, c0, i, bar, pol_first);
-          tma_2d_hint(dst + 29 * KT, &maps.qd, c0, i, bar, pol_first);
-          tma_2d_hint(dst + 30 * KT, &maps.tau, c0, i, bar, pol_first);
-        } else {  // pass C: records of link i
-          const int i = k - 2 * n;
-          mbar_expect_tx(bar, kRowsC * KT * 8);
-          tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
+          // free the slot, the ring rows, and (pass C) every pass-B step of this tile
+          while (gk - old >= (uint32_t)kSlots || (old < gk && vpos + rows - vstart[old % kSlots] > cap_rows) ||
+                 (k >= 2u * n && old < base + 2u * n)) {
+            mbar_wait(&empty[old % kSlots], (old / kSlots) & 1u);
+            ++old;
+          }
+          double* dst = ring + (size_t)phys * KT;
+          uint64_t* bar = &full[gk % kSlots];
+          if (k < (uint32_t)n) {  // pass A: kinematic rows 0..F_NKIN-1, q, qd
+            mbar_expect_tx(bar, kRowsA * KT * 8);
+            if (KEEP_A) {
+              tma_3d_hint(dst, &maps.model_kin, c0, (int)k, F_KIN, bar, pol_last);
+              tma_2d_hint(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar, pol_last);
+              tma_2d_hint(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar, pol_last);
+            } else {
+              tma_3d(dst, &maps.model_kin, c0, (int)k, F_KIN, bar);
+              tma_2d(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar);
+              tma_2d(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar);
+            }
+          } else if (k < 2u * n) {  // pass B: model rows 0..F_COUNT-1, q, qd, tau (last use)
+            const int i = 2 * n - 1 - (int)k;
+            mbar_expect_tx(bar, kRowsB * KT * 8);
+            tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
+            tma_2d_hint(dst + F_COUNT * KT, &maps.q, c0, i, bar, pol_first);
+            tma_2d_hint(dst + (F_COUNT + 1) * KT, &maps.qd, c0, i, bar, pol_first);
+            tma_2d_hint(dst + (F_COUNT + 2) * KT, &maps.tau, c0, i, bar, pol_first);
+          } else {  // pass C: records of link i
+            const int i = (int)k - 2 * n;
+            mbar_expect_tx(bar, kRowsC * KT * 8);
+            tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
+          }
+          vstart[gk % kSlots] = vpos;
+          vpos += rows;
+          phys += rows;
         }
-        vst[k % kSlots] = st;
-        pv = st + rows;
       }
     }
     return;
   }
-  const int64_t p = (int64_t)c0 + t;
-  const bool live = t < KT && p < io.B;  // lanes past KT (partial last warp) only keep the warp convergent
-  uint32_t cv = 0;  // consumer's virtual ring position (mirrors the producer's)
-  auto acquire = [&](int k) -> const double* {
-    const uint32_t st = start_of(cv, rows_of(k));
-    cv = st + rows_of(k);
-    mbar_wait(&full[k % kSlots], (uint32_t)((k / kSlots) & 1));
-    return ring + (size_t)(st % cap_rows) * KT + (t < KT ? t : 0);
+  uint32_t cphys = 0, gk = 0;  // consumer's ring position / step counter (mirror the producer's)
+  const int tt = t < KT ? t : 0;
+  auto acquire = [&](uint32_t k) -> const double* {
+    const uint32_t rows = rows_of(k);
+    if (cphys + rows > cap_rows) cphys = 0;
+    const uint32_t off = cphys;
+    cphys += rows;
+    mbar_wait(&full[gk % kSlots], (gk / kSlots) & 1u);
+    return ring + (size_t)off * KT + tt;
   };
-  auto release = [&](int k) {
+  auto release = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[k % kSlots]);
+    if (lane == 0) mbar_arrive(&empty[gk % kSlots]);
+    ++gk;
   };
 
-  const int64_t mc = live ? mv.model_of(p) : 0;
-  AbiaState st;
-  abia_init(st, live ? mv.gravity(mc) : mk(0, 0, 0));
-  int k = 0;
-  for (; k < n; ++k) {  // pass A
-    const double* f = acquire(k);
-    const Sv S = row_screw<KT>(f, 0);
-    const double q = f[18 * KT];
-    double sn, cs;
-    joint_angle_sincos(S, q, &sn, &cs);
-    abia_pass_a(st, row_rel<KT>(f, 0, S, q, sn, cs), S, f[19 * KT]);
-    release(k);
-  }
-  for (; k < 2 * n; ++k) {  // pass B
-    const double* f = acquire(k);
-    const int i = 2 * n - 1 - k;
-    const Sv S = row_screw<KT>(f, F_SCREW);
-    const double q = f[28 * KT];
-    double sn, cs;
-    joint_angle_sincos(S, q, &sn, &cs);
-    Inertia J;
-    J.m = f[F_MASS * KT];
-    J.c = mk(f[F_COM * KT], f[(F_COM + 1) * KT], f[(F_COM + 2) * KT]);
-#pragma unroll
-    for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
-    double rec[kRec];
-    abia_pass_b(st, i, n, row_rel<KT>(f, F_SCREW, S, q, sn, cs), S, f[29 * KT], J, f[30 * KT], rec);
-    if (live) {
-#pragma unroll
-      for (int j = 0; j < kRec; ++j) st_hint(scratch + ((int64_t)i * kRec + j) * scr_ld + p, rec[j], pol_last);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int c0 = tile * KT;
+    const int64_t p = (int64_t)c0 + t;
+    const bool live = t < KT && p < io.B;  // lanes past KT (partial last warp) only keep the warp convergent
+    const int64_t mc = live ? mv.model_of(p) : 0;
+    AbiaState st;
+    abia_init(st, live ? mv.gravity(mc) : mk(0, 0, 0));
+    uint32_t k = 0;
+    for (; k < (uint32_t)n; ++k) {  // pass A
+      const double* f = acquire(k);
+      const Sv S = row_screw<KT>(f, 0);
+      const double q = f[F_NKIN * KT];
+      double sn, cs;
+      joint_angle_sincos(S, q, &sn, &cs);
+      abia_pass_a(st, row_rel<KT>(f, 0, S, q, sn, cs), S, f[(F_NKIN + 1) * KT]);
+      release();
     }
-    if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
-    release(k);
-  }
-  for (; k < total; ++k) {  // pass C
-    const double* f = acquire(k);
-    const int i = k - 2 * n;
-    double rec[kRec];
+    for (; k < 2u * n; ++k) {  // pass B
+      const double* f = acquire(k);
+      const int i = 2 * n - 1 - (int)k;
+      const Sv S = row_screw<KT>(f, F_KIN);
+      const double q = f[F_COUNT * KT];
+      double sn, cs;
+      joint_angle_sincos(S, q, &sn, &cs);
+      Inertia J;
+      J.m = f[F_MASS * KT];
+      J.c = mk(f[F_COM * KT], f[(F_COM + 1) * KT], f[(F_COM + 2) * KT]);
 #pragma unroll
-    for (int j = 0; j < kRec; ++j) rec[j] = f[j * KT];
-    const double qdd = abia_pass_c(st, rec);
-    if (live) io.put_qdd(i, p, qdd);
-    if (KT % 16 == 0 && t < kRec * (KT / 16)) {  // drop the dead records' L2 lines without write-back
-      const int row = t / (KT / 16), seg = t % (KT / 16);
-      const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
-      if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
-    }
-    release(k);
-  }
-  if (live) {
-    const int32_t ms = __ldg(mv.mstatus + mc);
-    io.status[p] = ms != PD_SLOT_OK ? ms : st.code;
-    io.eround[p] = 0;
-    io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : st.eidx;
-  }
-}
-
-// Variant with the per-chain recursion state in TMEM: P0 (21 doubles), Z0 and
-// F0 (6 each) live in the thread's own TMEM lane between links and are loaded
-// only around the few instructions that use them; the last pass-A sin/cos
-// pairs too. That frees ~80 registers of live state, so 3 CTAs (12 warps) fit
-// per SM with a 2-stage ring. TMEM columns per thread:
-//   [0,42) P0   [42,54) Z0   [54,66) F0   [66,74) (sin, cos) of links n-1, n-2
-constexpr int kTmemCols = 128;
-__global__ void __launch_bounds__(kT, 3)
-    abia_tma_tmem_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
-                         int64_t scr_ld) {
-  constexpr int KSTAGES = 2;
-  extern __shared__ __align__(128) double ring[];  // [KSTAGES][kStageFields][kT]
-  __shared__ __align__(8) uint64_t full[KSTAGES];
-  __shared__ __align__(8) uint64_t empty[KSTAGES];
-  __shared__ uint32_t tmem_base;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int n = mv.n;
-  const int c0 = blockIdx.x * kT;
-  const int64_t p = (int64_t)c0 + t;
-  const bool live = p < io.B;
-  const int total = 3 * n;
-  if (warp == 0) tmem_alloc(&tmem_base, kTmemCols);
-  if (t == 0) {
-    for (int s = 0; s < KSTAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kT / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tm = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
-  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-
-  auto issue = [&](int k) {
-    const int s = k % KSTAGES;
-    double* dst = ring + (size_t)s * kStageFields * kT;
-    uint64_t* bar = &full[s];
-    if (k < n) {
-      mbar_expect_tx(bar, (18 + 2) * kT * 8);
-      tma_3d(dst + 10 * kT, &maps.model_kin, c0, k, 10, bar);
-      tma_2d(dst + kQ * kT, &maps.q, c0, k, bar);
-      tma_2d(dst + kQD * kT, &maps.qd, c0, k, bar);
-    } else if (k < 2 * n) {
-      const int i = 2 * n - 1 - k;
-      mbar_expect_tx(bar, (28 + 5) * kT * 8);
-      tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
-      tma_2d_hint(dst + kTAU * kT, &maps.tau, c0, i, bar, pol_first);
-      tma_2d_hint(dst + kSIN * kT, &maps.sc, c0, 2 * i, bar, pol_first);
-      tma_2d(dst + kQ * kT, &maps.q, c0, i, bar);
-      tma_2d(dst + kQD * kT, &maps.qd, c0, i, bar);
-    } else {
-      const int i = k - 2 * n;
-      mbar_expect_tx(bar, kRec * kT * 8);
-      tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
-    }
-  };
-  int next = 0;
-  if (t == 0)
-    for (; next < min(KSTAGES, min(total, 2 * n)); ++next) issue(next);
-  auto after_step = [&](int k) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[k % KSTAGES]);
-    if (t == 0) {
-      const int target = k < 2 * n - 1 ? min(2 * n, k + 1 + KSTAGES) : min(total, k + 1 + KSTAGES);
-      for (; next < target; ++next) {
-        const int prev = next - KSTAGES;
-        if (prev >= 0) mbar_wait(&empty[prev % KSTAGES], (uint32_t)((prev / KSTAGES) & 1));
-        if (next == 2 * n && prev != 2 * n - 1)
-          mbar_wait(&empty[(2 * n - 1) % KSTAGES], (uint32_t)(((2 * n - 1) / KSTAGES) & 1));
-        issue(next);
-      }
-    }
-  };
-
-  const int64_t mc = live ? mv.model_of(p) : 0;
-  const Vec3d grav = live ? mv.gravity(mc) : mk(0, 0, 0);
-  SE3d X;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) X.R.m[k] = (k % 4 == 0) ? 1.0 : 0.0;
-  X.p = mk(0, 0, 0);
-  Sv V0 = svzero();
-  Sv A0 = {mk(0, 0, 0), mk(-grav.x, -grav.y, -grav.z)};
-  {  // F0 = 0 in TMEM
-    double z[6] = {0, 0, 0, 0, 0, 0};
-    uint32_t r[12];
-    pack_doubles<6>(z, r);
-    uint32_t r8[8], r4[4];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r8[j] = r[j];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) r4[j] = r[8 + j];
-    tmem_st8(tm + 54, r8);
-    tmem_st4(tm + 62, r4);
-    tmem_st8(tm + 42, r8);  // Z0 = 0
-    tmem_st4(tm + 50, r4);
-  }
-  int k = 0;
-  for (; k < n; ++k) {  // pass A (base -> tip)
-    const int s = k % KSTAGES;
-    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * kT + t;
-    const Sv S = stage_screw(f);
-    double sn, cs;
-    joint_angle_sincos(S, f[kQ * kT], &sn, &cs);
-    const SE3d rel = stage_rel(f, sn, cs);
-    X = compose(rel, X);
-    const Sv S0 = adinv_screw(X, S);
-    const double qd = f[kQD * kT];
-    V0 = svfma(qd, S0, V0);
-    A0 = adv_acc(V0, qd * S0, A0);
-    if (k < n - KSTAGES) {
+      for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
+      double rec[kRec];
+      abia_pass_b(st, i, n, row_rel<KT>(f, F_KIN, S, q, sn, cs), S, f[(F_COUNT + 1) * KT], J, f[(F_COUNT + 2) * KT],
+                  rec);
       if (live) {
-        double* a = scratch + ((int64_t)n * kSC0 + 2 * k) * scr_ld + p;
-        st_hint(a, sn, pol_last);
-        st_hint(a + scr_ld, cs, pol_last);
-      }
-    } else {  // links n-1, n-2: TMEM slots 66 + 4*(n-1-k)
-      const double sc[2] = {sn, cs};
-      uint32_t r[4];
-      pack_doubles<2>(sc, r);
-      tmem_st4(tm + 66 + 4 * (n - 1 - k), r);
-    }
-    if (k == n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");
-    after_step(k);
-  }
-  int code = PD_SLOT_OK, eidx = 0;
-  for (; k < 2 * n; ++k) {  // pass B (tip -> base)
-    const int s = k % KSTAGES;
-    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * kT + t;
-    const int i = 2 * n - 1 - k;
-    double sn = f[kSIN * kT], cs = f[kCOS * kT];
-    if (i >= n - KSTAGES) {
-      uint32_t r[4];
-      tmem_ld_wait4(tm + 66 + 4 * (n - 1 - i), r);
-      double sc[2];
-      unpack_doubles<2>(r, sc);
-      sn = sc[0];
-      cs = sc[1];
-    }
-    const Sv S = stage_screw(f);
-    const double qd = f[kQD * kT];
-    const SE3d rel = stage_rel(f, sn, cs);
-    const Sv S0 = adinv_screw(X, S);
-    Inertia Jl;
-    Jl.m = f[F_MASS * kT];
-    Jl.c = mk(f[F_COM * kT], f[(F_COM + 1) * kT], f[(F_COM + 2) * kT]);
-#pragma unroll
-    for (int j = 0; j < 6; ++j) Jl.I[j] = f[(F_IC + j) * kT];
-    const Inertia J0 = inertia_to_base(Jl, X);
-    const Vec3d qshift = -1.0 * mulT(X.R, X.p);  // for the link-frame trace
-    X = step_back(rel, X);                        // X_{i-1}
-    // wrench sum and bias torque           inverse_dynamics.cpp:103-112,146-150
-    double tau_delta;
-    {
-      uint32_t r[12];
-      tmem_ld_wait12(tm + 54, r);
-      double fv[6];
-      unpack_doubles<6>(r, fv);
-      Sv F0 = {mk(fv[0], fv[1], fv[2]), mk(fv[3], fv[4], fv[5])};
-      const Sv h = inertia_apply(J0, V0);
-      F0 = neg_advT_acc(V0, h, inertia_apply_acc(J0, A0, F0));
-      tau_delta = f[kTAU * kT] - dot(S0, F0);
-      const double fo[6] = {F0.a.x, F0.a.y, F0.a.z, F0.l.x, F0.l.y, F0.l.z};
-      pack_doubles<6>(fo, r);
-      uint32_t r8[8], r4[4];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r8[j] = r[j];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) r4[j] = r[8 + j];
-      tmem_st8(tm + 54, r8);
-      tmem_st4(tm + 62, r4);
-    }
-    // parent's link states
-    const Sv rate0 = qd * S0;
-    A0 = adv_acc(V0, -1.0 * rate0, A0);
-    V0 = svfma(-qd, S0, V0);
-    // articulated inertia, z sweep, u            forward_dynamics.cpp:136-212
-    {
-      Sym6 Ia = inertia_sym6(J0);
-      double zv[6] = {0, 0, 0, 0, 0, 0};
-      uint32_t r[54];
-      tmem_ld_wait54(tm + 0, r);
-      double pz[27];
-      unpack_doubles<27>(r, pz);
-      if (i < n - 1) {
-#pragma unroll
-        for (int j = 0; j < 6; ++j) Ia.A[j] += pz[j];
-#pragma unroll
-        for (int j = 0; j < 9; ++j) Ia.B[j] += pz[6 + j];
-#pragma unroll
-        for (int j = 0; j < 6; ++j) Ia.D[j] += pz[15 + j];
-      }
-#pragma unroll
-      for (int j = 0; j < 6; ++j) zv[j] = pz[21 + j];
-      const Sv Z0 = {mk(zv[0], zv[1], zv[2]), mk(zv[3], zv[4], zv[5])};
-      const Sv U = sym6_apply(Ia, S0);
-      const double lambda = dot(S0, U);
-      // link-frame trace of Ia (shift q = -R^T p of X_i)
-      const double trD = Ia.D[0] + Ia.D[3] + Ia.D[5];
-      const double trBq = qshift.x * (Ia.B[5] - Ia.B[7]) + qshift.y * (Ia.B[6] - Ia.B[2]) +
-                          qshift.z * (Ia.B[1] - Ia.B[3]);
-      const double trI = Ia.A[0] + Ia.A[3] + Ia.A[5] + 2.0 * trBq - dot(qshift, sym3_mul(Ia.D, qshift)) +
-                         dot(qshift, qshift) * trD + trD;
-      if (!(lambda > 1e-14 * trI) && code == PD_SLOT_OK) {
-        code = PD_SLOT_DEGENERATE_ARTICULATION;
-        eidx = i;
-      }
-      const double inv_l = 1.0 / lambda;
-      const double u = (tau_delta - dot(S0, Z0)) * inv_l;
-      const Sv g0 = inv_l * U;
-      if (live) {
-        const double rec[kRec] = {g0.a.x, g0.a.y, g0.a.z, g0.l.x, g0.l.y, g0.l.z,
-                                  S0.a.x, S0.a.y, S0.a.z, S0.l.x, S0.l.y, S0.l.z, u};
 #pragma unroll
         for (int j = 0; j < kRec; ++j) st_hint(scratch + ((int64_t)i * kRec + j) * scr_ld + p, rec[j], pol_last);
       }
-      if (i > 0) {
-        const Sv Zn = svfma(u, U, Z0);
-        const double ua[3] = {U.a.x, U.a.y, U.a.z}, ul[3] = {U.l.x, U.l.y, U.l.z};
-        const double ga[3] = {g0.a.x, g0.a.y, g0.a.z}, gl[3] = {g0.l.x, g0.l.y, g0.l.z};
-        const int sidx[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+      if (k == 2u * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
+      release();
+    }
+    for (; k < total; ++k) {  // pass C
+      const double* f = acquire(k);
+      const int i = (int)k - 2 * n;
+      double rec[kRec];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          pz[j] = fma(-ua[sidx[j][0]], ga[sidx[j][1]], Ia.A[j]);
-          pz[15 + j] = fma(-ul[sidx[j][0]], gl[sidx[j][1]], Ia.D[j]);
-        }
-#pragma unroll
-        for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) pz[6 + 3 * rr + cc] = fma(-ua[rr], gl[cc], Ia.B[3 * rr + cc]);
-        pz[21] = Zn.a.x;
-        pz[22] = Zn.a.y;
-        pz[23] = Zn.a.z;
-        pz[24] = Zn.l.x;
-        pz[25] = Zn.l.y;
-        pz[26] = Zn.l.z;
-        pack_doubles<27>(pz, r);
-        uint32_t r32[32], r16[16], r4[4], r2[2];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r32[j] = r[j];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) r16[j] = r[32 + j];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) r4[j] = r[48 + j];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) r2[j] = r[52 + j];
-        tmem_st16(tm + 0, *reinterpret_cast<uint32_t(*)[16]>(r32));
-        tmem_st16(tm + 16, *reinterpret_cast<uint32_t(*)[16]>(r32 + 16));
-        tmem_st16(tm + 32, r16);
-        tmem_st4(tm + 48, r4);
-        tmem_st2(tm + 52, r2);
+      for (int j = 0; j < kRec; ++j) rec[j] = f[j * KT];
+      const double qdd = abia_pass_c(st, rec);
+      if (live) io.put_qdd(i, p, qdd);
+      if (KT % 16 == 0 && t < kRec * (KT / 16)) {  // drop the dead records' L2 lines without write-back
+        const int row = t / (KT / 16), seg = t % (KT / 16);
+        const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
+        if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
       }
+      release();
     }
-    if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");
-    after_step(k);
-  }
-  Sv a0 = svzero();
-  for (; k < total; ++k) {  // pass C (base -> tip)
-    const int s = k % KSTAGES;
-    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * kT + t;
-    const int i = k - 2 * n;
-    const Sv g0 = {mk(f[0], f[kT], f[2 * kT]), mk(f[3 * kT], f[4 * kT], f[5 * kT])};
-    const Sv S0 = {mk(f[6 * kT], f[7 * kT], f[8 * kT]), mk(f[9 * kT], f[10 * kT], f[11 * kT])};
-    const double qdd = f[12 * kT] - dot(g0, a0);
-    a0 = svfma(qdd, S0, a0);
-    if (live) io.put_qdd(i, p, qdd);
-    if (t < kRec * (kT * 8 / 128)) {
-      const int row = t / (kT * 8 / 128), seg = t % (kT * 8 / 128);
-      const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
-      if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
+    if (live) {
+      const int32_t ms = __ldg(mv.mstatus + mc);
+      io.status[p] = ms != PD_SLOT_OK ? ms : st.code;
+      io.eround[p] = 0;
+      io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : st.eidx;
     }
-    after_step(k);
   }
-  if (live) {
-    const int32_t ms = __ldg(mv.mstatus + mc);
-    io.status[p] = ms != PD_SLOT_OK ? ms : code;
-    io.eround[p] = 0;
-    io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : eidx;
-  }
-  tmem_wait_st();
-  tmem_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem_base, kTmemCols);
 }
 
 // ---------------------------------------------------------------- host side
@@ -836,7 +564,7 @@ bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scr
   {
     const cuuint64_t dims[3] = {(cuuint64_t)mv.M, (cuuint64_t)n, (cuuint64_t)F_COUNT};
     const cuuint64_t str[2] = {(cuuint64_t)mv.ld * 8, (cuuint64_t)mv.ld * n * 8};
-    const cuuint32_t box_all[3] = {kt, 1, 28}, box_kin[3] = {kt, 1, 18};
+    const cuuint32_t box_all[3] = {kt, 1, F_COUNT}, box_kin[3] = {kt, 1, F_NKIN};
     if (!encode(&maps.model_all, mv.f, 3, dims, str, box_all)) return false;
     if (!encode(&maps.model_kin, mv.f, 3, dims, str, box_kin)) return false;
   }
@@ -881,14 +609,23 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
   if (io.B >= (1ll << 31) || (int64_t)mv.n * kRec >= (1ll << 31)) return false;
   int v = abia_variant();
   if (v < 0) {
-    // Tile choice by wave balance. One CTA = one chain tile; an SM holds 256
-    // resident chains with 128-chain tiles (2 CTAs) or 224 with one 224-chain
-    // CTA. Pick the tiling whose last wave is fullest.
-    auto waste = [&](int per_sm) {
-      const double waves = (double)io.B / ((double)sm_count() * per_sm);
-      return std::ceil(waves) - waves;
-    };
-    v = waste(224) < waste(256) ? 4 : 0;
+    // Persistent ring kernel; tile by the makespan estimate: with more tiles
+    // than SMs the SM throughput is shared by its resident CTAs, so a tile
+    // costs KT * ctas chain-units per wave; with fewer tiles than SMs each
+    // tile runs alone and costs KT.
+    struct Cfg { int v, kt, ctas; };
+    const Cfg cfgs[3] = {{12, 224, 1}, {14, 96, 2}, {15, 64, 3}};
+    double best = 1e300;
+    for (const Cfg& c : cfgs) {
+      const int64_t tiles = (io.B + c.kt - 1) / c.kt;
+      const int64_t slots = (int64_t)sm_count() * c.ctas;
+      const double cost = tiles <= sm_count() ? (double)c.kt
+                                              : (double)((tiles + slots - 1) / slots) * c.kt * c.ctas;
+      if (cost < best) {
+        best = cost;
+        v = c.v;
+      }
+    }
   }
   if (v >= 10) {
     // ring kernels: (tile, CTAs per SM) per variant; the ring takes the SM's shared memory
@@ -898,9 +635,11 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
     if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
     const size_t smem = (size_t)(220 * 1024 / ctas) / (kt * 8) * (kt * 8);
     const uint32_t cap_rows = (uint32_t)(smem / (kt * 8));
+    const int64_t ntiles = (io.B + kt - 1) / kt;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * ctas);  // persistent CTAs
     auto go = [&](auto kernel) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kernel<<<(unsigned)((io.B + kt - 1) / kt), (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
+      kernel<<<grid, (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
     };
     switch (v) {
       case 11: go(abia_ring_kernel<128, 1, true>); break;
@@ -923,7 +662,6 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
   switch (v) {
     case 1: go(abia_tma_kernel<2, 3, 1, 128>, 2); break;
     case 2: go(abia_tma_kernel<3, 2, 0, 128>, 3); break;
-    case 3: go(abia_tma_tmem_kernel, 2); break;
     case 4: go(abia_tma_kernel<3, 1, 1, 224>, 3); break;
     // L2-retention experiments: pass-A model loads evict_last, demoted by pass B
     case 5: go(abia_tma_kernel<3, 1, 3, 224>, 3); break;

@@ -227,7 +227,8 @@ __device__ __forceinline__ void cta_kinematics(const ModelView& mv, const BatchI
   const int n = mv.n;
   const int i0 = threadIdx.x * lpt, i1 = min(n, i0 + lpt);
   for (int i = i0; i < i1; ++i) {
-    const SE3d T = joint_transform(mv.screw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p));
+    const SE3d T = joint_transform(mv.screw(i, mc), mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc),
+                                   io.ld(io.q, i, p));
     ws_put_se3(ws, n, F.rel, i, T);
     ws_put_se3(ws, n, F.x, i, T);
   }

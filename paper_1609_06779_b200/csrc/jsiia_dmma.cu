@@ -78,21 +78,25 @@ __device__ __forceinline__ void potrf_inv8(double (&c)[2], double (&x)[2], bool&
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     const int tm = m >> 1, e = m & 1;
-    const double d = shfl(c[e], 4 * m + tm);
+    // every operand of step m is fetched unscaled at once and scaled locally,
+    // so one shuffle latency and one rsqrt sit on the pivot-to-pivot path
+    const double d = shfl(c[e], 4 * m + tm);                                  // A[m][m]
+    const double ag = shfl(c[e], 4 * g + tm);                                 // A[g][m]
+    const double ac0 = shfl(c[e], 8 * t + tm), ac1 = shfl(c[e], 8 * t + 4 + tm);  // A[2t][m], A[2t+1][m]
+    const double xu0 = shfl(x[0], 4 * m + t), xu1 = shfl(x[1], 4 * m + t);   // X[m][2t], X[m][2t+1]
     spd = spd && (d > 0.0);
-    const double l = sqrt(d), il = 1.0 / l;
-    if (t == tm) c[e] = (g == m) ? l : ((g > m) ? c[e] * il : c[e]);
-    const double lg = shfl(c[e], 4 * g + tm);
-    const double lc0 = shfl(c[e], 8 * t + tm), lc1 = shfl(c[e], 8 * t + 4 + tm);
+    const double il = rsqrt(d);  // 1 / L[m][m]; L[m][m] itself is never needed again
+    const double lg = ag * il, lc0 = ac0 * il, lc1 = ac1 * il;
+    if (t == tm) c[e] = (g == m) ? d * il : ((g > m) ? lg : c[e]);
     if (g > m) {
       if (2 * t > m) c[0] = fma(-lg, lc0, c[0]);
       if (2 * t + 1 > m) c[1] = fma(-lg, lc1, c[1]);
     }
+    const double xm0 = xu0 * il, xm1 = xu1 * il;  // row m of L^{-1}
     if (g == m) {
-      x[0] *= il;
-      x[1] *= il;
+      x[0] = xm0;
+      x[1] = xm1;
     }
-    const double xm0 = shfl(x[0], 4 * m + t), xm1 = shfl(x[1], 4 * m + t);
     if (g > m) {
       x[0] = fma(-lg, xm0, x[0]);
       x[1] = fma(-lg, xm1, x[1]);
@@ -131,8 +135,28 @@ __device__ __forceinline__ Vk<K> warp_excl(Vk<K> x, int lane) {
 
 // Inclusive (or exclusive) scan of K-vectors over the chain's links, lane l
 // holding links l*LPL + e; REV = suffix sums.
+template <int K, bool REV>
+__device__ __forceinline__ Vk<K> warp_incl(Vk<K> x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Vk<K> y;
+#pragma unroll
+    for (int k = 0; k < K; ++k) y.v[k] = REV ? __shfl_down_sync(kFull, x.v[k], d) : __shfl_up_sync(kFull, x.v[k], d);
+    const bool take = REV ? (lane + d < 32) : (lane >= d);
+    if (take) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) x.v[k] += y.v[k];
+    }
+  }
+  return x;
+}
+
 template <int K, int LPL, bool REV, bool INCL>
 __device__ __forceinline__ void link_scan(Vk<K> (&a)[LPL], int lane) {
+  if (LPL == 1 && INCL) {
+    a[0] = warp_incl<K, REV>(a[0], lane);
+    return;
+  }
   Vk<K> tot;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -209,14 +233,14 @@ __global__ void __launch_bounds__(32 * kDWarps) jsiia_dmma_kernel(ModelView mv, 
       const bool on = i < n;
       const int li = on ? i : 0;
       auto F = [&](int f) { return on ? __ldg(m + f * n + li) : 0.0; };
-      S[e] = {mk(F(F_SCREW), F(F_SCREW + 1), F(F_SCREW + 2)), mk(F(F_SCREW + 3), F(F_SCREW + 4), F(F_SCREW + 5))};
+      S[e] = joint_screw(F(F_SW), F(F_SVX), F(F_SVZ));
       Mat3d HR;
 #pragma unroll
       for (int j = 0; j < 9; ++j) HR.m[j] = F(F_HR + j);
       const double q = on ? io.ld(io.q, li, p) : 0.0;
       qd[e] = on ? io.ld(io.qd, li, p) : 0.0;
       tau[e] = on ? io.ld(io.tau, li, p) : 0.0;
-      rel[e] = joint_transform(S[e], HR, mk(F(F_HP), F(F_HP + 1), F(F_HP + 2)), q);
+      rel[e] = joint_transform(S[e], F(F_SIW), HR, mk(F(F_HP), F(F_HP + 1), F(F_HP + 2)), q);
       if (!on) {
 #pragma unroll
         for (int k = 0; k < 9; ++k) rel[e].R.m[k] = (k % 4 == 0) ? 1.0 : 0.0;

@@ -123,14 +123,14 @@ __global__ void __launch_bounds__(32 * kWarps) jsiia_warp_kernel(ModelView mv, c
   auto F = [&](int f) { return on ? __ldg(m + f * n + li) : 0.0; };
 
   // ---- kinematics, X prefix --------------------------------------------------
-  const Sv S = {mk(F(F_SCREW), F(F_SCREW + 1), F(F_SCREW + 2)), mk(F(F_SCREW + 3), F(F_SCREW + 4), F(F_SCREW + 5))};
+  const Sv S = joint_screw(F(F_SW), F(F_SVX), F(F_SVZ));
   Mat3d HR;
 #pragma unroll
   for (int j = 0; j < 9; ++j) HR.m[j] = F(F_HR + j);
   const double q = on ? io.ld(io.q, li, p) : 0.0;
   const double qd = on ? io.ld(io.qd, li, p) : 0.0;
   const double tau = on ? io.ld(io.tau, li, p) : 0.0;
-  SE3d rel = joint_transform(S, HR, mk(F(F_HP), F(F_HP + 1), F(F_HP + 2)), q);
+  SE3d rel = joint_transform(S, F(F_SIW), HR, mk(F(F_HP), F(F_HP + 1), F(F_HP + 2)), q);
   if (!on) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) rel.R.m[k] = (k % 4 == 0) ? 1.0 : 0.0;

@@ -29,9 +29,9 @@ struct ModelView {
     return mk(__ldg(g + mc), __ldg(g + gld + mc), __ldg(g + 2 * gld + mc));
   }
   __device__ __forceinline__ Sv screw(int i, int64_t mc) const {
-    return {mk(at(F_SCREW, i, mc), at(F_SCREW + 1, i, mc), at(F_SCREW + 2, i, mc)),
-            mk(at(F_SCREW + 3, i, mc), at(F_SCREW + 4, i, mc), at(F_SCREW + 5, i, mc))};
+    return joint_screw(at(F_SW, i, mc), at(F_SVX, i, mc), at(F_SVZ, i, mc));
   }
+  __device__ __forceinline__ double screw_iw(int i, int64_t mc) const { return at(F_SIW, i, mc); }
   __device__ __forceinline__ Mat3d home_R(int i, int64_t mc) const {
     Mat3d R;
 #pragma unroll

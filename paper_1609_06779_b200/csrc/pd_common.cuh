@@ -15,16 +15,24 @@
 
 namespace pd {
 
-// Packed device model record, 28 doubles per link, stored SoA as
-// model[(field * n_links + link) * n_models + chain] (chain fastest).
+// Packed device model record, 26 doubles per link, stored SoA as
+// model[(field * n_links + link) * n_models + chain] (chain fastest), in the
+// joint-aligned link frames of capi.cu pack_models_kernel: the screw is
+// (0, 0, w, vx, 0, vz) and only its three free components are stored, with
+// 1/w beside them. The kinematic fields F_SW..F_HP are contiguous.
 enum ModelField : int {
   F_MASS = 0,
   F_COM = 1,    // 3
   F_IC = 4,     // 6: xx xy xz yy yz zz (rotational inertia about the COM)
-  F_SCREW = 10, // 6: angular, linear
-  F_HR = 16,    // 9: home rotation, row-major
-  F_HP = 25,    // 3: home translation
-  F_COUNT = 28
+  F_SW = 10,    // |w| of the joint screw
+  F_SVX = 11,   // v'x
+  F_SVZ = 12,   // v'z
+  F_SIW = 13,   // 1/|w| (0 for a pure translation, |w| < 1e-12)
+  F_HR = 14,    // 9: home rotation, row-major
+  F_HP = 23,    // 3: home translation
+  F_COUNT = 26,
+  F_KIN = F_SW,     // first kinematic field
+  F_NKIN = 16       // kinematic fields (screw, 1/w, home)
 };
 
 struct Vec3d {
@@ -294,8 +302,9 @@ __device__ __forceinline__ void joint_angle_sincos(const Sv& S, double q, double
   sincos(w * (-q), st, ct);
 }
 
-__device__ __forceinline__ SE3d joint_transform_sc(const Sv& S, const Mat3d& HR, Vec3d hp, double q, double st,
-                                                   double ct) {
+// iw = 1/w from the packed model (F_SIW)
+__device__ __forceinline__ SE3d joint_transform_sc(const Sv& S, double iw, const Mat3d& HR, Vec3d hp, double q,
+                                                   double st, double ct) {
   const double w = S.a.z, vx = S.l.x, vz = S.l.z;
   Vec3d t;
   double c = ct, s = st;
@@ -304,7 +313,6 @@ __device__ __forceinline__ SE3d joint_transform_sc(const Sv& S, const Mat3d& HR,
     s = 0.0;
     t = mk(-q * vx, 0.0, -q * vz);
   } else {
-    const double iw = 1.0 / w;
     t = mk(vx * (st * iw), vx * ((1.0 - ct) * iw), -q * vz);
   }
   SE3d T;
@@ -318,11 +326,14 @@ __device__ __forceinline__ SE3d joint_transform_sc(const Sv& S, const Mat3d& HR,
   return T;
 }
 
-__device__ __forceinline__ SE3d joint_transform(const Sv& S, const Mat3d& HR, Vec3d hp, double q) {
+__device__ __forceinline__ SE3d joint_transform(const Sv& S, double iw, const Mat3d& HR, Vec3d hp, double q) {
   double st, ct;
   joint_angle_sincos(S, q, &st, &ct);
-  return joint_transform_sc(S, HR, hp, q, st, ct);
+  return joint_transform_sc(S, iw, HR, hp, q, st, ct);
 }
+
+// joint screw from its stored components
+__device__ __forceinline__ Sv joint_screw(double w, double vx, double vz) { return {mk(0.0, 0.0, w), mk(vx, 0.0, vz)}; }
 
 // Ad(R,p)^{-1} S for a joint-aligned screw S = (0, 0, w, vx, 0, vz):
 // (w R^T e_z, R^T (v - p x w e_z)), p x (w e_z) = w (py, -px, 0)
