@@ -13,7 +13,10 @@
 //   jsiia_/abia_/cfa_forward_dynamics  forward_dynamics.hpp:38-42, 58-62, 98-101
 //   FdProblem / FdResult           forward_dynamics.hpp:111-123
 //   batch_forward_dynamics(...)    forward_dynamics.hpp:125-126
-//   inverse_dynamics / bias_torque inverse_dynamics.hpp:71-78 (default IdOptions)
+//   Twist / Wrench                 spatial.hpp:15-60 (stacked (angular, linear) / (moment, force))
+//   IdOptions / LinkStates         inverse_dynamics.hpp:23-34
+//   inverse_dynamics / bias_torque / link_states   inverse_dynamics.hpp:71-83
+//   joint_space_inertia            forward_dynamics.hpp:34-35 (MatrixXd stand-in)
 //   LinkSpec / RobotChain          model.hpp:17-30
 //   random_chain                   model.hpp:66-70
 //   ExecTrace                      trace.hpp:24-39
@@ -64,6 +67,37 @@ class JointVector {
 using Vec3 = std::array<double, 3>;
 using Vec6 = std::array<double, 6>;
 using Mat3 = std::array<double, 9>;  // row-major
+
+// Spatial vectors (spatial.hpp:15-60).
+struct Twist {
+  Vec3 angular{0.0, 0.0, 0.0};
+  Vec3 linear{0.0, 0.0, 0.0};
+  Vec6 stacked() const { return {angular[0], angular[1], angular[2], linear[0], linear[1], linear[2]}; }
+  static Twist from_stacked(const Vec6& v) { return {{v[0], v[1], v[2]}, {v[3], v[4], v[5]}}; }
+};
+struct Wrench {
+  Vec3 moment{0.0, 0.0, 0.0};
+  Vec3 force{0.0, 0.0, 0.0};
+  Vec6 stacked() const { return {moment[0], moment[1], moment[2], force[0], force[1], force[2]}; }
+  static Wrench from_stacked(const Vec6& v) { return {{v[0], v[1], v[2]}, {v[3], v[4], v[5]}}; }
+};
+
+// Dense row-major matrix (the Eigen::MatrixXd that joint_space_inertia returns).
+class MatrixXd {
+ public:
+  MatrixXd() = default;
+  MatrixXd(std::size_t r, std::size_t c) : r_(r), c_(c), v_(r * c, 0.0) {}
+  std::size_t rows() const { return r_; }
+  std::size_t cols() const { return c_; }
+  double& operator()(std::size_t i, std::size_t j) { return v_[i * c_ + j]; }
+  double operator()(std::size_t i, std::size_t j) const { return v_[i * c_ + j]; }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+
+ private:
+  std::size_t r_ = 0, c_ = 0;
+  std::vector<double> v_;
+};
 
 class ModelError : public std::runtime_error {
  public:
@@ -154,9 +188,27 @@ struct FdResult {
 
 std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems, FdAlgo algo);
 
+// inverse_dynamics.hpp:23-28
+struct IdOptions {
+  Twist base_velocity{};
+  Twist base_acceleration{};
+  Wrench tip_wrench{};
+  bool apply_gravity = true;
+};
+
+// inverse_dynamics.hpp:30-34
+struct LinkStates {
+  std::vector<Twist> velocity;
+  std::vector<Twist> acceleration;
+  std::vector<Wrench> force;
+};
+
 JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                             const JointVector& qddot);
+                             const JointVector& qddot, const IdOptions& opts = {});
 JointVector bias_torque(const RobotChain& chain, const JointVector& q, const JointVector& qdot);
+LinkStates link_states(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                       const JointVector& qddot, const IdOptions& opts = {});
+MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q);
 
 // ----------------------------------------------------------------- device
 namespace gpu {

@@ -21,9 +21,20 @@
  *   pd_forward_dynamics_device  same, on device-resident buffers
  *   pd_slot_message          <- FdResult::error strings (e.what() of the
  *                               reference exceptions, types.hpp:21-46)
- *   pd_inverse_dynamics      <- inverse_dynamics / bias_torque
- *                               (inverse_dynamics.hpp:71-78), default
+ *   pd_inverse_dynamics      <- inverse_dynamics(chain, q, qdot, qddot)
+ *                               (inverse_dynamics.hpp:71-74), default
  *                               IdOptions
+ *   pd_inverse_dynamics_opts <- inverse_dynamics(..., const IdOptions&)
+ *                               (inverse_dynamics.hpp:23-28,71-74;
+ *                               src/inverse_dynamics.cpp:122-173)
+ *   pd_inverse_dynamics_device  same, device buffers [link][problem]
+ *   pd_bias_torque           <- bias_torque (inverse_dynamics.hpp:77-78,
+ *                               src/inverse_dynamics.cpp:175-179)
+ *   pd_link_states           <- link_states (inverse_dynamics.hpp:81-83,
+ *                               src/inverse_dynamics.cpp:181-196)
+ *   pd_joint_space_inertia   <- joint_space_inertia(chain, q)
+ *                               (forward_dynamics.hpp:34-35,
+ *                               src/forward_dynamics.cpp:70-80)
  *
  * Layouts
  *   LinkSpec record: 31 doubles, the field order of LinkSpec (model.hpp:17-23)
@@ -129,6 +140,39 @@ pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, c
  * base motion, no tip wrench), host buffers [problem][link]. */
 pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot,
                               const double* qddot, double* tau);
+
+/* IdOptions (inverse_dynamics.hpp:23-28). Twists stack (angular, linear) in
+ * base coordinates; the tip wrench stacks (moment, force) in the last link's
+ * frame. A NULL options pointer means the defaults (zeros, gravity on). */
+typedef struct pd_id_options {
+  double base_velocity[6];
+  double base_acceleration[6];
+  double tip_wrench[6];
+  int32_t apply_gravity;
+} pd_id_options;
+
+/* Inverse dynamics with options, host buffers [problem][link]. A model that
+ * failed upload validation makes the call fail with PD_INVALID_ARGUMENT and
+ * the reference's spatial-inertia message (pd_last_error), as the
+ * reference's link_inertias throws. */
+pd_status pd_inverse_dynamics_opts(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot,
+                                   const double* qddot, const pd_id_options* opts, double* tau);
+
+/* Same on device buffers in [link][problem] layout, asynchronous. */
+pd_status pd_inverse_dynamics_device(pd_ctx* ctx, int64_t batch, const double* d_q, const double* d_qdot,
+                                     const double* d_qddot, const pd_id_options* opts, double* d_tau);
+
+/* Gravity, centrifugal and Coriolis torques (qddot = 0, default options). */
+pd_status pd_bias_torque(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, double* tau);
+
+/* Link twists, accelerations and wrenches of one inverse-dynamics evaluation,
+ * each [problem][link][6] in the reference's link frames. */
+pd_status pd_link_states(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
+                         const pd_id_options* opts, double* velocity, double* acceleration, double* force);
+
+/* Joint-space inertia matrices M(q), [problem][n][n] row-major (exactly
+ * symmetric, as the reference's 0.5 (M + M^T)). */
+pd_status pd_joint_space_inertia(pd_ctx* ctx, int64_t batch, const double* q, double* M);
 
 /* Reference error message of a slot outcome into buf (always terminated). */
 void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links, char* buf, int32_t buflen);

@@ -13,8 +13,10 @@ from .api import (  # noqa: F401
     FdAlgo,
     FdProblem,
     FdResult,
+    IdOptions,
     InvalidArgument,
     LinkSpec,
+    LinkStates,
     ModelError,
     RobotChain,
     SingularBlockError,
@@ -26,6 +28,8 @@ from .api import (  # noqa: F401
     default_context,
     forward_dynamics,
     inverse_dynamics,
+    joint_space_inertia,
     jsiia_forward_dynamics,
+    link_states,
 )
 from ._capi import LIB_PATH, LibraryMissing  # noqa: F401

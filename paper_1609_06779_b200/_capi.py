@@ -25,8 +25,15 @@ EXPORTS = (
     "pd_create", "pd_destroy", "pd_abi_version", "pd_status_string", "pd_last_error", "pd_set_stream",
     "pd_synchronize", "pd_set_models", "pd_forward_dynamics", "pd_forward_dynamics_device", "pd_inverse_dynamics",
     "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant", "pd_mix", "pd_workload_seed", "pd_random_chain",
-    "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak",
+    "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak", "pd_inverse_dynamics_opts",
+    "pd_inverse_dynamics_device", "pd_bias_torque", "pd_link_states", "pd_joint_space_inertia",
 )
+
+
+class IdOptions(C.Structure):
+    """pd_id_options (include/pardyn_c.h) <- IdOptions (inverse_dynamics.hpp:23-28)."""
+    _fields_ = [("base_velocity", C.c_double * 6), ("base_acceleration", C.c_double * 6),
+                ("tip_wrench", C.c_double * 6), ("apply_gravity", C.c_int32)]
 
 _lib = None
 _D = C.POINTER(C.c_double)
@@ -68,6 +75,18 @@ def load():
     L.pd_forward_dynamics_device.restype = C.c_int
     L.pd_inverse_dynamics.argtypes = [C.c_void_p, C.c_int64, _D, _D, _D, _D]
     L.pd_inverse_dynamics.restype = C.c_int
+    _OPT = C.POINTER(IdOptions)
+    L.pd_inverse_dynamics_opts.argtypes = [C.c_void_p, C.c_int64, _D, _D, _D, _OPT, _D]
+    L.pd_inverse_dynamics_opts.restype = C.c_int
+    L.pd_inverse_dynamics_device.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, _OPT,
+                                             C.c_void_p]
+    L.pd_inverse_dynamics_device.restype = C.c_int
+    L.pd_bias_torque.argtypes = [C.c_void_p, C.c_int64, _D, _D, _D]
+    L.pd_bias_torque.restype = C.c_int
+    L.pd_link_states.argtypes = [C.c_void_p, C.c_int64, _D, _D, _D, _OPT, _D, _D, _D]
+    L.pd_link_states.restype = C.c_int
+    L.pd_joint_space_inertia.argtypes = [C.c_void_p, C.c_int64, _D, _D]
+    L.pd_joint_space_inertia.restype = C.c_int
     L.pd_slot_message.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int32]
     L.pd_slot_message.restype = None
     L.pd_kernel_launches.argtypes = [C.c_void_p]

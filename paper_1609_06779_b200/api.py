@@ -8,7 +8,9 @@ proj/core/include/pardyn/forward_dynamics.hpp and inverse_dynamics.hpp:
   jsiia_/abia_/cfa_forward_dynamics            forward_dynamics.hpp:38-42,58-62,98-101
   FdProblem / FdResult                         forward_dynamics.hpp:111-123
   batch_forward_dynamics(problems, algo)       forward_dynamics.hpp:125-126
-  inverse_dynamics / bias_torque               inverse_dynamics.hpp:71-78
+  IdOptions / LinkStates                       inverse_dynamics.hpp:23-34
+  inverse_dynamics / bias_torque / link_states inverse_dynamics.hpp:71-83
+  joint_space_inertia(chain, q)                forward_dynamics.hpp:34-35
   LinkSpec / RobotChain                        model.hpp:17-30
   ModelError / DynamicsError / SingularBlockError(round, index)   types.hpp:21-46
   std::invalid_argument -> InvalidArgument (a ValueError)
@@ -132,6 +134,34 @@ class FdResult:
         return self.error == ""
 
 
+@dataclass
+class IdOptions:
+    """inverse_dynamics.hpp:23-28: base twist / acceleration (angular, linear),
+    tip wrench (moment, force) in the last link's frame, gravity switch."""
+    base_velocity: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    base_acceleration: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    tip_wrench: np.ndarray = field(default_factory=lambda: np.zeros(6))
+    apply_gravity: bool = True
+
+    def to_c(self) -> "_capi.IdOptions":
+        o = _capi.IdOptions()
+        for k in range(6):
+            o.base_velocity[k] = float(np.ravel(self.base_velocity)[k])
+            o.base_acceleration[k] = float(np.ravel(self.base_acceleration)[k])
+            o.tip_wrench[k] = float(np.ravel(self.tip_wrench)[k])
+        o.apply_gravity = 1 if self.apply_gravity else 0
+        return o
+
+
+@dataclass
+class LinkStates:
+    """inverse_dynamics.hpp:30-34: per-link twists, accelerations, wrenches,
+    each (n, 6) stacked (angular|moment, linear|force)."""
+    velocity: np.ndarray
+    acceleration: np.ndarray
+    force: np.ndarray
+
+
 def ceil_log2(n: int) -> int:
     k, p = 0, 1
     while p < n:
@@ -219,6 +249,49 @@ class Context:
         self._check(self._L.pd_inverse_dynamics(self._h, q.shape[0], _capi.dptr(q), _capi.dptr(qd), _capi.dptr(qdd),
                                                 _capi.dptr(tau)))
         return tau
+
+    def inverse_dynamics_opts(self, q, qdot, qddot, opts: Optional["IdOptions"] = None):
+        """(B, n) host arrays -> tau (B, n); opts None = defaults."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qdot, dtype=np.float64)
+        qdd = np.ascontiguousarray(qddot, dtype=np.float64)
+        tau = np.empty_like(q)
+        o = None if opts is None else C.byref(opts.to_c())
+        self._check(self._L.pd_inverse_dynamics_opts(self._h, q.shape[0], _capi.dptr(q), _capi.dptr(qd),
+                                                     _capi.dptr(qdd), o, _capi.dptr(tau)))
+        return tau
+
+    def inverse_dynamics_device(self, batch, d_q, d_qd, d_qdd, d_tau, opts: Optional["IdOptions"] = None):
+        """Device inverse dynamics on raw device pointers ([link][problem])."""
+        o = None if opts is None else C.byref(opts.to_c())
+        self._check(self._L.pd_inverse_dynamics_device(self._h, int(batch), d_q, d_qd, d_qdd, o, d_tau))
+
+    def bias_torque(self, q, qdot):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qdot, dtype=np.float64)
+        tau = np.empty_like(q)
+        self._check(self._L.pd_bias_torque(self._h, q.shape[0], _capi.dptr(q), _capi.dptr(qd), _capi.dptr(tau)))
+        return tau
+
+    def link_states(self, q, qdot, qddot, opts: Optional["IdOptions"] = None):
+        """(B, n) host arrays -> (velocity, acceleration, force), each (B, n, 6)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qdot, dtype=np.float64)
+        qdd = np.ascontiguousarray(qddot, dtype=np.float64)
+        B, n = q.shape
+        v, a, f = (np.empty((B, n, 6)) for _ in range(3))
+        o = None if opts is None else C.byref(opts.to_c())
+        self._check(self._L.pd_link_states(self._h, B, _capi.dptr(q), _capi.dptr(qd), _capi.dptr(qdd), o,
+                                           _capi.dptr(v), _capi.dptr(a), _capi.dptr(f)))
+        return v, a, f
+
+    def joint_space_inertia(self, q):
+        """(B, n) host array -> M (B, n, n)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        B, n = q.shape
+        M = np.empty((B, n, n))
+        self._check(self._L.pd_joint_space_inertia(self._h, B, _capi.dptr(q), _capi.dptr(M)))
+        return M
 
     def set_stream(self, stream_ptr):
         """Run on a CUDA stream (cudaStream_t as int). 0 = the legacy default
@@ -352,22 +425,64 @@ def batch_forward_dynamics(problems: Sequence[FdProblem], algo: FdAlgo, ctx: Opt
     return out
 
 
-def inverse_dynamics(chain: RobotChain, q, qdot, qddot, ctx: Optional[Context] = None) -> np.ndarray:
-    """inverse_dynamics.cpp:166-173 with default IdOptions."""
+def _id_sizes(chain: RobotChain, **vecs):
+    """inverse_dynamics.cpp:10-17 (check_length) and model.cpp:119-124."""
     n = chain.size()
-    for name, v in (("q", q), ("qdot", qdot), ("qddot", qddot)):
+    for name, v in vecs.items():
         if len(v) != n:
+            if name == "q":
+                raise InvalidArgument(f"assemble_kinematics: q has length {len(v)} but the chain has {n} links")
             raise InvalidArgument(f"{name} has length {len(v)} but the chain has {n} joints")
-    if n == 0:
-        return np.zeros(0)
+
+
+def _one_model(chain: RobotChain, ctx: Optional[Context]) -> Context:
     ctx = ctx or default_context()
     ms, mr = ctx.set_models(chain.to_records()[None], np.asarray(chain.gravity, np.float64)[None])
     if ms[0] != _capi.SLOT_OK:
-        raise InvalidArgument(_capi.slot_message(ms[0], 0, mr[0], n))
-    return ctx.inverse_dynamics(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
-                                np.asarray(qddot, np.float64)[None])[0]
+        raise InvalidArgument(_capi.slot_message(ms[0], 0, mr[0], chain.size()))
+    return ctx
+
+
+def inverse_dynamics(chain: RobotChain, q, qdot, qddot, opts: Optional[IdOptions] = None,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:166-173 (IdOptions defaults when opts is None)."""
+    _id_sizes(chain, q=q, qdot=qdot, qddot=qddot)
+    n = chain.size()
+    if n == 0:
+        return np.zeros(0)
+    ctx = _one_model(chain, ctx)
+    return ctx.inverse_dynamics_opts(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
+                                     np.asarray(qddot, np.float64)[None], opts)[0]
 
 
 def bias_torque(chain: RobotChain, q, qdot, ctx: Optional[Context] = None) -> np.ndarray:
     """inverse_dynamics.cpp:175-179."""
-    return inverse_dynamics(chain, q, qdot, np.zeros(chain.size()), ctx)
+    _id_sizes(chain, q=q, qdot=qdot)
+    if chain.size() == 0:
+        return np.zeros(0)
+    ctx = _one_model(chain, ctx)
+    return ctx.bias_torque(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None])[0]
+
+
+def link_states(chain: RobotChain, q, qdot, qddot, opts: Optional[IdOptions] = None,
+                ctx: Optional[Context] = None) -> LinkStates:
+    """inverse_dynamics.cpp:181-196."""
+    _id_sizes(chain, q=q, qdot=qdot, qddot=qddot)
+    if chain.size() == 0:
+        z = np.zeros((0, 6))
+        return LinkStates(z, z.copy(), z.copy())
+    ctx = _one_model(chain, ctx)
+    v, a, f = ctx.link_states(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
+                              np.asarray(qddot, np.float64)[None], opts)
+    return LinkStates(v[0], a[0], f[0])
+
+
+def joint_space_inertia(chain: RobotChain, q, ctx: Optional[Context] = None) -> np.ndarray:
+    """forward_dynamics.cpp:70-80: M(q), symmetric."""
+    n = chain.size()
+    if len(q) != n:
+        raise InvalidArgument("joint_space_inertia: q must have one entry per joint")
+    if n == 0:
+        return np.zeros((0, 0))
+    ctx = _one_model(chain, ctx)
+    return ctx.joint_space_inertia(np.asarray(q, np.float64)[None])[0]

@@ -211,31 +211,96 @@ std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems
   return out;
 }
 
-JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                             const JointVector& qddot) {
+namespace {
+
+void id_sizes(const RobotChain& chain, std::initializer_list<std::pair<const char*, const JointVector*>> args) {
   const std::size_t n = chain.links.size();
-  const struct {
-    const char* name;
-    const JointVector* v;
-  } args[] = {{"q", &q}, {"qdot", &qdot}, {"qddot", &qddot}};
-  for (const auto& a : args)
-    if (a.v->size() != n)
-      throw std::invalid_argument(std::string(a.name) + " has length " + std::to_string(a.v->size()) +
+  for (const auto& a : args)  // inverse_dynamics.cpp:10-17
+    if (a.second->size() != n)
+      throw std::invalid_argument(std::string(a.first) + " has length " + std::to_string(a.second->size()) +
                                   " but the chain has " + std::to_string(n) + " joints");
-  if (n == 0) return JointVector();
+}
+
+// One shared model on this thread's context; a bad link throws as
+// link_inertias -> spatial_inertia_from does (spatial.cpp:72-87).
+pd_ctx* one_model(const RobotChain& chain) {
+  const std::size_t n = chain.links.size();
   std::vector<double> links;
   for (const LinkSpec& l : chain.links) append_link(l, links);
   pd_ctx* c = ctx();
   int32_t ms = 0, mr = 0;
   check_call(c, pd_set_models(c, 1, static_cast<int32_t>(n), links.data(), chain.gravity.data(), &ms, &mr));
   if (ms != PD_SLOT_OK) throw std::invalid_argument(slot_message(ms, 0, mr, static_cast<int>(n)));
+  return c;
+}
+
+pd_id_options to_c(const IdOptions& o) {
+  pd_id_options r{};
+  const Vec6 bv = o.base_velocity.stacked(), ba = o.base_acceleration.stacked(), tw = o.tip_wrench.stacked();
+  for (int k = 0; k < 6; ++k) {
+    r.base_velocity[k] = bv[k];
+    r.base_acceleration[k] = ba[k];
+    r.tip_wrench[k] = tw[k];
+  }
+  r.apply_gravity = o.apply_gravity ? 1 : 0;
+  return r;
+}
+
+}  // namespace
+
+JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                             const JointVector& qddot, const IdOptions& opts) {
+  id_sizes(chain, {{"q", &q}, {"qdot", &qdot}, {"qddot", &qddot}});
+  const std::size_t n = chain.links.size();
+  if (n == 0) return JointVector();
+  pd_ctx* c = one_model(chain);
   JointVector tau(n);
-  check_call(c, pd_inverse_dynamics(c, 1, q.data(), qdot.data(), qddot.data(), tau.data()));
+  const pd_id_options o = to_c(opts);
+  check_call(c, pd_inverse_dynamics_opts(c, 1, q.data(), qdot.data(), qddot.data(), &o, tau.data()));
   return tau;
 }
 
 JointVector bias_torque(const RobotChain& chain, const JointVector& q, const JointVector& qdot) {
-  return inverse_dynamics(chain, q, qdot, JointVector::Zero(chain.links.size()));
+  id_sizes(chain, {{"q", &q}, {"qdot", &qdot}});
+  const std::size_t n = chain.links.size();
+  if (n == 0) return JointVector();
+  pd_ctx* c = one_model(chain);
+  JointVector tau(n);
+  check_call(c, pd_bias_torque(c, 1, q.data(), qdot.data(), tau.data()));
+  return tau;
+}
+
+LinkStates link_states(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                       const JointVector& qddot, const IdOptions& opts) {
+  id_sizes(chain, {{"q", &q}, {"qdot", &qdot}, {"qddot", &qddot}});
+  const std::size_t n = chain.links.size();
+  LinkStates out;
+  if (n == 0) return out;
+  pd_ctx* c = one_model(chain);
+  std::vector<double> v(6 * n), a(6 * n), f(6 * n);
+  const pd_id_options o = to_c(opts);
+  check_call(c, pd_link_states(c, 1, q.data(), qdot.data(), qddot.data(), &o, v.data(), a.data(), f.data()));
+  auto six = [](const std::vector<double>& x, std::size_t i) {
+    Vec6 r;
+    for (int k = 0; k < 6; ++k) r[k] = x[6 * i + k];
+    return r;
+  };
+  for (std::size_t i = 0; i < n; ++i) {
+    out.velocity.push_back(Twist::from_stacked(six(v, i)));
+    out.acceleration.push_back(Twist::from_stacked(six(a, i)));
+    out.force.push_back(Wrench::from_stacked(six(f, i)));
+  }
+  return out;
+}
+
+MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q) {
+  const std::size_t n = chain.links.size();
+  if (q.size() != n) throw std::invalid_argument("joint_space_inertia: q must have one entry per joint");
+  MatrixXd M(n, n);
+  if (n == 0) return M;
+  pd_ctx* c = one_model(chain);
+  check_call(c, pd_joint_space_inertia(c, 1, q.data(), M.data()));
+  return M;
 }
 
 }  // namespace pardyn

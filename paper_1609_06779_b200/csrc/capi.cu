@@ -11,7 +11,7 @@
 #include <string>
 #include <vector>
 
-#include "pd_batch.cuh"
+#include "frames.cuh"
 
 namespace pd {
 void launch_abia(const ModelView& mv, const BatchIO& io, double* scratch, cudaStream_t s);
@@ -28,6 +28,14 @@ bool jsiia_smem_path(int n);
 bool launch_jsiia_warp(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
 bool launch_jsiia_dmma(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
 size_t jsiia_workspace_bytes(int n);
+struct IdOpts {
+  double bv[6], ba[6], tip[6];
+  int gravity;
+};
+void launch_idyn(const ModelView& mv, const BatchIO& io, const IdOpts& o, const double* raw, double* vel, double* acc,
+                 double* frc, cudaStream_t s);
+void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count, double* d_M,
+                cudaStream_t s);
 }  // namespace pd
 
 using namespace pd;
@@ -65,9 +73,11 @@ struct pd_ctx {
   int64_t n_models = 0;
   int64_t model_ld = 0;
   DevBuf model, gravity, mstatus, mrule, raw;
+  std::vector<int32_t> h_mstatus, h_mrule;  // host copy of the upload validation
   DevBuf model_cl;        // link-fastest copy [chain][field][link] for warp-per-chain kernels
   bool model_cl_valid = false;
   // scratch
+  DevBuf states;  // link-state outputs and their host-order staging
   DevBuf abia_scratch, cta_ws, slots, io_q, io_qd, io_tau, io_qdd, io_status;
   // host-buffer path: copy-in / copy-out streams and per-chunk events
   static constexpr int kMaxChunks = 16;
@@ -91,60 +101,6 @@ pd_status cuda_fail(pd_ctx* c, cudaError_t e, const char* where) {
     cudaError_t e_ = (call);                                  \
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
   } while (0)
-
-// Joint-aligned link frames. Link i's coordinates are re-expressed in a
-// rotated frame F'_i = Q_i F_i (same origin) chosen so that its screw reads
-// S' = Ad(Q_i) S = (0, 0, |w|, v'x, 0, v'z): z' along the rotation axis (or
-// along v for a pure prismatic screw) and x' along the part of v normal to
-// it. The chain is physically unchanged: rel'_i = Q_i rel_i Q_{i-1}^T with
-// home' = (Q_i R_h Q_{i-1}^T, Q_i p_h), com' = Q_i c, Ic' = Q_i Ic Q_i^T, and
-// the base frame (Q_{-1} = I, gravity) untouched. Joint-space results (qdd,
-// tau, M, lambda, traces about the link origin) are frame invariant; the
-// kernels exploit the zeros: exp(-q S') is a rotation about z plus a
-// translation in the x-z plane (pd_common.cuh joint_transform_sc).
-__device__ void joint_frame(const double* s, double Q[9], double sz[3]) {
-  const double w2 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
-  const double v2 = s[3] * s[3] + s[4] * s[4] + s[5] * s[5];
-  double z[3] = {0.0, 0.0, 1.0};
-  if (w2 > 0.0) {
-    const double iw = 1.0 / sqrt(w2);
-    z[0] = s[0] * iw; z[1] = s[1] * iw; z[2] = s[2] * iw;
-  } else if (v2 > 0.0) {
-    const double iv = 1.0 / sqrt(v2);
-    z[0] = s[3] * iv; z[1] = s[4] * iv; z[2] = s[5] * iv;
-  }
-  // x': component u of v normal to z' (Gram-Schmidt twice, so x' is normal to
-  // z' to rounding even when u is small), else the world axis least aligned
-  // with z'. Either way |v'y| = |y'.u| is at rounding level and is stored as 0.
-  const double vz = z[0] * s[3] + z[1] * s[4] + z[2] * s[5];
-  double x[3] = {s[3] - vz * z[0], s[4] - vz * z[1], s[5] - vz * z[2]};
-  double x2 = x[0] * x[0] + x[1] * x[1] + x[2] * x[2];
-  if (!(x2 > 1e-280)) {
-    const int a = (fabs(z[0]) <= fabs(z[1]) && fabs(z[0]) <= fabs(z[2])) ? 0 : (fabs(z[1]) <= fabs(z[2]) ? 1 : 2);
-    x[0] = (a == 0) - z[a] * z[0]; x[1] = (a == 1) - z[a] * z[1]; x[2] = (a == 2) - z[a] * z[2];
-    x2 = x[0] * x[0] + x[1] * x[1] + x[2] * x[2];
-  }
-  for (int pass = 0; pass < 2; ++pass) {
-    const double ix = 1.0 / sqrt(x2);
-    x[0] *= ix; x[1] *= ix; x[2] *= ix;
-    const double xz = x[0] * z[0] + x[1] * z[1] + x[2] * z[2];
-    x[0] -= xz * z[0]; x[1] -= xz * z[1]; x[2] -= xz * z[2];
-    x2 = x[0] * x[0] + x[1] * x[1] + x[2] * x[2];
-  }
-  {
-    const double ix = 1.0 / sqrt(x2);
-    x[0] *= ix; x[1] *= ix; x[2] *= ix;
-  }
-  const double y[3] = {z[1] * x[2] - z[2] * x[1], z[2] * x[0] - z[0] * x[2], z[0] * x[1] - z[1] * x[0]};
-  for (int k = 0; k < 3; ++k) {
-    Q[k] = x[k];
-    Q[3 + k] = y[k];
-    Q[6 + k] = z[k];
-  }
-  sz[0] = sqrt(w2);                                  // |w| (the reference's w_n)
-  sz[1] = x[0] * s[3] + x[1] * s[4] + x[2] * s[5];   // v'x
-  sz[2] = vz;                                        // v'z
-}
 
 // raw [M][n][31] -> packed SoA [F_COUNT][n][M] in joint-aligned frames;
 // gravity [M][3] -> [3][M]
@@ -578,6 +534,8 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
         break;
       }
     }
+  ctx->h_mstatus = ms;
+  ctx->h_mrule = mr;
   if (model_status) std::memcpy(model_status, ms.data(), sizeof(int32_t) * n_models);
   if (model_rule) std::memcpy(model_rule, mr.data(), sizeof(int32_t) * n_models);
   std::vector<double> g(3 * n_models);
@@ -716,43 +674,190 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   return PD_OK;
 }
 
-pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
-                              double* tau) {
+namespace {
+
+IdOpts id_opts(const pd_id_options* o) {
+  IdOpts r{};
+  r.gravity = 1;
+  if (o) {
+    for (int k = 0; k < 6; ++k) {
+      r.bv[k] = o->base_velocity[k];
+      r.ba[k] = o->base_acceleration[k];
+      r.tip[k] = o->tip_wrench[k];
+    }
+    r.gravity = o->apply_gravity != 0;
+  }
+  return r;
+}
+
+// Reference behaviour for a bad model in the single-chain ID / JSI calls:
+// link_inertias -> spatial_inertia_from throws std::invalid_argument
+// (model.cpp:148-155, spatial.cpp:72-87).
+pd_status check_models(pd_ctx* ctx, int64_t batch, const char* what) {
+  if (ctx->n_models <= 0 || (ctx->n_models != 1 && ctx->n_models != batch)) {
+    ctx->last_error = std::string(what) + ": batch must equal the number of models (or use one shared model)";
+    return PD_INVALID_ARGUMENT;
+  }
+  const int64_t m_end = ctx->n_models == 1 ? 1 : batch;
+  for (int64_t m = 0; m < m_end && m < (int64_t)ctx->h_mstatus.size(); ++m)
+    if (ctx->h_mstatus[m] != PD_SLOT_OK) {
+      char buf[256];
+      pd_slot_message(ctx->h_mstatus[m], 0, ctx->h_mrule[m], ctx->n_links, buf, sizeof buf);
+      ctx->last_error = buf;
+      return PD_INVALID_ARGUMENT;
+    }
+  return PD_OK;
+}
+
+// Host-buffer inverse dynamics: [problem][link] in, [problem][link] out;
+// link states (nullable) [problem][link][6].
+pd_status run_idyn_host(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
+                        const pd_id_options* opts, double* tau, double* vel, double* acc, double* frc) {
   if (!ctx) return PD_INVALID_ARGUMENT;
-  if (batch < 0 || (batch > 0 && (!q || !qdot || !qddot || !tau))) {
+  if (batch < 0 || (batch > 0 && (!q || !qdot))) {
     ctx->last_error = "inverse dynamics: null buffer";
     return PD_INVALID_ARGUMENT;
   }
   if (batch == 0) return PD_OK;
-  if (ctx->n_models <= 0 || (ctx->n_models != 1 && ctx->n_models != batch)) {
-    ctx->last_error = "inverse dynamics: batch must equal the number of models (or use one shared model)";
-    return PD_INVALID_ARGUMENT;
-  }
+  pd_status cs = check_models(ctx, batch, "inverse dynamics");
+  if (cs != PD_OK) return cs;
   PD_CUDA(cudaSetDevice(ctx->device));
   const int n = ctx->n_links;
   const size_t bytes = sizeof(double) * (size_t)n * batch;
   const size_t half = (size_t)n * batch;
+  const bool states = vel || acc || frc;
   PD_CUDA(ctx->io_q.ensure(2 * bytes));
   PD_CUDA(ctx->io_qd.ensure(2 * bytes));
   PD_CUDA(ctx->io_tau.ensure(2 * bytes));
   PD_CUDA(ctx->io_qdd.ensure(2 * bytes));
   PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+  if (states) PD_CUDA(ctx->states.ensure(2 * 3 * 6 * bytes));
   double *sq = ctx->io_q.as<double>(), *sqd = ctx->io_qd.as<double>(), *sqdd = ctx->io_qdd.as<double>(),
          *stau = ctx->io_tau.as<double>();
   PD_CUDA(cudaMemcpyAsync(sq + half, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(sqd + half, qdot, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  PD_CUDA(cudaMemcpyAsync(sqdd + half, qddot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (qddot)
+    PD_CUDA(cudaMemcpyAsync(sqdd + half, qddot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    PD_CUDA(cudaMemsetAsync(sqdd, 0, bytes, ctx->stream));
   launch_transpose(ctx, sq + half, sq, batch, n, n, batch);
   launch_transpose(ctx, sqd + half, sqd, batch, n, n, batch);
-  launch_transpose(ctx, sqdd + half, sqdd, batch, n, n, batch);
+  if (qddot) launch_transpose(ctx, sqdd + half, sqdd, batch, n, n, batch);
   int32_t* st = ctx->io_status.as<int32_t>();
+  double* sv = states ? ctx->states.as<double>() : nullptr;  // 3 x [n][6][batch], then 3 x host-order staging
+  const size_t sn = 6 * half;
   // BatchIO: tau slot carries qddot in, qdd slot carries torques out
   BatchIO io{sq, sqd, sqdd, stau, st, st + batch, st + 2 * batch, batch, batch};
-  launch_invdyn(model_view(ctx), io, ctx->stream);
+  launch_idyn(model_view(ctx), io, id_opts(opts), ctx->raw.as<double>(), sv, sv ? sv + sn : nullptr,
+              sv ? sv + 2 * sn : nullptr, ctx->stream);
   ctx->launches++;
   PD_CUDA(cudaGetLastError());
-  launch_transpose(ctx, stau, stau + half, n, batch, batch, n);
-  PD_CUDA(cudaMemcpyAsync(tau, stau + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (tau) {
+    launch_transpose(ctx, stau, stau + half, n, batch, batch, n);
+    PD_CUDA(cudaMemcpyAsync(tau, stau + half, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  double* outs[3] = {vel, acc, frc};
+  for (int k = 0; k < 3; ++k)
+    if (outs[k]) {
+      // [link][6][problem] -> [problem][link][6]
+      launch_transpose(ctx, sv + k * sn, sv + (3 + k) * sn, 6 * (int64_t)n, batch, batch, 6 * (int64_t)n);
+      PD_CUDA(cudaMemcpyAsync(outs[k], sv + (3 + k) * sn, 6 * bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PD_OK;
+}
+
+}  // namespace
+
+pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
+                              double* tau) {
+  if (ctx && batch > 0 && (!qddot || !tau)) {
+    ctx->last_error = "inverse dynamics: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  return run_idyn_host(ctx, batch, q, qdot, qddot, nullptr, tau, nullptr, nullptr, nullptr);
+}
+
+pd_status pd_inverse_dynamics_opts(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot,
+                                   const double* qddot, const pd_id_options* opts, double* tau) {
+  if (ctx && batch > 0 && (!qddot || !tau)) {
+    ctx->last_error = "inverse dynamics: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  return run_idyn_host(ctx, batch, q, qdot, qddot, opts, tau, nullptr, nullptr, nullptr);
+}
+
+pd_status pd_bias_torque(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, double* tau) {
+  if (ctx && batch > 0 && !tau) {
+    ctx->last_error = "inverse dynamics: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  return run_idyn_host(ctx, batch, q, qdot, nullptr, nullptr, tau, nullptr, nullptr, nullptr);
+}
+
+pd_status pd_link_states(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
+                         const pd_id_options* opts, double* velocity, double* acceleration, double* force) {
+  if (ctx && batch > 0 && (!qddot || !velocity || !acceleration || !force)) {
+    ctx->last_error = "link states: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  return run_idyn_host(ctx, batch, q, qdot, qddot, opts, nullptr, velocity, acceleration, force);
+}
+
+pd_status pd_inverse_dynamics_device(pd_ctx* ctx, int64_t batch, const double* d_q, const double* d_qdot,
+                                     const double* d_qddot, const pd_id_options* opts, double* d_tau) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0 || (batch > 0 && (!d_q || !d_qdot || !d_qddot || !d_tau))) {
+    ctx->last_error = "inverse dynamics: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  pd_status cs = check_models(ctx, batch, "inverse dynamics");
+  if (cs != PD_OK) return cs;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+  int32_t* st = ctx->io_status.as<int32_t>();
+  BatchIO io{d_q, d_qdot, d_qddot, d_tau, st, st + batch, st + 2 * batch, batch, batch};
+  launch_idyn(model_view(ctx), io, id_opts(opts), ctx->raw.as<double>(), nullptr, nullptr, nullptr, ctx->stream);
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  return PD_OK;
+}
+
+pd_status pd_joint_space_inertia(pd_ctx* ctx, int64_t batch, const double* q, double* M) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0 || (batch > 0 && (!q || !M))) {
+    ctx->last_error = "joint_space_inertia: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  pd_status cs = check_models(ctx, batch, "joint_space_inertia");
+  if (cs != PD_OK) return cs;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int n = ctx->n_links;
+  const size_t bytes = sizeof(double) * (size_t)n * batch;
+  const size_t mbytes = sizeof(double) * (size_t)n * n * batch;
+  PD_CUDA(ctx->io_q.ensure(2 * bytes));
+  PD_CUDA(ctx->io_qdd.ensure(mbytes));
+  PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
+  double* sq = ctx->io_q.as<double>();
+  PD_CUDA(cudaMemcpyAsync(sq + (size_t)n * batch, q, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  launch_transpose(ctx, sq + (size_t)n * batch, sq, batch, n, n, batch);
+  PD_CUDA(ensure_model_cl(ctx));
+  ModelView mv = model_view(ctx);
+  mv.fcl = ctx->model_cl.as<double>();
+  int64_t slots = 0;
+  if (!jsiia_smem_path(n)) {
+    const size_t wsb = jsiia_workspace_bytes(n);
+    slots = cta_slots(ctx, wsb, batch);
+    PD_CUDA(ctx->cta_ws.ensure(wsb * slots));
+  }
+  int32_t* st = ctx->io_status.as<int32_t>();
+  BatchIO io{sq, sq, sq, nullptr, st, st + batch, st + 2 * batch, batch, batch};
+  launch_jsi(mv, io, ctx->cta_ws.as<double>(), slots, ctx->sm_count, ctx->io_qdd.as<double>(), ctx->stream);
+  ctx->launches += slots ? (batch + slots - 1) / slots : 1;
+  PD_CUDA(cudaGetLastError());
+  PD_CUDA(cudaMemcpyAsync(M, ctx->io_qdd.p, mbytes, cudaMemcpyDeviceToHost, ctx->stream));
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
   return PD_OK;
 }

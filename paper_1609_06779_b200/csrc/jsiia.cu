@@ -214,9 +214,11 @@ __device__ void warp_llt_solve(const double* Mb, int ld, int np, const double* i
 
 }  // namespace
 
-template <bool SMEM>
+// MOUT: joint_space_inertia (forward_dynamics.cpp:70-80) -- write M of every
+// problem to mout[p][i][j] after the build and stop (no bias torque, no solve).
+template <bool SMEM, bool MOUT = false>
 __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO io, double* __restrict__ gws,
-                                                           int64_t p_off) {
+                                                           int64_t p_off, double* __restrict__ mout = nullptr) {
   extern __shared__ __align__(16) double dyn_smem[];
   __shared__ ScanSmem scan_sm;
   __shared__ BlockReduce br;
@@ -245,7 +247,12 @@ __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO 
   // ---- kinematics + torque surplus ------------------------------------------
   const IdFields idf{jst::REL, jst::X, jst::V, jst::TMP, jst::TD};
   cta_kinematics(mv, io, p, mc, ws, idf, lpt);
-  cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);
+  if (MOUT) {  // the X_i = rel_i X_{i-1} scan the bias stage would run
+    __syncthreads();
+    ws_scan<12, false>(ws, n, jst::X, lpt, ComposeOp{}, scan_sm);
+    __syncthreads();
+  } else
+    cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);
 
   // ---- composite inertias in base coordinates ---------------------------------
   for (int i = i0; i < i1; ++i) {
@@ -295,6 +302,17 @@ __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO 
       Mb[(size_t)i * ld + j] = mij;
       if (i == j) dg[i] = mij;
     }
+  }
+  if (MOUT) {
+    __syncthreads();
+    double* out = mout + (size_t)p * n * n;
+    for (int e = t; e < n * n; e += nt) out[e] = Mb[(size_t)(e / n) * ld + e % n];
+    if (t == 0) {
+      io.status[p] = PD_SLOT_OK;
+      io.eround[p] = 0;
+      io.eindex[p] = 0;
+    }
+    return;
   }
   for (int i = t; i < npad; i += nt) vx[i] = (i < n) ? ws[jst::TD * n + i] : 0.0;
   __syncthreads();
@@ -392,6 +410,24 @@ void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t g
     for (int64_t b0 = 0; b0 < io.B; b0 += gws_slots) {
       const int64_t nb = (io.B - b0 < gws_slots) ? io.B - b0 : gws_slots;
       jsiia_tiled_kernel<false><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, b0);
+    }
+  }
+}
+
+// Joint-space inertia of every problem into d_M[p][i][j] (same build as the
+// solve path: CRBA closed form, exactly symmetric).
+void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count, double* d_M,
+                cudaStream_t s) {
+  const int n = mv.n;
+  const int nt = 32 * jsiia_warps(n, io.B, sm_count);
+  const size_t ws_bytes = jsiia_workspace_bytes(n);
+  if (jsiia_smem_path(n)) {
+    cudaFuncSetAttribute(jsiia_tiled_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
+    jsiia_tiled_kernel<true, true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, 0, d_M);
+  } else {
+    for (int64_t b0 = 0; b0 < io.B; b0 += gws_slots) {
+      const int64_t nb = (io.B - b0 < gws_slots) ? io.B - b0 : gws_slots;
+      jsiia_tiled_kernel<false, true><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, b0, d_M);
     }
   }
 }

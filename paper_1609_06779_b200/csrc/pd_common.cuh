@@ -292,6 +292,37 @@ __device__ __forceinline__ Sym6 sym6_congruence(const Sym6& P, const SE3d& T) {
 // zeros of S substituted), and rel = (E H, E h + t) mixes only two rows.
 // joint_angle_sincos gives (sin, cos) of theta (the expensive,
 // history-independent part); joint_transform_sc assembles rel from it.
+// sin / cos of x: Cody-Waite reduction by pi/2 (three-part constant, exact
+// products through FMA) and the fdlibm minimax kernels on [-pi/4, pi/4]
+// evaluated in Estrin form, so the dependent chain is ~10 FP64 ops instead of
+// a Horner chain (the joint angle sits on every pass's critical path). Error
+// <= ~1 ulp, like the reference's libm sin/cos. |x| > 2^20 (never a joint
+// angle in practice) falls back to the CUDA routine.
+__device__ __forceinline__ void fast_sincos(double x, double* s, double* c) {
+  if (!(fabs(x) < 1048576.0)) {
+    sincos(x, s, c);
+    return;
+  }
+  const double j = rint(x * 0.63661977236758134308);  // 2/pi
+  double r = fma(-j, 1.57079632673412561417e+00, x);
+  r = fma(-j, 6.07710050650619224932e-11, r);
+  r = fma(-j, 2.02226624871116645580e-21, r);
+  const double z = r * r, z2 = z * z, z4 = z2 * z2;
+  const double ps = fma(z4, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
+                        fma(z2, fma(z, 2.75573137070700676789e-06, -1.98412698298579493134e-04),
+                            fma(z, 8.33333333332248946124e-03, -1.66666666666666324348e-01)));
+  // cos kernel: 1 - z/2 + z^2 (C1 + z C2 + z^2 C3 + z^3 C4 + z^4 C5 + z^5 C6)
+  const double qc = fma(z4, fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09),
+                        fma(z2, fma(z, -2.75573143513906633035e-07, 2.48015872894767294178e-05),
+                            fma(z, -1.38888888888741095749e-03, 4.16666666666666019037e-02)));
+  const double sr = fma(r * z, ps, r);
+  const double cr = fma(z2, qc, fma(-0.5, z, 1.0));
+  const int qd = (int)(((long long)j) & 3);
+  const double sa = (qd & 1) ? cr : sr, ca = (qd & 1) ? sr : cr;
+  *s = (qd & 2) ? -sa : sa;
+  *c = ((qd + 1) & 2) ? -ca : ca;
+}
+
 __device__ __forceinline__ void joint_angle_sincos(const Sv& S, double q, double* st, double* ct) {
   const double w = S.a.z;
   if (w * w < 1e-24) {
@@ -299,7 +330,7 @@ __device__ __forceinline__ void joint_angle_sincos(const Sv& S, double q, double
     *ct = 1.0;
     return;
   }
-  sincos(w * (-q), st, ct);
+  fast_sincos(w * (-q), st, ct);
 }
 
 // iw = 1/w from the packed model (F_SIW)

@@ -161,6 +161,50 @@ int main() {
     check(pardyn::bias_torque(chain, q, qd) == pardyn::inverse_dynamics(chain, q, qd, JointVector::Zero(9)),
           "bias torque = ID(qdd = 0)");
   }
+  // IdOptions, link states, joint-space inertia vs the oracle
+  {
+    const pardyn::RobotChain chain = pardyn::random_chain(11, 3333);
+    std::mt19937_64 e(3333);
+    const JointVector q = uniform(e, 11, -3, 3), qd = uniform(e, 11, -2, 2), qdd = uniform(e, 11, -5, 5);
+    const JointVector a = uniform(e, 6, -1, 1), b = uniform(e, 6, -2, 2), w = uniform(e, 6, -3, 3);
+    pardyn::IdOptions opts;
+    opts.base_velocity = pardyn::Twist::from_stacked({a[0], a[1], a[2], a[3], a[4], a[5]});
+    opts.base_acceleration = pardyn::Twist::from_stacked({b[0], b[1], b[2], b[3], b[4], b[5]});
+    opts.tip_wrench = pardyn::Wrench::from_stacked({w[0], w[1], w[2], w[3], w[4], w[5]});
+    opts.apply_gravity = false;
+    oracle::IdOptions oo;
+    for (int k = 0; k < 6; ++k) {
+      oo.base_velocity[k] = a[k];
+      oo.base_acceleration[k] = b[k];
+      oo.tip_wrench[k] = w[k];
+    }
+    oo.apply_gravity = false;
+    const oracle::RobotChain oc = to_oracle(chain);
+    const auto want = oracle::inverse_dynamics(oc, as_vec(q), as_vec(qd), as_vec(qdd), oo);
+    check(rel_gap(pardyn::inverse_dynamics(chain, q, qd, qdd, opts), want) < 1e-12, "ID with IdOptions vs oracle");
+    const pardyn::LinkStates st = pardyn::link_states(chain, q, qd, qdd, opts);
+    const oracle::LinkStates ost = oracle::link_states(oc, as_vec(q), as_vec(qd), as_vec(qdd), oo);
+    double worst = 0.0;
+    for (int i = 0; i < 11; ++i) {
+      const pardyn::Vec6 v = st.velocity[i].stacked(), ac = st.acceleration[i].stacked(), f = st.force[i].stacked();
+      for (int k = 0; k < 6; ++k) {
+        worst = std::max(worst, std::fabs(v[k] - ost.velocity[i][k]) / std::max(1.0, std::fabs(ost.velocity[i][k])));
+        worst = std::max(worst,
+                         std::fabs(ac[k] - ost.acceleration[i][k]) / std::max(1.0, std::fabs(ost.acceleration[i][k])));
+        worst = std::max(worst, std::fabs(f[k] - ost.force[i][k]) / std::max(1.0, std::fabs(ost.force[i][k])));
+      }
+    }
+    check(worst < 1e-11, "link states vs oracle");
+    const pardyn::MatrixXd M = pardyn::joint_space_inertia(chain, q);
+    const oracle::MatX OM = oracle::joint_space_inertia(oc, as_vec(q));
+    double mg = 0.0, sym = 0.0;
+    for (int r = 0; r < 11; ++r)
+      for (int c = 0; c < 11; ++c) {
+        mg = std::max(mg, std::fabs(M(r, c) - OM(r, c)) / std::max(1.0, std::fabs(OM(r, c))));
+        sym = std::max(sym, std::fabs(M(r, c) - M(c, r)));
+      }
+    check(mg < 1e-12 && sym == 0.0, "joint-space inertia vs oracle, exactly symmetric");
+  }
   std::printf("%d failure(s)\n", failures);
   return failures;
 }
