@@ -116,9 +116,7 @@ __device__ __forceinline__ Sv stage_screw(const double* f) {
 }
 template <int KT = kT>
 __device__ __forceinline__ SE3d stage_rel(const double* f, double st, double ct) {
-  Mat3d HR;
-#pragma unroll
-  for (int j = 0; j < 9; ++j) HR.m[j] = f[(F_HR + j) * KT];
+  const Mat3d HR = quat_to_R(f[F_HQ * KT], f[(F_HQ + 1) * KT], f[(F_HQ + 2) * KT], f[(F_HQ + 3) * KT]);
   return joint_transform_sc(stage_screw<KT>(f), f[F_SIW * KT], HR, mk(f[F_HP * KT], f[(F_HP + 1) * KT], f[(F_HP + 2) * KT]),
                             f[kQ * KT], st, ct);
 }
@@ -340,22 +338,22 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return done != 0;
 }
 
-// rows r0.. = the kinematic block F_SW..F_HP: w, vx, vz, 1/w, home R (9), home p (3)
+// rows r0.. = the kinematic block F_SW..F_HP: w, vx, vz, 1/w, home quaternion (4), home p (3)
 template <int KT>
 __device__ __forceinline__ Sv row_screw(const double* f, int r0) {
   return joint_screw(f[r0 * KT], f[(r0 + 1) * KT], f[(r0 + 2) * KT]);
 }
 template <int KT>
 __device__ __forceinline__ SE3d row_rel(const double* f, int r0, const Sv& S, double q, double st, double ct) {
-  Mat3d HR;
-#pragma unroll
-  for (int j = 0; j < 9; ++j) HR.m[j] = f[(r0 + 4 + j) * KT];
-  return joint_transform_sc(S, f[(r0 + 3) * KT], HR, mk(f[(r0 + 13) * KT], f[(r0 + 14) * KT], f[(r0 + 15) * KT]), q,
+  const Mat3d HR = quat_to_R(f[(r0 + 4) * KT], f[(r0 + 5) * KT], f[(r0 + 6) * KT], f[(r0 + 7) * KT]);
+  return joint_transform_sc(S, f[(r0 + 3) * KT], HR, mk(f[(r0 + 8) * KT], f[(r0 + 9) * KT], f[(r0 + 10) * KT]), q,
                             st, ct);
 }
 
-template <int KT, int MINB, bool KEEP_A>
-__global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32, MINB)
+// MAXREG caps registers per thread (__maxnreg__) so that the wanted number of
+// CTAs fits the SM's 64K registers (e.g. 2 x 160 threads x 200).
+template <int KT, int MAXREG, bool KEEP_A>
+__global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
     abia_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
                      int64_t scr_ld, uint32_t cap_rows) {
   static_assert(KT % 16 == 0, "ring rows must stay 128-byte aligned for TMA");
@@ -629,8 +627,14 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
   }
   if (v >= 10) {
     // ring kernels: (tile, CTAs per SM) per variant; the ring takes the SM's shared memory
-    const uint32_t kt = v == 12 ? 224u : (v == 13 ? 112u : (v == 14 ? 96u : (v == 15 ? 64u : 128u)));
-    const int ctas = v == 13 ? 2 : (v == 14 ? 2 : (v == 15 ? 3 : 1));
+    const uint32_t kt = v == 12 ? 224u
+                        : (v == 13 || v == 17) ? 112u
+                        : v == 14 ? 96u
+                        : v == 15 ? 64u
+                        : v == 18 ? 160u
+                        : v == 19 ? 192u
+                                  : 128u;
+    const int ctas = (v == 13 || v == 14 || v == 16) ? 2 : (v == 15 ? 3 : 1);
     Maps maps;
     if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
     const size_t smem = (size_t)(220 * 1024 / ctas) / (kt * 8) * (kt * 8);
@@ -642,12 +646,16 @@ bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, in
       kernel<<<grid, (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
     };
     switch (v) {
-      case 11: go(abia_ring_kernel<128, 1, true>); break;
-      case 12: go(abia_ring_kernel<224, 1, false>); break;
-      case 13: go(abia_ring_kernel<112, 2, false>); break;
-      case 14: go(abia_ring_kernel<96, 2, false>); break;
-      case 15: go(abia_ring_kernel<64, 3, false>); break;
-      default: go(abia_ring_kernel<128, 1, false>); break;
+      case 11: go(abia_ring_kernel<128, 255, true>); break;
+      case 12: go(abia_ring_kernel<224, 255, false>); break;
+      case 13: go(abia_ring_kernel<112, 200, false>); break;
+      case 14: go(abia_ring_kernel<96, 248, false>); break;
+      case 15: go(abia_ring_kernel<64, 224, false>); break;
+      case 16: go(abia_ring_kernel<128, 200, false>); break;
+      case 17: go(abia_ring_kernel<112, 255, false>); break;
+      case 18: go(abia_ring_kernel<160, 255, false>); break;
+      case 19: go(abia_ring_kernel<192, 255, false>); break;
+      default: go(abia_ring_kernel<128, 255, false>); break;
     }
     return true;
   }

@@ -134,14 +134,35 @@ __global__ void pack_models_kernel(const double* __restrict__ raw, const double*
   put(F_SVX, sz[1]);
   put(F_SVZ, sz[2]);
   put(F_SIW, sz[0] * sz[0] < 1e-24 ? 0.0 : 1.0 / sz[0]);
-  // home' = (Q R_h Qp^T, Q p_h)
+  // home' = (Q R_h Qp^T, Q p_h), the rotation stored as a unit quaternion
   const double* Rh = r + 19;
   double U[9];  // Q R_h
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) U[3 * a + b] = Q[3 * a] * Rh[b] + Q[3 * a + 1] * Rh[3 + b] + Q[3 * a + 2] * Rh[6 + b];
+  double H[9];
   for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b)
-      put(F_HR + 3 * a + b, U[3 * a] * Qp[3 * b] + U[3 * a + 1] * Qp[3 * b + 1] + U[3 * a + 2] * Qp[3 * b + 2]);
+    for (int b = 0; b < 3; ++b) H[3 * a + b] = U[3 * a] * Qp[3 * b] + U[3 * a + 1] * Qp[3 * b + 1] + U[3 * a + 2] * Qp[3 * b + 2];
+  // as a unit quaternion (Shepperd: the largest of 4w^2, 4x^2, 4y^2, 4z^2 is the pivot)
+  double qw, qx, qy, qz;
+  const double tr = H[0] + H[4] + H[8];
+  if (tr >= H[0] && tr >= H[4] && tr >= H[8]) {
+    const double s = 2.0 * sqrt(fmax(1.0 + tr, 0.0));
+    qw = 0.25 * s; qx = (H[7] - H[5]) / s; qy = (H[2] - H[6]) / s; qz = (H[3] - H[1]) / s;
+  } else if (H[0] >= H[4] && H[0] >= H[8]) {
+    const double s = 2.0 * sqrt(fmax(1.0 + H[0] - H[4] - H[8], 0.0));
+    qw = (H[7] - H[5]) / s; qx = 0.25 * s; qy = (H[1] + H[3]) / s; qz = (H[2] + H[6]) / s;
+  } else if (H[4] >= H[8]) {
+    const double s = 2.0 * sqrt(fmax(1.0 + H[4] - H[0] - H[8], 0.0));
+    qw = (H[2] - H[6]) / s; qx = (H[1] + H[3]) / s; qy = 0.25 * s; qz = (H[5] + H[7]) / s;
+  } else {
+    const double s = 2.0 * sqrt(fmax(1.0 + H[8] - H[0] - H[4], 0.0));
+    qw = (H[3] - H[1]) / s; qx = (H[2] + H[6]) / s; qy = (H[5] + H[7]) / s; qz = 0.25 * s;
+  }
+  const double qn = 1.0 / sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  put(F_HQ, qw * qn);
+  put(F_HQ + 1, qx * qn);
+  put(F_HQ + 2, qy * qn);
+  put(F_HQ + 3, qz * qn);
   for (int k = 0; k < 3; ++k) put(F_HP + k, Q[3 * k] * r[28] + Q[3 * k + 1] * r[29] + Q[3 * k + 2] * r[30]);
   if (i == 0)
     for (int k = 0; k < 3; ++k) gout[(int64_t)k * M + m] = graw[m * 3 + k];

@@ -234,9 +234,7 @@ __global__ void __launch_bounds__(32 * kDWarps) jsiia_dmma_kernel(ModelView mv, 
       const int li = on ? i : 0;
       auto F = [&](int f) { return on ? __ldg(m + f * n + li) : 0.0; };
       S[e] = joint_screw(F(F_SW), F(F_SVX), F(F_SVZ));
-      Mat3d HR;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) HR.m[j] = F(F_HR + j);
+      const Mat3d HR = quat_to_R(F(F_HQ), F(F_HQ + 1), F(F_HQ + 2), F(F_HQ + 3));
       const double q = on ? io.ld(io.q, li, p) : 0.0;
       qd[e] = on ? io.ld(io.qd, li, p) : 0.0;
       tau[e] = on ? io.ld(io.tau, li, p) : 0.0;

@@ -124,9 +124,7 @@ __global__ void __launch_bounds__(32 * kWarps) jsiia_warp_kernel(ModelView mv, c
 
   // ---- kinematics, X prefix --------------------------------------------------
   const Sv S = joint_screw(F(F_SW), F(F_SVX), F(F_SVZ));
-  Mat3d HR;
-#pragma unroll
-  for (int j = 0; j < 9; ++j) HR.m[j] = F(F_HR + j);
+  const Mat3d HR = quat_to_R(F(F_HQ), F(F_HQ + 1), F(F_HQ + 2), F(F_HQ + 3));
   const double q = on ? io.ld(io.q, li, p) : 0.0;
   const double qd = on ? io.ld(io.qd, li, p) : 0.0;
   const double tau = on ? io.ld(io.tau, li, p) : 0.0;

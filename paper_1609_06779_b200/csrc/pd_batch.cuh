@@ -33,10 +33,7 @@ struct ModelView {
   }
   __device__ __forceinline__ double screw_iw(int i, int64_t mc) const { return at(F_SIW, i, mc); }
   __device__ __forceinline__ Mat3d home_R(int i, int64_t mc) const {
-    Mat3d R;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) R.m[k] = at(F_HR + k, i, mc);
-    return R;
+    return quat_to_R(at(F_HQ, i, mc), at(F_HQ + 1, i, mc), at(F_HQ + 2, i, mc), at(F_HQ + 3, i, mc));
   }
   __device__ __forceinline__ Vec3d home_p(int i, int64_t mc) const {
     return mk(at(F_HP, i, mc), at(F_HP + 1, i, mc), at(F_HP + 2, i, mc));

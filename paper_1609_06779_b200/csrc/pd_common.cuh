@@ -15,11 +15,13 @@
 
 namespace pd {
 
-// Packed device model record, 26 doubles per link, stored SoA as
+// Packed device model record, 21 doubles per link, stored SoA as
 // model[(field * n_links + link) * n_models + chain] (chain fastest), in the
 // joint-aligned link frames of capi.cu pack_models_kernel: the screw is
 // (0, 0, w, vx, 0, vz) and only its three free components are stored, with
-// 1/w beside them. The kinematic fields F_SW..F_HP are contiguous.
+// 1/w beside them; the home rotation is a unit quaternion (4 doubles instead
+// of 9: the model is streamed from HBM once per pass, so every field is
+// bandwidth). The kinematic fields F_SW..F_HP are contiguous.
 enum ModelField : int {
   F_MASS = 0,
   F_COM = 1,    // 3
@@ -28,11 +30,11 @@ enum ModelField : int {
   F_SVX = 11,   // v'x
   F_SVZ = 12,   // v'z
   F_SIW = 13,   // 1/|w| (0 for a pure translation, |w| < 1e-12)
-  F_HR = 14,    // 9: home rotation, row-major
-  F_HP = 23,    // 3: home translation
-  F_COUNT = 26,
+  F_HQ = 14,    // 4: home rotation as a unit quaternion (w, x, y, z)
+  F_HP = 18,    // 3: home translation
+  F_COUNT = 21,
   F_KIN = F_SW,     // first kinematic field
-  F_NKIN = 16       // kinematic fields (screw, 1/w, home)
+  F_NKIN = 11       // kinematic fields (screw, 1/w, home)
 };
 
 struct Vec3d {
@@ -82,6 +84,24 @@ __device__ __forceinline__ Mat3d matmul(const Mat3d& A, const Mat3d& B) {
     for (int c = 0; c < 3; ++c)
       C.m[3 * r + c] = fma(A.m[3 * r], B.m[c], fma(A.m[3 * r + 1], B.m[3 + c], A.m[3 * r + 2] * B.m[6 + c]));
   return C;
+}
+
+// Rotation matrix of a unit quaternion (w, x, y, z).
+__device__ __forceinline__ Mat3d quat_to_R(double w, double x, double y, double z) {
+  const double x2 = x + x, y2 = y + y, z2 = z + z;
+  const double xx = x * x2, yy = y * y2, zz = z * z2, xy = x * y2, xz = x * z2, yz = y * z2, wx = w * x2,
+               wy = w * y2, wz = w * z2;
+  Mat3d R;
+  R.m[0] = 1.0 - (yy + zz);
+  R.m[1] = xy - wz;
+  R.m[2] = xz + wy;
+  R.m[3] = xy + wz;
+  R.m[4] = 1.0 - (xx + zz);
+  R.m[5] = yz - wx;
+  R.m[6] = xz - wy;
+  R.m[7] = yz + wx;
+  R.m[8] = 1.0 - (xx + yy);
+  return R;
 }
 
 struct SE3d {
