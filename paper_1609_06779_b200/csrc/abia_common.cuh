@@ -34,12 +34,14 @@ __device__ __forceinline__ Inertia inertia_to_base(const Inertia& J, const SE3d&
 // trace of Ad(Y)^T P Ad(Y) for Y = X^{-1} = (R^T, -R^T p): the link-frame
 // trace the reference's degeneracy test uses (forward_dynamics.cpp:140).
 // Rotations keep traces; the shift by q = -R^T p adds 2 tr(B q^) - q^T D q + |q|^2 tr(D).
-__device__ __forceinline__ double link_frame_trace(const Sym6& P, const SE3d& X) {
-  const Vec3d q = -1.0 * mulT(X.R, X.p);
+__device__ __forceinline__ double link_frame_trace_q(const Sym6& P, const Vec3d q) {
   const double trD = P.D[0] + P.D[3] + P.D[5];
   const double trBq = q.x * (P.B[5] - P.B[7]) + q.y * (P.B[6] - P.B[2]) + q.z * (P.B[1] - P.B[3]);
   const Vec3d Dq = sym3_mul(P.D, q);
   return P.A[0] + P.A[3] + P.A[5] + 2.0 * trBq - dot(q, Dq) + dot(q, q) * trD + trD;
+}
+__device__ __forceinline__ double link_frame_trace(const Sym6& P, const SE3d& X) {
+  return link_frame_trace_q(P, -1.0 * mulT(X.R, X.p));
 }
 
 // X_{i-1} = rel_i^{-1} * X_i
