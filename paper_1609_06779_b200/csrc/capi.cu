@@ -34,6 +34,8 @@ struct IdOpts {
 };
 void launch_idyn(const ModelView& mv, const BatchIO& io, const IdOpts& o, const double* raw, double* vel, double* acc,
                  double* frc, cudaStream_t s);
+bool jsiia_coop_path(int n, int64_t batch);
+void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, cudaStream_t s);
 void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count, double* d_M,
                 cudaStream_t s);
 }  // namespace pd
@@ -369,6 +371,13 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
         break;
       }
       const size_t wsb = jsiia_workspace_bytes(n);
+      static const bool no_coop = std::getenv("PD_JSIIA_NO_COOP") != nullptr;
+      if (!no_coop && jsiia_coop_path(n, batch)) {  // long chain(s): grid-wide Cholesky
+        PD_CUDA(ctx->cta_ws.ensure(wsb * batch));
+        launch_jsiia_coop(mv, io, ctx->cta_ws.as<double>(), ctx->sm_count, ctx->stream);
+        ctx->launches += 3;
+        break;
+      }
       int64_t slots = 0;
       if (!jsiia_smem_path(n)) {
         slots = cta_slots(ctx, wsb, batch);
@@ -532,7 +541,8 @@ const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) 
     case PD_JSIIA: return n_links <= 64 ? "jsiia_dmma_kernel (warp per chain, M and blocked Cholesky on FP64 tensor cores, DMMA 8x8x4)"
                           : jsiia_smem_path(n_links)
                               ? "jsiia_tiled_kernel<smem> (CTA per chain, CRBA scans + 32x32-tile Cholesky in smem)"
-                              : "jsiia_tiled_kernel<global> (CTA per chain, 32x32-tile Cholesky, L2 workspace)";
+                              : "jsiia_tiled_kernel<global> (CTA per chain, 32x32-tile Cholesky, L2 workspace); batches "
+                                "<= 4: CTA build + grid-wide cooperative tile Cholesky (jsiia_factor_coop) + CTA solve";
   }
   return "unknown";
 }

@@ -28,6 +28,8 @@
 //    L overwrites the lower triangle; the strict upper triangle keeps M and
 //    the diagonal of M is saved, so the residual uses M itself, as the
 //    reference does.
+#include <cooperative_groups.h>
+
 #include "abia_common.cuh"
 #include "cta_common.cuh"
 
@@ -55,7 +57,7 @@ __host__ __device__ inline JstLayout jst_layout(int n) {
   L.ld = L.npad + 2;
   L.m_off = ((size_t)jst::KEEP * n + 1) & ~(size_t)1;  // 16-byte aligned
   L.v_off = L.m_off + (size_t)L.npad * L.ld;
-  size_t end = L.v_off + (size_t)jst::NVEC * L.npad;
+  size_t end = L.v_off + (size_t)jst::NVEC * L.npad + 1;  // + the cooperative path's fail flag (last double)
   const size_t phase_a = (size_t)jst::FIELDS * n;
   if (end < phase_a) end = phase_a;
   L.total = (end + 1) & ~(size_t)1;
@@ -83,10 +85,22 @@ __device__ double block_sum(double v, BlockReduce& br) {
   return s;
 }
 
+// CG: the tile lives in global memory written by other CTAs of a cooperative
+// grid -- read it through L2 (ld.global.cg), never from a stale L1 line.
+template <bool CG = false>
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return CG ? __ldcg(reinterpret_cast<const double2*>(p)) : *reinterpret_cast<const double2*>(p);
+}
+template <bool CG = false>
+__device__ __forceinline__ double ld1(const double* p) {
+  return CG ? __ldcg(p) : *p;
+}
+
+template <bool CG = false>
 __device__ __forceinline__ void load_row(double (&r)[32], const double* row) {
 #pragma unroll
   for (int j = 0; j < 32; j += 2) {
-    const double2 v = *reinterpret_cast<const double2*>(row + j);
+    const double2 v = ld2<CG>(row + j);
     r[j] = v.x;
     r[j + 1] = v.y;
   }
@@ -95,21 +109,23 @@ __device__ __forceinline__ void load_row(double (&r)[32], const double* row) {
 // Cholesky of a diagonal tile in place (lower triangle; the strict upper
 // triangle is read back unchanged). invd[i] = 1 / L_ii. Returns false iff a
 // pivot is <= 0 (Eigen LLT's failure condition). Warp-uniform result.
+template <bool CG = false>
 __device__ bool tile_potrf(double* A, int ld, double* invd, int lane) {
   double r[32];
-  load_row(r, A + lane * ld);
+  load_row<CG>(r, A + lane * ld);
   bool spd = true;
   double inv_d = 0.0;
 #pragma unroll
   for (int m = 0; m < 32; ++m) {
     double a4[4] = {r[m], 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], A[m * ld + p], a4[p & 3]);
+    for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], ld1<CG>(A + m * ld + p), a4[p & 3]);
     const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     const double dmm = __shfl_sync(0xffffffffu, acc, m);
     spd = spd && dmm > 0.0;
-    const double lmm = sqrt(dmm > 0.0 ? dmm : 1.0);
-    const double inv = 1.0 / lmm;
+    // one reciprocal square root per pivot: 1/L_mm, L_mm = d * (1/L_mm)
+    const double inv = rsqrt(dmm > 0.0 ? dmm : 1.0);
+    const double lmm = (dmm > 0.0 ? dmm : 1.0) * inv;
     inv_d = (lane == m) ? inv : inv_d;
     r[m] = (lane == m) ? lmm : ((lane > m) ? acc * inv : r[m]);
     A[lane * ld + m] = r[m];
@@ -120,15 +136,16 @@ __device__ bool tile_potrf(double* A, int ld, double* invd, int lane) {
 }
 
 // B := B L^{-T} for an off-diagonal tile B of the panel of the factored L.
+template <bool CG = false>
 __device__ void tile_trsm(const double* Lkk, int ld, const double* invd, double* B, int lane) {
   double r[32];
-  load_row(r, B + lane * ld);
+  load_row<CG>(r, B + lane * ld);
 #pragma unroll
   for (int m = 0; m < 32; ++m) {
     double a4[4] = {r[m], 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], Lkk[m * ld + p], a4[p & 3]);
-    r[m] = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * invd[m];
+    for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], ld1<CG>(Lkk + m * ld + p), a4[p & 3]);
+    r[m] = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * ld1<CG>(invd + m);
   }
 #pragma unroll
   for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(B + lane * ld + j) = make_double2(r[j], r[j + 1]);
@@ -136,15 +153,16 @@ __device__ void tile_trsm(const double* Lkk, int ld, const double* invd, double*
 
 // C -= A B^T (32x32 tiles). On a diagonal tile only the lower triangle is
 // written back (the strict upper triangle holds M).
+template <bool CG = false>
 __device__ void tile_gemm(double* C, const double* A, const double* Bt, int ld, bool diag, int lane) {
   double r[32];
-  load_row(r, C + lane * ld);
+  load_row<CG>(r, C + lane * ld);
 #pragma unroll 1
   for (int p = 0; p < 32; p += 2) {
-    const double2 a = *reinterpret_cast<const double2*>(A + lane * ld + p);
+    const double2 a = ld2<CG>(A + lane * ld + p);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const double2 b = *reinterpret_cast<const double2*>(Bt + j * ld + p);
+      const double2 b = ld2<CG>(Bt + j * ld + p);
       r[j] = fma(-a.x, b.x, r[j]);
       r[j] = fma(-a.y, b.y, r[j]);
     }
@@ -214,11 +232,17 @@ __device__ void warp_llt_solve(const double* Mb, int ld, int np, const double* i
 
 }  // namespace
 
-// MOUT: joint_space_inertia (forward_dynamics.cpp:70-80) -- write M of every
-// problem to mout[p][i][j] after the build and stop (no bias torque, no solve).
-template <bool SMEM, bool MOUT = false>
+// MODE 0: the whole solve in this CTA.
+// MODE 1: joint_space_inertia (forward_dynamics.cpp:70-80) -- write M of every
+//         problem to mout[p][i][j] after the build and stop.
+// MODE 2: build M and tau_delta in the (global) workspace and stop; the grid-
+//         wide Cholesky (jsiia_factor_coop) runs next, then MODE 3.
+// MODE 3: solve + residual contract on a workspace MODE 2 / the cooperative
+//         factorization left (fail flag in the workspace tail).
+template <bool SMEM, int MODE = 0>
 __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO io, double* __restrict__ gws,
                                                            int64_t p_off, double* __restrict__ mout = nullptr) {
+  constexpr bool MOUT = MODE == 1;
   extern __shared__ __align__(16) double dyn_smem[];
   __shared__ ScanSmem scan_sm;
   __shared__ BlockReduce br;
@@ -243,6 +267,10 @@ __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO 
   double* dg = vw + npad;
   double* invd = dg + npad;
   auto tile = [&](int I, int J) { return Mb + (size_t)(32 * I) * ld + 32 * J; };
+  if (MODE == 3) {
+    if (t == 0) s_fail = (int)ws[L.total - 1];
+    __syncthreads();
+  } else {
 
   // ---- kinematics + torque surplus ------------------------------------------
   const IdFields idf{jst::REL, jst::X, jst::V, jst::TMP, jst::TD};
@@ -282,6 +310,7 @@ __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO 
     ws_put_sv(ws, n, jst::FB, i, sym6_apply(Ic, ws_get_sv(ws, n, jst::S0, i)));
   }
   __syncthreads();
+  if (MODE == 2) return;  // M is built grid-wide by jsiia_factor_coop
 
   // ---- M_ij = S0_min(i,j) . FB_max(i,j), identity padding ---------------------
   for (int J = 0; J < np; ++J) {
@@ -340,6 +369,7 @@ __global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO 
     }
     __syncthreads();
   }
+  }  // MODE != 3
   if (s_fail) {
     if (t == 0) {
       io.status[p] = PD_SLOT_JSI_NOT_SPD;
@@ -414,6 +444,331 @@ void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t g
   }
 }
 
+// Grid-wide M build + blocked Cholesky for long chains in small batches (c4).
+// A MODE-2 build left S0, FB = Ic0 S0 and tau_delta of each chain in
+// workspace slots 0..count-1; here every warp of a cooperative grid works on
+// one chain after the other:
+//   phase 0: M tiles M_ij = S0_min . FB_max (both triangles, identity padding),
+//            diag(M), x = tau_delta -- a tile per warp task, rows staged in smem;
+//   panels:  TRSM of the panel, then the trailing update, with the next
+//            diagonal tile updated first by warp 0 and factored right away
+//            (two grid barriers per panel).
+// Tiles are staged through per-warp shared memory and read from global memory
+// through L2 (ld.global.cg, never a stale L1 line); the SPD verdict goes to
+// the slot's flag for the MODE-3 solve.
+constexpr int kTs = 34;  // smem tile leading dimension (16-byte rows)
+
+__device__ __forceinline__ void warp_tile_in(double* dst, const double* src, int ld, int lane) {
+#pragma unroll 4
+  for (int e = lane; e < 32 * 16; e += 32) {
+    const int r = e >> 4, c = (e & 15) * 2;
+    *reinterpret_cast<double2*>(dst + r * kTs + c) = __ldcg(reinterpret_cast<const double2*>(src + (size_t)r * ld + c));
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void warp_tile_out(double* dst, int ld, const double* src, int lane, bool lower_only) {
+  __syncwarp();
+#pragma unroll 4
+  for (int e = lane; e < 32 * 16; e += 32) {
+    const int r = e >> 4, c = (e & 15) * 2;
+    const double2 v = *reinterpret_cast<const double2*>(src + r * kTs + c);
+    if (!lower_only || c + 1 <= r) {
+      *reinterpret_cast<double2*>(dst + (size_t)r * ld + c) = v;
+    } else if (c <= r) {
+      dst[(size_t)r * ld + c] = v.x;
+    }
+  }
+  __syncwarp();
+}
+// r (row `lane` of C) -= row `lane` of A times B^T, A and B^T staged in smem.
+__device__ __forceinline__ void tile_gemm_rows(double (&r)[32], const double* sA, const double* sB, int lane) {
+#pragma unroll 1
+  for (int p = 0; p < 32; p += 2) {
+    const double2 a = *reinterpret_cast<const double2*>(sA + lane * kTs + p);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 b = *reinterpret_cast<const double2*>(sB + j * kTs + p);
+      r[j] = fma(-a.x, b.x, r[j]);
+      r[j] = fma(-a.y, b.y, r[j]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) jsiia_factor_coop(double* __restrict__ gws, int n, int count) {
+  namespace cgr = cooperative_groups;
+  cgr::grid_group grid = cgr::this_grid();
+  extern __shared__ __align__(16) double coop_smem[];  // per warp: A, B tiles + 32 reciprocals
+  double (*stile)[2][32 * kTs] = reinterpret_cast<double (*)[2][32 * kTs]>(coop_smem);
+  double (*sinv)[32] = reinterpret_cast<double (*)[32]>(coop_smem + 8 * 2 * 32 * kTs);
+  const JstLayout L = jst_layout(n);
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const int np = L.np, npad = L.npad, ld = L.ld;
+  double* sA = stile[wl][0];
+  double* sB = stile[wl][1];
+  for (int c = 0; c < count; ++c) {
+    double* ws = gws + (size_t)c * L.total;
+    double* Mb = ws + L.m_off;
+    double* vx = ws + L.v_off;
+    double* dg = vx + 2 * (size_t)npad;
+    double* invd = vx + 3 * (size_t)npad;
+    double* flag = ws + L.total - 1;
+    auto tile = [&](int I, int J) { return Mb + (size_t)(32 * I) * ld + 32 * J; };
+    // ---- phase 0: M = [S0_min . FB_max], identity padding, diag, x = td
+    for (int q = gw; q < np * np; q += nwarps) {
+      const int I = q / np, J = q % np;
+      // rows i = 32 I + r: S0_i (sA) and FB_i (sB), 6 doubles each, field-major in ws
+      for (int e = lane; e < 6 * 32; e += 32) {
+        const int f = e >> 5, r = e & 31, i = 32 * I + r;
+        sA[f * 32 + r] = i < n ? __ldcg(ws + (size_t)(jst::S0 + f) * n + i) : 0.0;
+        sB[f * 32 + r] = i < n ? __ldcg(ws + (size_t)(jst::FB + f) * n + i) : 0.0;
+      }
+      __syncwarp();
+      const int j = 32 * J + lane;
+      const bool jr = j < n;
+      double sj[6], fj[6];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) {
+        sj[f] = jr ? __ldcg(ws + (size_t)(jst::S0 + f) * n + j) : 0.0;
+        fj[f] = jr ? __ldcg(ws + (size_t)(jst::FB + f) * n + j) : 0.0;
+      }
+      for (int r = 0; r < 32; ++r) {
+        const int i = 32 * I + r;
+        double mij;
+        if (i < n && jr) {
+          const bool low = j <= i;  // lower: S0_j . FB_i, upper: S0_i . FB_j
+          double acc = 0.0;
+#pragma unroll
+          for (int f = 0; f < 6; ++f) acc = fma(low ? sj[f] : sA[f * 32 + r], low ? sB[f * 32 + r] : fj[f], acc);
+          mij = acc;
+        } else {
+          mij = (i == j) ? 1.0 : 0.0;
+        }
+        Mb[(size_t)i * ld + j] = mij;
+        if (i == j) dg[i] = mij;
+      }
+      __syncwarp();
+    }
+    for (int i = (int)(blockIdx.x * blockDim.x + threadIdx.x); i < npad; i += (int)(gridDim.x * blockDim.x))
+      vx[i] = i < n ? __ldcg(ws + (size_t)jst::TD * n + i) : 0.0;
+    grid.sync();
+    // ---- blocked Cholesky
+    if (gw == 0) {
+      warp_tile_in(sA, tile(0, 0), ld, lane);
+      const bool ok = tile_potrf(sA, kTs, invd, lane);
+      warp_tile_out(tile(0, 0), ld, sA, lane, true);
+      if (lane == 0) *flag = ok ? 0.0 : 1.0;
+    }
+    grid.sync();
+    for (int K = 0; K < np; ++K) {
+      if (__ldcg(flag) != 0.0) break;  // grid-uniform: forward_dynamics.cpp:93-98
+      if (K + 1 + gw < np) {
+        warp_tile_in(sA, tile(K, K), ld, lane);
+        sinv[wl][lane] = __ldcg(invd + 32 * K + lane);
+        __syncwarp();
+        for (int I = K + 1 + gw; I < np; I += nwarps) {
+          warp_tile_in(sB, tile(I, K), ld, lane);
+          tile_trsm(sA, kTs, sinv[wl], sB, lane);
+          warp_tile_out(tile(I, K), ld, sB, lane, false);
+        }
+      }
+      grid.sync();
+      const int m = np - 1 - K;  // trailing tiles (I, J), K < J <= I; task 0 = the next diagonal tile
+      const int tasks = m * (m + 1) / 2;
+      for (int q = gw; q < tasks; q += nwarps) {
+        int a = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+        while ((a + 1) * (a + 2) / 2 <= q) ++a;
+        while (a * (a + 1) / 2 > q) --a;
+        const int b = q - a * (a + 1) / 2;
+        const int I = K + 1 + a, J = K + 1 + b;
+        warp_tile_in(sA, tile(I, K), ld, lane);
+        warp_tile_in(sB, tile(J, K), ld, lane);
+        double r[32];
+        load_row<true>(r, tile(I, J) + (size_t)lane * ld);
+        tile_gemm_rows(r, sA, sB, lane);
+        if (q == 0) {  // the next diagonal tile: keep it in smem and factor it right away
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(sA + lane * kTs + j) = make_double2(r[j], r[j + 1]);
+          __syncwarp();
+          const bool ok = tile_potrf(sA, kTs, invd + 32 * (K + 1), lane);
+          warp_tile_out(tile(K + 1, K + 1), ld, sA, lane, true);
+          if (!ok && lane == 0) *flag = 1.0;
+        } else {
+          double* row = tile(I, J) + (size_t)lane * ld;
+          if (I == J) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j <= lane) row[j] = r[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(row + j) = make_double2(r[j], r[j + 1]);
+          }
+        }
+      }
+      grid.sync();
+    }
+  }
+}
+
+// Solve + residual contract (forward_dynamics.cpp:99-116) for the
+// cooperative path: one 1024-thread CTA per chain, warp J owns tile row J of
+// the right-hand side. Triangular solves by tile rows: the owner warp solves
+// its diagonal tile (shuffle recurrence against the tile staged in smem) and
+// publishes the block; after one barrier every later (earlier, for L^T) warp
+// folds it into its own block. The residual td - M x is formed tile by tile
+// from diag(M) and the strict upper triangle the factorization left intact.
+constexpr int kWideWarps = 32;
+
+__device__ void wide_llt_solve(const double* Mb, int ld, int np, const double* invd, double* v, double* sT,
+                               int warp, int lane) {
+  // forward: L y = v
+  for (int I = 0; I < np; ++I) {
+    if (warp == I % kWideWarps) {
+      for (int e = lane; e < 32 * 32; e += 32) sT[(e >> 5) * 33 + (e & 31)] = Mb[(size_t)(32 * I + (e >> 5)) * ld + 32 * I + (e & 31)];
+      __syncwarp();
+      double acc = v[32 * I + lane], yo = 0.0;
+      const double id = invd[32 * I + lane];
+#pragma unroll 8
+      for (int m = 0; m < 32; ++m) {
+        const double ym = __shfl_sync(0xffffffffu, acc * id, m);
+        yo = (lane == m) ? ym : yo;
+        acc = (lane > m) ? fma(-sT[lane * 33 + m], ym, acc) : acc;
+      }
+      v[32 * I + lane] = yo;
+    }
+    __syncthreads();
+    for (int J = I + 1 + ((warp - I - 1) % kWideWarps + kWideWarps) % kWideWarps; J < np; J += kWideWarps) {
+      const double* row = Mb + (size_t)(32 * J + lane) * ld + 32 * I;
+      const double* y = v + 32 * I;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < 32; c += 2) {
+        const double2 a = *reinterpret_cast<const double2*>(row + c);
+        acc = fma(a.x, y[c], fma(a.y, y[c + 1], acc));
+      }
+      v[32 * J + lane] -= acc;
+    }
+  }
+  __syncthreads();
+  // backward: L^T x = y
+  for (int I = np - 1; I >= 0; --I) {
+    if (warp == I % kWideWarps) {
+      for (int e = lane; e < 32 * 32; e += 32) sT[(e >> 5) * 33 + (e & 31)] = Mb[(size_t)(32 * I + (e >> 5)) * ld + 32 * I + (e & 31)];
+      __syncwarp();
+      double acc = v[32 * I + lane], xo = 0.0;
+      const double id = invd[32 * I + lane];
+#pragma unroll 8
+      for (int m = 31; m >= 0; --m) {
+        const double xm = __shfl_sync(0xffffffffu, acc * id, m);
+        xo = (lane == m) ? xm : xo;
+        acc = (lane < m) ? fma(-sT[m * 33 + lane], xm, acc) : acc;
+      }
+      v[32 * I + lane] = xo;
+    }
+    __syncthreads();
+    // y_K -= L_IK^T x_I for K < I: lane = row k of tile K, column reads of L_IK (coalesced)
+    for (int K = warp; K < I; K += kWideWarps) {
+      const double* col = Mb + (size_t)(32 * I) * ld + 32 * K + lane;
+      const double* x = v + 32 * I;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < 32; ++c) acc = fma(col[(size_t)c * ld], x[c], acc);
+      v[32 * K + lane] -= acc;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(32 * kWideWarps) jsiia_solve_wide(BatchIO io, double* __restrict__ gws, int n) {
+  __shared__ double sT[32 * 33];
+  __shared__ BlockReduce br;
+  const JstLayout L = jst_layout(n);
+  const int64_t p = blockIdx.x;
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
+  double* ws = gws + (size_t)blockIdx.x * L.total;
+  const int np = L.np, npad = L.npad, ld = L.ld;
+  const double* Mb = ws + L.m_off;
+  double* vx = ws + L.v_off;
+  double* vw = vx + npad;
+  const double* dg = vx + 2 * (size_t)npad;
+  const double* invd = vx + 3 * (size_t)npad;
+  if (ws[L.total - 1] != 0.0) {  // forward_dynamics.cpp:93-98
+    if (t == 0) {
+      io.status[p] = PD_SLOT_JSI_NOT_SPD;
+      io.eround[p] = 0;
+      io.eindex[p] = 0;
+    }
+    return;
+  }
+  const double* td = ws + (size_t)jst::TD * n;
+  wide_llt_solve(Mb, ld, np, invd, vx, sT, warp, lane);
+  double sq = 0.0;
+  for (int i = t; i < n; i += nt) sq = fma(td[i], td[i], sq);
+  const double scale = fmax(sqrt(block_sum(sq, br)), 2.2250738585072014e-308);
+  int code = PD_SLOT_OK;
+  for (int pass = 0; pass < 2; ++pass) {
+    // r = td - M x, tile row I per warp: lane = row
+    double rr = 0.0;
+    for (int I = warp; I < np; I += kWideWarps) {
+      const int i = 32 * I + lane;
+      double s = (i < n) ? td[i] : 0.0;
+      s = fma(-dg[i], vx[i], s);
+      for (int J = 0; J < np; ++J) {
+        const double* x = vx + 32 * J;
+        if (J > I) {  // upper tile: row i
+          const double* row = Mb + (size_t)i * ld + 32 * J;
+#pragma unroll 8
+          for (int c = 0; c < 32; ++c) s = fma(-row[c], x[c], s);
+        } else if (J < I) {  // lower tile = (upper tile (J, I))^T: column i
+          const double* col = Mb + (size_t)(32 * J) * ld + i;
+#pragma unroll 8
+          for (int c = 0; c < 32; ++c) s = fma(-col[(size_t)c * ld], x[c], s);
+        } else {  // diagonal tile: strict upper part, both ways
+          for (int c = 0; c < 32; ++c) {
+            const int j = 32 * J + c;
+            if (j > i) s = fma(-Mb[(size_t)i * ld + j], x[c], s);
+            else if (j < i) s = fma(-Mb[(size_t)j * ld + i], x[c], s);
+          }
+        }
+      }
+      vw[i] = s;
+      rr = fma(s, s, rr);
+    }
+    const double rn = sqrt(block_sum(rr, br));  // syncs
+    if (!(rn > 1e-9 * scale)) break;
+    if (pass == 1) {
+      code = PD_SLOT_JSI_REFINE_FAILED;
+      break;
+    }
+    wide_llt_solve(Mb, ld, np, invd, vw, sT, warp, lane);
+    for (int i = t; i < npad; i += nt) vx[i] += vw[i];
+    __syncthreads();
+  }
+  for (int i = t; i < n; i += nt) io.put_qdd(i, p, vx[i]);
+  if (t == 0) {
+    io.status[p] = code;
+    io.eround[p] = 0;
+    io.eindex[p] = 0;
+  }
+}
+
+// Long chains in small batches: build (MODE 2, a CTA per chain), grid-wide
+// factorization, solve (MODE 3). Workspace slots 0..B-1 of gws.
+bool jsiia_coop_path(int n, int64_t batch) { return !jsiia_smem_path(n) && batch <= 4; }
+
+void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, cudaStream_t s) {
+  const int n = mv.n;
+  const int nt = 32 * jsiia_warps(n, io.B, sm_count);
+  jsiia_tiled_kernel<false, 2><<<(unsigned)io.B, nt, 0, s>>>(mv, io, gws, 0);
+  int count = (int)io.B;
+  void* args[] = {&gws, (void*)&n, &count};
+  const size_t smem = sizeof(double) * 8 * (2 * 32 * kTs + 32);
+  cudaFuncSetAttribute(jsiia_factor_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchCooperativeKernel((const void*)jsiia_factor_coop, dim3((unsigned)sm_count), dim3(256), args, smem, s);
+  jsiia_solve_wide<<<(unsigned)io.B, 32 * kWideWarps, 0, s>>>(io, gws, n);
+}
+
 // Joint-space inertia of every problem into d_M[p][i][j] (same build as the
 // solve path: CRBA closed form, exactly symmetric).
 void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count, double* d_M,
@@ -422,12 +777,12 @@ void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws
   const int nt = 32 * jsiia_warps(n, io.B, sm_count);
   const size_t ws_bytes = jsiia_workspace_bytes(n);
   if (jsiia_smem_path(n)) {
-    cudaFuncSetAttribute(jsiia_tiled_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
-    jsiia_tiled_kernel<true, true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, 0, d_M);
+    cudaFuncSetAttribute(jsiia_tiled_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
+    jsiia_tiled_kernel<true, 1><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, 0, d_M);
   } else {
     for (int64_t b0 = 0; b0 < io.B; b0 += gws_slots) {
       const int64_t nb = (io.B - b0 < gws_slots) ? io.B - b0 : gws_slots;
-      jsiia_tiled_kernel<false, true><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, b0, d_M);
+      jsiia_tiled_kernel<false, 1><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, b0, d_M);
     }
   }
 }
