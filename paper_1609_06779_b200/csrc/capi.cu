@@ -21,6 +21,8 @@ size_t abia_cta_workspace_bytes(int n);
 int abia_scratch_doubles_per_link();
 void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+bool cfa_coop_path(int n, int64_t batch);
+void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
 void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count,
                   cudaStream_t s);
@@ -342,6 +344,14 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       PD_CUDA(ensure_model_cl(ctx));
       mv.fcl = ctx->model_cl.as<double>() + cl_off;
       const size_t wsb = cfa_workspace_bytes(n);
+      static const bool no_coop = std::getenv("PD_CFA_NO_COOP") != nullptr;
+      if (!no_coop && cfa_coop_path(n, batch)) {  // long chain(s): grid-wide OEE
+        PD_CUDA(ctx->cta_ws.ensure(wsb * batch + 64));
+        int* bad = reinterpret_cast<int*>(ctx->cta_ws.as<char>() + wsb * batch);
+        launch_cfa_coop(mv, io, ctx->cta_ws.as<double>(), bad, ctx->sm_count, ctx->stream);
+        ctx->launches += 2;
+        break;
+      }
       int64_t slots = 0;
       if (wsb > 220 * 1024) {
         slots = cta_slots(ctx, wsb, batch);
@@ -537,7 +547,8 @@ const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) 
     case PD_ABIA: return "abia_ring_kernel (lane per chain, 3 fused base-frame passes, persistent CTAs, TMA producer "
                          "warp + per-pass byte ring); abia_cta_kernel for n >= 64 in batches <= 2 x SMs (CTA per chain)";
     case PD_CFA: return cfa_workspace_bytes(n_links) <= 220 * 1024 ? "cfa_cta_kernel<smem> (CTA per chain, OEE in smem)"
-                                                                    : "cfa_cta_kernel<global> (CTA per chain, L2 workspace)";
+                                                                    : "cfa_cta_kernel<global> (CTA per chain, L2 workspace); batches "
+                                                                      "<= 4: CTA prologue + grid-wide cooperative OEE (cfa_oee_coop)";
     case PD_JSIIA: return n_links <= 64 ? "jsiia_dmma_kernel (warp per chain, M and blocked Cholesky on FP64 tensor cores, DMMA 8x8x4)"
                           : jsiia_smem_path(n_links)
                               ? "jsiia_tiled_kernel<smem> (CTA per chain, CRBA scans + 32x32-tile Cholesky in smem)"

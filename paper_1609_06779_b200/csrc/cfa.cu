@@ -20,6 +20,8 @@
 // §7.4.6), so a symmetric factorization is valid; the rank test mirrors
 // FullPivLU::isInvertible (|pivot| > 5 eps max|diag|). The reported error
 // is the reference's: smallest failing row, its first failing pivot.
+#include <cooperative_groups.h>
+
 #include "cta_common.cuh"
 
 namespace pd {
@@ -175,7 +177,9 @@ __device__ __forceinline__ void ws_store(double* ws, int n, int f0, int i, const
   for (int k = 0; k < K; ++k) ws[(f0 + k) * n + i] = in[k];
 }
 
-template <bool SMEM>
+// PREP: stop after the OEE initial state is in the (global) workspace; the
+// grid-wide rounds of cfa_oee_coop finish the solve (long chains, c4).
+template <bool SMEM, bool PREP = false>
 __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, double* __restrict__ gws, int lpt,
                                                        int64_t p_off) {
   extern __shared__ double dyn_smem[];
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     ws_store<5>(ws, n, cfa::OR, i, r5);
   }
   __syncthreads();
+  if (PREP) return;
 
   const int rounds = ceil_log2_dev(n);
   if (lpt == 1) {
@@ -635,6 +640,222 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     io.eround[p] = 0;
     io.eindex[p] = 0;
   }
+}
+
+// OEE rounds, final block solves and the q-dot extraction of long chains in
+// small batches (c4) on a cooperative grid: a thread per row spread over
+// many SMs (the row's D, U, R in registers, as in the CTA kernel), the
+// published pivot data in the global workspace read through L2
+// (ld.global.cg), a grid barrier where the CTA kernel has __syncthreads.
+// Chains one after the other; cfa_cta_kernel<false, true> left each chain's
+// initial state in workspace slot c.
+__device__ __forceinline__ void cg_load(const double* ws, int n, int f0, int i, double* out, int K) {
+  for (int k = 0; k < K; ++k) out[k] = __ldcg(ws + (size_t)(f0 + k) * n + i);
+}
+
+__global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restrict__ gws, int n, int count,
+                                                    int* __restrict__ bad) {
+  namespace cgr = cooperative_groups;
+  cgr::grid_group grid = cgr::this_grid();
+  const int i = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  const bool own = i < n;
+  const int rounds = ceil_log2_dev(n);
+  for (int c = 0; c < count; ++c) {
+    double* ws = gws + (size_t)c * cfa::FIELDS * n;
+    const int64_t p = c;
+    if (i == 0) *bad = n;
+    double D[15], U[25], R[5];
+    if (own) {
+#pragma unroll
+      for (int k = 0; k < 15; ++k) D[k] = __ldcg(ws + (size_t)(cfa::AD + k) * n + i);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) R[k] = __ldcg(ws + (size_t)(cfa::OR + k) * n + i);
+#pragma unroll
+      for (int k = 0; k < 25; ++k) U[k] = (i + 1 < n) ? __ldcg(ws + (size_t)(cfa::UP + k) * n + i) : 0.0;
+    }
+    grid.sync();
+    int h = 1;
+    bool failed = false;
+    for (int round = 1; round <= rounds; ++round, h <<= 1) {
+      if (own) {  // publish own pivot factorization
+        double Lk[10], dinv[5], rt[5];
+        const bool ok = ldlt5(D, Lk, dinv);
+        ws_store<10>(ws, n, cfa::PL, i, Lk);
+        ws_store<5>(ws, n, cfa::PI, i, dinv);
+        ws[(size_t)cfa::SG * n + i] = ok ? 0.0 : 1.0;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) rt[r] = R[r];
+        unit_lower_solve5(Lk, rt);
+        ws_store<5>(ws, n, cfa::PR, i, rt);
+        if (i < n - h) {
+#pragma unroll
+          for (int cc = 0; cc < 5; ++cc) {
+            double col[5];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) col[r] = U[r * 5 + cc];
+            unit_lower_solve5(Lk, col);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) ws[(size_t)(cfa::PY + r * 5 + cc) * n + i] = col[r];
+          }
+        }
+      }
+      grid.sync();
+      if (own) {
+        // singular pivots: smallest failing row, its first failing pivot (oee.hpp:88-138)
+        const bool up_bad = (i < n - h) && __ldcg(ws + (size_t)cfa::SG * n + i + h) != 0.0;
+        const bool dn_bad = (i >= h) && __ldcg(ws + (size_t)cfa::SG * n + i - h) != 0.0;
+        if (up_bad || dn_bad) atomicMin(bad, i);
+        if (i < n - h) {
+          const int k = i + h;
+          double Lk[10], dinv[5], rt[5];
+          cg_load(ws, n, cfa::PL, k, Lk, 10);
+          cg_load(ws, n, cfa::PI, k, dinv, 5);
+          cg_load(ws, n, cfa::PR, k, rt, 5);
+          double Z[5][5], Zs[5][5];
+#pragma unroll
+          for (int a2 = 0; a2 < 5; ++a2) {
+#pragma unroll
+            for (int r = 0; r < 5; ++r) Z[a2][r] = U[a2 * 5 + r];
+            unit_lower_solve5(Lk, Z[a2]);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) Zs[a2][r] = Z[a2][r] * dinv[r];
+          }
+#pragma unroll
+          for (int a2 = 0; a2 < 5; ++a2) {
+#pragma unroll
+            for (int b2 = 0; b2 <= a2; ++b2) {
+              double sacc = D[pk(a2, b2)];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], Z[b2][r], sacc);
+              D[pk(a2, b2)] = sacc;
+            }
+            double sacc = R[a2];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], rt[r], sacc);
+            R[a2] = sacc;
+          }
+          if (i < n - 2 * h) {
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) {
+              double yc[5];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) yc[r] = __ldcg(ws + (size_t)(cfa::PY + r * 5 + cc) * n + k);
+#pragma unroll
+              for (int a2 = 0; a2 < 5; ++a2) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int r = 0; r < 5; ++r) sacc = fma(Zs[a2][r], yc[r], sacc);
+                U[a2 * 5 + cc] = -sacc;
+              }
+            }
+          }
+        }
+        if (i >= h) {
+          const int k = i - h;
+          double dinv[5], rt[5], Ys[5][5], Y[5][5];
+          cg_load(ws, n, cfa::PI, k, dinv, 5);
+          cg_load(ws, n, cfa::PR, k, rt, 5);
+#pragma unroll
+          for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) {
+              Y[r][cc] = __ldcg(ws + (size_t)(cfa::PY + r * 5 + cc) * n + k);
+              Ys[r][cc] = Y[r][cc] * dinv[r];
+            }
+#pragma unroll
+          for (int a2 = 0; a2 < 5; ++a2) {
+#pragma unroll
+            for (int b2 = 0; b2 <= a2; ++b2) {
+              double sacc = D[pk(a2, b2)];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], Y[r][b2], sacc);
+              D[pk(a2, b2)] = sacc;
+            }
+            double sacc = R[a2];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], rt[r], sacc);
+            R[a2] = sacc;
+          }
+        }
+      }
+      grid.sync();
+      const int sb = __ldcg(bad);
+      if (sb < n) {
+        if (i == 0) {
+          const bool up_bad = (sb < n - h) && __ldcg(ws + (size_t)cfa::SG * n + sb + h) != 0.0;
+          io.status[p] = PD_SLOT_OEE_SINGULAR_PIVOT;
+          io.eround[p] = round;
+          io.eindex[p] = up_bad ? sb + h : sb - h;
+        }
+        failed = true;
+        break;  // grid-uniform
+      }
+    }
+    if (!failed) {
+      // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
+      if (own) {
+        double Lf[10], dinv[5];
+        if (!ldlt5(D, Lf, dinv)) atomicMin(bad, i);
+        unit_lower_solve5(Lf, R);
+#pragma unroll
+        for (int r = 0; r < 5; ++r) R[r] *= dinv[r];
+        unit_lowerT_solve5(Lf, R);
+        ws_store<5>(ws, n, cfa::OR, i, R);  // constraint force F_c,i
+      }
+      grid.sync();
+      const int sb = __ldcg(bad);
+      if (sb < n) {
+        if (i == 0) {
+          io.status[p] = PD_SLOT_OEE_SINGULAR_FINAL;
+          io.eround[p] = rounds;
+          io.eindex[p] = sb;
+        }
+      } else {
+        // qdd = apply_joint(td) + apply_cross_transpose(F_c)
+        if (own) {
+          auto g = [&](int f, int j) { return __ldcg(ws + (size_t)f * n + j); };
+          const double td = g(cfa::TD, i);
+          double v = g(cfa::JD, i) * td;
+#pragma unroll
+          for (int r = 0; r < 5; ++r) v = fma(g(cfa::XD + r, i), R[r], v);
+          if (i > 0) {
+            v = fma(g(cfa::JO, i - 1), g(cfa::TD, i - 1), v);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) v = fma(g(cfa::XS + r, i - 1), g(cfa::OR + r, i - 1), v);
+          }
+          if (i + 1 < n) {
+            v = fma(g(cfa::JO, i), g(cfa::TD, i + 1), v);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) v = fma(g(cfa::XB + r, i), g(cfa::OR + r, i + 1), v);
+          }
+          io.put_qdd(i, p, v);
+        }
+        if (i == 0) {
+          io.status[p] = PD_SLOT_OK;
+          io.eround[p] = 0;
+          io.eindex[p] = 0;
+        }
+      }
+    }
+    grid.sync();  // workspace / flag reuse by the next chain
+  }
+}
+
+bool cfa_coop_path(int n, int64_t batch) { return (size_t)cfa::FIELDS * n * sizeof(double) > 224 * 1024 && batch <= 4; }
+
+// Long chains in small batches: CTA prologue (kinematics, bias torque,
+// operators, OEE initial state) for every chain, then the grid-wide OEE.
+void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s) {
+  const int n = mv.n;
+  const int lpt = (n + 255) / 256;
+  cfa_cta_kernel<false, true><<<(unsigned)io.B, 256, 0, s>>>(mv, io, gws, lpt, 0);
+  int count = (int)io.B;
+  int nn = n;
+  BatchIO iol = io;
+  void* args[] = {&iol, &gws, &nn, &count, &bad};
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  (void)sm_count;
+  cudaLaunchCooperativeKernel((const void*)cfa_oee_coop, dim3(grid), dim3(128), args, 0, s);
 }
 
 size_t cfa_workspace_bytes(int n) { return (size_t)cfa::FIELDS * n * sizeof(double); }
