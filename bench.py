@@ -324,11 +324,15 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
     return res
 
 
-def roofline_entry(wl, ms_per_launch, bw_gbs, fp64_tflops, traffic=None):
+def roofline_entry(wl, ms_per_step, bw_gbs, fp64_tflops, traffic=None):
+    """Algorithmic work of one step (the whole batch) over the step's device
+    time. A step is one launch for the batched kernels; multi-kernel paths
+    (tau_delta pre-pass, cooperative long-chain pipelines, chunked global-
+    workspace launches) count all their kernels."""
     n, B, algo = wl["n"], wl["batch"], wl["algo"]
     bytes_ = b_alg(n, wl["shared"]) * B
     flops = f_alg(algo, n) * B
-    t = ms_per_launch * 1e-3
+    t = ms_per_step * 1e-3
     gbs = bytes_ / t / 1e9
     tfl = flops / t / 1e12
     t_hbm = bytes_ / (bw_gbs * 1e9)
@@ -392,10 +396,8 @@ def main():
     total = global_batch * args.steps
     value = total / (ms_max * 1e-3)
     ms_per_step = ms_max / args.steps
-    launches_per_step = res["launches"] / args.steps
-    # roofline of this rank's kernel on its own (local) batch
-    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B), res["ms_total"] / args.steps / max(launches_per_step, 1),
-                                            bw, fp64_peak)
+    # roofline of this rank's step on its own (local) batch
+    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B), res["ms_total"] / args.steps, bw, fp64_peak)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -435,7 +437,7 @@ def main():
             steps = 20 if w["batch"] > 1 else 3
             r = measure_workload(ctx, name, w, steps, 3, 0, local, stream, False, 0)
             mps = r["ms_total"] / steps
-            h, f, b, wk = roofline_entry(w, mps / max(r["launches"] / steps, 1), bw, fp64_peak)
+            h, f, b, wk = roofline_entry(w, mps, bw, fp64_peak)
             extra[name] = {"workload": w["desc"], "solves_per_s": w["batch"] * steps / (r["ms_total"] * 1e-3),
                            "ms_per_step": mps, "hbm_frac": h["frac"], "fp64_frac": f["frac"], "binding": b,
                            "roofline_frac_of_binding": wk["roofline_frac"]}

@@ -20,7 +20,9 @@ void launch_abia_cta(const ModelView& mv, const BatchIO& io, double* gws, int64_
 size_t abia_cta_workspace_bytes(int n);
 int abia_scratch_doubles_per_link();
 void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
-void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
+void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
+                const double* td_pre);
+void launch_tau_surplus(const ModelView& mv, const BatchIO& io, double* td, cudaStream_t s);
 bool cfa_coop_path(int n, int64_t batch);
 void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
@@ -82,6 +84,7 @@ struct pd_ctx {
   bool model_cl_valid = false;
   // scratch
   DevBuf states;  // link-state outputs and their host-order staging
+  DevBuf cfa_td;  // tau_delta [link][problem] for the batched CFA path
   DevBuf abia_scratch, cta_ws, slots, io_q, io_qd, io_tau, io_qdd, io_status;
   // host-buffer path: copy-in / copy-out streams and per-chunk events
   static constexpr int kMaxChunks = 16;
@@ -360,7 +363,17 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       } else {
         ctx->launches++;
       }
-      launch_cfa(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream);
+      // large batches: tau_delta by a lane-per-chain pass first (sequential
+      // recurrences, no CTA-wide scans); small batches keep the CTA scans
+      static const bool no_pre = std::getenv("PD_CFA_CTA_BIAS") != nullptr;
+      const double* td_pre = nullptr;
+      if (!no_pre && batch >= 128 * (int64_t)ctx->sm_count) {  // >= 4 warps of chains per SM
+        PD_CUDA(ctx->cfa_td.ensure(sizeof(double) * (size_t)n * io.lds));
+        launch_tau_surplus(model_view(ctx, m0, batch), io, ctx->cfa_td.as<double>(), ctx->stream);
+        ctx->launches++;
+        td_pre = ctx->cfa_td.as<double>();
+      }
+      launch_cfa(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream, td_pre);
       break;
     }
     case PD_JSIIA: {

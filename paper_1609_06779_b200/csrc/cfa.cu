@@ -179,9 +179,11 @@ __device__ __forceinline__ void ws_store(double* ws, int n, int f0, int i, const
 
 // PREP: stop after the OEE initial state is in the (global) workspace; the
 // grid-wide rounds of cfa_oee_coop finish the solve (long chains, c4).
+// td_pre: tau_delta precomputed by tau_surplus_lane_kernel ([link][problem],
+// stride io.lds) -- the CTA then skips its scan-based bias stage.
 template <bool SMEM, bool PREP = false>
 __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, double* __restrict__ gws, int lpt,
-                                                       int64_t p_off) {
+                                                       int64_t p_off, const double* __restrict__ td_pre = nullptr) {
   extern __shared__ double dyn_smem[];
   __shared__ ScanSmem scan_sm;
   __shared__ int s_bad, s_link_fail;
@@ -203,7 +205,12 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
   // ---- kinematics + torque surplus ----------------------------------------
   const IdFields idf{cfa::REL, cfa::X, cfa::V, cfa::TMP, cfa::TD};
   cta_kinematics(mv, io, p, mc, ws, idf, lpt);
-  cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);  // ends with a barrier
+  if (td_pre) {
+    for (int i = i0; i < i1; ++i) ws[cfa::TD * n + i] = __ldg(td_pre + (int64_t)i * io.lds + p);
+    __syncthreads();
+  } else {
+    cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);  // ends with a barrier
+  }
 
   // ---- operators (forward_dynamics.cpp:261-357) ----------------------------
   // Z_i = [W_i | S_i], C_i = Ad(rel_{i+1})^T Z_{i+1}, J_i = L L^T,
@@ -862,7 +869,8 @@ size_t cfa_workspace_bytes(int n) { return (size_t)cfa::FIELDS * n * sizeof(doub
 
 // Shared-memory workspace when it fits (n <= 260), otherwise one global slot
 // per CTA in flight, launched in waves of gws_slots CTAs.
-void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s) {
+void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
+                const double* td_pre) {
   const int n = mv.n;
   int nt = ((n + 31) / 32) * 32;
   if (nt > 256) nt = 256;
@@ -870,11 +878,11 @@ void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws
   const size_t ws_bytes = cfa_workspace_bytes(n);
   if (ws_bytes <= 224 * 1024) {
     cudaFuncSetAttribute(cfa_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
-    cfa_cta_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, lpt, 0);
+    cfa_cta_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, lpt, 0, td_pre);
   } else {
     for (int64_t b0 = 0; b0 < io.B; b0 += gws_slots) {
       const int64_t nb = (io.B - b0 < gws_slots) ? io.B - b0 : gws_slots;
-      cfa_cta_kernel<false><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, lpt, b0);
+      cfa_cta_kernel<false><<<(unsigned)nb, nt, 0, s>>>(mv, io, gws, lpt, b0, td_pre);
     }
   }
 }

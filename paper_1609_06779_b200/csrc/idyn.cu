@@ -95,6 +95,47 @@ __global__ void __launch_bounds__(128) idyn_lane_kernel(ModelView mv, BatchIO io
   io.eindex[p] = 0;
 }
 
+// Torque surplus tau_delta = tau - ID(q, qd, 0) (forward_dynamics.cpp:35-42),
+// lane per chain, into td[link][problem] (stride io.lds): the bias stage of
+// the CTA-per-chain CFA kernel for large batches, where sequential per-lane
+// recurrences beat CTA-wide scans (no barriers, work-optimal).
+__global__ void __launch_bounds__(128) tau_surplus_lane_kernel(ModelView mv, BatchIO io, double* __restrict__ td) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= io.B) return;
+  const int n = mv.n;
+  const int64_t mc = mv.model_of(p);
+  if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) return;  // the CFA kernel reports the model's rule
+  Sv V = svzero();
+  const Vec3d g = mv.gravity(mc);
+  Sv A = {mk(0, 0, 0), mk(-g.x, -g.y, -g.z)};  // inverse_dynamics.cpp:135-140
+  for (int i = 0; i < n; ++i) {
+    const Sv S = mv.screw(i, mc);
+    const SE3d T = joint_transform(S, mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p));
+    const Sv rate = io.ld(io.qd, i, p) * S;
+    V = ad_apply(T, V) + rate;
+    A = ad_apply(T, A) + adv_apply(V, rate);
+  }
+  Sv carryF = svzero();
+  for (int i = n - 1; i >= 0; --i) {
+    const Sv S = mv.screw(i, mc);
+    const SE3d T = joint_transform(S, mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p));
+    const Inertia J = mv.inertia(i, mc);
+    const Sv h = inertia_apply(J, V);
+    const Sv F = inertia_apply(J, A) + neg_advT_apply(V, h) + carryF;
+    td[(int64_t)i * io.lds + p] = io.ld(io.tau, i, p) - dot(S, F);
+    if (i > 0) {
+      carryF = adT_apply(T, F);
+      const Sv rate = io.ld(io.qd, i, p) * S;
+      A = adinv_apply(T, A - adv_apply(V, rate));
+      V = adinv_apply(T, V - rate);
+    }
+  }
+}
+
+void launch_tau_surplus(const ModelView& mv, const BatchIO& io, double* td, cudaStream_t s) {
+  tau_surplus_lane_kernel<<<(unsigned)((io.B + 127) / 128), 128, 0, s>>>(mv, io, td);
+}
+
 void launch_idyn(const ModelView& mv, const BatchIO& io, const IdOpts& o, const double* raw, double* vel, double* acc,
                  double* frc, cudaStream_t s) {
   const int threads = 128;
