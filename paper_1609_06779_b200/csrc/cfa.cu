@@ -11,11 +11,12 @@
 //
 // OEE (the paper's building block 2, Eq. 17, row-centric form of
 // oee.hpp:73-145). Each round every row factors its own pivot D_k once
-// (LDL^T, 5x5) and publishes (L_k, 1/d_k, L_k^{-1} U_k, L_k^{-1} R_k); after
-// one barrier every row applies both eliminations from published data only:
-//   up   (pivot i+h): Z = L^{-1} U_i^T, D_i -= Z^T d^{-1} Z, R_i -= Z^T d^{-1} Rt,
-//                     U_i <- -Z^T d^{-1} Y_{i+h}            (only if i+2h < n)
-//   down (pivot i-h): D_i -= Y^T d^{-1} Y, R_i -= Y^T d^{-1} Rt.
+// (Cholesky, 5x5) and publishes (L_k, 1/L_k,jj, Y_k = L_k^{-1} U_k,
+// Rt_k = L_k^{-1} R_k); after one barrier every row applies both eliminations
+// from published data only:
+//   up   (pivot i+h): W = L^{-1} U_i^T, D_i -= W^T W, R_i -= W^T Rt,
+//                     U_i <- -W^T Y_{i+h}                  (only if i+2h < n)
+//   down (pivot i-h): D_i -= Y^T Y, R_i -= Y^T Rt.
 // Pivots are Schur complements of the SPD constraint operator (SURVEY.md
 // §7.4.6), so a symmetric factorization is valid; the rank test mirrors
 // FullPivLU::isInvertible (|pivot| > 5 eps max|diag|). The reported error
@@ -121,49 +122,127 @@ __device__ __forceinline__ void lower_solve6(const double L[21], const double in
   }
 }
 
-// LDL^T of a packed symmetric 5x5 with the FullPivLU-style rank test.
-__device__ __forceinline__ bool ldlt5(const double D[15], double L[10], double dinv[5]) {
+// ---- OEE row algebra on packed 5x5 blocks (Cholesky form) -------------------
+// Pivots are Schur complements of the SPD constraint operator, so each is
+// factored D_k = L L^T (L lower with its diagonal kept as 1/L_jj); with
+// Y_k = L^{-1} U_k, rt_k = L^{-1} R_k and W = L_k^{-1} U_i^T the eliminations
+// are plain Gram products: D_i -= W^T W, R_i -= W^T rt_k, U_i <- -W^T Y_k (up),
+// D_i -= Y_k^T Y_k, R_i -= Y_k^T rt_k (down) -- no pivot scaling pass.
+// The rank test is FullPivLU::isInvertible's: the LDL^T pivot (the square of
+// L_jj, before the root) must exceed 5 eps max|diag| (oee.hpp:43,209,225).
+__device__ __forceinline__ bool chol5(const double D[15], double L[10], double il[5]) {
   double maxd = 0.0;
 #pragma unroll
   for (int k = 0; k < 5; ++k) maxd = fmax(maxd, fabs(D[pk(k, k)]));
   const double thr = 5.0 * 2.220446049250313e-16 * maxd;
-  double d[5];
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
     double x = D[pk(j, j)];
 #pragma unroll
-    for (int k = 0; k < j; ++k) x = fma(-L[pks(j, k)] * d[k], L[pks(j, k)], x);
-    d[j] = x;
-    ok = ok && (fabs(x) > thr);
-    dinv[j] = 1.0 / x;
+    for (int k = 0; k < j; ++k) x = fma(-L[pks(j, k)], L[pks(j, k)], x);
+    ok = ok && (x > thr);
+    il[j] = rsqrt(fabs(x));
 #pragma unroll
     for (int i = j + 1; i < 5; ++i) {
       double s = D[pk(i, j)];
 #pragma unroll
-      for (int k = 0; k < j; ++k) s = fma(-L[pks(i, k)] * d[k], L[pks(j, k)], s);
-      L[pks(i, j)] = s * dinv[j];
+      for (int k = 0; k < j; ++k) s = fma(-L[pks(i, k)], L[pks(j, k)], s);
+      L[pks(i, j)] = s * il[j];
     }
   }
   return ok;
 }
-__device__ __forceinline__ void unit_lower_solve5(const double L[10], double x[5]) {
+__device__ __forceinline__ void lsolve5(const double L[10], const double il[5], double x[5]) {  // x <- L^{-1} x
 #pragma unroll
-  for (int r = 1; r < 5; ++r) {
+  for (int r = 0; r < 5; ++r) {
     double s = x[r];
 #pragma unroll
     for (int c = 0; c < r; ++c) s = fma(-L[pks(r, c)], x[c], s);
-    x[r] = s;
+    x[r] = s * il[r];
   }
 }
-__device__ __forceinline__ void unit_lowerT_solve5(const double L[10], double x[5]) {  // x <- L^{-T} x
+__device__ __forceinline__ void ltsolve5(const double L[10], const double il[5], double x[5]) {  // x <- L^{-T} x
 #pragma unroll
-  for (int r = 3; r >= 0; --r) {
+  for (int r = 4; r >= 0; --r) {
     double s = x[r];
 #pragma unroll
     for (int c = r + 1; c < 5; ++c) s = fma(-L[pks(c, r)], x[c], s);
-    x[r] = s;
+    x[r] = s * il[r];
   }
+}
+// Up elimination of row i by pivot k = i + h. yk(r, c) = Y_k[r][c]; U is
+// replaced by the distance-2h coupling when next (i < n - 2h).
+template <class YF>
+__device__ __forceinline__ void oee_up(double D[15], double R[5], double U[25], const double L[10], const double il[5],
+                                       const double rt[5], bool next, YF yk) {
+  double W[5][5];
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+#pragma unroll
+    for (int r = 0; r < 5; ++r) W[a][r] = U[a * 5 + r];
+    lsolve5(L, il, W[a]);
+  }
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      double s = D[pk(a, b)];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) s = fma(-W[a][r], W[b][r], s);
+      D[pk(a, b)] = s;
+    }
+    double s = R[a];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) s = fma(-W[a][r], rt[r], s);
+    R[a] = s;
+  }
+  if (next) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      double yc[5];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) yc[r] = yk(r, c);
+#pragma unroll
+      for (int a = 0; a < 5; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) s = fma(W[a][r], yc[r], s);
+        U[a * 5 + c] = -s;
+      }
+    }
+  }
+}
+// Down elimination of row i by pivot k = i - h.
+template <class YF>
+__device__ __forceinline__ void oee_down(double D[15], double R[5], const double rt[5], YF yk) {
+  double Y[5][5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r)
+#pragma unroll
+    for (int c = 0; c < 5; ++c) Y[r][c] = yk(r, c);
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      double s = D[pk(a, b)];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) s = fma(-Y[r][a], Y[r][b], s);
+      D[pk(a, b)] = s;
+    }
+    double s = R[a];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) s = fma(-Y[r][a], rt[r], s);
+    R[a] = s;
+  }
+}
+// Final block solve x = D^{-1} R in place; false if the block is singular.
+__device__ __forceinline__ bool oee_final(const double D[15], double R[5]) {
+  double L[10], il[5];
+  const bool ok = chol5(D, L, il);
+  lsolve5(L, il, R);
+  ltsolve5(L, il, R);
+  return ok;
 }
 
 template <int K>
@@ -346,15 +425,15 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     __syncthreads();  // AD/UP/OR are overwritten by the published fields below
     int h = 1;
     for (int round = 1; round <= rounds; ++round, h <<= 1) {
-      if (own) {  // publish own pivot factorization
-        double Lk[10], dinv[5], rt[5];
-        const bool ok = ldlt5(D, Lk, dinv);
+      if (own) {  // publish own pivot factorization: L, 1/L_jj, L^{-1} R, L^{-1} U
+        double Lk[10], il[5], rt[5];
+        const bool ok = chol5(D, Lk, il);
         ws_store<10>(ws, n, cfa::PL, i, Lk);
-        ws_store<5>(ws, n, cfa::PI, i, dinv);
+        ws_store<5>(ws, n, cfa::PI, i, il);
         ws[cfa::SG * n + i] = ok ? 0.0 : 1.0;
 #pragma unroll
         for (int r = 0; r < 5; ++r) rt[r] = R[r];
-        unit_lower_solve5(Lk, rt);
+        lsolve5(Lk, il, rt);
         ws_store<5>(ws, n, cfa::PR, i, rt);
         if (i < n - h) {
 #pragma unroll
@@ -362,7 +441,7 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
             double col[5];
 #pragma unroll
             for (int r = 0; r < 5; ++r) col[r] = U[r * 5 + c];
-            unit_lower_solve5(Lk, col);
+            lsolve5(Lk, il, col);
 #pragma unroll
             for (int r = 0; r < 5; ++r) ws[(cfa::PY + r * 5 + c) * n + i] = col[r];
           }
@@ -376,75 +455,17 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
         if (up_bad || dn_bad) atomicMin(&s_bad, i);
         if (i < n - h) {
           const int k = i + h;
-          double Lk[10], dinv[5], rt[5];
+          double Lk[10], il[5], rt[5];
           ws_load<10>(ws, n, cfa::PL, k, Lk);
-          ws_load<5>(ws, n, cfa::PI, k, dinv);
+          ws_load<5>(ws, n, cfa::PI, k, il);
           ws_load<5>(ws, n, cfa::PR, k, rt);
-          double Z[5][5], Zs[5][5];
-#pragma unroll
-          for (int a2 = 0; a2 < 5; ++a2) {
-#pragma unroll
-            for (int r = 0; r < 5; ++r) Z[a2][r] = U[a2 * 5 + r];
-            unit_lower_solve5(Lk, Z[a2]);
-#pragma unroll
-            for (int r = 0; r < 5; ++r) Zs[a2][r] = Z[a2][r] * dinv[r];
-          }
-#pragma unroll
-          for (int a2 = 0; a2 < 5; ++a2) {
-#pragma unroll
-            for (int b2 = 0; b2 <= a2; ++b2) {
-              double sacc = D[pk(a2, b2)];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], Z[b2][r], sacc);
-              D[pk(a2, b2)] = sacc;
-            }
-            double sacc = R[a2];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], rt[r], sacc);
-            R[a2] = sacc;
-          }
-          if (i < n - 2 * h) {
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-              double yc[5];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) yc[r] = ws[(cfa::PY + r * 5 + c) * n + k];
-#pragma unroll
-              for (int a2 = 0; a2 < 5; ++a2) {
-                double sacc = 0.0;
-#pragma unroll
-                for (int r = 0; r < 5; ++r) sacc = fma(Zs[a2][r], yc[r], sacc);
-                U[a2 * 5 + c] = -sacc;
-              }
-            }
-          }
+          oee_up(D, R, U, Lk, il, rt, i < n - 2 * h, [&](int r, int c) { return ws[(cfa::PY + r * 5 + c) * n + k]; });
         }
         if (i >= h) {
           const int k = i - h;
-          double dinv[5], rt[5], Ys[5][5], Y[5][5];
-          ws_load<5>(ws, n, cfa::PI, k, dinv);
+          double rt[5];
           ws_load<5>(ws, n, cfa::PR, k, rt);
-#pragma unroll
-          for (int r = 0; r < 5; ++r)
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-              Y[r][c] = ws[(cfa::PY + r * 5 + c) * n + k];
-              Ys[r][c] = Y[r][c] * dinv[r];
-            }
-#pragma unroll
-          for (int a2 = 0; a2 < 5; ++a2) {
-#pragma unroll
-            for (int b2 = 0; b2 <= a2; ++b2) {
-              double sacc = D[pk(a2, b2)];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], Y[r][b2], sacc);
-              D[pk(a2, b2)] = sacc;
-            }
-            double sacc = R[a2];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], rt[r], sacc);
-            R[a2] = sacc;
-          }
+          oee_down(D, R, rt, [&](int r, int c) { return ws[(cfa::PY + r * 5 + c) * n + k]; });
         }
       }
       __syncthreads();
@@ -461,12 +482,7 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     }
     // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
     if (own) {
-      double Lf[10], dinv[5];
-      if (!ldlt5(D, Lf, dinv)) atomicMin(&s_bad, i);
-      unit_lower_solve5(Lf, R);
-#pragma unroll
-      for (int r = 0; r < 5; ++r) R[r] *= dinv[r];
-      unit_lowerT_solve5(Lf, R);
+      if (!oee_final(D, R)) atomicMin(&s_bad, i);
       ws_store<5>(ws, n, cfa::OR, i, R);  // constraint force F_c,i
     }
     __syncthreads();
@@ -476,15 +492,15 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
   for (int round = 1; round <= rounds; ++round, h <<= 1) {
     // publish own pivot factorization
     for (int k = i0; k < i1; ++k) {
-      double D[15], Lk[10], dinv[5];
+      double D[15], Lk[10], il[5];
       ws_load<15>(ws, n, cfa::AD, k, D);
-      const bool ok = ldlt5(D, Lk, dinv);
+      const bool ok = chol5(D, Lk, il);
       ws_store<10>(ws, n, cfa::PL, k, Lk);
-      ws_store<5>(ws, n, cfa::PI, k, dinv);
+      ws_store<5>(ws, n, cfa::PI, k, il);
       ws[cfa::SG * n + k] = ok ? 0.0 : 1.0;
       double rt[5];
       ws_load<5>(ws, n, cfa::OR, k, rt);
-      unit_lower_solve5(Lk, rt);
+      lsolve5(Lk, il, rt);
       ws_store<5>(ws, n, cfa::PR, k, rt);
       if (k < n - h) {  // U_k exists at distance h
 #pragma unroll
@@ -492,7 +508,7 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
           double col[5];
 #pragma unroll
           for (int r = 0; r < 5; ++r) col[r] = ws[(cfa::UP + r * 5 + c) * n + k];
-          unit_lower_solve5(Lk, col);
+          lsolve5(Lk, il, col);
 #pragma unroll
           for (int r = 0; r < 5; ++r) ws[(cfa::PY + r * 5 + c) * n + k] = col[r];
         }
@@ -518,80 +534,25 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     }
     // eliminate
     for (int i = i0; i < i1; ++i) {
-      double D[15], R[5];
+      double D[15], R[5], U[25];
       ws_load<15>(ws, n, cfa::AD, i, D);
       ws_load<5>(ws, n, cfa::OR, i, R);
       if (i < n - h) {
         const int k = i + h;
-        double Lk[10], dinv[5], rt[5];
+        double Lk[10], il[5], rt[5];
         ws_load<10>(ws, n, cfa::PL, k, Lk);
-        ws_load<5>(ws, n, cfa::PI, k, dinv);
+        ws_load<5>(ws, n, cfa::PI, k, il);
         ws_load<5>(ws, n, cfa::PR, k, rt);
-        double Z[5][5];  // Z[a] = L^{-1} (row a of U_i)^T  (column a of Z)
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-#pragma unroll
-          for (int r = 0; r < 5; ++r) Z[a][r] = ws[(cfa::UP + a * 5 + r) * n + i];
-          unit_lower_solve5(Lk, Z[a]);
-        }
-        double Zs[5][5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a)
-#pragma unroll
-          for (int r = 0; r < 5; ++r) Zs[a][r] = Z[a][r] * dinv[r];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-#pragma unroll
-          for (int b = 0; b <= a; ++b) {
-            double s = D[pk(a, b)];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) s = fma(-Zs[a][r], Z[b][r], s);
-            D[pk(a, b)] = s;
-          }
-          double s = R[a];
-#pragma unroll
-          for (int r = 0; r < 5; ++r) s = fma(-Zs[a][r], rt[r], s);
-          R[a] = s;
-        }
-        if (i < n - 2 * h) {
-#pragma unroll
-          for (int c = 0; c < 5; ++c) {
-            double yc[5];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) yc[r] = ws[(cfa::PY + r * 5 + c) * n + k];
-#pragma unroll
-            for (int a = 0; a < 5; ++a) {
-              double s = 0.0;
-#pragma unroll
-              for (int r = 0; r < 5; ++r) s = fma(Zs[a][r], yc[r], s);
-              ws[(cfa::UP + a * 5 + c) * n + i] = -s;
-            }
-          }
-        }
+        ws_load<25>(ws, n, cfa::UP, i, U);
+        const bool next = i < n - 2 * h;
+        oee_up(D, R, U, Lk, il, rt, next, [&](int r, int c) { return ws[(cfa::PY + r * 5 + c) * n + k]; });
+        if (next) ws_store<25>(ws, n, cfa::UP, i, U);
       }
       if (i >= h) {
         const int k = i - h;
-        double dinv[5], rt[5], Y[5][5];
-        ws_load<5>(ws, n, cfa::PI, k, dinv);
+        double rt[5];
         ws_load<5>(ws, n, cfa::PR, k, rt);
-#pragma unroll
-        for (int r = 0; r < 5; ++r)
-#pragma unroll
-          for (int c = 0; c < 5; ++c) Y[r][c] = ws[(cfa::PY + r * 5 + c) * n + k];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-#pragma unroll
-          for (int b = 0; b <= a; ++b) {
-            double s = D[pk(a, b)];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) s = fma(-Y[r][a] * dinv[r], Y[r][b], s);
-            D[pk(a, b)] = s;
-          }
-          double s = R[a];
-#pragma unroll
-          for (int r = 0; r < 5; ++r) s = fma(-Y[r][a] * dinv[r], rt[r], s);
-          R[a] = s;
-        }
+        oee_down(D, R, rt, [&](int r, int c) { return ws[(cfa::PY + r * 5 + c) * n + k]; });
       }
       ws_store<15>(ws, n, cfa::AD, i, D);
       ws_store<5>(ws, n, cfa::OR, i, R);
@@ -601,14 +562,10 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
 
   // ---- final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187) -------------
   for (int i = i0; i < i1; ++i) {
-    double D[15], L[10], dinv[5], x[5];
+    double D[15], x[5];
     ws_load<15>(ws, n, cfa::AD, i, D);
     ws_load<5>(ws, n, cfa::OR, i, x);
-    if (!ldlt5(D, L, dinv)) atomicMin(&s_bad, i);
-    unit_lower_solve5(L, x);
-#pragma unroll
-    for (int r = 0; r < 5; ++r) x[r] *= dinv[r];
-    unit_lowerT_solve5(L, x);
+    if (!oee_final(D, x)) atomicMin(&s_bad, i);
     ws_store<5>(ws, n, cfa::OR, i, x);  // constraint force F_c,i
   }
   __syncthreads();
@@ -685,14 +642,14 @@ __global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restri
     bool failed = false;
     for (int round = 1; round <= rounds; ++round, h <<= 1) {
       if (own) {  // publish own pivot factorization
-        double Lk[10], dinv[5], rt[5];
-        const bool ok = ldlt5(D, Lk, dinv);
+        double Lk[10], il[5], rt[5];
+        const bool ok = chol5(D, Lk, il);
         ws_store<10>(ws, n, cfa::PL, i, Lk);
-        ws_store<5>(ws, n, cfa::PI, i, dinv);
+        ws_store<5>(ws, n, cfa::PI, i, il);
         ws[(size_t)cfa::SG * n + i] = ok ? 0.0 : 1.0;
 #pragma unroll
         for (int r = 0; r < 5; ++r) rt[r] = R[r];
-        unit_lower_solve5(Lk, rt);
+        lsolve5(Lk, il, rt);
         ws_store<5>(ws, n, cfa::PR, i, rt);
         if (i < n - h) {
 #pragma unroll
@@ -700,7 +657,7 @@ __global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restri
             double col[5];
 #pragma unroll
             for (int r = 0; r < 5; ++r) col[r] = U[r * 5 + cc];
-            unit_lower_solve5(Lk, col);
+            lsolve5(Lk, il, col);
 #pragma unroll
             for (int r = 0; r < 5; ++r) ws[(size_t)(cfa::PY + r * 5 + cc) * n + i] = col[r];
           }
@@ -714,75 +671,18 @@ __global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restri
         if (up_bad || dn_bad) atomicMin(bad, i);
         if (i < n - h) {
           const int k = i + h;
-          double Lk[10], dinv[5], rt[5];
+          double Lk[10], il[5], rt[5];
           cg_load(ws, n, cfa::PL, k, Lk, 10);
-          cg_load(ws, n, cfa::PI, k, dinv, 5);
+          cg_load(ws, n, cfa::PI, k, il, 5);
           cg_load(ws, n, cfa::PR, k, rt, 5);
-          double Z[5][5], Zs[5][5];
-#pragma unroll
-          for (int a2 = 0; a2 < 5; ++a2) {
-#pragma unroll
-            for (int r = 0; r < 5; ++r) Z[a2][r] = U[a2 * 5 + r];
-            unit_lower_solve5(Lk, Z[a2]);
-#pragma unroll
-            for (int r = 0; r < 5; ++r) Zs[a2][r] = Z[a2][r] * dinv[r];
-          }
-#pragma unroll
-          for (int a2 = 0; a2 < 5; ++a2) {
-#pragma unroll
-            for (int b2 = 0; b2 <= a2; ++b2) {
-              double sacc = D[pk(a2, b2)];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], Z[b2][r], sacc);
-              D[pk(a2, b2)] = sacc;
-            }
-            double sacc = R[a2];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) sacc = fma(-Zs[a2][r], rt[r], sacc);
-            R[a2] = sacc;
-          }
-          if (i < n - 2 * h) {
-#pragma unroll
-            for (int cc = 0; cc < 5; ++cc) {
-              double yc[5];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) yc[r] = __ldcg(ws + (size_t)(cfa::PY + r * 5 + cc) * n + k);
-#pragma unroll
-              for (int a2 = 0; a2 < 5; ++a2) {
-                double sacc = 0.0;
-#pragma unroll
-                for (int r = 0; r < 5; ++r) sacc = fma(Zs[a2][r], yc[r], sacc);
-                U[a2 * 5 + cc] = -sacc;
-              }
-            }
-          }
+          oee_up(D, R, U, Lk, il, rt, i < n - 2 * h,
+                 [&](int r, int c) { return __ldcg(ws + (size_t)(cfa::PY + r * 5 + c) * n + k); });
         }
         if (i >= h) {
           const int k = i - h;
-          double dinv[5], rt[5], Ys[5][5], Y[5][5];
-          cg_load(ws, n, cfa::PI, k, dinv, 5);
+          double rt[5];
           cg_load(ws, n, cfa::PR, k, rt, 5);
-#pragma unroll
-          for (int r = 0; r < 5; ++r)
-#pragma unroll
-            for (int cc = 0; cc < 5; ++cc) {
-              Y[r][cc] = __ldcg(ws + (size_t)(cfa::PY + r * 5 + cc) * n + k);
-              Ys[r][cc] = Y[r][cc] * dinv[r];
-            }
-#pragma unroll
-          for (int a2 = 0; a2 < 5; ++a2) {
-#pragma unroll
-            for (int b2 = 0; b2 <= a2; ++b2) {
-              double sacc = D[pk(a2, b2)];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], Y[r][b2], sacc);
-              D[pk(a2, b2)] = sacc;
-            }
-            double sacc = R[a2];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) sacc = fma(-Ys[r][a2], rt[r], sacc);
-            R[a2] = sacc;
-          }
+          oee_down(D, R, rt, [&](int r, int c) { return __ldcg(ws + (size_t)(cfa::PY + r * 5 + c) * n + k); });
         }
       }
       grid.sync();
@@ -801,12 +701,7 @@ __global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restri
     if (!failed) {
       // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
       if (own) {
-        double Lf[10], dinv[5];
-        if (!ldlt5(D, Lf, dinv)) atomicMin(bad, i);
-        unit_lower_solve5(Lf, R);
-#pragma unroll
-        for (int r = 0; r < 5; ++r) R[r] *= dinv[r];
-        unit_lowerT_solve5(Lf, R);
+        if (!oee_final(D, R)) atomicMin(bad, i);
         ws_store<5>(ws, n, cfa::OR, i, R);  // constraint force F_c,i
       }
       grid.sync();
