@@ -19,6 +19,7 @@
 //   joint_space_inertia            forward_dynamics.hpp:34-35 (MatrixXd stand-in)
 //   LinkSpec / RobotChain          model.hpp:17-30
 //   random_chain                   model.hpp:66-70
+//   validate_chain / load_chain / save_chain   model.hpp:56-82 (JSON model files)
 //   ExecTrace                      trace.hpp:24-39
 //   ModelError / DynamicsError / SingularBlockError   types.hpp:21-46
 #pragma once
@@ -152,6 +153,16 @@ struct RobotChain {
 // Deterministic random chain (model.cpp:157-185), bit-identical to the
 // reference generator.
 RobotChain random_chain(int n, std::uint64_t seed);
+
+// model.cpp:75-115: throws ModelError naming the offending link and field.
+void validate_chain(const RobotChain& chain);
+
+// JSON model files (model.hpp:72-82, model.cpp:244-337): the reference's
+// layout {"n", "gravity", "links": [{"mass", "com", "inertia_rot",
+// "joint_screw", "home_transform": {"rotation", "translation"}}]}; load
+// validates, save round-trips exactly.
+RobotChain load_chain(const std::string& path);
+void save_chain(const RobotChain& chain, const std::string& path);
 
 // ----------------------------------------------------------------- trace
 struct ExecTrace {

@@ -31,5 +31,8 @@ from .api import (  # noqa: F401
     joint_space_inertia,
     jsiia_forward_dynamics,
     link_states,
+    load_chain,
+    save_chain,
+    validate_chain,
 )
 from ._capi import LIB_PATH, LibraryMissing  # noqa: F401

@@ -11,6 +11,7 @@ proj/core/include/pardyn/forward_dynamics.hpp and inverse_dynamics.hpp:
   IdOptions / LinkStates                       inverse_dynamics.hpp:23-34
   inverse_dynamics / bias_torque / link_states inverse_dynamics.hpp:71-83
   joint_space_inertia(chain, q)                forward_dynamics.hpp:34-35
+  validate_chain / load_chain / save_chain     model.hpp:56-82, model.cpp:75-115,244-337
   LinkSpec / RobotChain                        model.hpp:17-30
   ModelError / DynamicsError / SingularBlockError(round, index)   types.hpp:21-46
   std::invalid_argument -> InvalidArgument (a ValueError)
@@ -486,3 +487,117 @@ def joint_space_inertia(chain: RobotChain, q, ctx: Optional[Context] = None) -> 
         return np.zeros((0, 0))
     ctx = _one_model(chain, ctx)
     return ctx.joint_space_inertia(np.asarray(q, np.float64)[None])[0]
+
+
+# --------------------------------------------------------------------------- model files
+def _link_prefix(k: int) -> str:
+    return f"link {k}"
+
+
+def validate_chain(chain: RobotChain) -> None:
+    """model.cpp:75-115 (ModelError with the reference's messages)."""
+    if not chain.links:
+        raise ModelError("chain must have at least one link")
+    if not np.all(np.isfinite(chain.gravity)):
+        raise ModelError("gravity must be finite")
+    for k, l in enumerate(chain.links):
+        if not (l.mass > 0.0) or not np.isfinite(l.mass):
+            raise ModelError(f"{_link_prefix(k)}: mass must be positive")
+        if not np.all(np.isfinite(l.com)):
+            raise ModelError(f"{_link_prefix(k)}: com must be finite")
+        I = np.asarray(l.inertia_rot, np.float64).reshape(3, 3)
+        if not np.all(np.isfinite(I)) or np.abs(I - I.T).max() > 1e-9 * max(1.0, np.abs(I).max()):
+            raise ModelError(f"{_link_prefix(k)}: rotational inertia must be symmetric")
+        if not (np.linalg.eigvalsh(0.5 * (I + I.T)).min() > 0.0):
+            raise ModelError(f"{_link_prefix(k)}: rotational inertia must be positive definite")
+        s = np.asarray(l.joint_screw, np.float64)
+        if not np.all(np.isfinite(s)):
+            raise ModelError(f"{_link_prefix(k)}: joint_screw must be finite")
+        nrm = float(np.linalg.norm(s))
+        if abs(nrm - 1.0) > 1e-9:
+            raise ModelError(f"{_link_prefix(k)}: joint_screw must have unit norm (got {nrm:.6f})")
+        R = np.asarray(l.home_rotation, np.float64).reshape(3, 3)
+        ok = np.all(np.isfinite(R)) and np.all(np.isfinite(l.home_translation))
+        ok = ok and np.abs(R.T @ R - np.eye(3)).max() <= 1e-9 and np.linalg.det(R) > 0.0
+        if not ok:
+            raise ModelError(f"{_link_prefix(k)}: home_transform rotation must be orthonormal with determinant +1")
+
+
+def load_chain(path: str) -> RobotChain:
+    """model.cpp:254-310: the reference's JSON layout, validated."""
+    import json
+    import numbers
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        raise ModelError(f"cannot open model file '{path}'") from None
+    try:
+        doc = json.loads(text)
+    except json.JSONDecodeError as e:
+        raise ModelError(f"model file '{path}': {e}") from None
+    where = f"model file '{path}'"
+
+    def need(j, field, w):
+        if not isinstance(j, dict) or field not in j:
+            raise ModelError(f"{w}: missing field '{field}'")
+        return j[field]
+
+    def number(j, field, w):
+        v = need(j, field, w)
+        if isinstance(v, bool) or not isinstance(v, numbers.Real):
+            raise ModelError(f"{w}: field '{field}' must be a number")
+        return float(v)
+
+    def array(j, field, n, w):
+        v = need(j, field, w)
+        if not isinstance(v, list) or len(v) != n:
+            raise ModelError(f"{w}: field '{field}' must be an array of {n} numbers")
+        if any(isinstance(e, bool) or not isinstance(e, numbers.Real) for e in v):
+            raise ModelError(f"{w}: field '{field}' must contain only numbers")
+        return np.asarray(v, np.float64)
+
+    n = need(doc, "n", where)
+    if isinstance(n, bool) or not isinstance(n, int):
+        raise ModelError(f"{where}: field 'n' must be an integer")
+    gravity = array(doc, "gravity", 3, where)
+    links = need(doc, "links", where)
+    if not isinstance(links, list):
+        raise ModelError(f"{where}: field 'links' must be an array")
+    if len(links) != n:
+        raise ModelError(f"{where}: field 'n' (= {n}) does not match the length of 'links' (= {len(links)})")
+    out = []
+    for k, j in enumerate(links):
+        w = _link_prefix(k)
+        if not isinstance(j, dict):
+            raise ModelError(f"{w}: must be an object")
+        home = need(j, "home_transform", w)
+        mass = number(j, "mass", w)
+        com = array(j, "com", 3, w)
+        Ir = array(j, "inertia_rot", 9, w)
+        screw = array(j, "joint_screw", 6, w)
+        if not isinstance(home, dict):
+            raise ModelError(f"{w}: field 'home_transform' must be an object")
+        out.append(LinkSpec(mass, com, Ir.reshape(3, 3), screw, array(home, "rotation", 9, w).reshape(3, 3),
+                            array(home, "translation", 3, w)))
+    chain = RobotChain(out, gravity)
+    validate_chain(chain)
+    return chain
+
+
+def save_chain(chain: RobotChain, path: str) -> None:
+    """model.cpp:312-337: indented JSON in the reference's field order; repr
+    floats so that loading back reproduces the chain exactly."""
+    import json
+    doc = {"n": chain.size(), "gravity": [float(x) for x in chain.gravity], "links": [
+        {"mass": float(l.mass), "com": [float(x) for x in np.ravel(l.com)],
+         "inertia_rot": [float(x) for x in np.ravel(l.inertia_rot)],
+         "joint_screw": [float(x) for x in np.ravel(l.joint_screw)],
+         "home_transform": {"rotation": [float(x) for x in np.ravel(l.home_rotation)],
+                            "translation": [float(x) for x in np.ravel(l.home_translation)]}}
+        for l in chain.links]}
+    try:
+        with open(path, "w") as f:
+            f.write(json.dumps(doc, indent=2) + "\n")
+    except OSError:
+        raise ModelError(f"cannot open model file '{path}' for writing") from None
