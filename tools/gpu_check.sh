@@ -10,4 +10,5 @@ for w in c5a c5j c5c c3 c2j; do
   timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-extra --no-cpu --no-e2e >> gpurun_out/bench_wl.json 2>> gpurun_out/bench.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/launches_bench.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 exit 0
