@@ -32,6 +32,9 @@
  *                               src/inverse_dynamics.cpp:175-179)
  *   pd_link_states           <- link_states (inverse_dynamics.hpp:81-83,
  *                               src/inverse_dynamics.cpp:181-196)
+ *   pd_workload_chains_device, pd_set_models_workload
+ *                            <- workload_chains / random_chain on the device
+ *                               (bench.cpp:357-366, model.cpp:157-185)
  *   pd_joint_space_inertia   <- joint_space_inertia(chain, q)
  *                               (forward_dynamics.hpp:34-35,
  *                               src/forward_dynamics.cpp:70-80)
@@ -191,6 +194,23 @@ void pd_random_chain(int32_t n_links, uint64_t seed, double* links);
 void pd_workload_chains(uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count, double* links);
 void pd_workload_inputs(uint64_t cell_seed, int32_t n_links, int64_t n_groups, int64_t repeat, double* q,
                         double* qdot, double* drive);
+
+/* The same chains generated on the device (§8f row 3), one thread per chain:
+ *   pd_workload_chains_device  chains [g0, g0+count) into device memory,
+ *                              d_links[chain][link][31], asynchronous
+ *   pd_set_models_workload     generate, validate (spatial_inertia_from rules,
+ *                              on the device) and pack them as the model set
+ *                              without a host copy; gravity: 3 doubles for
+ *                              every model or NULL (default)
+ * Same mt19937_64 streams and arithmetic as pd_workload_chains (no FMA
+ * contraction, IEEE sqrt): draws are bit exact; fields through sin/cos may
+ * differ in the last bit, since the device's sin/cos are correctly rounded
+ * (double-double evaluation) and glibc's are not always (~0.3% of
+ * evaluations). */
+pd_status pd_workload_chains_device(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,
+                                    double* d_links);
+pd_status pd_set_models_workload(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,
+                                 const double* gravity, int32_t* model_status, int32_t* model_rule);
 
 /* Diagnostic: measured dense FP64 FMA throughput of this device (TFLOP/s),
  * the FP64 roofline denominator (no FP64 figure in MEASURED_PEAKS.json). */

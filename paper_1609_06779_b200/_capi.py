@@ -27,6 +27,7 @@ EXPORTS = (
     "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant", "pd_mix", "pd_workload_seed", "pd_random_chain",
     "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak", "pd_inverse_dynamics_opts",
     "pd_inverse_dynamics_device", "pd_bias_torque", "pd_link_states", "pd_joint_space_inertia",
+    "pd_workload_chains_device", "pd_set_models_workload",
 )
 
 
@@ -87,6 +88,10 @@ def load():
     L.pd_link_states.restype = C.c_int
     L.pd_joint_space_inertia.argtypes = [C.c_void_p, C.c_int64, _D, _D]
     L.pd_joint_space_inertia.restype = C.c_int
+    L.pd_workload_chains_device.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
+    L.pd_workload_chains_device.restype = C.c_int
+    L.pd_set_models_workload.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_int64, _D, _I32, _I32]
+    L.pd_set_models_workload.restype = C.c_int
     L.pd_slot_message.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int32]
     L.pd_slot_message.restype = None
     L.pd_kernel_launches.argtypes = [C.c_void_p]

@@ -222,6 +222,23 @@ class Context:
         self.n_links, self.n_models = n, M
         return ms, mr
 
+    def set_models_workload(self, cell_seed: int, n_links: int, count: int, g0: int = 0, gravity=None):
+        """Chains [g0, g0+count) of the reference benchmark cell generated,
+        validated and packed on the device (no host model buffer). Returns
+        (model_status, model_rule)."""
+        g = None if gravity is None else np.ascontiguousarray(gravity, dtype=np.float64).reshape(3)
+        ms = np.zeros(count, np.int32)
+        mr = np.zeros(count, np.int32)
+        self._check(self._L.pd_set_models_workload(self._h, int(cell_seed), int(n_links), int(g0), int(count),
+                                                   _capi.dptr(g), _capi.iptr(ms), _capi.iptr(mr)))
+        self.n_links, self.n_models = n_links, count
+        return ms, mr
+
+    def workload_chains_device(self, cell_seed: int, n_links: int, count: int, d_links, g0: int = 0):
+        """Raw link records [count][n][31] into the device pointer d_links."""
+        self._check(self._L.pd_workload_chains_device(self._h, int(cell_seed), int(n_links), int(g0), int(count),
+                                                      d_links))
+
     def solve(self, algo, q, qdot, tau, out=None):
         """Host-buffer solve: q/qdot/tau (B, n) -> (qddot, status, round, index).
         `out` may be a preallocated (pinned) (B, n) float64 array."""

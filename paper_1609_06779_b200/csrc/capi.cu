@@ -39,6 +39,8 @@ struct IdOpts {
 void launch_idyn(const ModelView& mv, const BatchIO& io, const IdOpts& o, const double* raw, double* vel, double* acc,
                  double* frc, cudaStream_t s);
 bool jsiia_coop_path(int n, int64_t batch);
+void launch_workload_chains(uint64_t cell, int n, int64_t g0, int64_t count, double* d_links, cudaStream_t s);
+void launch_validate_models(const double* raw, int n, int64_t M, int32_t* status, int32_t* rule, cudaStream_t s);
 void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, cudaStream_t s);
 void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count, double* d_M,
                 cudaStream_t s);
@@ -959,6 +961,71 @@ void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links
   }
   std::strncpy(buf, m.c_str(), (size_t)buflen - 1);
   buf[buflen - 1] = '\0';
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- device workloads
+extern "C" {
+
+pd_status pd_workload_chains_device(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,
+                                    double* d_links) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (n_links <= 0 || count < 0 || g0 < 0 || (count > 0 && !d_links)) {
+    ctx->last_error = "workload chains: invalid arguments";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (count == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  launch_workload_chains(cell_seed, n_links, g0, count, d_links, ctx->stream);
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  return PD_OK;
+}
+
+pd_status pd_set_models_workload(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,
+                                 const double* gravity, int32_t* model_status, int32_t* model_rule) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (count <= 0 || n_links <= 0 || g0 < 0) {
+    ctx->last_error = "forward dynamics: chain has no links";
+    return PD_INVALID_ARGUMENT;
+  }
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int64_t n_models = count;
+  const size_t raw_bytes = sizeof(double) * PD_LINK_FIELDS * n_links * (size_t)n_models;
+  PD_CUDA(ctx->raw.ensure(raw_bytes + sizeof(double) * 3 * n_models));
+  const int64_t model_ld = (n_models + 31) / 32 * 32;
+  PD_CUDA(ctx->model.ensure(sizeof(double) * F_COUNT * n_links * (size_t)model_ld));
+  PD_CUDA(ctx->gravity.ensure(sizeof(double) * 3 * n_models));
+  PD_CUDA(ctx->mstatus.ensure(sizeof(int32_t) * n_models));
+  PD_CUDA(ctx->mrule.ensure(sizeof(int32_t) * n_models));
+  double* raw = ctx->raw.as<double>();
+  double* graw = raw + PD_LINK_FIELDS * n_links * (size_t)n_models;
+  launch_workload_chains(cell_seed, n_links, g0, count, raw, ctx->stream);
+  std::vector<double> g(3 * n_models);
+  for (int64_t m = 0; m < n_models; ++m)
+    for (int k = 0; k < 3; ++k) g[3 * m + k] = gravity ? gravity[k] : (k == 2 ? -9.81 : 0.0);
+  PD_CUDA(cudaMemcpyAsync(graw, g.data(), sizeof(double) * 3 * n_models, cudaMemcpyHostToDevice, ctx->stream));
+  launch_validate_models(raw, n_links, n_models, ctx->mstatus.as<int32_t>(), ctx->mrule.as<int32_t>(), ctx->stream);
+  ctx->h_mstatus.assign(n_models, 0);
+  ctx->h_mrule.assign(n_models, 0);
+  PD_CUDA(cudaMemcpyAsync(ctx->h_mstatus.data(), ctx->mstatus.p, sizeof(int32_t) * n_models, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(ctx->h_mrule.data(), ctx->mrule.p, sizeof(int32_t) * n_models, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  dim3 grid((unsigned)((n_models + 127) / 128), (unsigned)n_links);
+  pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, model_ld, ctx->model.as<double>(),
+                                                     ctx->gravity.as<double>());
+  ctx->launches += 3;
+  PD_CUDA(cudaGetLastError());
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (model_status) std::memcpy(model_status, ctx->h_mstatus.data(), sizeof(int32_t) * n_models);
+  if (model_rule) std::memcpy(model_rule, ctx->h_mrule.data(), sizeof(int32_t) * n_models);
+  ctx->n_links = n_links;
+  ctx->n_models = n_models;
+  ctx->model_ld = model_ld;
+  ctx->model_cl_valid = false;
+  return PD_OK;
 }
 
 }  // extern "C"

@@ -133,3 +133,40 @@ def test_errors(oracle):
         pd.inverse_dynamics(pd.RobotChain.from_records(bad), np.zeros(3), np.zeros(3), np.zeros(3))
     with pytest.raises(pd.InvalidArgument, match="mass must be positive"):
         pd.joint_space_inertia(pd.RobotChain.from_records(bad), np.zeros(3))
+
+
+@pytest.mark.parametrize("n,count,g0", [(8, 3000, 0), (64, 1500, 123456), (1, 5, 7)])
+def test_device_workload_generator(oracle, gpu_ctx, n, count, g0):
+    """§8f row 3: the device generator reproduces the host generator (and
+    through it the reference's random_chain / workload_chains): the integer
+    streams and every draw are bit exact (mass, com); fields through sin/cos
+    are within a few ulp -- the device's sin/cos are correctly rounded, glibc's
+    return the other neighbour in ~0.3% of evaluations (profiles/)."""
+    import torch
+    cell = oracle.workload_seed(42, n, 1 << 20)
+    host = oracle.workload_chains(cell, n, count, g0)
+    d = torch.empty((count, n, 31), dtype=torch.float64, device="cuda")
+    gpu_ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    gpu_ctx.workload_chains_device(cell, n, count, d.data_ptr(), g0)
+    gpu_ctx.synchronize()
+    gpu_ctx.set_stream(None)
+    dev = d.cpu().numpy()
+    assert np.array_equal(dev[..., 0:4], host[..., 0:4])  # mass, com: pure draws
+    assert np.array_equal(dev[..., 16:19], host[..., 16:19])  # linear screw part (zeros)
+    # all fields are O(0.1..10): a last-bit difference in sin/cos moves them by ~1e-16
+    assert np.abs(dev - host).max() <= 1e-14
+    assert (dev != host).any(axis=2).mean() < 0.05
+
+
+def test_set_models_workload_matches_host_models(oracle, gpu_ctx):
+    n, B = 24, 2000
+    cell = oracle.workload_seed(42, n, B)
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    gpu_ctx.set_models(oracle.workload_chains(cell, n, B), None)
+    a, st, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    ms, _ = gpu_ctx.set_models_workload(cell, n, B)
+    assert (ms == 0).all()
+    b, st2, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    assert (st == 0).all() and (st2 == 0).all()
+    for k in range(0, B, 97):
+        assert rel_gap(b[k], a[k]) <= 1e-12
