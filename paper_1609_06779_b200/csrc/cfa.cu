@@ -256,11 +256,127 @@ __device__ __forceinline__ void ws_store(double* ws, int n, int f0, int i, const
   for (int k = 0; k < K; ++k) ws[(f0 + k) * n + i] = in[k];
 }
 
-// PREP: stop after the OEE initial state is in the (global) workspace; the
-// grid-wide rounds of cfa_oee_coop finish the solve (long chains, c4).
+// PREP 1: stop after the OEE initial state is in the (global) workspace;
+// PREP 2: stop after the joint transforms and tau_delta -- the grid-wide
+// cfa_oee_coop then builds the operators, the initial state and runs the OEE
+// (long chains, c4).
+// Operators of link i (forward_dynamics.cpp:261-357): Z_i = [W_i | S_i],
+// C_i = Ad(rel_{i+1})^T Z_{i+1}, J_i = L L^T, G = L^{-1} Z_i, H = L^{-1} C_i:
+// own blocks G^T G (AD, XD, JD), couplings G^T H (UP, XS, XB, JO), the next
+// row's carried blocks H^T H (HH). Reads rel_{i+1} from the workspace (HT is
+// this link's scratch). Returns false if J_i is not positive definite.
+__device__ __forceinline__ bool cfa_link_ops(const ModelView& mv, int64_t mc, double* ws, int n, int i) {
+    double L[21], linv[6];
+  const bool ok = llt_inertia(mv.inertia(i, mc), L, linv);
+  double G[6][6];
+  householder_basis(mv.screw(i, mc), G);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) lower_solve6(L, linv, G[c]);
+  {
+    double ad[15], xd[5];
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s = fma(G[r][k], G[c][k], s);
+      if (r < 5) ad[pk(r, c)] = s;
+      else if (c < 5) xd[c] = s;
+      else ws[cfa::JD * n + i] = s;
+    }
+    ws_store<15>(ws, n, cfa::AD, i, ad);
+    ws_store<5>(ws, n, cfa::XD, i, xd);
+  }
+  if (i + 1 < n) {
+    const SE3d T1 = ws_get_se3(ws, n, cfa::REL, i + 1);
+    double Z1[6][6];
+    householder_basis(mv.screw(i + 1, mc), Z1);
+    double up[25], xs[5], xb[5];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+    const Sv col = adT_apply(T1, Sv{mk(Z1[c][0], Z1[c][1], Z1[c][2]), mk(Z1[c][3], Z1[c][4], Z1[c][5])});
+    double h[6] = {col.a.x, col.a.y, col.a.z, col.l.x, col.l.y, col.l.z};
+    lower_solve6(L, linv, h);
+    ws_store<6>(ws, n, cfa::HT + 6 * c, i, h);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s = fma(G[r][k], h[k], s);
+      if (r < 5 && c < 5) up[r * 5 + c] = -s;       // upper_i       (:347)
+      else if (r < 5) xs[r] = -s;                    // cross_super_i (:348)
+      else if (c < 5) xb[c] = -s;                    // cross_sub_i   (:349)
+      else ws[cfa::JO * n + i] = -s;                 // joint_off_i   (:350)
+    }
+    }
+    ws_store<25>(ws, n, cfa::UP, i, up);
+    ws_store<5>(ws, n, cfa::XS, i, xs);
+    ws_store<5>(ws, n, cfa::XB, i, xb);
+    double hh[21];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+    double hr[6];
+    ws_load<6>(ws, n, cfa::HT + 6 * r, i, hr);
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s = fma(hr[k], ws[(cfa::HT + 6 * c + k) * n + i], s);
+      hh[pk(r, c)] = s;
+    }
+    }
+    ws_store<21>(ws, n, cfa::HH, i, hh);
+  }
+  return ok;
+}
+
+// OEE initial state of row i: D_i = A_diag (+ row i-1's H^T H), U_i = upper_i,
+// R_i = -apply_cross(td)_i; ld(f, j) reads neighbour fields (the grid-wide
+// path reads them through L2). Writes the updated AD / XD / JD and OR.
+template <class LD>
+__device__ __forceinline__ void cfa_oee_init(double* ws, int n, int i, LD ld) {
+  double d[15], xd[5];
+  ws_load<15>(ws, n, cfa::AD, i, d);
+  ws_load<5>(ws, n, cfa::XD, i, xd);
+  double jd = ws[cfa::JD * n + i];
+  if (i > 0) {
+    double hh[21];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) hh[k] = ld(cfa::HH + k, i - 1);
+#pragma unroll
+    for (int r = 0; r < 5; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) d[pk(r, c)] += hh[pk(r, c)];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) xd[r] += hh[pk(5, r)];
+    jd += hh[pk(5, 5)];
+  }
+  const double td = ld(cfa::TD, i);
+  double r5[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) r5[r] = xd[r] * td;
+  if (i > 0) {
+    const double tdm = ld(cfa::TD, i - 1);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) r5[r] = fma(ld(cfa::XB + r, i - 1), tdm, r5[r]);
+  }
+  if (i + 1 < n) {
+    const double tdp = ld(cfa::TD, i + 1);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) r5[r] = fma(ws[(cfa::XS + r) * n + i], tdp, r5[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < 5; ++r) r5[r] = -r5[r];
+  ws_store<15>(ws, n, cfa::AD, i, d);
+  ws_store<5>(ws, n, cfa::XD, i, xd);
+  ws[cfa::JD * n + i] = jd;
+  ws_store<5>(ws, n, cfa::OR, i, r5);
+}
+
 // td_pre: tau_delta precomputed by tau_surplus_lane_kernel ([link][problem],
 // stride io.lds) -- the CTA then skips its scan-based bias stage.
-template <bool SMEM, bool PREP = false>
+template <bool SMEM, int PREP = 0>
 __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, double* __restrict__ gws, int lpt,
                                                        int64_t p_off, const double* __restrict__ td_pre = nullptr) {
   extern __shared__ double dyn_smem[];
@@ -291,74 +407,10 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     cta_bias_torque(mv, io, p, mc, ws, idf, lpt, scan_sm);  // ends with a barrier
   }
 
+  if (PREP == 2) return;  // kinematics + tau_delta only: the grid-wide path does the rest
   // ---- operators (forward_dynamics.cpp:261-357) ----------------------------
-  // Z_i = [W_i | S_i], C_i = Ad(rel_{i+1})^T Z_{i+1}, J_i = L L^T,
-  // G = L^{-1} Z_i, H = L^{-1} C_i: own blocks G^T G, couplings G^T H,
-  // the next row's carried blocks H^T H.
-  for (int i = i0; i < i1; ++i) {
-    double L[21], linv[6];
-    if (!llt_inertia(mv.inertia(i, mc), L, linv)) atomicOr(&s_link_fail, 1);
-    double G[6][6];
-    householder_basis(mv.screw(i, mc), G);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) lower_solve6(L, linv, G[c]);
-    {
-      double ad[15], xd[5];
-#pragma unroll
-      for (int r = 0; r < 6; ++r)
-#pragma unroll
-        for (int c = 0; c <= r; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) s = fma(G[r][k], G[c][k], s);
-          if (r < 5) ad[pk(r, c)] = s;
-          else if (c < 5) xd[c] = s;
-          else ws[cfa::JD * n + i] = s;
-        }
-      ws_store<15>(ws, n, cfa::AD, i, ad);
-      ws_store<5>(ws, n, cfa::XD, i, xd);
-    }
-    if (i + 1 < n) {
-      const SE3d T1 = ws_get_se3(ws, n, cfa::REL, i + 1);
-      double Z1[6][6];
-      householder_basis(mv.screw(i + 1, mc), Z1);
-      double up[25], xs[5], xb[5];
-#pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        const Sv col = adT_apply(T1, Sv{mk(Z1[c][0], Z1[c][1], Z1[c][2]), mk(Z1[c][3], Z1[c][4], Z1[c][5])});
-        double h[6] = {col.a.x, col.a.y, col.a.z, col.l.x, col.l.y, col.l.z};
-        lower_solve6(L, linv, h);
-        ws_store<6>(ws, n, cfa::HT + 6 * c, i, h);
-#pragma unroll
-        for (int r = 0; r < 6; ++r) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) s = fma(G[r][k], h[k], s);
-          if (r < 5 && c < 5) up[r * 5 + c] = -s;       // upper_i       (:347)
-          else if (r < 5) xs[r] = -s;                    // cross_super_i (:348)
-          else if (c < 5) xb[c] = -s;                    // cross_sub_i   (:349)
-          else ws[cfa::JO * n + i] = -s;                 // joint_off_i   (:350)
-        }
-      }
-      ws_store<25>(ws, n, cfa::UP, i, up);
-      ws_store<5>(ws, n, cfa::XS, i, xs);
-      ws_store<5>(ws, n, cfa::XB, i, xb);
-      double hh[21];
-#pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        double hr[6];
-        ws_load<6>(ws, n, cfa::HT + 6 * r, i, hr);
-#pragma unroll
-        for (int c = 0; c <= r; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) s = fma(hr[k], ws[(cfa::HT + 6 * c + k) * n + i], s);
-          hh[pk(r, c)] = s;
-        }
-      }
-      ws_store<21>(ws, n, cfa::HH, i, hh);
-    }
-  }
+  for (int i = i0; i < i1; ++i)
+    if (!cfa_link_ops(mv, mc, ws, n, i)) atomicOr(&s_link_fail, 1);
   __syncthreads();
   if (s_link_fail) {  // forward_dynamics.cpp:317-320
     if (t == 0) {
@@ -369,45 +421,8 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
     return;
   }
 
-  // ---- OEE initial state: D_i = A_diag (symmetric), U_i = upper_i,
-  //      R_i = -apply_cross(td)_i; diag/cross/joint blocks gain row i-1's H^T H.
-  for (int i = i0; i < i1; ++i) {
-    double d[15], xd[5];
-    ws_load<15>(ws, n, cfa::AD, i, d);
-    ws_load<5>(ws, n, cfa::XD, i, xd);
-    double jd = ws[cfa::JD * n + i];
-    if (i > 0) {
-      double hh[21];
-      ws_load<21>(ws, n, cfa::HH, i - 1, hh);
-#pragma unroll
-      for (int r = 0; r < 5; ++r)
-#pragma unroll
-        for (int c = 0; c <= r; ++c) d[pk(r, c)] += hh[pk(r, c)];
-#pragma unroll
-      for (int r = 0; r < 5; ++r) xd[r] += hh[pk(5, r)];
-      jd += hh[pk(5, 5)];
-    }
-    const double td = ws[cfa::TD * n + i];
-    double r5[5];
-#pragma unroll
-    for (int r = 0; r < 5; ++r) r5[r] = xd[r] * td;
-    if (i > 0) {
-      const double tdm = ws[cfa::TD * n + i - 1];
-#pragma unroll
-      for (int r = 0; r < 5; ++r) r5[r] = fma(ws[(cfa::XB + r) * n + i - 1], tdm, r5[r]);
-    }
-    if (i + 1 < n) {
-      const double tdp = ws[cfa::TD * n + i + 1];
-#pragma unroll
-      for (int r = 0; r < 5; ++r) r5[r] = fma(ws[(cfa::XS + r) * n + i], tdp, r5[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < 5; ++r) r5[r] = -r5[r];
-    ws_store<15>(ws, n, cfa::AD, i, d);
-    ws_store<5>(ws, n, cfa::XD, i, xd);
-    ws[cfa::JD * n + i] = jd;
-    ws_store<5>(ws, n, cfa::OR, i, r5);
-  }
+  // ---- OEE initial state ----------------------------------------------------
+  for (int i = i0; i < i1; ++i) cfa_oee_init(ws, n, i, [&](int f, int j) { return ws[f * n + j]; });
   __syncthreads();
   if (PREP) return;
 
@@ -611,14 +626,14 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
 // many SMs (the row's D, U, R in registers, as in the CTA kernel), the
 // published pivot data in the global workspace read through L2
 // (ld.global.cg), a grid barrier where the CTA kernel has __syncthreads.
-// Chains one after the other; cfa_cta_kernel<false, true> left each chain's
-// initial state in workspace slot c.
+// Chains one after the other; cfa_cta_kernel<false, 2> left each chain's
+// joint transforms and tau_delta in workspace slot c.
 __device__ __forceinline__ void cg_load(const double* ws, int n, int f0, int i, double* out, int K) {
   for (int k = 0; k < K; ++k) out[k] = __ldcg(ws + (size_t)(f0 + k) * n + i);
 }
 
-__global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restrict__ gws, int n, int count,
-                                                    int* __restrict__ bad) {
+__global__ void __launch_bounds__(128) cfa_oee_coop(ModelView mv, BatchIO io, double* __restrict__ gws, int n,
+                                                    int count, int* __restrict__ bad) {
   namespace cgr = cooperative_groups;
   cgr::grid_group grid = cgr::this_grid();
   const int i = (int)(blockIdx.x * blockDim.x + threadIdx.x);
@@ -627,7 +642,24 @@ __global__ void __launch_bounds__(128) cfa_oee_coop(BatchIO io, double* __restri
   for (int c = 0; c < count; ++c) {
     double* ws = gws + (size_t)c * cfa::FIELDS * n;
     const int64_t p = c;
+    if (__ldg(mv.mstatus + mv.model_of(p)) != PD_SLOT_OK) continue;  // the CTA kernel reported the model's rule
     if (i == 0) *bad = n;
+    grid.sync();
+    // operators and the OEE initial state, a thread per link (the CTA kernel
+    // left rel_i and tau_delta in the workspace)
+    if (own && !cfa_link_ops(mv, mv.model_of(p), ws, n, i)) atomicMin(bad, -1);
+    grid.sync();
+    if (__ldcg(bad) < 0) {  // forward_dynamics.cpp:317-320
+      if (i == 0) {
+        io.status[p] = PD_SLOT_LINK_INERTIA_NOT_PD;
+        io.eround[p] = 0;
+        io.eindex[p] = 0;
+      }
+      grid.sync();
+      continue;
+    }
+    if (own) cfa_oee_init(ws, n, i, [&](int f, int j) { return __ldcg(ws + (size_t)f * n + j); });
+    grid.sync();
     double D[15], U[25], R[5];
     if (own) {
 #pragma unroll
@@ -750,11 +782,12 @@ bool cfa_coop_path(int n, int64_t batch) { return (size_t)cfa::FIELDS * n * size
 void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s) {
   const int n = mv.n;
   const int lpt = (n + 255) / 256;
-  cfa_cta_kernel<false, true><<<(unsigned)io.B, 256, 0, s>>>(mv, io, gws, lpt, 0);
+  cfa_cta_kernel<false, 2><<<(unsigned)io.B, 256, 0, s>>>(mv, io, gws, lpt, 0);
   int count = (int)io.B;
   int nn = n;
   BatchIO iol = io;
-  void* args[] = {&iol, &gws, &nn, &count, &bad};
+  ModelView mvl = mv;
+  void* args[] = {&mvl, &iol, &gws, &nn, &count, &bad};
   const unsigned grid = (unsigned)((n + 127) / 128);
   (void)sm_count;
   cudaLaunchCooperativeKernel((const void*)cfa_oee_coop, dim3(grid), dim3(128), args, 0, s);
