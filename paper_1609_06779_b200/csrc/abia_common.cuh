@@ -116,11 +116,18 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   }
   const Sv U = sym6_apply(Ia, S0);
   const double lambda = dot(S0, U);
-  if (!(lambda > 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
-    st.code = PD_SLOT_DEGENERATE_ARTICULATION;
-    st.eidx = i;
+  // degeneracy test on the link-frame trace (forward_dynamics.cpp:140-144).
+  // ||Ad(X^-1)|| <= 1 + |p|, so tr_link <= (1 + |p|)^2 tr_base <= 2 (1 + |p|^2)
+  // tr_base: the exact trace is only needed when lambda fails that cheap bound
+  // (never, for sane chains).
+  const double pn2 = dot(st.X.p, st.X.p);
+  if (!(lambda > 2e-14 * (1.0 + pn2) * sym6_trace(Ia))) {
+    if (!(lambda > 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
+      st.code = PD_SLOT_DEGENERATE_ARTICULATION;
+      st.eidx = i;
+    }
   }
-  const double inv_l = 1.0 / lambda;
+  const double inv_l = rcp_nr(lambda);
   const double u = (tau_delta - dot(S0, st.Z0)) * inv_l;  // forward_dynamics.cpp:202-212
   const Sv g0 = inv_l * U;                                 // gain (base frame)
   rec[0] = g0.a.x;

@@ -34,16 +34,6 @@ size_t abia_cta_workspace_bytes(int n) { return (size_t)abc::FIELDS * n * sizeof
 // Thread 0 prefetches link i-1 into registers while it works on link i.
 constexpr int kCh = 64;  // links per staged chunk
 
-// 1/x without the division routine's branches: hardware approximation and two
-// Newton steps (relative error ~1e-16); x is an articulated-inertia projection.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 // staged per link (backward): S0 6 | J0 21 | td | JS = J0 S0 6 | lamJ | trJ | q 3
 constexpr int kS0 = 0, kJ0 = 6, kTd = 27, kJS = 28, kLJ = 34, kTJ = 35, kQv = 36, kStB = 39;
 constexpr int kStC = 13;  // forward: g0 6 | S0 6 | u

@@ -63,10 +63,10 @@ __device__ __forceinline__ void householder_basis(const Sv& S, double z[6][6]) {
   if (tail > 2.2250738585072014e-308) {
     double beta = sqrt(fma(c0, c0, tail));
     if (c0 >= 0.0) beta = -beta;
-    const double den = c0 - beta;
+    const double iden = rcp_nr(c0 - beta);  // branch-free reciprocals instead of 6 divisions
 #pragma unroll
-    for (int k = 1; k < 6; ++k) v[k] = s[k] / den;
-    tau = (beta - c0) / beta;
+    for (int k = 1; k < 6; ++k) v[k] = s[k] * iden;
+    tau = (beta - c0) * rcp_nr(beta);
   }
 #pragma unroll
   for (int c = 0; c < 5; ++c)
@@ -99,9 +99,8 @@ __device__ __forceinline__ bool llt_inertia(const Inertia& J, double L[21], doub
 #pragma unroll
     for (int j = 0; j < k; ++j) x = fma(-L[pk(k, j)], L[pk(k, j)], x);
     ok = ok && (x > 0.0);
-    const double l = sqrt(x);
-    L[pk(k, k)] = l;
-    inv[k] = 1.0 / l;
+    inv[k] = rsqrt(x);  // one reciprocal square root per pivot
+    L[pk(k, k)] = x * inv[k];
 #pragma unroll
     for (int i = k + 1; i < 6; ++i) {
       double s = a[pk(i, k)];
