@@ -99,7 +99,7 @@ __device__ __forceinline__ bool llt_inertia(const Inertia& J, double L[21], doub
 #pragma unroll
     for (int j = 0; j < k; ++j) x = fma(-L[pk(k, j)], L[pk(k, j)], x);
     ok = ok && (x > 0.0);
-    inv[k] = rsqrt(x);  // one reciprocal square root per pivot
+    inv[k] = rsqrt_nr(x);  // one reciprocal square root per pivot
     L[pk(k, k)] = x * inv[k];
 #pragma unroll
     for (int i = k + 1; i < 6; ++i) {
@@ -141,7 +141,7 @@ __device__ __forceinline__ bool chol5(const double D[15], double L[10], double i
 #pragma unroll
     for (int k = 0; k < j; ++k) x = fma(-L[pks(j, k)], L[pks(j, k)], x);
     ok = ok && (x > thr);
-    il[j] = rsqrt(fabs(x));
+    il[j] = rsqrt_nr(fabs(x));
 #pragma unroll
     for (int i = j + 1; i < 5; ++i) {
       double s = D[pk(i, j)];

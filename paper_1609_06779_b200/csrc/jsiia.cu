@@ -124,7 +124,7 @@ __device__ bool tile_potrf(double* A, int ld, double* invd, int lane) {
     const double dmm = __shfl_sync(0xffffffffu, acc, m);
     spd = spd && dmm > 0.0;
     // one reciprocal square root per pivot: 1/L_mm, L_mm = d * (1/L_mm)
-    const double inv = rsqrt(dmm > 0.0 ? dmm : 1.0);
+    const double inv = rsqrt_nr(dmm > 0.0 ? dmm : 1.0);
     const double lmm = (dmm > 0.0 ? dmm : 1.0) * inv;
     inv_d = (lane == m) ? inv : inv_d;
     r[m] = (lane == m) ? lmm : ((lane > m) ? acc * inv : r[m]);

@@ -396,6 +396,19 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 
+// 1/sqrt(x) without the library routine's range-check branch: the hardware
+// approximation (rel. error ~1e-6) and two Newton steps (~1 ulp;
+// tools/micro/rsqrt_probe.cu). Used on pivot chains of the factorizations,
+// where a CALL to the slow path would split the unrolled code into blocks.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y * y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x, y * y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
 // joint screw from its stored components
 __device__ __forceinline__ Sv joint_screw(double w, double vx, double vz) { return {mk(0.0, 0.0, w), mk(vx, 0.0, vz)}; }
 
