@@ -521,7 +521,8 @@ void pd_destroy(pd_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->model, &ctx->gravity, &ctx->mstatus, &ctx->mrule, &ctx->raw, &ctx->abia_scratch, &ctx->cta_ws,
-                    &ctx->slots, &ctx->io_q, &ctx->io_qd, &ctx->io_tau, &ctx->io_qdd, &ctx->io_status})
+                    &ctx->slots, &ctx->io_q, &ctx->io_qd, &ctx->io_tau, &ctx->io_qdd, &ctx->io_status, &ctx->model_cl,
+                    &ctx->states, &ctx->cfa_td})
     b->release();
   if (ctx->cp_in) {
     cudaStreamSynchronize(ctx->cp_in);

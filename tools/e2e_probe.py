@@ -45,3 +45,22 @@ for algo in ("abia", "jsiia"):
         ctx.solve(pd.FdAlgo[algo], *pin, out=out)
     dt = (time.perf_counter() - t0) / 20
     print(f"solve {algo}: {dt * 1e3:.3f} ms/step, {B / dt / 1e6:.1f} M solves/s (chunks env {os.environ.get('PD_E2E_CHUNKS')})")
+
+# raw PCIe duplex: H2D of the inputs and D2H of an output on separate streams at once
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+d2 = torch.empty((B, n), dtype=torch.float64, device="cuda")
+for _ in range(3):
+    with torch.cuda.stream(s1):
+        d.copy_(x, non_blocking=True)
+    with torch.cuda.stream(s2):
+        y.copy_(d2, non_blocking=True)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(10):
+    with torch.cuda.stream(s1):
+        d.copy_(x, non_blocking=True)
+    with torch.cuda.stream(s2):
+        y.copy_(d2, non_blocking=True)
+torch.cuda.synchronize()
+both = (time.perf_counter() - t0) / 10
+print(f"H2D + D2H concurrently: {both * 1e3:.3f} ms (serial would be {(h2d + d2h) * 1e3:.3f} ms)")
