@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128) idyn_lane_kernel(ModelView mv, BatchIO io
 // lane per chain, into td[link][problem] (stride io.lds): the bias stage of
 // the CTA-per-chain CFA kernel for large batches, where sequential per-lane
 // recurrences beat CTA-wide scans (no barriers, work-optimal).
-__global__ void __launch_bounds__(128) tau_surplus_lane_kernel(ModelView mv, BatchIO io, double* __restrict__ td) {
+__global__ void __launch_bounds__(128, 4) tau_surplus_lane_kernel(ModelView mv, BatchIO io, double* __restrict__ td) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= io.B) return;
   const int n = mv.n;
