@@ -22,6 +22,7 @@
 // FullPivLU::isInvertible (|pivot| > 5 eps max|diag|). The reported error
 // is the reference's: smallest failing row, its first failing pivot.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "cta_common.cuh"
 
@@ -792,6 +793,242 @@ void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* b
   cudaLaunchCooperativeKernel((const void*)cfa_oee_coop, dim3(grid), dim3(128), args, 0, s);
 }
 
+
+// ---------------------------------------------------------------------------
+// cfa_row_kernel: the n <= 256 case (a thread per link / row, everything in
+// shared memory). The operator blocks a row owns (its diagonal block D and
+// coupling U, the H columns) stay in registers from the operator stage through
+// the OEE rounds, so only what neighbours read lives in shared memory and the
+// workspace shrinks from 110 to 70 doubles per link (fields reused across
+// stages) and each round's shared-memory traffic is only the published pivot
+// data. (c5: 46.8 -> 35.7 ms against the workspace-resident kernel.)
+namespace cfr {
+constexpr int TD = 0, XS = 1, XB = 6, XD = 11, JD = 16, JO = 17;  // persistent
+constexpr int REL = 18, X = 30, V = 42, TMP = 48;                 // kinematics / bias stage
+constexpr int HH = 30;                                            // 21: operators -> initial state
+constexpr int PL = 18, SG = 28, PY = 30, PR = 55, PI = 60, OR = 65;  // OEE
+constexpr int FIELDS = 70;
+}  // namespace cfr
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO io, const double* __restrict__ td_pre) {
+  extern __shared__ double dyn_smem[];
+  __shared__ ScanSmem scan_sm;
+  __shared__ int s_bad, s_link_fail;
+  const int n = mv.n;
+  const int64_t p = blockIdx.x;
+  const int64_t mc = mv.model_of(p);
+  double* ws = dyn_smem;
+  const int t = threadIdx.x, i = t;
+  const bool own = i < n;
+  if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) {
+    if (t == 0) model_rejected(mv, io, p, mc);
+    return;
+  }
+  if (t == 0) {
+    s_bad = n;
+    s_link_fail = 0;
+  }
+  // ---- kinematics + torque surplus
+  const IdFields idf{cfr::REL, cfr::X, cfr::V, cfr::TMP, cfr::TD};
+  cta_kinematics(mv, io, p, mc, ws, idf, 1);
+  if (td_pre) {
+    if (own) ws[cfr::TD * n + i] = __ldg(td_pre + (int64_t)i * io.lds + p);
+    __syncthreads();
+  } else {
+    cta_bias_torque(mv, io, p, mc, ws, idf, 1, scan_sm);  // ends with a barrier
+  }
+  // ---- operators (forward_dynamics.cpp:261-357): own blocks into registers
+  double D[15], U[25], R[5];
+  if (own) {
+    double L[21], linv[6];
+    if (!llt_inertia(mv.inertia(i, mc), L, linv)) atomicOr(&s_link_fail, 1);
+    double G[6][6];
+    householder_basis(mv.screw(i, mc), G);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) lower_solve6(L, linv, G[c]);
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) sacc = fma(G[r][k], G[c][k], sacc);
+        if (r < 5) D[pk(r, c)] = sacc;
+        else if (c < 5) ws[(cfr::XD + c) * n + i] = sacc;
+        else ws[cfr::JD * n + i] = sacc;
+      }
+    if (i + 1 < n) {
+      const SE3d T1 = ws_get_se3(ws, n, cfr::REL, i + 1);
+      double Z1[6][6], H[6][6];
+      householder_basis(mv.screw(i + 1, mc), Z1);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const Sv col = adT_apply(T1, Sv{mk(Z1[c][0], Z1[c][1], Z1[c][2]), mk(Z1[c][3], Z1[c][4], Z1[c][5])});
+        double* h = H[c];
+        h[0] = col.a.x; h[1] = col.a.y; h[2] = col.a.z; h[3] = col.l.x; h[4] = col.l.y; h[5] = col.l.z;
+        lower_solve6(L, linv, h);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) sacc = fma(G[r][k], h[k], sacc);
+          if (r < 5 && c < 5) U[r * 5 + c] = -sacc;            // upper_i       (:347)
+          else if (r < 5) ws[(cfr::XS + r) * n + i] = -sacc;   // cross_super_i (:348)
+          else if (c < 5) ws[(cfr::XB + c) * n + i] = -sacc;   // cross_sub_i   (:349)
+          else ws[cfr::JO * n + i] = -sacc;                    // joint_off_i   (:350)
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) sacc = fma(H[r][k], H[c][k], sacc);
+          ws[(cfr::HH + pk(r, c)) * n + i] = sacc;
+        }
+    }
+  }
+  __syncthreads();
+  if (s_link_fail) {  // forward_dynamics.cpp:317-320
+    if (t == 0) {
+      io.status[p] = PD_SLOT_LINK_INERTIA_NOT_PD;
+      io.eround[p] = 0;
+      io.eindex[p] = 0;
+    }
+    return;
+  }
+  // ---- OEE initial state: D_i gains row i-1's H^T H; R_i = -apply_cross(td)_i
+  if (own) {
+    double xd[5];
+    ws_load<5>(ws, n, cfr::XD, i, xd);
+    double jd = ws[cfr::JD * n + i];
+    if (i > 0) {
+#pragma unroll
+      for (int r = 0; r < 5; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) D[pk(r, c)] += ws[(cfr::HH + pk(r, c)) * n + i - 1];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) xd[r] += ws[(cfr::HH + pk(5, r)) * n + i - 1];
+      jd += ws[(cfr::HH + pk(5, 5)) * n + i - 1];
+    }
+    const double td = ws[cfr::TD * n + i];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) R[r] = xd[r] * td;
+    if (i > 0) {
+      const double tdm = ws[cfr::TD * n + i - 1];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) R[r] = fma(ws[(cfr::XB + r) * n + i - 1], tdm, R[r]);
+    }
+    if (i + 1 < n) {
+      const double tdp = ws[cfr::TD * n + i + 1];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) R[r] = fma(ws[(cfr::XS + r) * n + i], tdp, R[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) R[r] = -R[r];
+    ws_store<5>(ws, n, cfr::XD, i, xd);
+    ws[cfr::JD * n + i] = jd;
+  }
+  __syncthreads();  // HH is reused by the published pivots below
+  // ---- OEE rounds (oee.hpp:73-145), row state in registers
+  const int rounds = ceil_log2_dev(n);
+  int h = 1;
+  for (int round = 1; round <= rounds; ++round, h <<= 1) {
+    if (own) {
+      double Lk[10], il[5], rt[5];
+      const bool ok = chol5(D, Lk, il);
+      ws_store<10>(ws, n, cfr::PL, i, Lk);
+      ws_store<5>(ws, n, cfr::PI, i, il);
+      ws[cfr::SG * n + i] = ok ? 0.0 : 1.0;
+#pragma unroll
+      for (int r = 0; r < 5; ++r) rt[r] = R[r];
+      lsolve5(Lk, il, rt);
+      ws_store<5>(ws, n, cfr::PR, i, rt);
+      if (i < n - h) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          double col[5];
+#pragma unroll
+          for (int r = 0; r < 5; ++r) col[r] = U[r * 5 + c];
+          lsolve5(Lk, il, col);
+#pragma unroll
+          for (int r = 0; r < 5; ++r) ws[(cfr::PY + r * 5 + c) * n + i] = col[r];
+        }
+      }
+    }
+    __syncthreads();
+    if (own) {
+      const bool up_bad = (i < n - h) && ws[cfr::SG * n + i + h] != 0.0;
+      const bool dn_bad = (i >= h) && ws[cfr::SG * n + i - h] != 0.0;
+      if (up_bad || dn_bad) atomicMin(&s_bad, i);
+      if (i < n - h) {
+        const int k = i + h;
+        double Lk[10], il[5], rt[5];
+        ws_load<10>(ws, n, cfr::PL, k, Lk);
+        ws_load<5>(ws, n, cfr::PI, k, il);
+        ws_load<5>(ws, n, cfr::PR, k, rt);
+        oee_up(D, R, U, Lk, il, rt, i < n - 2 * h, [&](int r, int c) { return ws[(cfr::PY + r * 5 + c) * n + k]; });
+      }
+      if (i >= h) {
+        const int k = i - h;
+        double rt[5];
+        ws_load<5>(ws, n, cfr::PR, k, rt);
+        oee_down(D, R, rt, [&](int r, int c) { return ws[(cfr::PY + r * 5 + c) * n + k]; });
+      }
+    }
+    __syncthreads();
+    if (s_bad < n) {
+      if (t == 0) {
+        const int ib = s_bad;
+        const bool up_bad = (ib < n - h) && ws[cfr::SG * n + ib + h] != 0.0;
+        io.status[p] = PD_SLOT_OEE_SINGULAR_PIVOT;
+        io.eround[p] = round;
+        io.eindex[p] = up_bad ? ib + h : ib - h;
+      }
+      return;
+    }
+  }
+  // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
+  if (own) {
+    if (!oee_final(D, R)) atomicMin(&s_bad, i);
+    ws_store<5>(ws, n, cfr::OR, i, R);  // constraint force F_c,i
+  }
+  __syncthreads();
+  if (s_bad < n) {
+    if (t == 0) {
+      io.status[p] = PD_SLOT_OEE_SINGULAR_FINAL;
+      io.eround[p] = rounds;
+      io.eindex[p] = s_bad;
+    }
+    return;
+  }
+  // ---- qdd = apply_joint(td) + apply_cross_transpose(F_c) (:378-416, :441-442)
+  if (own) {
+    const double td = ws[cfr::TD * n + i];
+    double v = ws[cfr::JD * n + i] * td;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) v = fma(ws[(cfr::XD + r) * n + i], R[r], v);
+    if (i > 0) {
+      v = fma(ws[cfr::JO * n + i - 1], ws[cfr::TD * n + i - 1], v);
+#pragma unroll
+      for (int r = 0; r < 5; ++r) v = fma(ws[(cfr::XS + r) * n + i - 1], ws[(cfr::OR + r) * n + i - 1], v);
+    }
+    if (i + 1 < n) {
+      v = fma(ws[cfr::JO * n + i], ws[cfr::TD * n + i + 1], v);
+#pragma unroll
+      for (int r = 0; r < 5; ++r) v = fma(ws[(cfr::XB + r) * n + i], ws[(cfr::OR + r) * n + i + 1], v);
+    }
+    io.put_qdd(i, p, v);
+  }
+  if (t == 0) {
+    io.status[p] = PD_SLOT_OK;
+    io.eround[p] = 0;
+    io.eindex[p] = 0;
+  }
+}
+
 size_t cfa_workspace_bytes(int n) { return (size_t)cfa::FIELDS * n * sizeof(double); }
 
 // Shared-memory workspace when it fits (n <= 260), otherwise one global slot
@@ -803,7 +1040,22 @@ void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws
   if (nt > 256) nt = 256;
   const int lpt = (n + nt - 1) / nt;
   const size_t ws_bytes = cfa_workspace_bytes(n);
-  if (ws_bytes <= 224 * 1024) {
+  static const bool old_kernel = std::getenv("PD_CFA_CTA_KERNEL") != nullptr;
+  if (n <= 256 && !old_kernel) {  // thread per row, compact workspace, register cap per size class
+    const size_t rb = (size_t)cfr::FIELDS * n * sizeof(double);
+    auto go = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
+      kernel<<<(unsigned)io.B, nt, rb, s>>>(mv, io, td_pre);
+    };
+    // (a c5 sweep of 4 / 5 / 6 chains per SM: register caps that spill lose more
+    // than the extra warps gain; 4 x 64 threads at <= 255 registers is best)
+    if (nt <= 64)
+      go(cfa_row_kernel<64, 4>);
+    else if (nt <= 128)
+      go(cfa_row_kernel<128, 2>);
+    else
+      go(cfa_row_kernel<256, 1>);
+  } else if (ws_bytes <= 224 * 1024) {
     cudaFuncSetAttribute(cfa_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
     cfa_cta_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, lpt, 0, td_pre);
   } else {
