@@ -324,9 +324,11 @@ __device__ __forceinline__ void fast_sincos(double x, double* s, double* c) {
     return;
   }
   const double j = rint(x * 0.63661977236758134308);  // 2/pi
+  // pi/2 = pio2_1 (33 bits) + pio2_2 (33 bits) + pio2_2t (fdlibm's split):
+  // j * pio2_1 and j * pio2_2 are exact for |j| < 2^20, the FMAs round once
   double r = fma(-j, 1.57079632673412561417e+00, x);
-  r = fma(-j, 6.07710050650619224932e-11, r);
-  r = fma(-j, 2.02226624871116645580e-21, r);
+  r = fma(-j, 6.07710050630396597660e-11, r);
+  r = fma(-j, 2.02226624879595063154e-21, r);
   const double z = r * r, z2 = z * z, z4 = z2 * z2;
   const double ps = fma(z4, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
                         fma(z2, fma(z, 2.75573137070700676789e-06, -1.98412698298579493134e-04),
