@@ -200,7 +200,7 @@ constexpr __host__ __device__ int bidx(int i, int j) { return i * (i + 1) / 2 + 
 
 // Model read from the link-fastest copy mcl[(chain * F_COUNT + field) * n + link].
 template <int NB>
-__global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 4 : 3) jsiia_dmma_kernel(ModelView mv, const double* __restrict__ mcl,
+__global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 5 : 3) jsiia_dmma_kernel(ModelView mv, const double* __restrict__ mcl,
                                                                  BatchIO io) {
   constexpr int NP = NB * 8;               // padded links
   constexpr int LPL = (NP + 31) / 32;      // links per lane
