@@ -698,12 +698,13 @@ struct FullPivLU {
   }
 };
 
-// Cholesky with Eigen::LLT semantics (failure iff a pivot <= 0).
+// Cholesky with Eigen::LLT semantics: failure iff a pivot x <= 0 (Eigen's
+// llt_inplace test -- a NaN pivot does not fail, the NaN propagates).
 inline bool llt_inplace(double* a, int n) {  // row-major n x n; lower L on return
   for (int k = 0; k < n; ++k) {
     double x = a[k * n + k];
     for (int j = 0; j < k; ++j) x -= a[k * n + j] * a[k * n + j];
-    if (!(x > 0.0)) return false;
+    if (x <= 0.0) return false;
     x = std::sqrt(x);
     a[k * n + k] = x;
     for (int i = k + 1; i < n; ++i) {

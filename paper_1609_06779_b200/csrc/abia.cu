@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(128) abia_lane_kernel(ModelView mv, BatchIO io
     double rec[kRec];
     const Sv S = mv.screw(i, mc);
     abia_pass_b(st, i, n, joint_transform(S, mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc), io.ld(io.q, i, p)), S,
-                io.ld(io.qd, i, p), mv.inertia(i, mc), io.ld(io.tau, i, p), rec);
+                io.ld(io.qd, i, p), mv.inertia(i, mc), io.ld(io.tau, i, p), rec, io.ld(io.q, i, p));
 #pragma unroll
     for (int k = 0; k < kRec; ++k) scratch[((int64_t)i * kRec + k) * B + p] = rec[k];
   }

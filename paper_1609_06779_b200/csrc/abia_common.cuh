@@ -67,6 +67,7 @@ struct AbiaState {
   Sym6 P0;      // projected articulated inertia of the child link
   Sv a0;        // pass C acceleration
   int code, eidx;
+  bool nan_tip;  // some joint angle q_k, k > current link, is not finite
 };
 
 __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
@@ -80,6 +81,19 @@ __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
   st.a0 = svzero();
   st.code = PD_SLOT_OK;
   st.eidx = 0;
+  st.nan_tip = false;
+}
+
+// The reference's degeneracy verdict for link i (forward_dynamics.cpp:140-144),
+// !(lambda > 1e-14 tr(I^A_i)), evaluated on its link-frame quantities. Those
+// depend on the joint angles of the links beyond i only, while the base-frame
+// lambda here also sees the links before i; so with a non-finite joint angle
+// the reference's lambda_i is NaN iff one lies beyond i (nan_tip), and a NaN
+// reaching lambda only from the base side leaves the reference's test passing.
+__device__ __forceinline__ bool abia_degenerate(bool nan_tip, double lambda, double threshold) {
+  if (nan_tip) return true;
+  if (lambda != lambda) return false;
+  return !(lambda > threshold);
 }
 
 // pass A, link i (base -> tip): X_i = rel_i X_{i-1}, V0 and A0 (qddot = 0)
@@ -96,7 +110,7 @@ __device__ __forceinline__ void abia_pass_a(AbiaState& st, const SE3d& rel, cons
 // pass B, link i (tip -> base): link wrench and tau_delta, articulated
 // inertia, z sweep and u; writes the 13-double record; steps back to link i-1.
 __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const SE3d& rel, const Sv& S, double qd,
-                                            const Inertia& Jl, double tau, double rec[kRec]) {
+                                            const Inertia& Jl, double tau, double rec[kRec], double q) {
   const Sv S0 = adinv_screw(st.X, S);
   const Inertia J0 = inertia_to_base(Jl, st.X);
   // link wrench, bias torque                      inverse_dynamics.cpp:103-112,146-150
@@ -121,8 +135,8 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   // tr_base: the exact trace is only needed when lambda fails that cheap bound
   // (never, for sane chains).
   const double pn2 = dot(st.X.p, st.X.p);
-  if (!(lambda > 2e-14 * (1.0 + pn2) * sym6_trace(Ia))) {
-    if (!(lambda > 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
+  if (st.nan_tip || !(lambda > 2e-14 * (1.0 + pn2) * sym6_trace(Ia))) {
+    if (abia_degenerate(st.nan_tip, lambda, 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
       st.code = PD_SLOT_DEGENERATE_ARTICULATION;
       st.eidx = i;
     }
@@ -165,6 +179,7 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
     st.V0 = svfma(-qd, S0, st.V0);
     st.X = step_back(rel, st.X);
   }
+  st.nan_tip = st.nan_tip || !isfinite(q);
 }
 
 // pass C, link i (base -> tip): qdd_i = u_i - g0_i . a0_{i-1}; a0_i = a0_{i-1} + S0_i qdd_i

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(KT, MINB)
 #pragma unroll
     for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
     double rec[kRec];
-    abia_pass_b(st, i, n, stage_rel<KT>(f, sn, cs), stage_screw<KT>(f), f[kQD * KT], J, f[kTAU * KT], rec);
+    abia_pass_b(st, i, n, stage_rel<KT>(f, sn, cs), stage_screw<KT>(f), f[kQD * KT], J, f[kTAU * KT], rec, f[kQ * KT]);
     if (live) {
 #pragma unroll
       for (int j = 0; j < kRec; ++j) {
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
       for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
       double rec[kRec];
       abia_pass_b(st, i, n, row_rel<KT>(f, F_KIN, S, q, sn, cs), S, f[(F_COUNT + 1) * KT], J, f[(F_COUNT + 2) * KT],
-                  rec);
+                  rec, q);
       if (live) {
 #pragma unroll
         for (int j = 0; j < kRec; ++j) st_hint(scratch + ((int64_t)i * kRec + j) * scr_ld + p, rec[j], pol_last);

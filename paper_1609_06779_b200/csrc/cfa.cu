@@ -99,7 +99,7 @@ __device__ __forceinline__ bool llt_inertia(const Inertia& J, double L[21], doub
     double x = a[pk(k, k)];
 #pragma unroll
     for (int j = 0; j < k; ++j) x = fma(-L[pk(k, j)], L[pk(k, j)], x);
-    ok = ok && (x > 0.0);
+    ok = ok && !(x <= 0.0);  // Eigen LLT's failure test
     inv[k] = rsqrt_nr(x);  // one reciprocal square root per pivot
     L[pk(k, k)] = x * inv[k];
 #pragma unroll

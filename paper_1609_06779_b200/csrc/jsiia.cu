@@ -122,7 +122,7 @@ __device__ bool tile_potrf(double* A, int ld, double* invd, int lane) {
     for (int p = 0; p < m; ++p) a4[p & 3] = fma(-r[p], ld1<CG>(A + m * ld + p), a4[p & 3]);
     const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     const double dmm = __shfl_sync(0xffffffffu, acc, m);
-    spd = spd && dmm > 0.0;
+    spd = spd && !(dmm <= 0.0);  // Eigen LLT: fails iff a pivot <= 0 (NaN propagates)
     // one reciprocal square root per pivot: 1/L_mm, L_mm = d * (1/L_mm)
     const double inv = rsqrt_nr(dmm > 0.0 ? dmm : 1.0);
     const double lmm = (dmm > 0.0 ? dmm : 1.0) * inv;

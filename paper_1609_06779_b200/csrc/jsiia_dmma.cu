@@ -84,7 +84,7 @@ __device__ __forceinline__ void potrf_inv8(double (&c)[2], double (&x)[2], bool&
     const double ag = shfl(c[e], 4 * g + tm);                                 // A[g][m]
     const double ac0 = shfl(c[e], 8 * t + tm), ac1 = shfl(c[e], 8 * t + 4 + tm);  // A[2t][m], A[2t+1][m]
     const double xu0 = shfl(x[0], 4 * m + t), xu1 = shfl(x[1], 4 * m + t);   // X[m][2t], X[m][2t+1]
-    spd = spd && (d > 0.0);
+    spd = spd && !(d <= 0.0);  // Eigen LLT: fails iff a pivot <= 0 (NaN propagates)
     const double il = rsqrt_nr(d);  // 1 / L[m][m]; L[m][m] itself is never needed again
     const double lg = ag * il, lc0 = ac0 * il, lc1 = ac1 * il;
     if (t == tm) c[e] = (g == m) ? d * il : ((g > m) ? lg : c[e]);

@@ -234,3 +234,33 @@ def test_cfa_large_batch_with_lane_bias_pass(oracle, gpu_ctx, n):
     ref, _ = oracle.batch_forward_dynamics("cfa", links[idx], [0, 0, -9.81], q[idx], qd[idx], tau[idx])
     for k, b in enumerate(idx):
         assert rel_gap(qdd[b], ref[k]) <= TOL
+
+
+@pytest.mark.parametrize("n,B", [(12, 6), (80, 4)])
+def test_nan_inputs_follow_the_reference(oracle, gpu_ctx, n, B):
+    """Non-finite inputs take the reference's error paths: Eigen's LLT only
+    fails on a pivot <= 0, so JSIIA returns NaN without an error
+    (forward_dynamics.cpp:93-116); ABIA's `!(lambda > 1e-14 tr)` fails at the
+    first joint (tip side) whose link-frame articulated inertia sees the NaN,
+    i.e. one below a NaN joint angle (:140-144), and never for NaN rates or
+    torques. The GPU's base-frame ABIA emulates that propagation. (80, 4) runs
+    the CTA-per-chain ABIA path."""
+    cell = oracle.workload_seed(42, n, B)
+    links = oracle.workload_chains(cell, n, B)
+    q, qd, tau = (a.copy() for a in oracle.workload_inputs(cell, n, B, 0))
+    q[1, 5] = np.nan      # -> ABIA degenerate at joint 4
+    q[2, 0] = np.inf      # base joint: no degeneracy, NaN result
+    qd[3, n // 2] = np.nan  # rates: NaN result only
+    gpu_ctx.set_models(links, None)
+    for algo in (pd.FdAlgo.jsiia, pd.FdAlgo.abia):
+        qdd, st, rd, ix = gpu_ctx.solve(algo, q, qd, tau)
+        for b in range(B):
+            try:
+                ref = oracle.forward_dynamics(ONAME[algo], links[b], [0, 0, -9.81], q[b], qd[b], tau[b])
+                msg = ""
+            except oracle.OracleError as e:
+                ref, msg = None, str(e)
+            got = pd.api._capi.slot_message(st[b], rd[b], ix[b], n) if st[b] else ""
+            assert got == msg, (algo, b, got, msg)
+            if b == 0:
+                assert rel_gap(qdd[b], ref) <= TOL
