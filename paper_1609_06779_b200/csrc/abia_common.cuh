@@ -67,7 +67,7 @@ struct AbiaState {
   Sym6 P0;      // projected articulated inertia of the child link
   Sv a0;        // pass C acceleration
   int code, eidx;
-  bool nan_tip;  // some joint angle q_k, k > current link, is not finite
+  double qpoison;  // sum of 0 * q_k over the links beyond the current one: NaN iff one is not finite
 };
 
 __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
@@ -81,7 +81,7 @@ __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
   st.a0 = svzero();
   st.code = PD_SLOT_OK;
   st.eidx = 0;
-  st.nan_tip = false;
+  st.qpoison = 0.0;
 }
 
 // The reference's degeneracy verdict for link i (forward_dynamics.cpp:140-144),
@@ -135,8 +135,9 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   // tr_base: the exact trace is only needed when lambda fails that cheap bound
   // (never, for sane chains).
   const double pn2 = dot(st.X.p, st.X.p);
-  if (st.nan_tip || !(lambda > 2e-14 * (1.0 + pn2) * sym6_trace(Ia))) {
-    if (abia_degenerate(st.nan_tip, lambda, 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
+  const bool nan_tip = st.qpoison != st.qpoison;
+  if (nan_tip || !(lambda > 2e-14 * (1.0 + pn2) * sym6_trace(Ia))) {
+    if (abia_degenerate(nan_tip, lambda, 1e-14 * link_frame_trace(Ia, st.X)) && st.code == PD_SLOT_OK) {
       st.code = PD_SLOT_DEGENERATE_ARTICULATION;
       st.eidx = i;
     }
@@ -179,7 +180,7 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
     st.V0 = svfma(-qd, S0, st.V0);
     st.X = step_back(rel, st.X);
   }
-  st.nan_tip = st.nan_tip || !isfinite(q);
+  st.qpoison = fma(q, 0.0, st.qpoison);  // NaN / inf angle poisons the links below it
 }
 
 // pass C, link i (base -> tip): qdd_i = u_i - g0_i . a0_{i-1}; a0_i = a0_{i-1} + S0_i qdd_i

@@ -264,3 +264,29 @@ def test_nan_inputs_follow_the_reference(oracle, gpu_ctx, n, B):
             assert got == msg, (algo, b, got, msg)
             if b == 0:
                 assert rel_gap(qdd[b], ref) <= TOL
+
+
+@pytest.mark.parametrize("n", [6, 70])
+def test_degenerate_articulation(oracle, gpu_ctx, n):
+    """A valid model whose tip link has (almost) no inertia about its joint
+    axis: the reference's ABIA throws 'degenerate articulation at joint n-1'
+    (forward_dynamics.cpp:140-144); the GPU reports the same slot error and
+    message, per problem, leaving the batch's other problems solved."""
+    B = 3
+    cell = oracle.workload_seed(7, n, B)
+    links = oracle.workload_chains(cell, n, B).copy()
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    tip = links[1, n - 1]
+    tip[0] = 1e-30                                   # mass
+    tip[1:4] = 0.0                                   # com on the axis
+    tip[4:13] = [1.0, 0, 0, 0, 1.0, 0, 0, 0, 1e-30]  # Izz ~ 0
+    tip[13:19] = [0, 0, 1.0, 0, 0, 0]                # revolute about z through the origin
+    gpu_ctx.set_models(links, None)
+    qdd, st, rd, ix = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.forward_dynamics("abia", links[1], [0, 0, -9.81], q[1], qd[1], tau[1])
+    assert pd.api._capi.slot_message(st[1], rd[1], ix[1], n) == str(e.value)
+    assert ix[1] == n - 1
+    for b in (0, 2):
+        assert st[b] == 0
+        assert rel_gap(qdd[b], oracle.forward_dynamics("abia", links[b], [0, 0, -9.81], q[b], qd[b], tau[b])) <= TOL
