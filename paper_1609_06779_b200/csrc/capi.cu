@@ -212,53 +212,6 @@ void launch_transpose(pd_ctx* ctx, const double* in, double* out, int64_t rows, 
   ctx->launches++;
 }
 
-// Smallest eigenvalue of a symmetric 3x3 (cyclic Jacobi) for the
-// positive-definiteness rule of spatial_inertia_from (spatial.cpp:83-87).
-double sym3_min_eig(double m[3][3]) {
-  for (int sweep = 0; sweep < 64; ++sweep) {
-    const double off = m[0][1] * m[0][1] + m[0][2] * m[0][2] + m[1][2] * m[1][2];
-    if (off < 1e-300) break;
-    for (int p = 0; p < 2; ++p)
-      for (int q = p + 1; q < 3; ++q) {
-        if (m[p][q] == 0.0) continue;
-        const double th = (m[q][q] - m[p][p]) / (2.0 * m[p][q]);
-        const double tt = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
-        const double c = 1.0 / std::sqrt(tt * tt + 1.0), s = tt * c;
-        for (int k = 0; k < 3; ++k) {
-          const double a = m[k][p], b = m[k][q];
-          m[k][p] = c * a - s * b;
-          m[k][q] = s * a + c * b;
-        }
-        for (int k = 0; k < 3; ++k) {
-          const double a = m[p][k], b = m[q][k];
-          m[p][k] = c * a - s * b;
-          m[q][k] = s * a + c * b;
-        }
-      }
-  }
-  return std::min(m[0][0], std::min(m[1][1], m[2][2]));
-}
-
-// spatial_inertia_from's rules (spatial.cpp:72-87), first failing rule or 0.
-int link_rule(const double* r) {
-  const double mass = r[0];
-  if (!(mass > 0.0) || !std::isfinite(mass)) return PD_RULE_MASS;
-  for (int k = 1; k < 13; ++k)
-    if (!std::isfinite(r[k])) return PD_RULE_FINITE;
-  double scale = 0.0, asym = 0.0;
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) {
-      scale = std::max(scale, std::fabs(r[4 + 3 * a + b]));
-      asym = std::max(asym, std::fabs(r[4 + 3 * a + b] - r[4 + 3 * b + a]));
-    }
-  if (asym > 1e-9 * std::max(scale, 1.0)) return PD_RULE_SYMMETRIC;
-  double m[3][3];
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) m[a][b] = r[4 + 3 * a + b];
-  if (!(sym3_min_eig(m) > 0.0)) return PD_RULE_PD;
-  return 0;
-}
-
 // View of models [m0, m0 + count) (count = batch of a sub-range; a shared
 // model is never offset).
 ModelView model_view(const pd_ctx* c, int64_t m0 = 0, int64_t count = -1) {
@@ -584,20 +537,6 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
     return PD_INVALID_ARGUMENT;
   }
   PD_CUDA(cudaSetDevice(ctx->device));
-  std::vector<int32_t> ms(n_models, PD_SLOT_OK), mr(n_models, 0);
-  for (int64_t m = 0; m < n_models; ++m)
-    for (int i = 0; i < n_links; ++i) {
-      const int rule = link_rule(links + ((size_t)m * n_links + i) * PD_LINK_FIELDS);
-      if (rule) {
-        ms[m] = PD_SLOT_BAD_MODEL;
-        mr[m] = rule;
-        break;
-      }
-    }
-  ctx->h_mstatus = ms;
-  ctx->h_mrule = mr;
-  if (model_status) std::memcpy(model_status, ms.data(), sizeof(int32_t) * n_models);
-  if (model_rule) std::memcpy(model_rule, mr.data(), sizeof(int32_t) * n_models);
   std::vector<double> g(3 * n_models);
   for (int64_t m = 0; m < n_models; ++m)
     for (int k = 0; k < 3; ++k) g[3 * m + k] = gravity ? gravity[3 * m + k] : (k == 2 ? -9.81 : 0.0);
@@ -612,14 +551,24 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   double* graw = raw + PD_LINK_FIELDS * n_links * (size_t)n_models;
   PD_CUDA(cudaMemcpyAsync(raw, links, raw_bytes, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(graw, g.data(), sizeof(double) * 3 * n_models, cudaMemcpyHostToDevice, ctx->stream));
-  PD_CUDA(cudaMemcpyAsync(ctx->mstatus.p, ms.data(), sizeof(int32_t) * n_models, cudaMemcpyHostToDevice, ctx->stream));
-  PD_CUDA(cudaMemcpyAsync(ctx->mrule.p, mr.data(), sizeof(int32_t) * n_models, cudaMemcpyHostToDevice, ctx->stream));
+  // spatial_inertia_from's rules for every link, on the device (one thread per
+  // model, the same arithmetic as the host link_rule; 67M links of a c5 model
+  // set would take seconds on one host thread)
+  launch_validate_models(raw, n_links, n_models, ctx->mstatus.as<int32_t>(), ctx->mrule.as<int32_t>(), ctx->stream);
+  ctx->h_mstatus.assign(n_models, 0);
+  ctx->h_mrule.assign(n_models, 0);
+  PD_CUDA(cudaMemcpyAsync(ctx->h_mstatus.data(), ctx->mstatus.p, sizeof(int32_t) * n_models, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(ctx->h_mrule.data(), ctx->mrule.p, sizeof(int32_t) * n_models, cudaMemcpyDeviceToHost,
+                          ctx->stream));
   dim3 grid((unsigned)((n_models + 127) / 128), (unsigned)n_links);
   pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, model_ld,
                                                      ctx->model.as<double>(), ctx->gravity.as<double>());
-  ctx->launches++;
+  ctx->launches += 2;
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (model_status) std::memcpy(model_status, ctx->h_mstatus.data(), sizeof(int32_t) * n_models);
+  if (model_rule) std::memcpy(model_rule, ctx->h_mrule.data(), sizeof(int32_t) * n_models);
   ctx->n_links = n_links;
   ctx->n_models = n_models;
   ctx->model_ld = model_ld;
