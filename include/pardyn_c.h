@@ -32,6 +32,8 @@
  *                               src/inverse_dynamics.cpp:175-179)
  *   pd_link_states           <- link_states (inverse_dynamics.hpp:81-83,
  *                               src/inverse_dynamics.cpp:181-196)
+ *   pd_block_tridiag_solve5  <- oee_solve<5,1> / SymBlockTriDiagSystem
+ *                               (include/pardyn/oee.hpp:28-32,149-189)
  *   pd_workload_chains_device, pd_set_models_workload
  *                            <- workload_chains / random_chain on the device
  *                               (bench.cpp:357-366, model.cpp:157-185)
@@ -194,6 +196,18 @@ void pd_random_chain(int32_t n_links, uint64_t seed, double* links);
 void pd_workload_chains(uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count, double* links);
 void pd_workload_inputs(uint64_t cell_seed, int32_t n_links, int64_t n_groups, int64_t repeat, double* q,
                         double* qdot, double* drive);
+
+/* The paper's building block 2 on its own: `batch` symmetric block
+ * tri-diagonal systems of n <= 256 block rows with 5x5 blocks solved by
+ * odd-even elimination (oee_solve<5,1>, include/pardyn/oee.hpp:149-189):
+ * diag [batch][n][25] (row-major, symmetric), upper [batch][n-1][25] (block
+ * row k to k+1; the sub-diagonal blocks are their transposes), rhs
+ * [batch][n][5] -> x [batch][n][5], host buffers. Per system: PD_SLOT_OK,
+ * PD_SLOT_OEE_SINGULAR_PIVOT (round, block) or PD_SLOT_OEE_SINGULAR_FINAL
+ * (rounds, block), the reference's smallest-failing-row rule. */
+pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const double* diag, const double* upper,
+                                  const double* rhs, double* x, int32_t* slot_status, int32_t* slot_round,
+                                  int32_t* slot_index);
 
 /* The same chains generated on the device (§8f row 3), one thread per chain:
  *   pd_workload_chains_device  chains [g0, g0+count) into device memory,

@@ -311,6 +311,20 @@ class Context:
         self._check(self._L.pd_joint_space_inertia(self._h, B, _capi.dptr(q), _capi.dptr(M)))
         return M
 
+    def block_tridiag_solve5(self, diag, upper, rhs):
+        """Batched OEE (oee_solve<5,1>): diag (B, n, 5, 5), upper (B, n-1, 5, 5),
+        rhs (B, n, 5) -> (x (B, n, 5), status, round, index)."""
+        diag = np.ascontiguousarray(diag, dtype=np.float64)
+        B, n = diag.shape[0], diag.shape[1]
+        upper = np.ascontiguousarray(upper, dtype=np.float64) if n > 1 else np.zeros((B, 0, 5, 5))
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty((B, n, 5))
+        st, rd, ix = (np.zeros(B, np.int32) for _ in range(3))
+        self._check(self._L.pd_block_tridiag_solve5(self._h, B, n, _capi.dptr(diag), _capi.dptr(upper),
+                                                    _capi.dptr(rhs), _capi.dptr(x), _capi.iptr(st), _capi.iptr(rd),
+                                                    _capi.iptr(ix)))
+        return x, st, rd, ix
+
     def set_stream(self, stream_ptr):
         """Run on a CUDA stream (cudaStream_t as int). 0 = the legacy default
         stream (what torch.cuda.current_stream() is unless a stream is set);

@@ -91,9 +91,7 @@ __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
 // the reference's lambda_i is NaN iff one lies beyond i (nan_tip), and a NaN
 // reaching lambda only from the base side leaves the reference's test passing.
 __device__ __forceinline__ bool abia_degenerate(bool nan_tip, double lambda, double threshold) {
-  if (nan_tip) return true;
-  if (lambda != lambda) return false;
-  return !(lambda > threshold);
+  return nan_tip | ((lambda == lambda) & !(lambda > threshold));  // branch-free
 }
 
 // pass A, link i (base -> tip): X_i = rel_i X_{i-1}, V0 and A0 (qddot = 0)

@@ -34,7 +34,7 @@ size_t abia_cta_workspace_bytes(int n) { return (size_t)abc::FIELDS * n * sizeof
 // Thread 0 prefetches link i-1 into registers while it works on link i.
 constexpr int kCh = 64;  // links per staged chunk
 
-// staged per link (backward): S0 6 | J0 21 | td | JS = J0 S0 6 | lamJ | trJ | q 3 | joint angle finite
+// staged per link (backward): S0 6 | J0 21 | td | JS = J0 S0 6 | lamJ | trJ | q 3 | 0 * joint angle
 constexpr int kS0 = 0, kJ0 = 6, kTd = 27, kJS = 28, kLJ = 34, kTJ = 35, kQv = 36, kQf = 39, kStB = 40;
 constexpr int kStC = 13;  // forward: g0 6 | S0 6 | u
 // g0 / u of every link stay in shared memory when they fit, else in the
@@ -72,7 +72,7 @@ __device__ __forceinline__ void sequential_staged(const ModelView& mv, const Bat
                               ws[abc::TD * n + i],
                               JS.a.x, JS.a.y, JS.a.z, JS.l.x, JS.l.y, JS.l.z,
                               dot(S0, JS), link_frame_trace_q(J, qv), qv.x, qv.y, qv.z,
-                              isfinite(io.ld(io.q, i, p)) ? 1.0 : 0.0};
+                              io.ld(io.q, i, p) * 0.0};
 #pragma unroll
       for (int f = 0; f < kStB; ++f) b[f * kCh + j] = v[f];
     }
@@ -90,7 +90,7 @@ __device__ __forceinline__ void sequential_staged(const ModelView& mv, const Bat
   Sym6 P = {};
   Sv Z = svzero();
   int code = PD_SLOT_OK, eidx = 0;
-  bool nan_tip = false;
+  double qpoison = 0.0;  // NaN once a non-finite joint angle beyond the current link was seen
   for (int c = 0; c < nch; ++c) {
     if (t >= 32) {
       if (c + 1 < nch) stage_b(c + 1, t - 32, nt - 32);
@@ -109,8 +109,8 @@ __device__ __forceinline__ void sequential_staged(const ModelView& mv, const Bat
         const double lambda = cur[kLJ] + dot(S0, PS);
         // degeneracy test on the link-frame trace of I^A (forward_dynamics.cpp:140-144)
         const double tr = cur[kTJ] + link_frame_trace_q(P, mk(cur[kQv], cur[kQv + 1], cur[kQv + 2]));
-        const bool bad = abia_degenerate(nan_tip, lambda, 1e-14 * tr) && code == PD_SLOT_OK;
-        nan_tip = nan_tip || cur[kQf] == 0.0;
+        const bool bad = abia_degenerate(qpoison != qpoison, lambda, 1e-14 * tr) & (code == PD_SLOT_OK);
+        qpoison += cur[kQf];  // 0, or NaN for a non-finite joint angle
         code = bad ? PD_SLOT_DEGENERATE_ARTICULATION : code;
         eidx = bad ? i : eidx;
         const double inv_l = rcp_nr(lambda);

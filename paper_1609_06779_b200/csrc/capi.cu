@@ -23,6 +23,8 @@ void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
                 const double* td_pre);
 void launch_tau_surplus(const ModelView& mv, const BatchIO& io, double* td, cudaStream_t s);
+bool launch_oee5(const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
+                 int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s);
 bool cfa_coop_path(int n, int64_t batch);
 void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
@@ -919,6 +921,39 @@ void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links
 
 // ---------------------------------------------------------------- device workloads
 extern "C" {
+
+pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const double* diag, const double* upper,
+                                  const double* rhs, double* x, int32_t* slot_status, int32_t* slot_round,
+                                  int32_t* slot_index) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0 || n < 1 || n > 256 || (batch > 0 && (!diag || !rhs || !x || (n > 1 && !upper)))) {
+    ctx->last_error = "block tri-diagonal solve: need 1 <= n <= 256 rows and non-null buffers";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const size_t nd = (size_t)batch * n * 25, nu = (size_t)batch * (n - 1) * 25, nr = (size_t)batch * n * 5;
+  PD_CUDA(ctx->states.ensure(sizeof(double) * (nd + nu + 2 * nr) + sizeof(int32_t) * 3 * batch));
+  double* d = ctx->states.as<double>();
+  double* u = d + nd;
+  double* r = u + nu;
+  double* xo = r + nr;
+  int32_t* st = reinterpret_cast<int32_t*>(xo + nr);
+  PD_CUDA(cudaMemcpyAsync(d, diag, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+  if (nu) PD_CUDA(cudaMemcpyAsync(u, upper, sizeof(double) * nu, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * nr, cudaMemcpyHostToDevice, ctx->stream));
+  launch_oee5(d, u, r, xo, batch, n, st, st + batch, st + 2 * batch, ctx->stream);
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  PD_CUDA(cudaMemcpyAsync(x, xo, sizeof(double) * nr, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<int32_t> hs(3 * batch);
+  PD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (slot_status) std::memcpy(slot_status, hs.data(), sizeof(int32_t) * batch);
+  if (slot_round) std::memcpy(slot_round, hs.data() + batch, sizeof(int32_t) * batch);
+  if (slot_index) std::memcpy(slot_index, hs.data() + 2 * batch, sizeof(int32_t) * batch);
+  return PD_OK;
+}
 
 pd_status pd_workload_chains_device(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,
                                     double* d_links) {

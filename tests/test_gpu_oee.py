@@ -1,0 +1,65 @@
+"""GPU parity of the paper's building block 2 on its own: batched symmetric
+block tri-diagonal solves by odd-even elimination with 5x5 blocks
+(pd_block_tridiag_solve5 <- oee_solve<5,1>, include/pardyn/oee.hpp:149-189)
+against the oracle's restatement, including the reference's singular-pivot
+report (tests/test_oee.cpp:106-126: round, block)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def random_system(rng, n):
+    diag = np.empty((n, 5, 5))
+    for k in range(n):
+        a = rng.uniform(-1, 1, (5, 5))
+        diag[k] = a @ a.T + 6.0 * np.eye(5)
+    upper = rng.uniform(-1, 1, (max(n - 1, 0), 5, 5))
+    rhs = rng.uniform(-5, 5, (n, 5))
+    return diag, upper, rhs
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 33, 64, 200, 256])
+def test_oee5_matches_oracle(oracle, gpu_ctx, n):
+    rng = np.random.default_rng(n)
+    B = 4
+    systems = [random_system(rng, n) for _ in range(B)]
+    diag = np.stack([s[0] for s in systems])
+    upper = np.stack([s[1] for s in systems]) if n > 1 else np.zeros((B, 0, 5, 5))
+    rhs = np.stack([s[2] for s in systems])
+    x, st, rd, ix = gpu_ctx.block_tridiag_solve5(diag, upper, rhs)
+    assert (st == 0).all()
+    for b in range(B):
+        want, rounds = oracle.tridiag_solve(diag[b], upper[b] if n > 1 else np.zeros((1, 5, 5)), rhs[b])
+        want = want.reshape(n, 5)
+        assert np.linalg.norm(x[b] - want) / max(1.0, np.linalg.norm(want)) <= 1e-12
+        # and it solves the system
+        full = np.zeros((5 * n, 5 * n))
+        for k in range(n):
+            full[5 * k:5 * k + 5, 5 * k:5 * k + 5] = diag[b, k]
+            if k + 1 < n:
+                full[5 * k:5 * k + 5, 5 * k + 5:5 * k + 10] = upper[b, k]
+                full[5 * k + 5:5 * k + 10, 5 * k:5 * k + 5] = upper[b, k].T
+        assert np.linalg.norm(full @ x[b].ravel() - rhs[b].ravel()) <= 1e-10 * np.linalg.norm(rhs[b])
+
+
+@pytest.mark.parametrize("case", ["pivot_row1", "pivot_row0", "final"])
+def test_oee5_singular_reports_like_the_reference(oracle, gpu_ctx, case):
+    n = 3
+    eye = np.eye(5)
+    if case == "pivot_row1":     # test_oee.cpp:106-126 with 5x5 blocks
+        diag = np.stack([eye, np.zeros((5, 5)), eye])
+    elif case == "pivot_row0":
+        diag = np.stack([np.zeros((5, 5)), eye, eye])
+    else:                        # n = 1: no rounds, the final solve is singular
+        n = 1
+        diag = np.zeros((1, 5, 5))
+    upper = np.stack([0.1 * eye] * (n - 1)) if n > 1 else np.zeros((0, 5, 5))
+    rhs = np.ones((n, 5))
+    x, st, rd, ix = gpu_ctx.block_tridiag_solve5(diag[None], upper[None], rhs[None])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.tridiag_solve(diag, upper if n > 1 else np.zeros((1, 5, 5)), rhs)
+    assert st[0] != 0
+    assert (rd[0], ix[0]) == (e.value.round, e.value.index)
+    import paper_1609_06779_b200 as pd
+    assert pd.api._capi.slot_message(st[0], rd[0], ix[0], n) == str(e.value)
