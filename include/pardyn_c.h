@@ -32,6 +32,8 @@
  *                               src/inverse_dynamics.cpp:175-179)
  *   pd_link_states           <- link_states (inverse_dynamics.hpp:81-83,
  *                               src/inverse_dynamics.cpp:181-196)
+ *   pd_block_bidiag_solve6   <- solve_lower_bidiag / solve_upper_bidiag
+ *                               (include/pardyn/scan.hpp:100-168)
  *   pd_block_tridiag_solve5  <- oee_solve<5,1> / SymBlockTriDiagSystem
  *                               (include/pardyn/oee.hpp:28-32,149-189)
  *   pd_workload_chains_device, pd_set_models_workload
@@ -196,6 +198,15 @@ void pd_random_chain(int32_t n_links, uint64_t seed, double* links);
 void pd_workload_chains(uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count, double* links);
 void pd_workload_inputs(uint64_t cell_seed, int32_t n_links, int64_t n_groups, int64_t repeat, double* q,
                         double* qdot, double* drive);
+
+/* The paper's building block 1 on its own: `batch` block bi-diagonal
+ * systems with 6x6 blocks and implicit identity diagonal (BlockBiDiagSystem<6>,
+ * include/pardyn/scan.hpp:100-168), solved by an all-prefix scan of affine
+ * elements: lower (upper = 0): x[0] = rhs[0], x[k] = coupling[k-1] x[k-1] +
+ * rhs[k]; upper: x[n-1] = rhs[n-1], x[k] = coupling[k] x[k+1] + rhs[k].
+ * coupling [batch][n-1][36] row-major, rhs / x [batch][n][6], host buffers. */
+pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t upper, const double* coupling,
+                                 const double* rhs, double* x);
 
 /* The paper's building block 2 on its own: `batch` symmetric block
  * tri-diagonal systems of n <= 256 block rows with 5x5 blocks solved by

@@ -27,7 +27,7 @@ EXPORTS = (
     "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant", "pd_mix", "pd_workload_seed", "pd_random_chain",
     "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak", "pd_inverse_dynamics_opts",
     "pd_inverse_dynamics_device", "pd_bias_torque", "pd_link_states", "pd_joint_space_inertia",
-    "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5",
+    "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5", "pd_block_bidiag_solve6",
 )
 
 
@@ -92,6 +92,8 @@ def load():
     L.pd_workload_chains_device.restype = C.c_int
     L.pd_set_models_workload.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_int64, _D, _I32, _I32]
     L.pd_set_models_workload.restype = C.c_int
+    L.pd_block_bidiag_solve6.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, _D, _D, _D]
+    L.pd_block_bidiag_solve6.restype = C.c_int
     L.pd_block_tridiag_solve5.argtypes = [C.c_void_p, C.c_int64, C.c_int32, _D, _D, _D, _D, _I32, _I32, _I32]
     L.pd_block_tridiag_solve5.restype = C.c_int
     L.pd_slot_message.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int32]

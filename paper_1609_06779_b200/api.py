@@ -311,6 +311,17 @@ class Context:
         self._check(self._L.pd_joint_space_inertia(self._h, B, _capi.dptr(q), _capi.dptr(M)))
         return M
 
+    def block_bidiag_solve6(self, coupling, rhs, upper=False):
+        """Batched scan solve of BlockBiDiagSystem<6>: coupling (B, n-1, 6, 6),
+        rhs (B, n, 6) -> x (B, n, 6) (scan.hpp:100-168)."""
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        B, n = rhs.shape[0], rhs.shape[1]
+        coupling = np.ascontiguousarray(coupling, dtype=np.float64) if n > 1 else np.zeros((B, 0, 6, 6))
+        x = np.empty_like(rhs)
+        self._check(self._L.pd_block_bidiag_solve6(self._h, B, n, 1 if upper else 0, _capi.dptr(coupling),
+                                                   _capi.dptr(rhs), _capi.dptr(x)))
+        return x
+
     def block_tridiag_solve5(self, diag, upper, rhs):
         """Batched OEE (oee_solve<5,1>): diag (B, n, 5, 5), upper (B, n-1, 5, 5),
         rhs (B, n, 5) -> (x (B, n, 5), status, round, index)."""

@@ -23,6 +23,8 @@ void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
                 const double* td_pre);
 void launch_tau_surplus(const ModelView& mv, const BatchIO& io, double* td, cudaStream_t s);
+void launch_bidiag6(const double* coupling, const double* rhs, double* x, int64_t batch, int n, int upper,
+                    cudaStream_t s);
 bool launch_oee5(const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
                  int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s);
 bool cfa_coop_path(int n, int64_t batch);
@@ -921,6 +923,30 @@ void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links
 
 // ---------------------------------------------------------------- device workloads
 extern "C" {
+
+pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t upper, const double* coupling,
+                                 const double* rhs, double* x) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (batch < 0 || n < 0 || (batch > 0 && n > 0 && (!rhs || !x || (n > 1 && !coupling)))) {
+    ctx->last_error = "block bi-diagonal solve: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0 || n == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const size_t nc = (size_t)batch * (n - 1) * 36, nr = (size_t)batch * n * 6;
+  PD_CUDA(ctx->states.ensure(sizeof(double) * (nc + 2 * nr)));
+  double* c = ctx->states.as<double>();
+  double* r = c + nc;
+  double* xo = r + nr;
+  if (nc) PD_CUDA(cudaMemcpyAsync(c, coupling, sizeof(double) * nc, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * nr, cudaMemcpyHostToDevice, ctx->stream));
+  launch_bidiag6(c, r, xo, batch, n, upper ? 1 : 0, ctx->stream);
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  PD_CUDA(cudaMemcpyAsync(x, xo, sizeof(double) * nr, cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PD_OK;
+}
 
 pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const double* diag, const double* upper,
                                   const double* rhs, double* x, int32_t* slot_status, int32_t* slot_round,

@@ -63,3 +63,31 @@ def test_oee5_singular_reports_like_the_reference(oracle, gpu_ctx, case):
     assert (rd[0], ix[0]) == (e.value.round, e.value.index)
     import paper_1609_06779_b200 as pd
     assert pd.api._capi.slot_message(st[0], rd[0], ix[0], n) == str(e.value)
+
+
+# ---- building block 1: the block bi-diagonal scan (scan.hpp:100-168)
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 100, 1024, 1500])
+@pytest.mark.parametrize("upper", [False, True])
+def test_bidiag6_matches_oracle(oracle, gpu_ctx, n, upper):
+    rng = np.random.default_rng(n + 7 * upper)
+    B = 3
+    coupling = rng.uniform(-0.25, 0.25, (B, max(n - 1, 0), 6, 6))  # contractive: well-conditioned recursion
+    rhs = rng.uniform(-1, 1, (B, n, 6))
+    x = gpu_ctx.block_bidiag_solve6(coupling, rhs, upper)
+    for b in range(B):
+        want, _ = oracle.bidiag_solve(coupling[b] if n > 1 else np.zeros((1, 6, 6)), rhs[b], upper)
+        assert np.linalg.norm(x[b] - want) / max(1.0, np.linalg.norm(want)) <= 1e-13
+
+
+def test_bidiag6_spec_known_answer(gpu_ctx):
+    """b = [2, 2], c = [1, 0, 0] -> [1, 2, 4] (scalar blocks
+    embedded as 2 I and e), and the upper orientation -> [4, 2, 1]."""
+    coupling = np.stack([2.0 * np.eye(6)] * 2)[None]
+    rhs = np.zeros((1, 3, 6))
+    rhs[0, 0] = 1.0
+    x = gpu_ctx.block_bidiag_solve6(coupling, rhs, False)
+    assert np.array_equal(x[0, :, 0], [1.0, 2.0, 4.0]) and np.array_equal(x[0, :, 5], [1.0, 2.0, 4.0])
+    rhs_u = np.zeros((1, 3, 6))
+    rhs_u[0, 2] = 1.0
+    xu = gpu_ctx.block_bidiag_solve6(coupling, rhs_u, True)
+    assert np.array_equal(xu[0, :, 0], [4.0, 2.0, 1.0])
