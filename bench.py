@@ -324,6 +324,28 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
     return res
 
 
+# ncu --set full captures of the dominant kernel per workload (profiles/, same
+# kernel and config as the bench command): DRAM bytes per launch
+NCU_TRAFFIC = {"c2": "profiles/ncu_c2_r1_s3d.txt", "c3": "profiles/ncu_c3_r1_s3c.txt",
+               "c2j": "profiles/ncu_c2j_r1_s3c.txt", "c5j": "profiles/ncu_c5j_r1_s3c.txt"}
+
+
+def ncu_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the committed capture, or None."""
+    path = os.path.join(ROOT, NCU_TRAFFIC.get(workload, ""))
+    if workload not in NCU_TRAFFIC or not os.path.exists(path):
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    found = 0
+    for line in open(path):
+        parts = line.split()
+        if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += float(parts[1]) * scale.get(parts[2], 1.0)
+            found += 1
+    return {"bytes_per_launch": total, "source": NCU_TRAFFIC[workload]} if found == 2 else None
+
+
 def roofline_entry(wl, ms_per_step, bw_gbs, fp64_tflops, traffic=None):
     """Algorithmic work of one step (the whole batch) over the step's device
     time. A step is one launch for the batched kernels; multi-kernel paths
@@ -337,7 +359,8 @@ def roofline_entry(wl, ms_per_step, bw_gbs, fp64_tflops, traffic=None):
     tfl = flops / t / 1e12
     t_hbm = bytes_ / (bw_gbs * 1e9)
     t_fp = flops / (fp64_tflops * 1e12)
-    hbm = {"bound": "hbm", "achieved": gbs, "peak": bw_gbs, "unit": "GB/s", "frac": gbs / bw_gbs, "traffic": traffic}
+    hbm = {"bound": "hbm", "achieved": gbs, "peak": bw_gbs, "unit": "GB/s", "frac": gbs / bw_gbs, "traffic": traffic,
+           "algorithmic_bytes": bytes_}
     fp = {"achieved": tfl, "peak": fp64_tflops, "unit": "TFLOP/s (FP64)", "frac": tfl / fp64_tflops}
     binding = "hbm" if t_hbm >= t_fp else "fp64"
     return hbm, fp, binding, {"bytes_per_launch": bytes_, "flops_per_launch": flops,
@@ -397,7 +420,9 @@ def main():
     value = total / (ms_max * 1e-3)
     ms_per_step = ms_max / args.steps
     # roofline of this rank's step on its own (local) batch
-    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B), res["ms_total"] / args.steps, bw, fp64_peak)
+    tr = ncu_traffic(args.workload) if world == 1 else None
+    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B), res["ms_total"] / args.steps, bw, fp64_peak,
+                                            traffic=tr["bytes_per_launch"] if tr else None)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -409,6 +434,8 @@ def main():
                    "l2": "inputs larger than L2 (%.0f MB streamed per step)" % (work["bytes_per_launch"] / 1e6)
                    if work["bytes_per_launch"] > 126e6 else "L2 not flushed (small workload)"},
         "roofline": hbm,
+        "roofline_traffic_source": (tr["source"] + " (ncu --set full, DRAM read + write bytes per launch)") if tr
+        else None,
         "roofline_fp64": fp,
         "roofline_binding": binding,
         "roofline_frac_of_binding": work["roofline_frac"],
