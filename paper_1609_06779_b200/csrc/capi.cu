@@ -95,6 +95,8 @@ struct pd_ctx {
   // host-buffer path: copy-in / copy-out streams and per-chunk events
   static constexpr int kMaxChunks = 16;
   int32_t* host_status = nullptr;  // pinned staging for slot status
+  int32_t* h_flag = nullptr;       // pinned: OR of the slot codes of the last host-buffer call
+  DevBuf d_flag;
   size_t host_status_n = 0;
   cudaStream_t cp_in = nullptr, cp_out = nullptr;
   cudaEvent_t ev_entry = nullptr, ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
@@ -179,6 +181,15 @@ __global__ void pack_models_kernel(const double* __restrict__ raw, const double*
   for (int k = 0; k < 3; ++k) put(F_HP + k, Q[3 * k] * r[28] + Q[3 * k + 1] * r[29] + Q[3 * k + 2] * r[30]);
   if (i == 0)
     for (int k = 0; k < 3; ++k) gout[(int64_t)k * M + m] = graw[m * 3 + k];
+}
+
+// OR of the slot codes into *flag (non-zero iff some slot failed).
+__global__ void any_status_kernel(const int32_t* __restrict__ st, int64_t n, int32_t* __restrict__ flag) {
+  int32_t acc = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    acc |= st[k];
+  acc = __reduce_or_sync(0xffffffffu, acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicOr(flag, acc);
 }
 
 // [field][link][chain] (stride ld) -> [chain][field][link]
@@ -493,6 +504,8 @@ void pd_destroy(pd_ctx* ctx) {
     }
   }
   if (ctx->host_status) cudaFreeHost(ctx->host_status);
+  if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  ctx->d_flag.release();
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -642,8 +655,11 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   // compute stream transposes and solves chunk c and the copy-out stream
   // returns chunk c-1. Chunks are 32-aligned (TMA bases stay 16-byte aligned).
   static const int chunk_env = std::getenv("PD_E2E_CHUNKS") ? std::atoi(std::getenv("PD_E2E_CHUNKS")) : 0;
-  const int nch = (int)std::min<int64_t>(pd_ctx::kMaxChunks,
-                                         chunk_env > 0 ? chunk_env : std::max<int64_t>(1, batch / 4096));
+  // ~8K problems per chunk, at most 8 chunks: smaller chunks add per-chunk
+  // launch / event overhead faster than they shorten the pipeline's tail
+  // (tools/e2e_probe.py: c2 1.50 ms at 16 chunks, 1.35 ms at 8)
+  const int nch = (int)std::min<int64_t>(chunk_env > 0 ? pd_ctx::kMaxChunks : 8,
+                                         chunk_env > 0 ? chunk_env : std::max<int64_t>(1, batch / 8192));
   const int64_t csz = ((batch + nch - 1) / nch + 31) / 32 * 32;
   PD_CUDA(cudaEventRecord(ctx->ev_entry, ctx->stream));  // earlier work on the staging buffers
   PD_CUDA(cudaStreamWaitEvent(ctx->cp_in, ctx->ev_entry, 0));
@@ -669,16 +685,37 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
     PD_CUDA(cudaMemcpyAsync(qddot + off, sqdd + half + off, bytes, cudaMemcpyDeviceToHost, ctx->cp_out));
   }
   const bool want_status = slot_status || slot_round || slot_index;
-  if (want_status) {
-    if (ctx->host_status_n < (size_t)(3 * batch)) {
-      if (ctx->host_status) cudaFreeHost(ctx->host_status);
-      ctx->host_status = nullptr;
-      ctx->host_status_n = 0;
-      PD_CUDA(cudaMallocHost(&ctx->host_status, sizeof(int32_t) * 3 * batch));
-      ctx->host_status_n = (size_t)(3 * batch);
-    }
-    PD_CUDA(cudaMemcpyAsync(ctx->host_status, st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->cp_out));
+  if (!want_status) {
+    PD_CUDA(cudaStreamSynchronize(ctx->cp_out));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
   }
+  // Slot outcomes: one device-side OR over the statuses; when every slot
+  // succeeded (round and index are then 0 too) the host arrays are zero-
+  // filled instead of copying 12 bytes per problem back over PCIe.
+  if (!ctx->h_flag) PD_CUDA(cudaMallocHost(&ctx->h_flag, sizeof(int32_t)));
+  PD_CUDA(ctx->d_flag.ensure(sizeof(int32_t)));
+  PD_CUDA(cudaMemsetAsync(ctx->d_flag.p, 0, sizeof(int32_t), ctx->stream));
+  any_status_kernel<<<(unsigned)std::min<int64_t>((batch + 255) / 256, 1024), 256, 0, ctx->stream>>>(
+      st, batch, ctx->d_flag.as<int32_t>());
+  ctx->launches++;
+  PD_CUDA(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (*ctx->h_flag == 0) {
+    PD_CUDA(cudaStreamSynchronize(ctx->cp_out));
+    if (slot_status) std::memset(slot_status, 0, sizeof(int32_t) * batch);
+    if (slot_round) std::memset(slot_round, 0, sizeof(int32_t) * batch);
+    if (slot_index) std::memset(slot_index, 0, sizeof(int32_t) * batch);
+    return PD_OK;
+  }
+  if (ctx->host_status_n < (size_t)(3 * batch)) {
+    if (ctx->host_status) cudaFreeHost(ctx->host_status);
+    ctx->host_status = nullptr;
+    ctx->host_status_n = 0;
+    PD_CUDA(cudaMallocHost(&ctx->host_status, sizeof(int32_t) * 3 * batch));
+    ctx->host_status_n = (size_t)(3 * batch);
+  }
+  PD_CUDA(cudaMemcpyAsync(ctx->host_status, st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->cp_out));
   PD_CUDA(cudaStreamSynchronize(ctx->cp_out));
   const int32_t* hs = ctx->host_status;
   if (slot_status) std::memcpy(slot_status, hs, sizeof(int32_t) * batch);
