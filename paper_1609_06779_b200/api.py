@@ -239,17 +239,20 @@ class Context:
         self._check(self._L.pd_workload_chains_device(self._h, int(cell_seed), int(n_links), int(g0), int(count),
                                                       d_links))
 
-    def solve(self, algo, q, qdot, tau, out=None):
+    def solve(self, algo, q, qdot, tau, out=None, status_out=None):
         """Host-buffer solve: q/qdot/tau (B, n) -> (qddot, status, round, index).
-        `out` may be a preallocated (pinned) (B, n) float64 array."""
+        `out` may be a preallocated (pinned) (B, n) float64 array and
+        `status_out` a preallocated triple of (B,) int32 arrays (reused across
+        calls, like C callers reuse their slot arrays)."""
         q = np.ascontiguousarray(q, dtype=np.float64)
         qd = np.ascontiguousarray(qdot, dtype=np.float64)
         tau = np.ascontiguousarray(tau, dtype=np.float64)
         B = q.shape[0]
         qdd = np.empty_like(q) if out is None else out
-        st = np.zeros(B, np.int32)
-        rd = np.zeros(B, np.int32)
-        ix = np.zeros(B, np.int32)
+        if status_out is None:
+            st, rd, ix = np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32)
+        else:
+            st, rd, ix = status_out
         self._check(self._L.pd_forward_dynamics(self._h, int(algo), B, _capi.dptr(q), _capi.dptr(qd), _capi.dptr(tau),
                                                 _capi.dptr(qdd), _capi.iptr(st), _capi.iptr(rd), _capi.iptr(ix)))
         return qdd, st, rd, ix
