@@ -220,6 +220,32 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
   }
 }
 
+// Three same-shaped transposes (q, qdot, tau of a chunk) in one launch.
+__global__ void transpose3_kernel(const double* __restrict__ a0, const double* __restrict__ a1,
+                                  const double* __restrict__ a2, double* __restrict__ b0, double* __restrict__ b1,
+                                  double* __restrict__ b2, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out) {
+  __shared__ double tile[32][33];
+  const double* in = blockIdx.z == 0 ? a0 : (blockIdx.z == 1 ? a1 : a2);
+  double* out = blockIdx.z == 0 ? b0 : (blockIdx.z == 1 ? b1 : b2);
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * ld_in + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * ld_out + r] = tile[threadIdx.x][k];
+  }
+}
+
+void launch_transpose3(pd_ctx* ctx, const double* a0, const double* a1, const double* a2, double* b0, double* b1,
+                       double* b2, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), 3);
+  transpose3_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(a0, a1, a2, b0, b1, b2, rows, cols, ld_in, ld_out);
+  ctx->launches++;
+}
+
 void launch_transpose(pd_ctx* ctx, const double* in, double* out, int64_t rows, int64_t cols, int64_t ld_in,
                       int64_t ld_out) {
   dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
@@ -673,9 +699,8 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
     PD_CUDA(cudaMemcpyAsync(stau + half + off, tau + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
     PD_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->cp_in));
     PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[c], 0));
-    launch_transpose(ctx, sq + half + off, sq + b0, nb, n, n, lds);
-    launch_transpose(ctx, sqd + half + off, sqd + b0, nb, n, n, lds);
-    launch_transpose(ctx, stau + half + off, stau + b0, nb, n, n, lds);
+    launch_transpose3(ctx, sq + half + off, sqd + half + off, stau + half + off, sq + b0, sqd + b0, stau + b0, nb, n,
+                      n, lds);
     pd_status s = run_device(ctx, algo, nb, lds, sq + b0, sqd + b0, stau + b0, sqdd + b0, st + b0, st + batch + b0,
                              st + 2 * batch + b0, b0);
     if (s != PD_OK) return s;
