@@ -17,6 +17,7 @@
 //   IdOptions / LinkStates         inverse_dynamics.hpp:23-34
 //   inverse_dynamics / bias_torque / link_states   inverse_dynamics.hpp:71-83
 //   joint_space_inertia            forward_dynamics.hpp:34-35 (MatrixXd stand-in)
+//   solve_lower_bidiag / solve_upper_bidiag / oee_solve   scan.hpp:100-168, oee.hpp:149-189
 //   LinkSpec / RobotChain          model.hpp:17-30
 //   random_chain                   model.hpp:66-70
 //   validate_chain / load_chain / save_chain   model.hpp:56-82 (JSON model files)
@@ -220,6 +221,40 @@ JointVector bias_torque(const RobotChain& chain, const JointVector& q, const Joi
 LinkStates link_states(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
                        const JointVector& qddot, const IdOptions& opts = {});
 MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q);
+
+// ----------------------------------------------------------------- building blocks
+// The paper's two solvers on their own (scan.hpp:100-168, oee.hpp:28-32,
+// 149-189), on the GPU: 6x6 block bi-diagonal systems by the affine scan,
+// symmetric 5x5 block tri-diagonal systems by odd-even elimination (the
+// block sizes the dynamics use). Blocks are row-major.
+enum class BiDiagOrientation { lower, upper };
+
+template <int D>
+struct BlockBiDiagSystem {
+  BiDiagOrientation orientation = BiDiagOrientation::lower;
+  std::vector<std::array<double, D * D>> coupling;  // n - 1 blocks
+  std::vector<std::array<double, D>> rhs;           // n blocks
+};
+
+template <int B>
+struct SymBlockTriDiagSystem {
+  std::vector<std::array<double, B * B>> diag;   // n blocks
+  std::vector<std::array<double, B * B>> upper;  // n - 1 blocks
+};
+
+struct ScanTrace {
+  int rounds = 0;
+};
+struct OeeTrace {
+  int rounds = 0;
+};
+
+std::vector<std::array<double, 6>> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
+std::vector<std::array<double, 6>> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
+// Throws SingularBlockError(round, index) like the reference.
+std::vector<std::array<double, 5>> oee_solve(const SymBlockTriDiagSystem<5>& sys,
+                                             const std::vector<std::array<double, 5>>& rhs,
+                                             OeeTrace* trace = nullptr);
 
 // ----------------------------------------------------------------- device
 namespace gpu {

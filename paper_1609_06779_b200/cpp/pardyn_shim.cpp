@@ -303,4 +303,56 @@ MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q) {
   return M;
 }
 
+namespace {
+
+std::vector<std::array<double, 6>> bidiag(const BlockBiDiagSystem<6>& sys, bool upper, ScanTrace* trace) {
+  const std::size_t n = sys.rhs.size();
+  if (sys.coupling.size() + 1 != n && !(n == 0 && sys.coupling.empty()))
+    throw std::invalid_argument("block bi-diagonal solve: need n - 1 coupling blocks for n right-hand sides");
+  if (trace) trace->rounds = ceil_log2(n);  // the scan's designed depth (scan.hpp:32-65)
+  std::vector<std::array<double, 6>> x(n);
+  if (n == 0) return x;
+  std::vector<double> c, r, xo(6 * n);
+  for (const auto& b : sys.coupling) c.insert(c.end(), b.begin(), b.end());
+  for (const auto& b : sys.rhs) r.insert(r.end(), b.begin(), b.end());
+  pd_ctx* cx = ctx();
+  check_call(cx, pd_block_bidiag_solve6(cx, 1, static_cast<int32_t>(n), upper ? 1 : 0, c.empty() ? nullptr : c.data(),
+                                       r.data(), xo.data()));
+  for (std::size_t k = 0; k < n; ++k)
+    for (int e = 0; e < 6; ++e) x[k][e] = xo[6 * k + e];
+  return x;
+}
+
+}  // namespace
+
+std::vector<std::array<double, 6>> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
+  return bidiag(sys, false, trace);
+}
+
+std::vector<std::array<double, 6>> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
+  return bidiag(sys, true, trace);
+}
+
+std::vector<std::array<double, 5>> oee_solve(const SymBlockTriDiagSystem<5>& sys,
+                                             const std::vector<std::array<double, 5>>& rhs, OeeTrace* trace) {
+  const std::size_t n = sys.diag.size();
+  if (rhs.size() != n || (n > 0 && sys.upper.size() + 1 != n))
+    throw std::invalid_argument("odd-even elimination: inconsistent block counts");
+  if (trace) trace->rounds = ceil_log2(n);
+  std::vector<std::array<double, 5>> x(n);
+  if (n == 0) return x;
+  std::vector<double> d, u, r, xo(5 * n);
+  for (const auto& b : sys.diag) d.insert(d.end(), b.begin(), b.end());
+  for (const auto& b : sys.upper) u.insert(u.end(), b.begin(), b.end());
+  for (const auto& b : rhs) r.insert(r.end(), b.begin(), b.end());
+  pd_ctx* cx = ctx();
+  int32_t st = 0, rd = 0, ix = 0;
+  check_call(cx, pd_block_tridiag_solve5(cx, 1, static_cast<int32_t>(n), d.data(), u.empty() ? nullptr : u.data(),
+                                         r.data(), xo.data(), &st, &rd, &ix));
+  if (st != PD_SLOT_OK) throw SingularBlockError(rd, ix, slot_message(st, rd, ix, static_cast<int>(n)));
+  for (std::size_t k = 0; k < n; ++k)
+    for (int e = 0; e < 5; ++e) x[k][e] = xo[5 * k + e];
+  return x;
+}
+
 }  // namespace pardyn

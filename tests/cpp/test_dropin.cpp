@@ -205,6 +205,50 @@ int main() {
       }
     check(mg < 1e-12 && sym == 0.0, "joint-space inertia vs oracle, exactly symmetric");
   }
+  // the building blocks: scan and OEE (test_oee.cpp:106-126)
+  {
+    pardyn::BlockBiDiagSystem<6> sys;
+    std::array<double, 36> two{};
+    for (int k = 0; k < 6; ++k) two[7 * k] = 2.0;
+    sys.coupling = {two, two};
+    sys.rhs = {std::array<double, 6>{1, 1, 1, 1, 1, 1}, {}, {}};
+    pardyn::ScanTrace tr;
+    const auto x = pardyn::solve_lower_bidiag(sys, &tr);
+    check(x[0][0] == 1.0 && x[1][0] == 2.0 && x[2][5] == 4.0 && tr.rounds == 2, "scan known answer [1, 2, 4]");
+    sys.orientation = pardyn::BiDiagOrientation::upper;
+    sys.rhs = {std::array<double, 6>{}, {}, std::array<double, 6>{1, 1, 1, 1, 1, 1}};
+    const auto xu = pardyn::solve_upper_bidiag(sys);
+    check(xu[0][0] == 4.0 && xu[2][0] == 1.0, "upper scan known answer [4, 2, 1]");
+    pardyn::SymBlockTriDiagSystem<5> t3;
+    std::array<double, 25> eye{}, tenth{};
+    for (int k = 0; k < 5; ++k) {
+      eye[6 * k] = 1.0;
+      tenth[6 * k] = 0.1;
+    }
+    t3.diag = {eye, std::array<double, 25>{}, eye};
+    t3.upper = {tenth, tenth};
+    const std::vector<std::array<double, 5>> ones(3, std::array<double, 5>{1, 1, 1, 1, 1});
+    int rd = -1, ix = -1;
+    try {
+      pardyn::oee_solve(t3, ones);
+    } catch (const pardyn::SingularBlockError& e) {
+      rd = e.round();
+      ix = e.index();
+    }
+    check(rd == 1 && ix == 1, "OEE singular pivot reports (round 1, block 1)");
+    t3.diag = {eye, eye, eye};
+    pardyn::OeeTrace ot;
+    const auto xs = pardyn::oee_solve(t3, ones, &ot);
+    double res = 0.0;  // (I + 0.1 (shift + shift^T)) x = 1
+    for (int k = 0; k < 3; ++k)
+      for (int e = 0; e < 5; ++e) {
+        double v = xs[k][e];
+        if (k > 0) v += 0.1 * xs[k - 1][e];
+        if (k < 2) v += 0.1 * xs[k + 1][e];
+        res = std::max(res, std::fabs(v - 1.0));
+      }
+    check(res < 1e-14 && ot.rounds == 2, "OEE solves a 3-block system");
+  }
   std::printf("%d failure(s)\n", failures);
   return failures;
 }
