@@ -687,6 +687,16 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   const int nch = (int)std::min<int64_t>(chunk_env > 0 ? pd_ctx::kMaxChunks : 8,
                                          chunk_env > 0 ? chunk_env : std::max<int64_t>(1, batch / 8192));
   const int64_t csz = ((batch + nch - 1) / nch + 31) / 32 * 32;
+  // PD_E2E_TRACE=1: timing events per stage, timeline printed to stderr
+  // (tools/e2e_trace.py; profiles/e2e_timeline_r1_s3.txt)
+  static const bool trace = std::getenv("PD_E2E_TRACE") != nullptr;
+  static cudaEvent_t tev[4 * pd_ctx::kMaxChunks + 2];
+  if (trace && !tev[0])
+    for (auto& e : tev) PD_CUDA(cudaEventCreate(&e));
+  auto mark = [&](int k, cudaStream_t s) {
+    if (trace) cudaEventRecord(tev[k], s);
+  };
+  mark(0, ctx->stream);
   PD_CUDA(cudaEventRecord(ctx->ev_entry, ctx->stream));  // earlier work on the staging buffers
   PD_CUDA(cudaStreamWaitEvent(ctx->cp_in, ctx->ev_entry, 0));
   PD_CUDA(cudaStreamWaitEvent(ctx->cp_out, ctx->ev_entry, 0));
@@ -694,9 +704,11 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
     const int64_t b0 = c * csz, nb = std::min<int64_t>(csz, batch - b0);
     if (nb <= 0) break;
     const size_t off = (size_t)b0 * n, bytes = sizeof(double) * (size_t)n * nb;
+    mark(2 + 4 * c, ctx->cp_in);
     PD_CUDA(cudaMemcpyAsync(sq + half + off, q + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
     PD_CUDA(cudaMemcpyAsync(sqd + half + off, qdot + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
     PD_CUDA(cudaMemcpyAsync(stau + half + off, tau + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
+    mark(3 + 4 * c, ctx->cp_in);
     PD_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->cp_in));
     PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[c], 0));
     launch_transpose3(ctx, sq + half + off, sqd + half + off, stau + half + off, sq + b0, sqd + b0, stau + b0, nb, n,
@@ -705,9 +717,19 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
                              st + 2 * batch + b0, b0);
     if (s != PD_OK) return s;
     launch_transpose(ctx, sqdd + b0, sqdd + half + off, n, nb, lds, n);
+    mark(4 + 4 * c, ctx->stream);
     PD_CUDA(cudaEventRecord(ctx->ev_out[c], ctx->stream));
     PD_CUDA(cudaStreamWaitEvent(ctx->cp_out, ctx->ev_out[c], 0));
     PD_CUDA(cudaMemcpyAsync(qddot + off, sqdd + half + off, bytes, cudaMemcpyDeviceToHost, ctx->cp_out));
+    mark(5 + 4 * c, ctx->cp_out);
+  }
+  if (trace) {
+    PD_CUDA(cudaDeviceSynchronize());
+    float t[4];
+    for (int c = 0; c < nch && c * csz < batch; ++c) {
+      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], tev[0], tev[2 + 4 * c + k]);
+      std::fprintf(stderr, "chunk %2d: in %.3f-%.3f  compute done %.3f  out done %.3f ms\n", c, t[0], t[1], t[2], t[3]);
+    }
   }
   const bool want_status = slot_status || slot_round || slot_index;
   if (!want_status) {
