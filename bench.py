@@ -327,8 +327,8 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
 
 # ncu --set full captures of the dominant kernel per workload (profiles/, same
 # kernel and config as the bench command): DRAM bytes per launch
-NCU_TRAFFIC = {"c2": "profiles/ncu_c2_r1_s3d.txt", "c3": "profiles/ncu_c3_r1_s3c.txt",
-               "c2j": "profiles/ncu_c2j_r1_s3c.txt", "c5j": "profiles/ncu_c5j_r1_s3c.txt"}
+NCU_TRAFFIC = {"c2": "profiles/ncu_c2_r1_s3g.txt", "c3": "profiles/ncu_c3_r1_s3g.txt",
+               "c2j": "profiles/ncu_c2j_r1_s3g.txt", "c5j": "profiles/ncu_c5j_r1_s3c.txt"}
 
 
 def ncu_traffic(workload: str):
