@@ -18,7 +18,9 @@ from .api import (  # noqa: F401
     LinkSpec,
     LinkStates,
     ModelError,
+    OeeTrace,
     RobotChain,
+    ScanTrace,
     SingularBlockError,
     abia_forward_dynamics,
     batch_forward_dynamics,
@@ -31,8 +33,11 @@ from .api import (  # noqa: F401
     joint_space_inertia,
     jsiia_forward_dynamics,
     link_states,
+    oee_solve,
     load_chain,
     save_chain,
+    solve_lower_bidiag,
+    solve_upper_bidiag,
     validate_chain,
 )
 from ._capi import LIB_PATH, LibraryMissing  # noqa: F401

@@ -535,6 +535,65 @@ def joint_space_inertia(chain: RobotChain, q, ctx: Optional[Context] = None) -> 
 
 
 # --------------------------------------------------------------------------- model files
+# --------------------------------------------------------------------------- building blocks
+@dataclass
+class ScanTrace:
+    """trace.hpp ScanTrace: rounds of the Hillis-Steele scan (ceil_log2(n))."""
+    rounds: int = 0
+
+
+@dataclass
+class OeeTrace:
+    """trace.hpp OeeTrace: odd-even elimination rounds (ceil_log2(n))."""
+    rounds: int = 0
+
+
+def _bidiag(coupling, rhs, upper, trace, ctx):
+    rhs = np.asarray(rhs, dtype=np.float64)
+    n = rhs.shape[0]
+    if rhs.ndim != 2 or rhs.shape[1] != 6:
+        raise InvalidArgument("block bi-diagonal solve: rhs must be (n, 6)")
+    coupling = np.asarray(coupling, dtype=np.float64).reshape(-1, 6, 6)
+    if n > 0 and coupling.shape[0] != n - 1:
+        raise InvalidArgument("block bi-diagonal solve: need n - 1 coupling blocks for n right-hand sides")
+    if trace is not None:
+        trace.rounds = ceil_log2(n)
+    if n == 0:
+        return np.zeros((0, 6))
+    return (ctx or default_context()).block_bidiag_solve6(coupling[None], rhs[None], upper=upper)[0]
+
+
+def solve_lower_bidiag(coupling, rhs, trace: Optional[ScanTrace] = None, ctx: Optional[Context] = None):
+    """solve_lower_bidiag (scan.hpp:115-140) of one BlockBiDiagSystem<6>:
+    x_0 = r_0, x_i = C_i x_{i-1} + r_i; coupling (n-1, 6, 6), rhs (n, 6)."""
+    return _bidiag(coupling, rhs, False, trace, ctx)
+
+
+def solve_upper_bidiag(coupling, rhs, trace: Optional[ScanTrace] = None, ctx: Optional[Context] = None):
+    """solve_upper_bidiag (scan.hpp:143-168): the reversed index order."""
+    return _bidiag(coupling, rhs, True, trace, ctx)
+
+
+def oee_solve(diag, upper, rhs, trace: Optional[OeeTrace] = None, ctx: Optional[Context] = None):
+    """oee_solve<5,1> (oee.hpp:149-189) of one SymBlockTriDiagSystem<5>:
+    diag (n, 5, 5), upper (n-1, 5, 5), rhs (n, 5) -> x (n, 5). Raises
+    SingularBlockError(round, index) with the reference's message."""
+    diag = np.asarray(diag, dtype=np.float64).reshape(-1, 5, 5)
+    n = diag.shape[0]
+    rhs = np.asarray(rhs, dtype=np.float64).reshape(-1, 5)
+    upper = np.asarray(upper, dtype=np.float64).reshape(-1, 5, 5)
+    if rhs.shape[0] != n or (n > 0 and upper.shape[0] != n - 1):
+        raise InvalidArgument("odd-even elimination: inconsistent block counts")
+    if trace is not None:
+        trace.rounds = ceil_log2(n)
+    if n == 0:
+        return np.zeros((0, 5))
+    x, st, rd, ix = (ctx or default_context()).block_tridiag_solve5(diag[None], upper[None], rhs[None])
+    if st[0] != 0:
+        _raise_slot(int(st[0]), int(rd[0]), int(ix[0]), n)
+    return x[0]
+
+
 def _link_prefix(k: int) -> str:
     return f"link {k}"
 

@@ -91,3 +91,27 @@ def test_bidiag6_spec_known_answer(gpu_ctx):
     rhs_u[0, 2] = 1.0
     xu = gpu_ctx.block_bidiag_solve6(coupling, rhs_u, True)
     assert np.array_equal(xu[0, :, 0], [4.0, 2.0, 1.0])
+
+
+def test_single_system_api(oracle, gpu_ctx):
+    """Module-level mirrors of the reference's single-system calls
+    (solve_lower/upper_bidiag, oee_solve) with their traces and errors."""
+    import paper_1609_06779_b200 as pd
+    st = pd.ScanTrace()
+    x = pd.solve_lower_bidiag(np.stack([2.0 * np.eye(6)] * 2), np.vstack([np.ones(6), np.zeros((2, 6))]), st,
+                              ctx=gpu_ctx)
+    assert np.array_equal(x[:, 0], [1.0, 2.0, 4.0]) and st.rounds == 2
+    xu = pd.solve_upper_bidiag(np.stack([2.0 * np.eye(6)] * 2), np.vstack([np.zeros((2, 6)), np.ones(6)]),
+                               ctx=gpu_ctx)
+    assert np.array_equal(xu[:, 0], [4.0, 2.0, 1.0])
+    rng = np.random.default_rng(11)
+    diag, upper, rhs = random_system(rng, 40)
+    ot = pd.OeeTrace()
+    x5 = pd.oee_solve(diag, upper, rhs, ot, ctx=gpu_ctx)
+    want, _ = gpu_ctx.block_tridiag_solve5(diag[None], upper[None], rhs[None])[:2]
+    assert np.array_equal(x5, want[0]) and ot.rounds == 6
+    d3 = np.stack([np.eye(5), np.zeros((5, 5)), np.eye(5)])
+    with pytest.raises(pd.SingularBlockError) as e:
+        pd.oee_solve(d3, np.stack([0.1 * np.eye(5)] * 2), np.ones((3, 5)), ctx=gpu_ctx)
+    assert (e.value.round(), e.value.index()) == (1, 1)
+    assert "odd-even elimination: singular pivot block (round 1, block 1)" in str(e.value)
