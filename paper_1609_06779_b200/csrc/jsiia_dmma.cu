@@ -110,10 +110,12 @@ struct Vk {
 };
 
 // Warp scan over lanes of per-lane totals: exclusive prefix (REV: suffix over
-// higher lanes) of K doubles; Hillis-Steele inclusive + one shift.
-template <int K, bool REV>
+// higher lanes) of K doubles; Hillis-Steele inclusive + one shift. ROLL keeps
+// the 5 rounds as a loop: for the NB > 4 kernels the smaller instruction
+// footprint wins (c5j 25.6 -> 24.3 ms), for NB <= 4 it loses (c2j 559 -> 569 us).
+template <int K, bool REV, bool ROLL>
 __device__ __forceinline__ Vk<K> warp_excl(Vk<K> x, int lane) {
-#pragma unroll
+#pragma unroll(ROLL ? 1 : 5)
   for (int d = 1; d < 32; d <<= 1) {
     Vk<K> y;
 #pragma unroll
@@ -165,7 +167,7 @@ __device__ __forceinline__ void link_scan(Vk<K> (&a)[LPL], int lane) {
     for (int e = 0; e < LPL; ++e) s += a[REV ? LPL - 1 - e : e].v[k];
     tot.v[k] = s;
   }
-  const Vk<K> base = warp_excl<K, REV>(tot, lane);
+  const Vk<K> base = warp_excl<K, REV, (LPL > 1)>(tot, lane);
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double run = base.v[k];
