@@ -177,10 +177,22 @@ def dist_barrier(world: int, local: int):
 
 
 # ----------------------------------------------------------------------------- CPU arm
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_reference(algo: str, n: int, links, q, qd, tau, budget_s: float, reps: int, warm: int):
     """Times the CPU restatement of the reference path (oracle/) on the
     largest prefix of the workload that keeps reps+warm calls within budget_s.
-    Returns (solves/s, sample size, cores)."""
+    Returns (solves/s, sample size, cores, oracle qdd of the sample)."""
     from oracle import pyoracle as po
     cores = po.lib().orc_num_threads()
     probe = min(len(q), 512 if algo != "jsiia" else 128)
@@ -193,9 +205,9 @@ def cpu_reference(algo: str, n: int, links, q, qd, tau, budget_s: float, reps: i
         po.batch_forward_dynamics(algo, ls, [0, 0, -9.81], q[:S], qd[:S], tau[:S])
     t0 = time.perf_counter()
     for _ in range(reps):
-        po.batch_forward_dynamics(algo, ls, [0, 0, -9.81], q[:S], qd[:S], tau[:S])
+        ref, _ = po.batch_forward_dynamics(algo, ls, [0, 0, -9.81], q[:S], qd[:S], tau[:S])
     dt = time.perf_counter() - t0
-    return S * reps / dt, S, cores
+    return S * reps / dt, S, cores, ref
 
 
 def gen_workload(wl: dict, rank: int, world: int = 1):
@@ -220,22 +232,44 @@ def gen_workload(wl: dict, rank: int, world: int = 1):
     return links, inputs, inputs2
 
 
+def oracle_workload(wl: dict):
+    """The same workload as gen_workload, generated by the oracle's restatement
+    of the reference generators (bench.cpp:350-383, model.cpp:157-185), so the
+    reference arm maps only oracle/build/liboracle.so."""
+    from oracle import pyoracle as po
+    n, B = wl["n"], wl["batch"]
+    cell = po.workload_seed(42, n, B)
+    if wl["shared"]:
+        links = po.workload_chains(cell, n, 1)
+        qs = [po.workload_inputs(cell, n, 1, r) for r in range(B)]
+        return links, tuple(np.concatenate([x[k] for x in qs]) for k in range(3))
+    return None, (cell, n, B)
+
+
 def run_reference_arm(args, wl):
-    world, rank, local = dist_setup()
+    world, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+                      int(os.environ.get("LOCAL_RANK", "0")))
     if rank != 0:
         return
-    links, (q, qd, tau), _ = gen_workload(wl, 0)
     from oracle import pyoracle as po
     cores = po.lib().orc_num_threads()
     algo, n = wl["algo"], wl["n"]
+    links, spec = oracle_workload(wl)
+    if links is None:  # independent chains: generate the prefix the CPU can time
+        cell, _, B = spec
+        probe_links = po.workload_chains(cell, n, min(B, 256))
+        q, qd, tau = po.workload_inputs(cell, n, B, 0)
+    else:
+        probe_links = links
+        q, qd, tau = spec
     # bound the whole --steps/--warmup run to ~90 s of CPU work
     probe = min(len(q), 256)
     t0 = time.perf_counter()
-    po.batch_forward_dynamics(algo, links[:1] if wl["shared"] else links[:probe], [0, 0, -9.81], q[:probe],
+    po.batch_forward_dynamics(algo, probe_links if wl["shared"] else probe_links[:probe], [0, 0, -9.81], q[:probe],
                               qd[:probe], tau[:probe])
     rate = probe / max(time.perf_counter() - t0, 1e-6)
     S = int(max(32, min(len(q), rate * 90.0 / max(args.steps + args.warmup, 1))))
-    ls = links[:1] if wl["shared"] else links[:S]
+    ls = links if wl["shared"] else po.workload_chains(spec[0], n, S)
     for _ in range(args.warmup):
         po.batch_forward_dynamics(algo, ls, [0, 0, -9.81], q[:S], qd[:S], tau[:S])
     t0 = time.perf_counter()
@@ -244,17 +278,31 @@ def run_reference_arm(args, wl):
     dt = time.perf_counter() - t0
     value = S * args.steps / dt
     sample = (f"first {S} of {wl['batch']} problems of {args.workload} per step "
-              f"(reference CPU path restated in oracle/, OpenMP dynamic over {cores} threads)")
+              f"(reference CPU path restated in oracle/, OpenMP dynamic over {cores} threads; {cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generators, seed 42)",
-        "config": {"workload": f"{args.workload}: {wl['desc']}", "algo": algo, "n_links": n,
-                   "batch_per_gpu": wl["batch"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if wl.get("sharded") else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": DATA,
+        "config": workload_config(args.workload, wl, wl["batch"], wl["batch"] * (1 if wl.get("sharded") else world),
+                                  world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+DATA = "synthetic: reference generators workload_chains/workload_inputs (seed 42), random-init chains"
+
+
+def workload_config(name: str, wl: dict, batch_per_gpu: int, global_batch: int, world: int) -> dict:
+    """The `config` object both arms print (same keys and values)."""
+    return {"workload": f"{name}: {wl['desc']}", "algo": wl["algo"], "n_links": wl["n"],
+            "batch_per_gpu": batch_per_gpu, "global_batch": global_batch, "parallelism": f"batch-sharded x{world}",
+            "l2": "inputs larger than L2 (%.0f MB streamed per step)" % (b_alg(wl["n"], wl["shared"]) * batch_per_gpu
+                                                                        / 1e6)
+            if b_alg(wl["n"], wl["shared"]) * batch_per_gpu > 126e6 else "L2 not flushed (small workload)"}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -287,6 +335,19 @@ def time_device(ctx, algo, B, n, dev_inputs, steps, warmup, stream):
     return e0.elapsed_time(e1), ctx.kernel_launches() - l0, qdd
 
 
+def qdd_for_first_inputs(ctx, algo, B, n, dev_inputs, qdd, steps):
+    """Host copy ([link][problem]) of the qdd the timed loop computed for the
+    first input set (re-solved untimed if the last step used another set)."""
+    import torch
+    from paper_1609_06779_b200 import FdAlgo
+    if (steps - 1) % len(dev_inputs) != 0:
+        q, qd, tau = dev_inputs[0]
+        ctx.solve_device(FdAlgo[algo], B, q.data_ptr(), qd.data_ptr(), tau.data_ptr(), qdd.data_ptr())
+        ctx.synchronize()
+    torch.cuda.synchronize()
+    return qdd.cpu().numpy()
+
+
 def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e, e2e_steps, world=1):
     import torch
     n, algo = wl["n"], wl["algo"]
@@ -303,7 +364,10 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
     if inp2 is not None:
         dev_inputs.append(tuple(to_dev(a) for a in inp2))
     ms_total, launches, qdd = time_device(ctx, algo, B, n, dev_inputs, steps, warmup, stream)
-    res = {"ms_total": ms_total, "launches": launches, "links": links, "inputs": inp, "B": B}
+    res = {"ms_total": ms_total, "launches": launches, "links": links, "inputs": inp, "B": B,
+           "variant": ctx.last_variant(),
+           # qdd of the last timed step (inputs set len(dev_inputs) - 1 ... wrap): keep the one matching inp
+           "qdd": qdd_for_first_inputs(ctx, algo, B, n, dev_inputs, qdd, steps)}
     if want_e2e:
         pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in inp]
         out = torch.empty((B, n), dtype=torch.float64).pin_memory()
@@ -321,7 +385,10 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
         res["e2e_s"] = dt
         res["e2e_steps"] = e2e_steps
         res["h2d"] = 3 * B * n * 8
-        res["d2h"] = B * n * 8 + 3 * B * 4
+        # qddot, plus the 4-byte OR of the slot codes: when every slot succeeded
+        # (asserted above) the per-slot arrays are zero-filled on the host
+        # instead of copied (capi.cu host_forward_dynamics)
+        res["d2h"] = B * n * 8 + 4
     return res
 
 
@@ -429,11 +496,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: reference generators workload_chains/workload_inputs (seed 42), random-init chains",
-        "config": {"workload": f"{args.workload}: {wl['desc']}", "algo": wl["algo"], "n_links": n,
-                   "batch_per_gpu": B, "global_batch": global_batch, "parallelism": f"batch-sharded x{world}",
-                   "l2": "inputs larger than L2 (%.0f MB streamed per step)" % (work["bytes_per_launch"] / 1e6)
-                   if work["bytes_per_launch"] > 126e6 else "L2 not flushed (small workload)"},
+        "data": DATA,
+        "config": workload_config(args.workload, wl, B, global_batch, world),
         "roofline": hbm,
         "roofline_traffic_source": (tr["source"] + " (ncu --set full, DRAM read + write bytes per launch)") if tr
         else None,
@@ -451,10 +515,17 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_cpu:
         q, qd, tau = res["inputs"]
-        v, S, cores = cpu_reference(wl["algo"], n, res["links"], q, qd, tau, budget_s=12.0, reps=5, warm=1)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+        v, S, cores, ref = cpu_reference(wl["algo"], n, res["links"], q, qd, tau, budget_s=12.0, reps=5, warm=1)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                                 "sample": f"first {S} problems of {args.workload}, 1 warm-up + 5 timed whole-batch "
                                           f"calls, reference CPU path restated in oracle/ (OpenMP dynamic)"}
+        # the checker, outside every timed region: the timed loop's qdd of the
+        # sampled problems against the oracle's (rel_gap, oracles.hpp:64-66)
+        got = res["qdd"][:, :S].T if res["qdd"].shape[1] >= S else None
+        if got is not None:
+            gaps = np.linalg.norm(got - ref, axis=1) / np.maximum(1.0, np.linalg.norm(ref, axis=1))
+            line["parity"] = {"max_rel_gap": float(gaps.max()), "tolerance": 1e-9, "slots": int(S),
+                              "ok": bool(gaps.max() <= 1e-9), "against": "oracle/ (CPU restatement)"}
 
     if rank == 0 and world == 1 and not args.no_extra:
         extra = {}

@@ -42,6 +42,11 @@
  *   pd_joint_space_inertia   <- joint_space_inertia(chain, q)
  *                               (forward_dynamics.hpp:34-35,
  *                               src/forward_dynamics.cpp:70-80)
+ *   pd_forward_dynamics_traced, pd_exec_trace
+ *                            <- forward_dynamics(..., ExecTrace* trace) and
+ *                               the per-algorithm entry points with a trace
+ *                               (forward_dynamics.hpp:38-42,58-62,98-105;
+ *                               trace.hpp:24-39)
  *
  * Layouts
  *   LinkSpec record: 31 doubles, the field order of LinkSpec (model.hpp:17-23)
@@ -106,6 +111,19 @@ typedef enum pd_model_rule {
 
 typedef struct pd_ctx pd_ctx;
 
+/* ExecTrace (trace.hpp:24-39): the dependency profile of the kernel variant
+ * that ran. parallel_link_stages = per-link stages whose iterations ran
+ * independently (a thread per link); longest_sequential_link_chain = the
+ * longest link walk one thread carried a dependency through;
+ * scan_rounds_max = Hillis-Steele combine rounds of the deepest link scan;
+ * oee_rounds = odd-even elimination rounds. */
+typedef struct pd_exec_trace {
+  int32_t parallel_link_stages;
+  int32_t longest_sequential_link_chain;
+  int32_t scan_rounds_max;
+  int32_t oee_rounds;
+} pd_exec_trace;
+
 /* Context on one CUDA device (ordinal). Owns device buffers and a stream. */
 pd_status pd_create(pd_ctx** out, int device);
 void pd_destroy(pd_ctx* ctx);
@@ -137,11 +155,32 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
                               int32_t* slot_index);
 
 /* Same on device buffers in [link][problem] layout, asynchronous on the
- * context's stream. d_slot_* must be device int32 arrays of length batch
- * (nullable -> internal scratch). */
+ * context's stream. d_slot_* must be device int32 arrays of length batch;
+ * each is nullable on its own (internal scratch then takes that output). */
 pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* d_q,
                                      const double* d_qdot, const double* d_tau, double* d_qddot,
                                      int32_t* d_slot_status, int32_t* d_slot_round, int32_t* d_slot_index);
+
+/* A traced solve (host buffers, as pd_forward_dynamics): runs the
+ * CTA-per-chain variants whose link recursions are log-depth scans and OEE
+ * rounds -- the parallel structure the reference's counters describe -- and
+ * fills *trace (nullable) from that variant. The reference's expectations
+ * (tests/test_fwddyn.cpp:263-283): JSIIA and CFA longest chain 0, ABIA n,
+ * scan rounds ceil(log2 n), CFA OEE rounds ceil(log2 n). */
+pd_status pd_forward_dynamics_traced(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q,
+                                     const double* qdot, const double* tau, double* qddot, int32_t* slot_status,
+                                     int32_t* slot_round, int32_t* slot_index, pd_exec_trace* trace);
+
+/* The kernel variant(s) the last forward-dynamics call on this context ran
+ * (e.g. "abia_ring_kernel<224> grid 148 tiles 293") and their ExecTrace. */
+const char* pd_last_variant(const pd_ctx* ctx);
+pd_status pd_last_trace(const pd_ctx* ctx, pd_exec_trace* trace);
+
+/* Kernel choice depends on (algorithm, n, batch). A caller that splits one
+ * batch over several calls or devices sets the whole batch here (0 = each
+ * call's own batch): every part then runs the same variants and the results
+ * are bit-identical to the unsplit call's (acceptance_main.cpp:495-580). */
+pd_status pd_set_selection_batch(pd_ctx* ctx, int64_t batch);
 
 /* Joint torques of inverse dynamics with default IdOptions (gravity on, no
  * base motion, no tip wrench), host buffers [problem][link]. */

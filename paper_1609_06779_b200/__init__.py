@@ -28,6 +28,7 @@ from .api import (  # noqa: F401
     cfa_forward_dynamics,
     ceil_log2,
     default_context,
+    set_device,
     forward_dynamics,
     inverse_dynamics,
     joint_space_inertia,

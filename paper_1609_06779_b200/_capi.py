@@ -28,6 +28,7 @@ EXPORTS = (
     "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak", "pd_inverse_dynamics_opts",
     "pd_inverse_dynamics_device", "pd_bias_torque", "pd_link_states", "pd_joint_space_inertia",
     "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5", "pd_block_bidiag_solve6",
+    "pd_forward_dynamics_traced", "pd_last_variant", "pd_last_trace", "pd_set_selection_batch",
 )
 
 
@@ -35,6 +36,12 @@ class IdOptions(C.Structure):
     """pd_id_options (include/pardyn_c.h) <- IdOptions (inverse_dynamics.hpp:23-28)."""
     _fields_ = [("base_velocity", C.c_double * 6), ("base_acceleration", C.c_double * 6),
                 ("tip_wrench", C.c_double * 6), ("apply_gravity", C.c_int32)]
+
+class ExecTraceC(C.Structure):
+    """pd_exec_trace (include/pardyn_c.h) <- ExecTrace (trace.hpp:24-39)."""
+    _fields_ = [("parallel_link_stages", C.c_int32), ("longest_sequential_link_chain", C.c_int32),
+                ("scan_rounds_max", C.c_int32), ("oee_rounds", C.c_int32)]
+
 
 _lib = None
 _D = C.POINTER(C.c_double)
@@ -114,6 +121,15 @@ def load():
     L.pd_workload_inputs.restype = None
     L.pd_probe_fp64_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.pd_probe_fp64_peak.restype = C.c_int
+    _TR = C.POINTER(ExecTraceC)
+    L.pd_forward_dynamics_traced.argtypes = [C.c_void_p, C.c_int, C.c_int64, _D, _D, _D, _D, _I32, _I32, _I32, _TR]
+    L.pd_forward_dynamics_traced.restype = C.c_int
+    L.pd_last_variant.argtypes = [C.c_void_p]
+    L.pd_last_variant.restype = C.c_char_p
+    L.pd_last_trace.argtypes = [C.c_void_p, _TR]
+    L.pd_last_trace.restype = C.c_int
+    L.pd_set_selection_batch.argtypes = [C.c_void_p, C.c_int64]
+    L.pd_set_selection_batch.restype = C.c_int
     _lib = L
     return L
 

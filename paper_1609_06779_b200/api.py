@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 from dataclasses import dataclass, field
 from typing import Iterable, List, Optional, Sequence
 
@@ -257,6 +258,37 @@ class Context:
                                                 _capi.dptr(qdd), _capi.iptr(st), _capi.iptr(rd), _capi.iptr(ix)))
         return qdd, st, rd, ix
 
+    def solve_traced(self, algo, q, qdot, tau):
+        """Host-buffer solve through the log-depth (CTA-per-chain) variants,
+        returning (qddot, status, round, index, ExecTrace of the variant)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qdot, dtype=np.float64)
+        tau = np.ascontiguousarray(tau, dtype=np.float64)
+        B = q.shape[0]
+        qdd = np.empty_like(q)
+        st, rd, ix = np.zeros(B, np.int32), np.zeros(B, np.int32), np.zeros(B, np.int32)
+        tr = _capi.ExecTraceC()
+        self._check(self._L.pd_forward_dynamics_traced(self._h, int(algo), B, _capi.dptr(q), _capi.dptr(qd),
+                                                       _capi.dptr(tau), _capi.dptr(qdd), _capi.iptr(st),
+                                                       _capi.iptr(rd), _capi.iptr(ix), C.byref(tr)))
+        return qdd, st, rd, ix, ExecTrace(tr.parallel_link_stages, tr.longest_sequential_link_chain,
+                                          tr.scan_rounds_max, tr.oee_rounds)
+
+    def last_variant(self) -> str:
+        """Kernel variant(s) the last forward-dynamics call ran."""
+        return self._L.pd_last_variant(self._h).decode()
+
+    def last_trace(self) -> "ExecTrace":
+        tr = _capi.ExecTraceC()
+        self._check(self._L.pd_last_trace(self._h, C.byref(tr)))
+        return ExecTrace(tr.parallel_link_stages, tr.longest_sequential_link_chain, tr.scan_rounds_max,
+                         tr.oee_rounds)
+
+    def set_selection_batch(self, batch: int):
+        """Select kernels for `batch` problems (0 = each call's own batch):
+        the parts of a split batch then run the whole batch's variants."""
+        self._check(self._L.pd_set_selection_batch(self._h, int(batch)))
+
     def solve_device(self, algo, batch, d_q, d_qd, d_tau, d_qdd, d_st=None, d_rd=None, d_ix=None):
         """Device solve on raw device pointers ([link][problem] layout)."""
         self._check(self._L.pd_forward_dynamics_device(self._h, int(algo), int(batch), d_q, d_qd, d_tau, d_qdd, d_st,
@@ -364,14 +396,29 @@ class Context:
         return self._L.pd_kernel_variant(self._h, int(algo), int(n)).decode()
 
 
-_default_ctx: Optional[Context] = None
+_tls = threading.local()
+_default_device = 0
+
+
+def set_device(device: int) -> None:
+    """CUDA device the calling thread's free-function solves run on
+    (pardyn::gpu::set_device in the C++ drop-in)."""
+    global _default_device
+    _default_device = int(device)
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is not None and ctx.device != _default_device:
+        _tls.ctx = None
 
 
 def default_context() -> Context:
-    global _default_ctx
-    if _default_ctx is None:
-        _default_ctx = Context(0)
-    return _default_ctx
+    """The calling thread's context. A pd_ctx is used from one host thread at
+    a time and the free functions are set_models + solve pairs, so every
+    thread gets its own (the reference's free functions are reentrant,
+    SPEC.md:97-98)."""
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = _tls.ctx = Context(_default_device)
+    return ctx
 
 
 # --------------------------------------------------------------------------- errors
@@ -394,21 +441,6 @@ def _check_sizes(chain: RobotChain, q, qdot, tau):
                               f"(chain has {n})")
 
 
-def _fill_trace(trace: Optional[ExecTrace], algo: FdAlgo, n: int):
-    if trace is None:
-        return
-    L = ceil_log2(n)
-    trace.scan_rounds_max = max(trace.scan_rounds_max, L)
-    if algo == FdAlgo.jsiia:
-        trace.parallel_link_stages += 6
-    elif algo == FdAlgo.abia:
-        trace.parallel_link_stages += 6
-        trace.longest_sequential_link_chain = max(trace.longest_sequential_link_chain, n)
-    else:
-        trace.parallel_link_stages += 9
-        trace.oee_rounds = L
-
-
 # --------------------------------------------------------------------------- API
 def forward_dynamics(chain: RobotChain, q, qdot, tau, algo: FdAlgo, trace: Optional[ExecTrace] = None,
                      ctx: Optional[Context] = None) -> np.ndarray:
@@ -419,11 +451,19 @@ def forward_dynamics(chain: RobotChain, q, qdot, tau, algo: FdAlgo, trace: Optio
     _check_sizes(chain, q, qdot, tau)
     ctx = ctx or default_context()
     ctx.set_models(chain.to_records()[None], np.asarray(chain.gravity, np.float64)[None])
-    qdd, st, rd, ix = ctx.solve(algo, np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
-                                np.asarray(tau, np.float64)[None])
+    args = (np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None], np.asarray(tau, np.float64)[None])
+    if trace is None:
+        qdd, st, rd, ix = ctx.solve(algo, *args)
+    else:  # the log-depth variants, counters from the variant that ran
+        qdd, st, rd, ix, tr = ctx.solve_traced(algo, *args)
     if st[0] != _capi.SLOT_OK:
         _raise_slot(st[0], rd[0], ix[0], chain.size())
-    _fill_trace(trace, algo, chain.size())
+    if trace is not None:
+        trace.parallel_link_stages += tr.parallel_link_stages
+        trace.longest_sequential_link_chain = max(trace.longest_sequential_link_chain,
+                                                  tr.longest_sequential_link_chain)
+        trace.scan_rounds_max = max(trace.scan_rounds_max, tr.scan_rounds_max)
+        trace.oee_rounds = tr.oee_rounds if algo == FdAlgo.cfa else trace.oee_rounds
     return qdd[0]
 
 
@@ -472,16 +512,20 @@ def batch_forward_dynamics(problems: Sequence[FdProblem], algo: FdAlgo, ctx: Opt
 
 
 def _id_sizes(chain: RobotChain, **vecs):
-    """inverse_dynamics.cpp:10-17 (check_length) and model.cpp:119-124."""
+    """inverse_dynamics.cpp:10-17 (check_joint_size)."""
     n = chain.size()
     for name, v in vecs.items():
         if len(v) != n:
-            if name == "q":
-                raise InvalidArgument(f"assemble_kinematics: q has length {len(v)} but the chain has {n} links")
             raise InvalidArgument(f"{name} has length {len(v)} but the chain has {n} joints")
 
 
-def _one_model(chain: RobotChain, ctx: Optional[Context]) -> Context:
+def _one_model(chain: RobotChain, q, ctx: Optional[Context]) -> Context:
+    """The reference's order: assemble_kinematics checks q (model.cpp:117-124),
+    then link_inertias validates every link (model.cpp:148-155,
+    spatial.cpp:72-87); the rate checks come after (inverse_dynamics.cpp:10-17)."""
+    n = chain.size()
+    if len(q) != n:
+        raise InvalidArgument(f"assemble_kinematics: q has length {len(q)} but the chain has {n} joints")
     ctx = ctx or default_context()
     ms, mr = ctx.set_models(chain.to_records()[None], np.asarray(chain.gravity, np.float64)[None])
     if ms[0] != _capi.SLOT_OK:
@@ -492,32 +536,34 @@ def _one_model(chain: RobotChain, ctx: Optional[Context]) -> Context:
 def inverse_dynamics(chain: RobotChain, q, qdot, qddot, opts: Optional[IdOptions] = None,
                      ctx: Optional[Context] = None) -> np.ndarray:
     """inverse_dynamics.cpp:166-173 (IdOptions defaults when opts is None)."""
-    _id_sizes(chain, q=q, qdot=qdot, qddot=qddot)
-    n = chain.size()
-    if n == 0:
+    if chain.size() == 0:
+        _id_sizes(chain, q=q, qdot=qdot, qddot=qddot)
         return np.zeros(0)
-    ctx = _one_model(chain, ctx)
+    ctx = _one_model(chain, q, ctx)
+    _id_sizes(chain, qdot=qdot, qddot=qddot)
     return ctx.inverse_dynamics_opts(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
                                      np.asarray(qddot, np.float64)[None], opts)[0]
 
 
 def bias_torque(chain: RobotChain, q, qdot, ctx: Optional[Context] = None) -> np.ndarray:
     """inverse_dynamics.cpp:175-179."""
-    _id_sizes(chain, q=q, qdot=qdot)
     if chain.size() == 0:
+        _id_sizes(chain, q=q, qdot=qdot)
         return np.zeros(0)
-    ctx = _one_model(chain, ctx)
+    ctx = _one_model(chain, q, ctx)
+    _id_sizes(chain, qdot=qdot)
     return ctx.bias_torque(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None])[0]
 
 
 def link_states(chain: RobotChain, q, qdot, qddot, opts: Optional[IdOptions] = None,
                 ctx: Optional[Context] = None) -> LinkStates:
     """inverse_dynamics.cpp:181-196."""
-    _id_sizes(chain, q=q, qdot=qdot, qddot=qddot)
     if chain.size() == 0:
+        _id_sizes(chain, q=q, qdot=qdot, qddot=qddot)
         z = np.zeros((0, 6))
         return LinkStates(z, z.copy(), z.copy())
-    ctx = _one_model(chain, ctx)
+    ctx = _one_model(chain, q, ctx)
+    _id_sizes(chain, qdot=qdot, qddot=qddot)
     v, a, f = ctx.link_states(np.asarray(q, np.float64)[None], np.asarray(qdot, np.float64)[None],
                               np.asarray(qddot, np.float64)[None], opts)
     return LinkStates(v[0], a[0], f[0])
@@ -525,12 +571,9 @@ def link_states(chain: RobotChain, q, qdot, qddot, opts: Optional[IdOptions] = N
 
 def joint_space_inertia(chain: RobotChain, q, ctx: Optional[Context] = None) -> np.ndarray:
     """forward_dynamics.cpp:70-80: M(q), symmetric."""
-    n = chain.size()
-    if len(q) != n:
-        raise InvalidArgument("joint_space_inertia: q must have one entry per joint")
-    if n == 0:
+    if chain.size() == 0 and len(q) == 0:
         return np.zeros((0, 0))
-    ctx = _one_model(chain, ctx)
+    ctx = _one_model(chain, q, ctx)
     return ctx.joint_space_inertia(np.asarray(q, np.float64)[None])[0]
 
 

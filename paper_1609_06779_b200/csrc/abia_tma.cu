@@ -10,11 +10,10 @@
 //   pass A: the F_NKIN kinematic fields + q, qd
 //   pass B: all F_COUNT model fields + q, qd, tau
 //   pass C: the 13-double records pass B wrote (after a proxy fence)
-// abia_ring_kernel (default): a dedicated producer warp streams the steps of
-// all the CTA's tiles (persistent CTAs) through one byte ring with per-pass
-// stage sizes, so cheap passes run many links ahead and the next tile's pass
-// A streams in during this tile's pass C. abia_tma_kernel: the earlier fixed
-// 3-stage ring with the producer inside warp 0 (PD_ABIA_VARIANT 0..9).
+// abia_ring_kernel: a dedicated producer warp streams the steps of all the
+// CTA's tiles (persistent CTAs) through one byte ring with per-pass stage
+// sizes, so cheap passes run many links ahead and the next tile's pass A
+// streams in during this tile's pass C.
 #include <cuda.h>
 
 #include <algorithm>
@@ -26,11 +25,6 @@
 namespace pd {
 
 namespace {
-
-constexpr int kT = 128;          // chains per CTA
-constexpr int kStageFields = F_COUNT + 5;  // model + q, qd, tau, sin, cos; pass C uses 13
-constexpr int kQ = F_COUNT, kQD = F_COUNT + 1, kTAU = F_COUNT + 2, kSIN = F_COUNT + 3, kCOS = F_COUNT + 4;
-constexpr int kSC0 = kRec;       // scratch rows n*kRec + 2*i + {0,1}: (sin, cos) of link i's joint angle
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -105,212 +99,12 @@ struct Maps {
   CUtensorMap model_kin;  // box {T, 1, F_NKIN} from field F_KIN
   CUtensorMap q, qd, tau; // box {T, 1}
   CUtensorMap scr;        // box {T, 13}
-  CUtensorMap sc;         // box {T, 2}: (sin, cos) rows written by pass A
 };
 
 }  // namespace
 
-template <int KT = kT>
-__device__ __forceinline__ Sv stage_screw(const double* f) {
-  return joint_screw(f[F_SW * KT], f[F_SVX * KT], f[F_SVZ * KT]);
-}
-template <int KT = kT>
-__device__ __forceinline__ SE3d stage_rel(const double* f, double st, double ct) {
-  const Mat3d HR = quat_to_R(f[F_HQ * KT], f[(F_HQ + 1) * KT], f[(F_HQ + 2) * KT], f[(F_HQ + 3) * KT]);
-  return joint_transform_sc(stage_screw<KT>(f), f[F_SIW * KT], HR, mk(f[F_HP * KT], f[(F_HP + 1) * KT], f[(F_HP + 2) * KT]),
-                            f[kQ * KT], st, ct);
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
-}
-
-// KSTAGES-deep ring; MINB CTAs per SM; HINTS = L2 policy (records evict_last
-// + discard after use, last-use streams evict_first).
-//
-// Synchronisation: full[s] (TMA transaction count) tells consumers a stage
-// landed; empty[s] (one arrival per warp) tells the producer (thread 0) that
-// every warp is done with it. There is no CTA-wide barrier per link: warps
-// drift freely within the ring and only the producer waits for the slowest.
-// Pass A stores sin/cos of each joint angle for pass B (one sincos per link);
-// the last KSTAGES links of pass A, whose pass-B loads are issued before pass A
-// reaches them, keep theirs in registers.
-template <int KSTAGES, int MINB, int HINTS, int KT>
-__global__ void __launch_bounds__(KT, MINB)
-    abia_tma_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
-                    int64_t scr_ld) {
-  static_assert(KSTAGES == 2 || KSTAGES == 3, "the register hand-off of the last pass-A links covers <= 3 stages");
-  extern __shared__ __align__(128) double ring[];  // [KSTAGES][kStageFields][KT]
-  __shared__ __align__(8) uint64_t full[KSTAGES];
-  __shared__ __align__(8) uint64_t empty[KSTAGES];
-  const int t = threadIdx.x, lane = t & 31;
-  const int n = mv.n;
-  const int c0 = blockIdx.x * KT;
-  const int64_t p = (int64_t)c0 + t;
-  const bool live = p < io.B;
-  const int total = 3 * n;
-  if (t == 0) {
-    for (int s = 0; s < KSTAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], KT / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint64_t pol_first = 0, pol_last = 0;
-  if (HINTS) {
-    pol_first = policy_evict_first();
-    pol_last = policy_evict_last();
-  }
-
-  // step k: pass A link k (k < n), pass B link 2n-1-k, pass C link k-2n
-  auto issue = [&](int k) {
-    const int s = k % KSTAGES;
-    double* dst = ring + (size_t)s * kStageFields * KT;
-    uint64_t* bar = &full[s];
-    if (k < n) {  // re-read in pass B: default policy, or evict_last (HINTS & 2)
-      mbar_expect_tx(bar, (F_NKIN + 2) * KT * 8);
-      if (HINTS & 2) {
-        tma_3d_hint(dst + F_KIN * KT, &maps.model_kin, c0, k, F_KIN, bar, pol_last);
-        tma_2d_hint(dst + kQ * KT, &maps.q, c0, k, bar, pol_last);
-        tma_2d_hint(dst + kQD * KT, &maps.qd, c0, k, bar, pol_last);
-      } else {
-        tma_3d(dst + F_KIN * KT, &maps.model_kin, c0, k, F_KIN, bar);
-        tma_2d(dst + kQ * KT, &maps.q, c0, k, bar);
-        tma_2d(dst + kQD * KT, &maps.qd, c0, k, bar);
-      }
-    } else if (k < 2 * n) {  // last use of the model
-      const int i = 2 * n - 1 - k;
-      mbar_expect_tx(bar, (F_COUNT + 5) * KT * 8);
-      if (HINTS) {
-        tma_3d_hint(dst, &maps.model_all, c0, i, 0, bar, pol_first);
-        tma_2d_hint(dst + kTAU * KT, &maps.tau, c0, i, bar, pol_first);
-        tma_2d_hint(dst + kSIN * KT, &maps.sc, c0, 2 * i, bar, pol_first);
-      } else {
-        tma_3d(dst, &maps.model_all, c0, i, 0, bar);
-        tma_2d(dst + kTAU * KT, &maps.tau, c0, i, bar);
-        tma_2d(dst + kSIN * KT, &maps.sc, c0, 2 * i, bar);
-      }
-      if (HINTS & 2) {  // last use of q, qd: demote
-        tma_2d_hint(dst + kQ * KT, &maps.q, c0, i, bar, pol_first);
-        tma_2d_hint(dst + kQD * KT, &maps.qd, c0, i, bar, pol_first);
-      } else {
-        tma_2d(dst + kQ * KT, &maps.q, c0, i, bar);
-        tma_2d(dst + kQD * KT, &maps.qd, c0, i, bar);
-      }
-    } else {
-      const int i = k - 2 * n;
-      mbar_expect_tx(bar, kRec * KT * 8);
-      if (HINTS)
-        tma_2d_hint(dst, &maps.scr, c0, i * kRec, bar, pol_first);
-      else
-        tma_2d(dst, &maps.scr, c0, i * kRec, bar);
-    }
-  };
-  // Producer = thread 0: steps [0, KSTAGES) up front; at the end of step k it
-  // waits until every warp released step k's stage, then issues step
-  // k + KSTAGES into it. Pass-C steps read pass B's records, so they are
-  // issued only once every warp released the last pass-B step (2n - 1).
-  int next = 0;
-  if (t == 0)
-    for (; next < min(KSTAGES, min(total, 2 * n)); ++next) issue(next);
-  auto after_step = [&](int k) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[k % KSTAGES]);
-    if (t == 0) {
-      const int target = k < 2 * n - 1 ? min(2 * n, k + 1 + KSTAGES) : min(total, k + 1 + KSTAGES);
-      for (; next < target; ++next) {
-        const int prev = next - KSTAGES;  // previous user of the stage
-        if (prev >= 0) mbar_wait(&empty[prev % KSTAGES], (uint32_t)((prev / KSTAGES) & 1));
-        if (next == 2 * n && prev != 2 * n - 1)
-          mbar_wait(&empty[(2 * n - 1) % KSTAGES], (uint32_t)(((2 * n - 1) / KSTAGES) & 1));
-        issue(next);
-      }
-    }
-  };
-
-  const int64_t mc = live ? mv.model_of(p) : 0;
-  AbiaState st;
-  abia_init(st, live ? mv.gravity(mc) : mk(0, 0, 0));
-  double s0 = 0, c0r = 1, s1 = 0, c1r = 1, s2 = 0, c2r = 1;  // (sin, cos) of links n-1, n-2, n-3
-  int k = 0;
-  for (; k < n; ++k) {  // pass A
-    const int s = k % KSTAGES;
-    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * KT + t;
-    const Sv S = stage_screw<KT>(f);
-    double sn, cs;
-    joint_angle_sincos(S, f[kQ * KT], &sn, &cs);
-    abia_pass_a(st, stage_rel<KT>(f, sn, cs), S, f[kQD * KT]);
-    if (k < n - KSTAGES) {
-      if (live) {
-        double* a = scratch + ((int64_t)n * kSC0 + 2 * k) * scr_ld + p;
-        if (HINTS) {
-          st_hint(a, sn, pol_last);
-          st_hint(a + scr_ld, cs, pol_last);
-        } else {
-          a[0] = sn;
-          a[scr_ld] = cs;
-        }
-      }
-    } else {
-      s2 = s1; c2r = c1r; s1 = s0; c1r = c0r; s0 = sn; c0r = cs;
-    }
-    if (k == n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // sin/cos rows -> TMA reads
-    after_step(k);
-  }
-  for (; k < 2 * n; ++k) {  // pass B
-    const int s = k % KSTAGES;
-    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * KT + t;
-    const int i = 2 * n - 1 - k;
-    double sn = f[kSIN * KT], cs = f[kCOS * KT];
-    if (i == n - 1) { sn = s0; cs = c0r; }
-    if (i == n - 2) { sn = s1; cs = c1r; }
-    if (i == n - 3) { sn = s2; cs = c2r; }
-    Inertia J;
-    J.m = f[F_MASS * KT];
-    J.c = mk(f[F_COM * KT], f[(F_COM + 1) * KT], f[(F_COM + 2) * KT]);
-#pragma unroll
-    for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
-    double rec[kRec];
-    abia_pass_b(st, i, n, stage_rel<KT>(f, sn, cs), stage_screw<KT>(f), f[kQD * KT], J, f[kTAU * KT], rec, f[kQ * KT]);
-    if (live) {
-#pragma unroll
-      for (int j = 0; j < kRec; ++j) {
-        double* a = scratch + ((int64_t)i * kRec + j) * scr_ld + p;
-        if (HINTS)
-          st_hint(a, rec[j], pol_last);
-        else
-          *a = rec[j];
-      }
-    }
-    if (k == 2 * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
-    after_step(k);
-  }
-  for (; k < total; ++k) {  // pass C
-    const int s = k % KSTAGES;
-    mbar_wait(&full[s], (uint32_t)((k / KSTAGES) & 1));
-    const double* f = ring + (size_t)s * kStageFields * KT + t;
-    const int i = k - 2 * n;
-    double rec[kRec];
-#pragma unroll
-    for (int j = 0; j < kRec; ++j) rec[j] = f[j * KT];
-    const double qdd = abia_pass_c(st, rec);
-    if (live) io.put_qdd(i, p, qdd);
-    if (HINTS && t < kRec * (KT * 8 / 128)) {
-      // the records of link i are dead: drop their L2 lines without write-back
-      const int row = t / (KT * 8 / 128), seg = t % (KT * 8 / 128);
-      const double* line = scratch + ((int64_t)i * kRec + row) * scr_ld + c0 + seg * 16;
-      if (c0 + seg * 16 + 16 <= io.B) discard_l2(line);
-    }
-    after_step(k);
-  }
-  if (live) {
-    const int32_t ms = __ldg(mv.mstatus + mc);
-    io.status[p] = ms != PD_SLOT_OK ? ms : st.code;
-    io.eround[p] = 0;
-    io.eindex[p] = ms != PD_SLOT_OK ? __ldg(mv.mrule + mc) : st.eidx;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -326,18 +120,6 @@ __global__ void __launch_bounds__(KT, MINB)
 constexpr int kSlots = 16;
 constexpr int kRowsA = F_NKIN + 2, kRowsB = F_COUNT + 3, kRowsC = kRec;
 
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(done)
-      : "r"(saddr(bar)), "r"(parity)
-      : "memory");
-  return done != 0;
-}
-
 // rows r0.. = the kinematic block F_SW..F_HP: w, vx, vz, 1/w, home quaternion (4), home p (3)
 template <int KT>
 __device__ __forceinline__ Sv row_screw(const double* f, int r0) {
@@ -352,7 +134,7 @@ __device__ __forceinline__ SE3d row_rel(const double* f, int r0, const Sv& S, do
 
 // MAXREG caps registers per thread (__maxnreg__) so that the wanted number of
 // CTAs fits the SM's 64K registers (e.g. 2 x 160 threads x 200).
-template <int KT, int MAXREG, bool KEEP_A>
+template <int KT, int MAXREG>
 __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
     abia_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
                      int64_t scr_ld, uint32_t cap_rows) {
@@ -401,15 +183,9 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
           uint64_t* bar = &full[gk % kSlots];
           if (k < (uint32_t)n) {  // pass A: kinematic rows 0..F_NKIN-1, q, qd
             mbar_expect_tx(bar, kRowsA * KT * 8);
-            if (KEEP_A) {
-              tma_3d_hint(dst, &maps.model_kin, c0, (int)k, F_KIN, bar, pol_last);
-              tma_2d_hint(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar, pol_last);
-              tma_2d_hint(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar, pol_last);
-            } else {
-              tma_3d(dst, &maps.model_kin, c0, (int)k, F_KIN, bar);
-              tma_2d(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar);
-              tma_2d(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar);
-            }
+            tma_3d(dst, &maps.model_kin, c0, (int)k, F_KIN, bar);
+            tma_2d(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar);
+            tma_2d(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar);
           } else if (k < 2u * n) {  // pass B: model rows 0..F_COUNT-1, q, qd, tau (last use)
             const int i = 2 * n - 1 - (int)k;
             mbar_expect_tx(bar, kRowsB * KT * 8);
@@ -542,19 +318,6 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Kernel variant: PD_ABIA_VARIANT forces one (tuning experiments); by
-// default the tile size is chosen for wave balance (0 or 4).
-// 0 = 128-chain tiles, 3 stages, 2 CTAs/SM, L2 hints; 1 = 2 stages, 3 CTAs/SM;
-// 2 = no L2 hints; 3 = TMEM-state kernel; 4 = 224-chain tiles, 1 CTA/SM.
-int abia_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PD_ABIA_VARIANT");
-    v = e ? std::atoi(e) : -1;
-  }
-  return v;
-}
-
 }  // namespace
 
 bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, uint32_t kt) {
@@ -579,9 +342,6 @@ bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scr
     const cuuint64_t str[1] = {(cuuint64_t)scr_ld * 8};
     const cuuint32_t box[2] = {kt, kRec};
     if (!encode(&maps.scr, scratch, 2, dims, str, box)) return false;
-    const cuuint64_t dims_sc[2] = {(cuuint64_t)io.B, (cuuint64_t)n * 2};
-    const cuuint32_t box_sc[2] = {kt, 2};
-    if (!encode(&maps.sc, scratch + (size_t)n * kSC0 * scr_ld, 2, dims_sc, str, box_sc)) return false;
   }
   return true;
 }
@@ -596,90 +356,61 @@ int sm_count() {
   return c;
 }
 
-// Returns false (caller falls back to the plain kernel) when the batch does
+// Returns 0 (caller falls back to the plain lane kernel) when the batch does
 // not meet TMA's layout rules: one model per chain, 16-byte aligned bases,
-// link strides that are multiples of 16 bytes, 32-bit coordinates.
-bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, cudaStream_t s) {
-  if (mv.M == 1 || mv.M != io.B) return false;
-  if ((io.lds & 1) || (mv.ld & 1) || (scr_ld & 1)) return false;
-  if (!aligned16(mv.f) || !aligned16(io.q) || !aligned16(io.qd) || !aligned16(io.tau) || !aligned16(scratch))
-    return false;
-  if (io.B >= (1ll << 31) || (int64_t)mv.n * kRec >= (1ll << 31)) return false;
-  int v = abia_variant();
-  if (v < 0) {
-    // Persistent ring kernel; tile by the makespan estimate: with more tiles
-    // than SMs the SM throughput is shared by its resident CTAs, so a tile
-    // costs KT * ctas chain-units per wave; with fewer tiles than SMs each
-    // tile runs alone and costs KT.
-    struct Cfg { int v, kt, ctas; };
-    const Cfg cfgs[3] = {{12, 224, 1}, {14, 96, 2}, {15, 64, 3}};
-    double best = 1e300;
-    for (const Cfg& c : cfgs) {
-      const int64_t tiles = (io.B + c.kt - 1) / c.kt;
-      const int64_t slots = (int64_t)sm_count() * c.ctas;
-      const double cost = tiles <= sm_count() ? (double)c.kt
-                                              : (double)((tiles + slots - 1) / slots) * c.kt * c.ctas;
-      if (cost < best) {
-        best = cost;
-        v = c.v;
-      }
+// link strides that are multiples of 16 bytes, 32-bit coordinates. Otherwise
+// launches the persistent ring kernel and returns its tile size.
+//
+// Tile size by the makespan estimate over the selection batch `sel_B` (the
+// global batch when a caller shards it, so every shard runs the same
+// instantiation): with more tiles than SMs the SM throughput is shared by its
+// resident CTAs, so a tile costs KT * ctas chain-units per wave; with fewer
+// tiles than SMs each tile runs alone and costs KT. The arithmetic per chain
+// is the same for every tile size (abia_common.cuh).
+int abia_ring_tile(int64_t sel_B) {
+  struct Cfg { int kt, ctas; };
+  const Cfg cfgs[3] = {{224, 1}, {96, 2}, {64, 3}};
+  double best = 1e300;
+  int kt = 224;
+  for (const Cfg& c : cfgs) {
+    const int64_t tiles = (sel_B + c.kt - 1) / c.kt;
+    const int64_t slots = (int64_t)sm_count() * c.ctas;
+    const double cost = tiles <= sm_count() ? (double)c.kt : (double)((tiles + slots - 1) / slots) * c.kt * c.ctas;
+    if (cost < best) {
+      best = cost;
+      kt = c.kt;
     }
   }
-  if (v >= 10) {
-    // ring kernels: (tile, CTAs per SM) per variant; the ring takes the SM's shared memory
-    const uint32_t kt = v == 12 ? 224u
-                        : (v == 13 || v == 17) ? 112u
-                        : v == 14 ? 96u
-                        : v == 15 ? 64u
-                        : v == 18 ? 160u
-                        : v == 19 ? 192u
-                                  : 128u;
-    const int ctas = (v == 13 || v == 14 || v == 16) ? 2 : (v == 15 ? 3 : 1);
-    Maps maps;
-    if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
-    const size_t smem = (size_t)(220 * 1024 / ctas) / (kt * 8) * (kt * 8);
-    const uint32_t cap_rows = (uint32_t)(smem / (kt * 8));
-    const int64_t ntiles = (io.B + kt - 1) / kt;
-    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * ctas);  // persistent CTAs
-    auto go = [&](auto kernel) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kernel<<<grid, (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
-    };
-    switch (v) {
-      case 11: go(abia_ring_kernel<128, 255, true>); break;
-      case 12: go(abia_ring_kernel<224, 255, false>); break;
-      case 13: go(abia_ring_kernel<112, 200, false>); break;
-      case 14: go(abia_ring_kernel<96, 248, false>); break;
-      case 15: go(abia_ring_kernel<64, 224, false>); break;
-      case 16: go(abia_ring_kernel<128, 200, false>); break;
-      case 17: go(abia_ring_kernel<112, 255, false>); break;
-      case 18: go(abia_ring_kernel<160, 255, false>); break;
-      case 19: go(abia_ring_kernel<192, 255, false>); break;
-      default: go(abia_ring_kernel<128, 255, false>); break;
-    }
-    return true;
-  }
-  const uint32_t kt = (v == 4 || v == 5) ? 224u : (v == 9 ? 96u : 128u);
+  return kt;
+}
+
+int launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, int64_t sel_B,
+                    unsigned* grid_out, cudaStream_t s) {
+  if (mv.M == 1 || mv.M != io.B) return 0;
+  if ((io.lds & 1) || (mv.ld & 1) || (scr_ld & 1)) return 0;
+  if (!aligned16(mv.f) || !aligned16(io.q) || !aligned16(io.qd) || !aligned16(io.tau) || !aligned16(scratch)) return 0;
+  if (io.B >= (1ll << 31) || (int64_t)mv.n * kRec >= (1ll << 31)) return 0;
+  const uint32_t kt = (uint32_t)abia_ring_tile(sel_B);
+  const int ctas = kt == 224 ? 1 : (kt == 96 ? 2 : 3);
   Maps maps;
-  if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return false;
-  auto go = [&](auto kernel, int stages) {
-    const size_t smem = (size_t)stages * kStageFields * kt * sizeof(double);
+  if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return 0;
+  // the ring takes the SM's shared memory
+  const size_t smem = (size_t)(220 * 1024 / ctas) / (kt * 8) * (kt * 8);
+  const uint32_t cap_rows = (uint32_t)(smem / (kt * 8));
+  const int64_t ntiles = (io.B + kt - 1) / kt;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * ctas);  // persistent CTAs
+  auto go = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kernel<<<(unsigned)((io.B + kt - 1) / kt), kt, smem, s>>>(maps, mv, io, scratch, scr_ld);
+    kernel<<<grid, (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
   };
-  switch (v) {
-    case 1: go(abia_tma_kernel<2, 3, 1, 128>, 2); break;
-    case 2: go(abia_tma_kernel<3, 2, 0, 128>, 3); break;
-    case 4: go(abia_tma_kernel<3, 1, 1, 224>, 3); break;
-    // L2-retention experiments: pass-A model loads evict_last, demoted by pass B
-    case 5: go(abia_tma_kernel<3, 1, 3, 224>, 3); break;
-    case 6: go(abia_tma_kernel<3, 1, 3, 128>, 3); break;
-    case 7: go(abia_tma_kernel<3, 2, 3, 128>, 3); break;
-    case 8: go(abia_tma_kernel<3, 1, 1, 128>, 3); break;
-    case 9: go(abia_tma_kernel<3, 1, 3, 96>, 3); break;
-    default: go(abia_tma_kernel<3, 2, 1, 128>, 3); break;
-  }
-  return true;
+  if (kt == 224)
+    go(abia_ring_kernel<224, 255>);
+  else if (kt == 96)
+    go(abia_ring_kernel<96, 248>);
+  else
+    go(abia_ring_kernel<64, 224>);
+  if (grid_out) *grid_out = grid;
+  return (int)kt;
 }
 
 }  // namespace pd

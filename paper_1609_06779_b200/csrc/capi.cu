@@ -15,7 +15,8 @@
 
 namespace pd {
 void launch_abia(const ModelView& mv, const BatchIO& io, double* scratch, cudaStream_t s);
-bool launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, cudaStream_t s);
+int launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, int64_t sel_B,
+                    unsigned* grid_out, cudaStream_t s);
 void launch_abia_cta(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s);
 size_t abia_cta_workspace_bytes(int n);
 int abia_scratch_doubles_per_link();
@@ -31,10 +32,10 @@ bool cfa_coop_path(int n, int64_t batch);
 void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
 void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count,
-                  cudaStream_t s);
+                  int64_t sel_B, cudaStream_t s);
 bool jsiia_smem_path(int n);
-bool launch_jsiia_warp(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
 bool launch_jsiia_dmma(const ModelView& mv, const double* mcl, const BatchIO& io, cudaStream_t s);
+int jsiia_warps(int n, int64_t batch, int sm_count);
 size_t jsiia_workspace_bytes(int n);
 struct IdOpts {
   double bv[6], ba[6], tip[6];
@@ -45,7 +46,8 @@ void launch_idyn(const ModelView& mv, const BatchIO& io, const IdOpts& o, const 
 bool jsiia_coop_path(int n, int64_t batch);
 void launch_workload_chains(uint64_t cell, int n, int64_t g0, int64_t count, double* d_links, cudaStream_t s);
 void launch_validate_models(const double* raw, int n, int64_t M, int32_t* status, int32_t* rule, cudaStream_t s);
-void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, cudaStream_t s);
+void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, int64_t sel_B,
+                       cudaStream_t s);
 void launch_jsi(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count, double* d_M,
                 cudaStream_t s);
 }  // namespace pd
@@ -102,6 +104,13 @@ struct pd_ctx {
   cudaEvent_t ev_entry = nullptr, ev_in[kMaxChunks] = {}, ev_out[kMaxChunks] = {};
   int64_t launches = 0;
   std::string last_error;
+  // variant selection: batch size the kernel choice is made for (0 = each
+  // call's own batch; a sharding caller sets the global batch so every shard
+  // runs the same instantiations and the results are partition independent)
+  int64_t selection_batch = 0;
+  // what the last forward-dynamics call ran (pd_last_variant / pd_last_trace)
+  std::string last_variant;
+  pd_exec_trace last_trace{};
 };
 
 namespace {
@@ -205,10 +214,13 @@ __global__ void repack_link_fastest_kernel(const double* __restrict__ in, int n,
 }
 
 // [rows][cols] (row stride ld_in) -> [cols][rows] (row stride ld_out)
+// Tiles enumerated on grid.x (column tile fastest): a batch-sized dimension
+// on grid.y would cap at 65535 tiles.
 __global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t rows, int64_t cols,
                                  int64_t ld_in, int64_t ld_out) {
   __shared__ double tile[32][33];
-  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  const int64_t ctiles = (cols + 31) / 32;
+  const int64_t c0 = ((int64_t)blockIdx.x % ctiles) * 32, r0 = ((int64_t)blockIdx.x / ctiles) * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t r = r0 + k, c = c0 + threadIdx.x;
     if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * ld_in + c];
@@ -225,9 +237,10 @@ __global__ void transpose3_kernel(const double* __restrict__ a0, const double* _
                                   const double* __restrict__ a2, double* __restrict__ b0, double* __restrict__ b1,
                                   double* __restrict__ b2, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out) {
   __shared__ double tile[32][33];
-  const double* in = blockIdx.z == 0 ? a0 : (blockIdx.z == 1 ? a1 : a2);
-  double* out = blockIdx.z == 0 ? b0 : (blockIdx.z == 1 ? b1 : b2);
-  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  const double* in = blockIdx.y == 0 ? a0 : (blockIdx.y == 1 ? a1 : a2);
+  double* out = blockIdx.y == 0 ? b0 : (blockIdx.y == 1 ? b1 : b2);
+  const int64_t ctiles = (cols + 31) / 32;
+  const int64_t c0 = ((int64_t)blockIdx.x % ctiles) * 32, r0 = ((int64_t)blockIdx.x / ctiles) * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t r = r0 + k, c = c0 + threadIdx.x;
     if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * ld_in + c];
@@ -241,14 +254,14 @@ __global__ void transpose3_kernel(const double* __restrict__ a0, const double* _
 
 void launch_transpose3(pd_ctx* ctx, const double* a0, const double* a1, const double* a2, double* b0, double* b1,
                        double* b2, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out) {
-  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), 3);
+  dim3 grid((unsigned)(((cols + 31) / 32) * ((rows + 31) / 32)), 3);
   transpose3_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(a0, a1, a2, b0, b1, b2, rows, cols, ld_in, ld_out);
   ctx->launches++;
 }
 
 void launch_transpose(pd_ctx* ctx, const double* in, double* out, int64_t rows, int64_t cols, int64_t ld_in,
                       int64_t ld_out) {
-  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  dim3 grid((unsigned)(((cols + 31) / 32) * ((rows + 31) / 32)));
   transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, out, rows, cols, ld_in, ld_out);
   ctx->launches++;
 }
@@ -291,10 +304,47 @@ cudaError_t ensure_model_cl(pd_ctx* ctx) {
   return cudaGetLastError();
 }
 
+int ceil_log2_host(int64_t n) {
+  int r = 0;
+  while ((int64_t(1) << r) < n) ++r;
+  return r;
+}
+
+// Structure of a CTA-per-chain variant's link-level stages: T threads hold
+// ceil(n / lpt) groups of lpt consecutive links; every CTA scan runs
+// ceil_log2(groups) Hillis-Steele rounds (cta_common.cuh block_exclusive) after
+// a local walk of lpt links.
+struct CtaShape {
+  int lpt, groups;
+};
+CtaShape cta_shape(int n, int nt) {
+  const int lpt = (n + nt - 1) / nt;
+  return {lpt, (n + lpt - 1) / lpt};
+}
+int cta_threads(int n) { return std::min(256, (n + 31) / 32 * 32); }
+
+void note_variant(pd_ctx* ctx, std::string name, int stages, int seq, int rounds, int oee) {
+  ctx->last_variant = std::move(name);
+  ctx->last_trace.parallel_link_stages = stages;
+  ctx->last_trace.longest_sequential_link_chain = seq;
+  ctx->last_trace.scan_rounds_max = rounds;
+  ctx->last_trace.oee_rounds = oee;
+}
+
+enum Route { ROUTE_AUTO = 0, ROUTE_LOG_DEPTH = 1 };
+
 // Problems [m0, m0 + batch) of the model set (m0 > 0: one chunk of a larger
 // host-buffer call; the caller checked the full batch against the models).
+// Kernel choice depends on (algo, n, selection batch, route) only:
+//   ROUTE_AUTO       the fastest variant for the batch;
+//   ROUTE_LOG_DEPTH  the CTA-per-chain variants whose recursions run as
+//                    log-depth scans / OEE rounds -- what a traced
+//                    single-problem call runs, so ExecTrace
+//                    describes the parallel structure the reference's
+//                    counters describe (trace.hpp:24-39).
 pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, const double* q, const double* qd,
-                     const double* tau, double* qdd, int32_t* st, int32_t* er, int32_t* ei, int64_t m0 = 0) {
+                     const double* tau, double* qdd, int32_t* st, int32_t* er, int32_t* ei, int64_t m0 = 0,
+                     int64_t sel_batch = 0, Route route = ROUTE_AUTO) {
   if (ctx->n_models <= 0 || ctx->n_links <= 0) {
     ctx->last_error = "forward dynamics: no models set (pd_set_models)";
     return PD_INVALID_ARGUMENT;
@@ -305,21 +355,24 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
   }
   if (batch == 0) return PD_OK;
   const int n = ctx->n_links;
-  if (!st || !er || !ei) {
+  const int64_t selB = sel_batch > 0 ? sel_batch : (ctx->selection_batch > 0 ? ctx->selection_batch : batch);
+  if (!st || !er || !ei) {  // internal scratch only for the slot arrays the caller did not pass
     PD_CUDA(ctx->io_status.ensure(sizeof(int32_t) * 3 * batch));
-    st = ctx->io_status.as<int32_t>();
-    er = st + batch;
-    ei = er + batch;
+    int32_t* scr = ctx->io_status.as<int32_t>();
+    st = st ? st : scr;
+    er = er ? er : scr + batch;
+    ei = ei ? ei : scr + 2 * batch;
   }
   BatchIO io{q, qd, tau, qdd, st, er, ei, batch, lds};
   ModelView mv = model_view(ctx, m0, batch);
   const size_t cl_off = ctx->n_models == 1 ? 0 : (size_t)m0 * F_COUNT * n;  // link-fastest copy offset
+  const int L = ceil_log2_host(n);
   switch (algo) {
     case PD_ABIA: {
-      // long chains in small batches: CTA per chain (parallel kinematics and
-      // bias torque, sequential articulated recursion); otherwise lane per chain
-      static const bool force_cta = std::getenv("PD_ABIA_CTA") != nullptr;
-      if (force_cta || (n >= 64 && batch <= 2 * ctx->sm_count)) {
+      // long chains in small batches (or a traced call): CTA per chain --
+      // parallel kinematics and bias torque, sequential articulated
+      // recursion; otherwise lane per chain
+      if (route == ROUTE_LOG_DEPTH || (n >= 64 && selB <= 2 * ctx->sm_count)) {
         PD_CUDA(ensure_model_cl(ctx));
         mv.fcl = ctx->model_cl.as<double>() + cl_off;
         const size_t wsb = abia_cta_workspace_bytes(n);
@@ -330,12 +383,24 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
         }
         launch_abia_cta(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream);
         ctx->launches += slots ? (batch + slots - 1) / slots : 1;
+        const CtaShape cs = cta_shape(n, cta_threads(n));
+        // stages: kinematics, 5 bias-torque maps, S0 / J0; one thread walks the
+        // articulated recursion over all n links (forward_dynamics.cpp:120-163)
+        note_variant(ctx, std::string("abia_cta_kernel<") + (slots ? "global" : "smem") + ">", 7, n,
+                     ceil_log2_host(cs.groups), 0);
         break;
       }
       const int64_t scr_ld = (batch + 31) / 32 * 32;
       PD_CUDA(ctx->abia_scratch.ensure(sizeof(double) * abia_scratch_doubles_per_link() * (size_t)n * scr_ld));
-      if (!launch_abia_tma(mv, io, ctx->abia_scratch.as<double>(), scr_ld, ctx->stream))
+      unsigned grid = 0;
+      const int kt = launch_abia_tma(mv, io, ctx->abia_scratch.as<double>(), scr_ld, selB, &grid, ctx->stream);
+      if (kt)
+        note_variant(ctx, "abia_ring_kernel<" + std::to_string(kt) + "> grid " + std::to_string(grid) + " tiles " +
+                              std::to_string((batch + kt - 1) / kt), 0, n, 0, 0);
+      else {
         launch_abia(mv, io, ctx->abia_scratch.as<double>(), ctx->stream);
+        note_variant(ctx, "abia_lane_kernel", 0, n, 0, 0);
+      }
       ctx->launches++;
       break;
     }
@@ -343,16 +408,18 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       PD_CUDA(ensure_model_cl(ctx));
       mv.fcl = ctx->model_cl.as<double>() + cl_off;
       const size_t wsb = cfa_workspace_bytes(n);
-      static const bool no_coop = std::getenv("PD_CFA_NO_COOP") != nullptr;
-      if (!no_coop && cfa_coop_path(n, batch)) {  // long chain(s): grid-wide OEE
+      const CtaShape cs = cta_shape(n, cta_threads(n));
+      if (cfa_coop_path(n, selB)) {  // long chain(s): CTA prologue + grid-wide OEE
         PD_CUDA(ctx->cta_ws.ensure(wsb * batch + 64));
         int* bad = reinterpret_cast<int*>(ctx->cta_ws.as<char>() + wsb * batch);
         launch_cfa_coop(mv, io, ctx->cta_ws.as<double>(), bad, ctx->sm_count, ctx->stream);
         ctx->launches += 2;
+        note_variant(ctx, "cfa_cta_kernel<global, prologue> + cfa_oee_coop", 9, cs.lpt > 1 ? cs.lpt : 0,
+                     ceil_log2_host(cs.groups), L);
         break;
       }
       int64_t slots = 0;
-      if (wsb > 220 * 1024) {
+      if (n > 256 && wsb > 220 * 1024) {
         slots = cta_slots(ctx, wsb, batch);
         PD_CUDA(ctx->cta_ws.ensure(wsb * slots));
         ctx->launches += (batch + slots - 1) / slots;
@@ -361,40 +428,40 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       }
       // large batches: tau_delta by a lane-per-chain pass first (sequential
       // recurrences, no CTA-wide scans); small batches keep the CTA scans
-      static const bool no_pre = std::getenv("PD_CFA_CTA_BIAS") != nullptr;
       const double* td_pre = nullptr;
-      if (!no_pre && batch >= 128 * (int64_t)ctx->sm_count) {  // >= 4 warps of chains per SM
+      if (route == ROUTE_AUTO && selB >= 128 * (int64_t)ctx->sm_count) {  // >= 4 warps of chains per SM
         PD_CUDA(ctx->cfa_td.ensure(sizeof(double) * (size_t)n * io.lds));
         launch_tau_surplus(model_view(ctx, m0, batch), io, ctx->cfa_td.as<double>(), ctx->stream);
         ctx->launches++;
         td_pre = ctx->cfa_td.as<double>();
       }
+      const char* kname = n <= 256 ? "cfa_row_kernel" : (slots ? "cfa_cta_kernel<global>" : "cfa_cta_kernel<smem>");
       launch_cfa(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream, td_pre);
+      if (td_pre)  // tau_delta walked sequentially per chain; operators, OEE and extraction per row
+        note_variant(ctx, std::string("tau_surplus_lane_kernel + ") + kname, 3, n, 0, L);
+      else
+        note_variant(ctx, kname, 9, cs.lpt > 1 ? cs.lpt : 0, ceil_log2_host(cs.groups), L);
       break;
     }
     case PD_JSIIA: {
-      static const bool force_cta = std::getenv("PD_JSIIA_CTA") != nullptr;
       PD_CUDA(ensure_model_cl(ctx));
       mv.fcl = ctx->model_cl.as<double>() + cl_off;
-      // n <= 64: warp per chain, M and its Cholesky on the FP64 tensor cores
-      // (PD_JSIIA_WARP selects the earlier register-row kernel for n <= 32)
-      static const bool use_warp = std::getenv("PD_JSIIA_WARP") != nullptr;
-      if (n <= 32 && use_warp && !force_cta) {
-        launch_jsiia_warp(mv, mv.fcl, io, ctx->stream);
-        ctx->launches++;
-        break;
-      }
-      if (n <= 64 && !force_cta) {
+      if (n <= 64 && route == ROUTE_AUTO) {  // warp per chain, M and its Cholesky on the FP64 tensor cores
         launch_jsiia_dmma(mv, mv.fcl, io, ctx->stream);
         ctx->launches++;
+        const int lpl = (n + 31) / 32;  // links per lane; warp-shuffle scans of 5 rounds
+        note_variant(ctx, "jsiia_dmma_kernel", 5, lpl > 1 ? lpl : 0, 5, 0);
         break;
       }
       const size_t wsb = jsiia_workspace_bytes(n);
-      static const bool no_coop = std::getenv("PD_JSIIA_NO_COOP") != nullptr;
-      if (!no_coop && jsiia_coop_path(n, batch)) {  // long chain(s): grid-wide Cholesky
+      const int nt = 32 * jsiia_warps(n, selB, ctx->sm_count);
+      const CtaShape cs = cta_shape(n, nt);
+      if (jsiia_coop_path(n, selB)) {  // long chain(s): grid-wide Cholesky
         PD_CUDA(ctx->cta_ws.ensure(wsb * batch));
-        launch_jsiia_coop(mv, io, ctx->cta_ws.as<double>(), ctx->sm_count, ctx->stream);
+        launch_jsiia_coop(mv, io, ctx->cta_ws.as<double>(), ctx->sm_count, selB, ctx->stream);
         ctx->launches += 3;
+        note_variant(ctx, "jsiia_tiled_kernel<global, prologue> + jsiia_factor_coop + jsiia_solve_wide", 6,
+                     cs.lpt > 1 ? cs.lpt : 0, ceil_log2_host(cs.groups), 0);
         break;
       }
       int64_t slots = 0;
@@ -405,7 +472,9 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       } else {
         ctx->launches++;
       }
-      launch_jsiia(mv, io, ctx->cta_ws.as<double>(), slots, ctx->sm_count, ctx->stream);
+      launch_jsiia(mv, io, ctx->cta_ws.as<double>(), slots, ctx->sm_count, selB, ctx->stream);
+      note_variant(ctx, std::string("jsiia_tiled_kernel<") + (slots ? "global" : "smem") + ">", 6,
+                   cs.lpt > 1 ? cs.lpt : 0, ceil_log2_host(cs.groups), 0);
       break;
     }
     default:
@@ -636,9 +705,19 @@ pd_status pd_forward_dynamics_device(pd_ctx* ctx, pd_algo algo, int64_t batch, c
                     d_slot_index);
 }
 
-pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
-                              const double* tau, double* qddot, int32_t* slot_status, int32_t* slot_round,
-                              int32_t* slot_index) {
+}  // extern "C"
+
+namespace {
+
+// Host buffers [problem][link] in and out through a chunked pipeline: the
+// copy-in stream streams chunk c+1 over PCIe while the compute stream
+// transposes and solves chunk c and the copy-out stream returns chunk c-1.
+// Chunks are 32-aligned (TMA bases stay 16-byte aligned); every chunk selects
+// its kernels for the whole batch, so the results are those of the device
+// path on the same problems.
+pd_status host_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
+                                const double* tau, double* qddot, int32_t* slot_status, int32_t* slot_round,
+                                int32_t* slot_index, Route route) {
   if (!ctx) return PD_INVALID_ARGUMENT;
   if (batch < 0 || (batch > 0 && (!q || !qdot || !tau || !qddot))) {
     ctx->last_error = "forward dynamics: null buffer";
@@ -677,60 +756,37 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   double* stau = ctx->io_tau.as<double>();
   double* sqdd = ctx->io_qdd.as<double>();
   int32_t* st = ctx->io_status.as<int32_t>();
-  // Chunked pipeline: the copy-in stream streams chunk c+1 over PCIe while the
-  // compute stream transposes and solves chunk c and the copy-out stream
-  // returns chunk c-1. Chunks are 32-aligned (TMA bases stay 16-byte aligned).
-  static const int chunk_env = std::getenv("PD_E2E_CHUNKS") ? std::atoi(std::getenv("PD_E2E_CHUNKS")) : 0;
   // ~8K problems per chunk, at most 8 chunks: smaller chunks add per-chunk
   // launch / event overhead faster than they shorten the pipeline's tail
   // (tools/e2e_probe.py: c2 1.50 ms at 16 chunks, 1.35 ms at 8)
-  const int nch = (int)std::min<int64_t>(chunk_env > 0 ? pd_ctx::kMaxChunks : 8,
-                                         chunk_env > 0 ? chunk_env : std::max<int64_t>(1, batch / 8192));
+  const int nch = (int)std::min<int64_t>(8, std::max<int64_t>(1, batch / 8192));
   const int64_t csz = ((batch + nch - 1) / nch + 31) / 32 * 32;
-  // PD_E2E_TRACE=1: timing events per stage, timeline printed to stderr
-  // (tools/e2e_trace.py; profiles/e2e_timeline_r1_s3.txt)
-  static const bool trace = std::getenv("PD_E2E_TRACE") != nullptr;
-  static cudaEvent_t tev[4 * pd_ctx::kMaxChunks + 2];
-  if (trace && !tev[0])
-    for (auto& e : tev) PD_CUDA(cudaEventCreate(&e));
-  auto mark = [&](int k, cudaStream_t s) {
-    if (trace) cudaEventRecord(tev[k], s);
-  };
-  mark(0, ctx->stream);
+  const int64_t selB = ctx->selection_batch > 0 ? ctx->selection_batch : batch;
   PD_CUDA(cudaEventRecord(ctx->ev_entry, ctx->stream));  // earlier work on the staging buffers
   PD_CUDA(cudaStreamWaitEvent(ctx->cp_in, ctx->ev_entry, 0));
   PD_CUDA(cudaStreamWaitEvent(ctx->cp_out, ctx->ev_entry, 0));
+  std::string variant;
   for (int c = 0; c < nch; ++c) {
     const int64_t b0 = c * csz, nb = std::min<int64_t>(csz, batch - b0);
     if (nb <= 0) break;
     const size_t off = (size_t)b0 * n, bytes = sizeof(double) * (size_t)n * nb;
-    mark(2 + 4 * c, ctx->cp_in);
     PD_CUDA(cudaMemcpyAsync(sq + half + off, q + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
     PD_CUDA(cudaMemcpyAsync(sqd + half + off, qdot + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
     PD_CUDA(cudaMemcpyAsync(stau + half + off, tau + off, bytes, cudaMemcpyHostToDevice, ctx->cp_in));
-    mark(3 + 4 * c, ctx->cp_in);
     PD_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->cp_in));
     PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[c], 0));
     launch_transpose3(ctx, sq + half + off, sqd + half + off, stau + half + off, sq + b0, sqd + b0, stau + b0, nb, n,
                       n, lds);
     pd_status s = run_device(ctx, algo, nb, lds, sq + b0, sqd + b0, stau + b0, sqdd + b0, st + b0, st + batch + b0,
-                             st + 2 * batch + b0, b0);
+                             st + 2 * batch + b0, b0, selB, route);
     if (s != PD_OK) return s;
+    if (c == 0) variant = ctx->last_variant;
     launch_transpose(ctx, sqdd + b0, sqdd + half + off, n, nb, lds, n);
-    mark(4 + 4 * c, ctx->stream);
     PD_CUDA(cudaEventRecord(ctx->ev_out[c], ctx->stream));
     PD_CUDA(cudaStreamWaitEvent(ctx->cp_out, ctx->ev_out[c], 0));
     PD_CUDA(cudaMemcpyAsync(qddot + off, sqdd + half + off, bytes, cudaMemcpyDeviceToHost, ctx->cp_out));
-    mark(5 + 4 * c, ctx->cp_out);
   }
-  if (trace) {
-    PD_CUDA(cudaDeviceSynchronize());
-    float t[4];
-    for (int c = 0; c < nch && c * csz < batch; ++c) {
-      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], tev[0], tev[2 + 4 * c + k]);
-      std::fprintf(stderr, "chunk %2d: in %.3f-%.3f  compute done %.3f  out done %.3f ms\n", c, t[0], t[1], t[2], t[3]);
-    }
-  }
+  if (nch > 1) ctx->last_variant = variant + " x " + std::to_string(nch) + " chunks";
   const bool want_status = slot_status || slot_round || slot_index;
   if (!want_status) {
     PD_CUDA(cudaStreamSynchronize(ctx->cp_out));
@@ -770,6 +826,42 @@ pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const do
   if (slot_index) std::memcpy(slot_index, hs + 2 * batch, sizeof(int32_t) * batch);
   return PD_OK;
 }
+
+}  // namespace
+
+extern "C" {
+
+pd_status pd_forward_dynamics(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
+                              const double* tau, double* qddot, int32_t* slot_status, int32_t* slot_round,
+                              int32_t* slot_index) {
+  return host_forward_dynamics(ctx, algo, batch, q, qdot, tau, qddot, slot_status, slot_round, slot_index,
+                               ROUTE_AUTO);
+}
+
+pd_status pd_forward_dynamics_traced(pd_ctx* ctx, pd_algo algo, int64_t batch, const double* q, const double* qdot,
+                                     const double* tau, double* qddot, int32_t* slot_status, int32_t* slot_round,
+                                     int32_t* slot_index, pd_exec_trace* trace) {
+  pd_status s = host_forward_dynamics(ctx, algo, batch, q, qdot, tau, qddot, slot_status, slot_round, slot_index,
+                                      ROUTE_LOG_DEPTH);
+  if (s == PD_OK && trace && batch > 0) *trace = ctx->last_trace;
+  return s;
+}
+
+const char* pd_last_variant(const pd_ctx* ctx) { return ctx ? ctx->last_variant.c_str() : ""; }
+
+pd_status pd_last_trace(const pd_ctx* ctx, pd_exec_trace* trace) {
+  if (!ctx || !trace) return PD_INVALID_ARGUMENT;
+  *trace = ctx->last_trace;
+  return PD_OK;
+}
+
+pd_status pd_set_selection_batch(pd_ctx* ctx, int64_t batch) {
+  if (!ctx || batch < 0) return PD_INVALID_ARGUMENT;
+  ctx->selection_batch = batch;
+  return PD_OK;
+}
+
+}  // extern "C"
 
 namespace {
 
@@ -865,6 +957,8 @@ pd_status run_idyn_host(pd_ctx* ctx, int64_t batch, const double* q, const doubl
 }
 
 }  // namespace
+
+extern "C" {
 
 pd_status pd_inverse_dynamics(pd_ctx* ctx, int64_t batch, const double* q, const double* qdot, const double* qddot,
                               double* tau) {

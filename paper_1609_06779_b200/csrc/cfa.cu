@@ -1030,123 +1030,11 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
 }
 
 
-// ---------------------------------------------------------------------------
-// The paper's building block 2 on its own: batched symmetric block
-// tri-diagonal solves by odd-even elimination with 5x5 blocks
-// (oee_solve<5,1>, include/pardyn/oee.hpp:149-189 -- the system CFA reduces
-// to). A CTA per system, a thread per block row with its D, U, R in
-// registers, the same Cholesky-form rounds and error rule as the CFA kernels.
-// diag [n][25] row-major symmetric, upper [n-1][25] (coupling of row k to
-// k+1; the sub-diagonal block is its transpose), rhs [n][5] -> x [n][5].
-__global__ void __launch_bounds__(256) oee5_kernel(const double* __restrict__ diag, const double* __restrict__ upper,
-                                                   const double* __restrict__ rhs, double* __restrict__ x, int n,
-                                                   int32_t* __restrict__ status, int32_t* __restrict__ eround,
-                                                   int32_t* __restrict__ eindex) {
-  extern __shared__ double dyn_smem[];
-  __shared__ int s_bad;
-  double* ws = dyn_smem;  // published fields, cfr layout (PL, SG, PY, PR, PI)
-  const int64_t p = blockIdx.x;
-  const int i = threadIdx.x;
-  const bool own = i < n;
-  const double* Dg = diag + (size_t)p * n * 25;
-  const double* Ug = upper + (size_t)p * (n > 0 ? n - 1 : 0) * 25;
-  const double* Rg = rhs + (size_t)p * n * 5;
-  if (i == 0) s_bad = n;
-  double D[15], U[25], R[5];
-  if (own) {
-#pragma unroll
-    for (int r = 0; r < 5; ++r)
-#pragma unroll
-      for (int c = 0; c <= r; ++c) D[pk(r, c)] = __ldg(Dg + (size_t)i * 25 + r * 5 + c);
-#pragma unroll
-    for (int k = 0; k < 25; ++k) U[k] = (i + 1 < n) ? __ldg(Ug + (size_t)i * 25 + k) : 0.0;
-#pragma unroll
-    for (int r = 0; r < 5; ++r) R[r] = __ldg(Rg + (size_t)i * 5 + r);
-  }
-  __syncthreads();
-  const int rounds = ceil_log2_dev(n);
-  int h = 1;
-  for (int round = 1; round <= rounds; ++round, h <<= 1) {
-    if (own) {
-      double Lk[10], il[5], rt[5];
-      const bool ok = chol5(D, Lk, il);
-      ws_store<10>(ws, n, cfr::PL, i, Lk);
-      ws_store<5>(ws, n, cfr::PI, i, il);
-      ws[cfr::SG * n + i] = ok ? 0.0 : 1.0;
-#pragma unroll
-      for (int r = 0; r < 5; ++r) rt[r] = R[r];
-      lsolve5(Lk, il, rt);
-      ws_store<5>(ws, n, cfr::PR, i, rt);
-      if (i < n - h) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          double col[5];
-#pragma unroll
-          for (int r = 0; r < 5; ++r) col[r] = U[r * 5 + c];
-          lsolve5(Lk, il, col);
-#pragma unroll
-          for (int r = 0; r < 5; ++r) ws[(cfr::PY + r * 5 + c) * n + i] = col[r];
-        }
-      }
-    }
-    __syncthreads();
-    if (own) {
-      const bool up_bad = (i < n - h) && ws[cfr::SG * n + i + h] != 0.0;
-      const bool dn_bad = (i >= h) && ws[cfr::SG * n + i - h] != 0.0;
-      if (up_bad || dn_bad) atomicMin(&s_bad, i);
-      if (i < n - h) {
-        const int k = i + h;
-        double Lk[10], il[5], rt[5];
-        ws_load<10>(ws, n, cfr::PL, k, Lk);
-        ws_load<5>(ws, n, cfr::PI, k, il);
-        ws_load<5>(ws, n, cfr::PR, k, rt);
-        oee_up(D, R, U, Lk, il, rt, i < n - 2 * h, [&](int r, int c) { return ws[(cfr::PY + r * 5 + c) * n + k]; });
-      }
-      if (i >= h) {
-        const int k = i - h;
-        double rt[5];
-        ws_load<5>(ws, n, cfr::PR, k, rt);
-        oee_down(D, R, rt, [&](int r, int c) { return ws[(cfr::PY + r * 5 + c) * n + k]; });
-      }
-    }
-    __syncthreads();
-    if (s_bad < n) {
-      if (i == 0) {
-        const int ib = s_bad;
-        const bool up_bad = (ib < n - h) && ws[cfr::SG * n + ib + h] != 0.0;
-        status[p] = PD_SLOT_OEE_SINGULAR_PIVOT;
-        eround[p] = round;
-        eindex[p] = up_bad ? ib + h : ib - h;
-      }
-      return;
-    }
-  }
-  if (own) {
-    if (!oee_final(D, R)) atomicMin(&s_bad, i);
-#pragma unroll
-    for (int r = 0; r < 5; ++r) x[((size_t)p * n + i) * 5 + r] = R[r];
-  }
-  __syncthreads();
-  if (i == 0) {
-    status[p] = s_bad < n ? PD_SLOT_OEE_SINGULAR_FINAL : PD_SLOT_OK;
-    eround[p] = s_bad < n ? rounds : 0;
-    eindex[p] = s_bad < n ? s_bad : 0;
-  }
-}
-
-bool launch_oee5(const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
-                 int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s) {
-  if (n < 1 || n > 256) return false;
-  const size_t bytes = (size_t)cfr::FIELDS * n * sizeof(double);
-  cudaFuncSetAttribute(oee5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  oee5_kernel<<<(unsigned)batch, ((n + 31) / 32) * 32, bytes, s>>>(diag, upper, rhs, x, n, status, eround, eindex);
-  return true;
-}
-
 size_t cfa_workspace_bytes(int n) { return (size_t)cfa::FIELDS * n * sizeof(double); }
 
-// Shared-memory workspace when it fits (n <= 260), otherwise one global slot
-// per CTA in flight, launched in waves of gws_slots CTAs.
+// Shared-memory workspace when the caller passes no global slots (n <= 256
+// rows with the compact row kernel, the full workspace up to 220 KB), otherwise
+// one global slot per CTA in flight, launched in waves of gws_slots CTAs.
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
                 const double* td_pre) {
   const int n = mv.n;
@@ -1154,8 +1042,7 @@ void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws
   if (nt > 256) nt = 256;
   const int lpt = (n + nt - 1) / nt;
   const size_t ws_bytes = cfa_workspace_bytes(n);
-  static const bool old_kernel = std::getenv("PD_CFA_CTA_KERNEL") != nullptr;
-  if (n <= 256 && !old_kernel) {  // thread per row, compact workspace, register cap per size class
+  if (n <= 256) {  // thread per row, compact workspace, register cap per size class
     const size_t rb = (size_t)cfr::FIELDS * n * sizeof(double);
     auto go = [&](auto kernel) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
@@ -1169,7 +1056,7 @@ void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws
       go(cfa_row_kernel<128, 2>);
     else
       go(cfa_row_kernel<256, 1>);
-  } else if (ws_bytes <= 224 * 1024) {
+  } else if (gws_slots == 0) {
     cudaFuncSetAttribute(cfa_cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
     cfa_cta_kernel<true><<<(unsigned)io.B, nt, ws_bytes, s>>>(mv, io, nullptr, lpt, 0, td_pre);
   } else {

@@ -105,15 +105,22 @@ __device__ __forceinline__ Arr<K> shfl_idx(const Arr<K>& x, int src) {
 }
 
 // Exclusive scan of one element per thread across the CTA (thread order, or
-// reversed thread order for REVERSE). Returns the combination of all earlier
-// threads' elements (identity for the first). Contains two __syncthreads.
+// reversed thread order for REVERSE) over the first `nact` threads (the ones
+// holding links; the rest hold identity and get unspecified results). Returns
+// the combination of all earlier threads' elements (identity for the first).
+// Runs only the combine rounds that can combine data: ceil_log2(min(32, nact))
+// shuffle rounds plus ceil_log2(ceil(nact / 32)) cross-warp rounds, i.e.
+// exactly ceil_log2(nact) Hillis-Steele rounds like scan.hpp:46-61 (the
+// rounds ExecTrace reports, cta_scan_rounds). Contains three __syncthreads
+// unless one warp holds every link (then none).
 template <int K, bool REVERSE, class Op>
-__device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+__device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm, int nact) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int span = nact < 32 ? nact : 32;    // lanes of a warp that can hold data
+  const int nwa = (nact + 31) >> 5;          // warps holding data
   // warp inclusive scan in (reversed) lane order
   Arr<K> inc = x;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
+  for (int d = 1; d < span; d <<= 1) {
     const Arr<K> y = REVERSE ? shfl_down(inc, d) : shfl_up(inc, d);
     const bool take = REVERSE ? (lane + d < 32) : (lane >= d);
     if (take) inc = op(y, inc);
@@ -121,8 +128,9 @@ __device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm) {
   Arr<K> exc = REVERSE ? shfl_down(inc, 1) : shfl_up(inc, 1);
   const bool first_in_warp = REVERSE ? (lane == 31) : (lane == 0);
   if (first_in_warp) exc = op.template identity<K>();
+  if (nwa == 1) return exc;  // one warp holds every link: no cross-warp level
   const int last_lane = REVERSE ? 0 : 31;
-  if (lane == last_lane) {
+  if (lane == last_lane && warp < nwa) {
 #pragma unroll
     for (int k = 0; k < K; ++k) sm.tot[warp][k] = inc.v[k];
   }
@@ -130,18 +138,17 @@ __device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm) {
   if (warp == 0) {
     // scan of warp totals in (reversed) warp order; lane w holds warp w
     Arr<K> t;
-    const bool valid = lane < nw;
+    const bool valid = lane < nwa;
 #pragma unroll
     for (int k = 0; k < K; ++k) t.v[k] = valid ? sm.tot[lane][k] : op.template identity<K>().v[k];
     Arr<K> ti = t;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
+    for (int d = 1; d < nwa; d <<= 1) {
       const Arr<K> y = REVERSE ? shfl_down(ti, d) : shfl_up(ti, d);
-      const bool take = REVERSE ? (lane + d < nw) : (lane >= d);
+      const bool take = REVERSE ? (lane + d < nwa) : (lane >= d);
       if (take && valid) ti = op(y, ti);
     }
     Arr<K> te = REVERSE ? shfl_down(ti, 1) : shfl_up(ti, 1);
-    const bool first_w = REVERSE ? (lane == nw - 1) : (lane == 0);
+    const bool first_w = REVERSE ? (lane == nwa - 1) : (lane == 0);
     if (first_w) te = op.template identity<K>();
     __syncwarp();
     if (valid) {
@@ -150,11 +157,20 @@ __device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm) {
     }
   }
   __syncthreads();
-  Arr<K> wp;
+  Arr<K> wp = op.template identity<K>();
+  if (warp < nwa) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) wp.v[k] = sm.tot[warp][k];
+    for (int k = 0; k < K; ++k) wp.v[k] = sm.tot[warp][k];
+  }
   __syncthreads();  // sm reusable by the next scan
   return op(wp, exc);
+}
+
+// Hillis-Steele rounds one block_exclusive over `nact` threads runs.
+__host__ __device__ inline int cta_scan_rounds(int nact) {
+  int r = 0;
+  while ((1 << r) < nact) ++r;
+  return r;
 }
 
 // Inclusive scan over the chain's links of a K-field array stored in the
@@ -174,7 +190,7 @@ __device__ void ws_scan(double* ws, int n, int f0, int lpt, Op op, ScanSmem& sm)
 #pragma unroll
     for (int k = 0; k < K; ++k) ws[(f0 + k) * n + i] = agg.v[k];
   }
-  const Arr<K> pre = block_exclusive<K, REVERSE>(agg, op, sm);
+  const Arr<K> pre = block_exclusive<K, REVERSE>(agg, op, sm, (n + lpt - 1) / lpt);
   for (int i = i0; i < i1; ++i) {
     Arr<K> x;
 #pragma unroll

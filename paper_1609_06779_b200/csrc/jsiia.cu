@@ -429,9 +429,9 @@ int jsiia_warps(int n, int64_t batch, int sm_count) {
 bool jsiia_smem_path(int n) { return jsiia_workspace_bytes(n) <= 200 * 1024; }
 
 void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, int sm_count,
-                  cudaStream_t s) {
+                  int64_t sel_B, cudaStream_t s) {
   const int n = mv.n;
-  const int nt = 32 * jsiia_warps(n, io.B, sm_count);
+  const int nt = 32 * jsiia_warps(n, sel_B, sm_count);
   const size_t ws_bytes = jsiia_workspace_bytes(n);
   if (jsiia_smem_path(n)) {
     cudaFuncSetAttribute(jsiia_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
@@ -757,9 +757,10 @@ __global__ void __launch_bounds__(32 * kWideWarps) jsiia_solve_wide(BatchIO io, 
 // factorization, solve (MODE 3). Workspace slots 0..B-1 of gws.
 bool jsiia_coop_path(int n, int64_t batch) { return !jsiia_smem_path(n) && batch <= 4; }
 
-void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, cudaStream_t s) {
+void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, int64_t sel_B,
+                       cudaStream_t s) {
   const int n = mv.n;
-  const int nt = 32 * jsiia_warps(n, io.B, sm_count);
+  const int nt = 32 * jsiia_warps(n, sel_B, sm_count);
   jsiia_tiled_kernel<false, 2><<<(unsigned)io.B, nt, 0, s>>>(mv, io, gws, 0);
   int count = (int)io.B;
   void* args[] = {&gws, (void*)&n, &count};

@@ -125,14 +125,19 @@ def test_errors(oracle):
     chain = pd.RobotChain.from_records(links)
     with pytest.raises(pd.InvalidArgument, match="qdot has length 2 but the chain has 3 joints"):
         pd.inverse_dynamics(chain, np.zeros(3), np.zeros(2), np.zeros(3))
-    with pytest.raises(pd.InvalidArgument, match="joint_space_inertia: q must have one entry per joint"):
+    with pytest.raises(pd.InvalidArgument, match="assemble_kinematics: q has length 4 but the chain has 3 joints"):
         pd.joint_space_inertia(chain, np.zeros(4))
+    with pytest.raises(pd.InvalidArgument, match="assemble_kinematics: q has length 2 but the chain has 3 joints"):
+        pd.inverse_dynamics(chain, np.zeros(2), np.zeros(2), np.zeros(2))
     bad = links.copy()
     bad[1, 0] = -1.0  # mass
     with pytest.raises(pd.InvalidArgument, match="mass must be positive"):
         pd.inverse_dynamics(pd.RobotChain.from_records(bad), np.zeros(3), np.zeros(3), np.zeros(3))
     with pytest.raises(pd.InvalidArgument, match="mass must be positive"):
         pd.joint_space_inertia(pd.RobotChain.from_records(bad), np.zeros(3))
+    # the reference validates the link inertias before the rate lengths (model.cpp:148-155 first)
+    with pytest.raises(pd.InvalidArgument, match="mass must be positive"):
+        pd.inverse_dynamics(pd.RobotChain.from_records(bad), np.zeros(3), np.zeros(2), np.zeros(3))
 
 
 @pytest.mark.parametrize("n,count,g0", [(8, 3000, 0), (64, 1500, 123456), (1, 5, 7)])

@@ -43,6 +43,45 @@ def test_oee5_matches_oracle(oracle, gpu_ctx, n):
         assert np.linalg.norm(full @ x[b].ravel() - rhs[b].ravel()) <= 1e-10 * np.linalg.norm(rhs[b])
 
 
+@pytest.mark.parametrize("kind", ["negative_definite", "indefinite"])
+@pytest.mark.parametrize("n", [1, 2, 9, 64])
+def test_oee5_non_spd_pivots(oracle, gpu_ctx, kind, n):
+    """Invertible but not positive definite pivots: the reference's
+    coefficient_solve uses FullPivLU (oee.hpp:40-51), not a Cholesky, so
+    these systems solve (oee.hpp notes intermediate pivots are symmetric but
+    not guaranteed positive definite)."""
+    rng = np.random.default_rng(100 + n)
+    B = 3
+    diag = np.empty((B, n, 5, 5))
+    for b in range(B):
+        for k in range(n):
+            if kind == "negative_definite":
+                a = rng.uniform(-1, 1, (5, 5))
+                diag[b, k] = -(a @ a.T + 6.0 * np.eye(5))
+            else:
+                q, _ = np.linalg.qr(rng.uniform(-1, 1, (5, 5)))
+                diag[b, k] = q @ np.diag([7.0, -6.5, 8.0, -7.5, 6.0]) @ q.T
+    upper = rng.uniform(-1, 1, (B, max(n - 1, 0), 5, 5))
+    rhs = rng.uniform(-5, 5, (B, n, 5))
+    x, st, rd, ix = gpu_ctx.block_tridiag_solve5(diag, upper, rhs)
+    assert (st == 0).all(), (st, rd, ix)
+    for b in range(B):
+        want, _ = oracle.tridiag_solve(diag[b], upper[b] if n > 1 else np.zeros((1, 5, 5)), rhs[b])
+        want = want.reshape(n, 5)
+        assert np.linalg.norm(x[b] - want) / max(1.0, np.linalg.norm(want)) <= 1e-11
+
+
+def test_oee5_diag_minus_identity(oracle, gpu_ctx):
+    """The advisor's case: diag = -I, upper = 0 (invertible, negative definite)."""
+    n = 4
+    diag = np.stack([-np.eye(5)] * n)[None]
+    upper = np.zeros((1, n - 1, 5, 5))
+    rhs = np.arange(n * 5, dtype=float).reshape(1, n, 5)
+    x, st, _, _ = gpu_ctx.block_tridiag_solve5(diag, upper, rhs)
+    assert st[0] == 0
+    assert np.array_equal(x[0], -rhs[0])
+
+
 @pytest.mark.parametrize("case", ["pivot_row1", "pivot_row0", "final"])
 def test_oee5_singular_reports_like_the_reference(oracle, gpu_ctx, case):
     n = 3

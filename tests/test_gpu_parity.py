@@ -174,15 +174,17 @@ def test_jsiia_tiled_paths(oracle, gpu_ctx, n, B):
 @pytest.mark.parametrize("shared", [False, True])
 def test_host_path_chunked_pipeline(oracle, gpu_ctx, algo, shared):
     """Host buffers large enough for the chunked copy-in / solve / copy-out
-    pipeline (several chunks, a ragged last chunk): every slot matches the
-    oracle, so chunk offsets of states, models and status are right."""
-    n, B = 6, 3 * 4096 + 77
+    pipeline (3 chunks of ~8K problems, a ragged last chunk): every slot
+    matches the oracle, so chunk offsets of states, models and status are
+    right."""
+    n, B = 6, 3 * 8192 + 77
     cell = oracle.workload_seed(7, n, B)
     links = oracle.workload_chains(cell, n, 1 if shared else B)
     q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
     ms, _ = gpu_ctx.set_models(links, None)
     assert (ms == 0).all()
     qdd, st, _, _ = gpu_ctx.solve(algo, q, qd, tau)
+    assert gpu_ctx.last_variant().endswith("x 3 chunks"), gpu_ctx.last_variant()
     assert (st == 0).all()
     ref, ost = oracle.batch_forward_dynamics(ONAME[algo], links, [0, 0, -9.81], q, qd, tau)
     assert (ost == 0).all()
