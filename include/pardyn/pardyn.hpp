@@ -4,9 +4,9 @@
 // (/root/reference/proj/core/include/pardyn/{types,model,trace,
 // forward_dynamics,inverse_dynamics}.hpp) with the same names, argument
 // meaning and error behaviour; every solve runs on the GPU. Eigen is not a
-// dependency: JointVector / Vec3 / Mat3 / Vec6 are small value types with the
-// subset of Eigen's interface the reference API and its callers use
-// (size(), operator[], operator(), data(), Zero(), norm()).
+// dependency: JointVector / Vec3 / Mat3 / Vec6 / Mat6 / MatrixXd are small
+// value types (include/pardyn/linalg.hpp) with the subset of Eigen's
+// interface the reference API and its callers use.
 //
 //   FdAlgo                         forward_dynamics.hpp:29
 //   forward_dynamics(...)          forward_dynamics.hpp:103-105
@@ -19,6 +19,12 @@
 //   joint_space_inertia            forward_dynamics.hpp:34-35 (MatrixXd stand-in)
 //   solve_lower_bidiag / solve_upper_bidiag / oee_solve   scan.hpp:100-168, oee.hpp:149-189
 //   LinkSpec / RobotChain          model.hpp:17-30
+//   SE3Transform / AdjointMap / SpatialInertia, skew, small_adjoint,
+//   adjoint_of, screw_exp, spatial_inertia_from   spatial.hpp:75-150
+//   ChainKinematics / assemble_kinematics / link_inertias   model.hpp:37-61
+//   ArticulatedBodyInertias / articulated_body_inertias   forward_dynamics.hpp:44-56
+//   ConstraintBasis / build_constraint_basis      forward_dynamics.hpp:64-71
+//   CfaOperators (+ apply_*) / build_cfa_operators   forward_dynamics.hpp:73-96
 //   random_chain                   model.hpp:66-70
 //   validate_chain / load_chain / save_chain   model.hpp:56-82 (JSON model files)
 //   ExecTrace                      trace.hpp:24-39
@@ -34,72 +40,98 @@
 #include <string>
 #include <vector>
 
+#include "linalg.hpp"
+
 namespace pardyn {
 
-// ----------------------------------------------------------------- types
-class JointVector {
- public:
-  JointVector() = default;
-  explicit JointVector(std::size_t n) : v_(n, 0.0) {}
-  JointVector(std::initializer_list<double> l) : v_(l) {}
-  static JointVector Zero(std::size_t n) { return JointVector(n); }
-  std::size_t size() const { return v_.size(); }
-  double& operator[](std::size_t i) { return v_[i]; }
-  double operator[](std::size_t i) const { return v_[i]; }
-  double& operator()(std::size_t i) { return v_[i]; }
-  double operator()(std::size_t i) const { return v_[i]; }
-  double* data() { return v_.data(); }
-  const double* data() const { return v_.data(); }
-  double norm() const {
-    double s = 0.0;
-    for (double x : v_) s += x * x;
-    return std::sqrt(s);
-  }
-  JointVector operator-(const JointVector& o) const {
-    JointVector r(size());
-    for (std::size_t i = 0; i < size(); ++i) r[i] = v_[i] - o[i];
-    return r;
-  }
-  bool operator==(const JointVector& o) const { return v_ == o.v_; }
-
- private:
-  std::vector<double> v_;
-};
-
-using Vec3 = std::array<double, 3>;
-using Vec6 = std::array<double, 6>;
-using Mat3 = std::array<double, 9>;  // row-major
-
-// Spatial vectors (spatial.hpp:15-60).
+// ----------------------------------------------------------------- spatial types (spatial.hpp)
+// Rigid-body velocity (angular, linear) (spatial.hpp:15-33).
 struct Twist {
-  Vec3 angular{0.0, 0.0, 0.0};
-  Vec3 linear{0.0, 0.0, 0.0};
-  Vec6 stacked() const { return {angular[0], angular[1], angular[2], linear[0], linear[1], linear[2]}; }
-  static Twist from_stacked(const Vec6& v) { return {{v[0], v[1], v[2]}, {v[3], v[4], v[5]}}; }
+  Vec3 angular = Vec3::Zero();
+  Vec3 linear = Vec3::Zero();
+  Twist() = default;
+  Twist(const Vec3& ang, const Vec3& lin) : angular(ang), linear(lin) {}
+  static Twist from_stacked(const Vec6& v) { return {v.head<3>(), v.tail<3>()}; }
+  Vec6 stacked() const {
+    Vec6 v;
+    for (int k = 0; k < 3; ++k) {
+      v(k) = angular(k);
+      v(3 + k) = linear(k);
+    }
+    return v;
+  }
+  bool is_finite() const { return angular.allFinite() && linear.allFinite(); }
 };
+inline Twist operator+(const Twist& a, const Twist& b) { return {a.angular + b.angular, a.linear + b.linear}; }
+inline Twist operator-(const Twist& a, const Twist& b) { return {a.angular - b.angular, a.linear - b.linear}; }
+inline Twist operator*(double s, const Twist& a) { return {s * a.angular, s * a.linear}; }
+
+// Generalised force (moment, force) (spatial.hpp:44-69).
 struct Wrench {
-  Vec3 moment{0.0, 0.0, 0.0};
-  Vec3 force{0.0, 0.0, 0.0};
-  Vec6 stacked() const { return {moment[0], moment[1], moment[2], force[0], force[1], force[2]}; }
-  static Wrench from_stacked(const Vec6& v) { return {{v[0], v[1], v[2]}, {v[3], v[4], v[5]}}; }
+  Vec3 moment = Vec3::Zero();
+  Vec3 force = Vec3::Zero();
+  Wrench() = default;
+  Wrench(const Vec3& m, const Vec3& f) : moment(m), force(f) {}
+  static Wrench from_stacked(const Vec6& v) { return {v.head<3>(), v.tail<3>()}; }
+  Vec6 stacked() const {
+    Vec6 v;
+    for (int k = 0; k < 3; ++k) {
+      v(k) = moment(k);
+      v(3 + k) = force(k);
+    }
+    return v;
+  }
+  bool is_finite() const { return moment.allFinite() && force.allFinite(); }
+};
+inline Wrench operator+(const Wrench& a, const Wrench& b) { return {a.moment + b.moment, a.force + b.force}; }
+inline Wrench operator-(const Wrench& a, const Wrench& b) { return {a.moment - b.moment, a.force - b.force}; }
+inline Wrench operator*(double s, const Wrench& a) { return {s * a.moment, s * a.force}; }
+
+// x_target = rotation * x_source + translation (spatial.hpp:75-97).
+struct SE3Transform {
+  Mat3 rotation = Mat3::Identity();
+  Vec3 translation = Vec3::Zero();
+  SE3Transform operator*(const SE3Transform& rhs) const {
+    return {rotation * rhs.rotation, rotation * rhs.translation + translation};
+  }
+  SE3Transform inverse() const {
+    const Mat3 rt = rotation.transpose();
+    return {rt, -(rt * translation)};
+  }
+  Vec3 apply(const Vec3& point) const { return rotation * point + translation; }
+  // Rotation orthonormal with determinant +1, translation finite.
+  bool is_valid(double tol = 1e-9) const;
 };
 
-// Dense row-major matrix (the Eigen::MatrixXd that joint_space_inertia returns).
-class MatrixXd {
+// Frame change of twists (apply) and wrenches (transpose_apply) (spatial.hpp:99-109).
+struct AdjointMap {
+  Mat6 mat = Mat6::Identity();
+  Twist apply(const Twist& v) const { return Twist::from_stacked(mat * v.stacked()); }
+  Wrench transpose_apply(const Wrench& f) const { return Wrench::from_stacked(mat.transpose() * f.stacked()); }
+};
+
+struct RobotChain;
+
+// 6x6 SPD link inertia, built by spatial_inertia_from (spatial.hpp:111-127).
+class SpatialInertia {
  public:
-  MatrixXd() = default;
-  MatrixXd(std::size_t r, std::size_t c) : r_(r), c_(c), v_(r * c, 0.0) {}
-  std::size_t rows() const { return r_; }
-  std::size_t cols() const { return c_; }
-  double& operator()(std::size_t i, std::size_t j) { return v_[i * c_ + j]; }
-  double operator()(std::size_t i, std::size_t j) const { return v_[i * c_ + j]; }
-  double* data() { return v_.data(); }
-  const double* data() const { return v_.data(); }
+  SpatialInertia() : mat_(Mat6::Identity()) {}
+  const Mat6& matrix() const { return mat_; }
+  Wrench apply(const Twist& v) const { return Wrench::from_stacked(mat_ * v.stacked()); }
 
  private:
-  std::size_t r_ = 0, c_ = 0;
-  std::vector<double> v_;
+  explicit SpatialInertia(const Mat6& m) : mat_(m) {}
+  friend SpatialInertia spatial_inertia_from(double mass, const Vec3& com, const Mat3& inertia_rot);
+  friend std::vector<SpatialInertia> link_inertias(const RobotChain& chain);
+  Mat6 mat_;
 };
+
+Mat3 skew(const Vec3& a);                       // spatial.hpp:129-130
+Mat6 small_adjoint(const Twist& v);             // spatial.hpp:132-135
+AdjointMap adjoint_of(const SE3Transform& t);   // spatial.hpp:137-138
+SE3Transform screw_exp(const Twist& s, double q);  // spatial.hpp:140-143
+// spatial.hpp:145-150: throws std::invalid_argument with the reference's texts.
+SpatialInertia spatial_inertia_from(double mass, const Vec3& com, const Mat3& inertia_rot);
 
 class ModelError : public std::runtime_error {
  public:
@@ -136,20 +168,42 @@ inline int ceil_log2(std::size_t n) {
 }
 
 // ----------------------------------------------------------------- model
+// model.hpp:17-23: link i hangs off link i-1 (link 0 off the base) by a
+// one-degree-of-freedom joint of screw `joint_screw` in the link-i frame.
 struct LinkSpec {
   double mass = 1.0;
-  Vec3 com{0.0, 0.0, 0.0};
-  Mat3 inertia_rot{1, 0, 0, 0, 1, 0, 0, 0, 1};
-  Vec6 joint_screw{0, 0, 1, 0, 0, 0};  // (angular, linear), unit 6-norm
-  Mat3 home_rotation{1, 0, 0, 0, 1, 0, 0, 0, 1};
-  Vec3 home_translation{0.0, 0.0, 0.0};
+  Vec3 com = Vec3::Zero();              // centre of mass, link frame
+  Mat3 inertia_rot = Mat3::Identity();  // rotational inertia about the COM
+  Twist joint_screw{Vec3::UnitZ(), Vec3::Zero()};  // unit 6-norm
+  SE3Transform home_transform;          // parent-frame -> link-frame map at q = 0
 };
 
-struct RobotChain {
+struct RobotChain {  // model.hpp:25-30
   std::vector<LinkSpec> links;
-  Vec3 gravity{0.0, 0.0, -9.81};
+  Vec3 gravity = Vec3(0.0, 0.0, -9.81);
   int size() const { return static_cast<int>(links.size()); }
 };
+
+// Exact field-for-field comparison (model.hpp:32-35).
+bool operator==(const LinkSpec& a, const LinkSpec& b);
+bool operator==(const RobotChain& a, const RobotChain& b);
+
+// Configuration-dependent operators at q (model.hpp:37-49): rel[i] maps
+// link-(i-1) coordinates into link-i coordinates, transport[i] is the adjoint
+// of rel[i+1].
+struct ChainKinematics {
+  std::vector<SE3Transform> rel;      // n
+  AdjointMap base_transport;          // adjoint of rel[0]
+  std::vector<AdjointMap> transport;  // n - 1
+  std::vector<Twist> screw;           // n
+  int size() const { return static_cast<int>(rel.size()); }
+};
+
+// model.hpp:51-58 (model.cpp:117-146), evaluated on the device.
+ChainKinematics assemble_kinematics(const RobotChain& chain, const JointVector& q);
+// model.hpp:60-61 (model.cpp:148-155), evaluated on the device; throws
+// std::invalid_argument with spatial_inertia_from's message for a bad link.
+std::vector<SpatialInertia> link_inertias(const RobotChain& chain);
 
 // Deterministic random chain (model.cpp:157-185), bit-identical to the
 // reference generator.
@@ -165,41 +219,58 @@ void validate_chain(const RobotChain& chain);
 RobotChain load_chain(const std::string& path);
 void save_chain(const RobotChain& chain, const std::string& path);
 
-// ----------------------------------------------------------------- trace
+// ----------------------------------------------------------------- trace (trace.hpp:12-39)
+struct ScanTrace {
+  int rounds = 0;
+};
+struct OeeTrace {
+  int rounds = 0;
+};
+// Filled from the kernel variant that ran (pd_last_trace): a traced call runs
+// the CTA-per-chain variants whose recursions are log-depth scans / OEE rounds.
 struct ExecTrace {
   int parallel_link_stages = 0;
   int longest_sequential_link_chain = 0;
   int scan_rounds_max = 0;
   int oee_rounds = 0;
+  void note_parallel_stage() { ++parallel_link_stages; }
+  void note_sequential_chain(int length) {
+    longest_sequential_link_chain = length > longest_sequential_link_chain ? length : longest_sequential_link_chain;
+  }
+  void note_scan(const ScanTrace& t) { scan_rounds_max = t.rounds > scan_rounds_max ? t.rounds : scan_rounds_max; }
+  void note_oee(const OeeTrace& t) { oee_rounds = t.rounds; }
 };
 
-// ----------------------------------------------------------------- dynamics
-enum class FdAlgo { jsiia, abia, cfa };
+// ----------------------------------------------------------------- building blocks (scan.hpp, oee.hpp)
+// The paper's two solvers on their own, on the GPU: 6x6 block bi-diagonal
+// systems by the affine scan (scan.hpp:100-168), symmetric 5x5 block
+// tri-diagonal systems by odd-even elimination (oee.hpp:28-32, 149-189) --
+// the block sizes the dynamics use.
+enum class BiDiagOrientation { lower, upper };
 
-JointVector forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                             const JointVector& tau, FdAlgo algo, ExecTrace* trace = nullptr);
-JointVector jsiia_forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                                   const JointVector& tau, ExecTrace* trace = nullptr);
-JointVector abia_forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                                  const JointVector& tau, ExecTrace* trace = nullptr);
-JointVector cfa_forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                                 const JointVector& tau, ExecTrace* trace = nullptr);
-
-struct FdProblem {
-  RobotChain chain;
-  JointVector q;
-  JointVector qdot;
-  JointVector tau;
+// lower: x[0] = rhs[0], x[k] = coupling[k-1] x[k-1] + rhs[k];
+// upper: x[n-1] = rhs[n-1], x[k] = coupling[k] x[k+1] + rhs[k].
+template <int D>
+struct BlockBiDiagSystem {
+  BiDiagOrientation orientation = BiDiagOrientation::lower;
+  std::vector<Matrix<D, D>> coupling;  // n - 1 blocks
+  std::vector<Matrix<D, 1>> rhs;       // n blocks
 };
 
-struct FdResult {
-  JointVector qddot;
-  std::string error;
-  bool ok() const { return error.empty(); }
+// diag[i] symmetric, upper[i] couples row i to row i+1 (sub-diagonal = upper^T).
+template <int B>
+struct SymBlockTriDiagSystem {
+  std::vector<Matrix<B, B>> diag;   // n blocks
+  std::vector<Matrix<B, B>> upper;  // n - 1 blocks
 };
 
-std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems, FdAlgo algo);
+std::vector<Vec6> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
+std::vector<Vec6> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
+// Exactly ceil_log2(n) rounds; throws SingularBlockError(round, index) like the reference.
+std::vector<Vec5> oee_solve(const SymBlockTriDiagSystem<5>& sys, const std::vector<Vec5>& rhs,
+                            OeeTrace* trace = nullptr);
 
+// ----------------------------------------------------------------- inverse dynamics (inverse_dynamics.hpp)
 // inverse_dynamics.hpp:23-28
 struct IdOptions {
   Twist base_velocity{};
@@ -216,51 +287,90 @@ struct LinkStates {
 };
 
 JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                             const JointVector& qddot, const IdOptions& opts = {});
-JointVector bias_torque(const RobotChain& chain, const JointVector& q, const JointVector& qdot);
+                             const JointVector& qddot, const IdOptions& opts = {}, ExecTrace* trace = nullptr);
+JointVector bias_torque(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                        ExecTrace* trace = nullptr);
 LinkStates link_states(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
                        const JointVector& qddot, const IdOptions& opts = {});
-MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q);
 
-// ----------------------------------------------------------------- building blocks
-// The paper's two solvers on their own (scan.hpp:100-168, oee.hpp:28-32,
-// 149-189), on the GPU: 6x6 block bi-diagonal systems by the affine scan,
-// symmetric 5x5 block tri-diagonal systems by odd-even elimination (the
-// block sizes the dynamics use). Blocks are row-major.
-enum class BiDiagOrientation { lower, upper };
+// ----------------------------------------------------------------- forward dynamics (forward_dynamics.hpp)
+enum class FdAlgo { jsiia, abia, cfa };
 
-template <int D>
-struct BlockBiDiagSystem {
-  BiDiagOrientation orientation = BiDiagOrientation::lower;
-  std::vector<std::array<double, D * D>> coupling;  // n - 1 blocks
-  std::vector<std::array<double, D>> rhs;           // n blocks
+// forward_dynamics.hpp:31-35: column j = ID(q, 0, e_j) without gravity, symmetrised.
+MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q, ExecTrace* trace = nullptr);
+
+JointVector jsiia_forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                                   const JointVector& tau, ExecTrace* trace = nullptr);
+
+// forward_dynamics.hpp:44-56: joint_inertia[i] = S_i^T abi[i] S_i,
+// gain[i] = abi[i] S_i / joint_inertia[i].
+struct ArticulatedBodyInertias {
+  std::vector<Mat6> inertia;
+  JointVector joint_inertia;
+  std::vector<Vec6> gain;
+};
+ArticulatedBodyInertias articulated_body_inertias(const ChainKinematics& kin, std::span<const SpatialInertia> inertia,
+                                                  ExecTrace* trace = nullptr);
+
+JointVector abia_forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                                  const JointVector& tau, ExecTrace* trace = nullptr);
+
+// forward_dynamics.hpp:64-71: basis[i]^T screw[i] = 0, [basis[i] screw[i]] orthogonal.
+struct ConstraintBasis {
+  std::vector<Matrix<6, 5>> basis;
+};
+ConstraintBasis build_constraint_basis(const RobotChain& chain);
+
+// forward_dynamics.hpp:73-96: projections of (I - G) J^-1 (I - G)^T.
+struct CfaOperators {
+  SymBlockTriDiagSystem<5> constraint_op;
+  std::vector<Vec5> cross_sub;    // n-1: couples row i+1 to column i
+  std::vector<Vec5> cross_diag;   // n
+  std::vector<Vec5> cross_super;  // n-1: couples row i to column i+1
+  JointVector joint_diag;         // n
+  JointVector joint_off;          // n-1
+
+  std::vector<Vec5> apply_cross(const JointVector& v) const;
+  JointVector apply_cross_transpose(std::span<const Vec5> f) const;
+  JointVector apply_joint(const JointVector& v) const;
+};
+CfaOperators build_cfa_operators(const RobotChain& chain, const ChainKinematics& kin, const ConstraintBasis& basis,
+                                 ExecTrace* trace = nullptr);
+
+JointVector cfa_forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                                 const JointVector& tau, ExecTrace* trace = nullptr);
+
+JointVector forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
+                             const JointVector& tau, FdAlgo algo, ExecTrace* trace = nullptr);
+
+struct FdProblem {
+  RobotChain chain;
+  JointVector q;
+  JointVector qdot;
+  JointVector tau;
 };
 
-template <int B>
-struct SymBlockTriDiagSystem {
-  std::vector<std::array<double, B * B>> diag;   // n blocks
-  std::vector<std::array<double, B * B>> upper;  // n - 1 blocks
+struct FdResult {
+  JointVector qddot;
+  std::string error;
+  bool ok() const { return error.empty(); }
 };
 
-struct ScanTrace {
-  int rounds = 0;
-};
-struct OeeTrace {
-  int rounds = 0;
-};
-
-std::vector<std::array<double, 6>> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
-std::vector<std::array<double, 6>> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
-// Throws SingularBlockError(round, index) like the reference.
-std::vector<std::array<double, 5>> oee_solve(const SymBlockTriDiagSystem<5>& sys,
-                                             const std::vector<std::array<double, 5>>& rhs,
-                                             OeeTrace* trace = nullptr);
+// forward_dynamics.cpp:466-481: never throws per problem; the batch is
+// bucketed by link count, one device call per bucket.
+std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems, FdAlgo algo);
 
 // ----------------------------------------------------------------- device
 namespace gpu {
-// CUDA device the calling thread's solves run on (default 0).
+// CUDA device the calling thread's single-problem calls run on (default 0).
 void set_device(int device);
 int device();
+// Devices batch_forward_dynamics shards a bucket across (default: {device()}).
+// Contiguous slices, one context per device, no collective; every slice
+// selects kernels for the whole bucket, so results do not depend on the
+// device count.
+void set_devices(const std::vector<int>& devices);
+std::vector<int> devices();
 }  // namespace gpu
 
 }  // namespace pardyn

@@ -276,6 +276,66 @@ pd_status pd_workload_chains_device(pd_ctx* ctx, uint64_t cell_seed, int32_t n_l
 pd_status pd_set_models_workload(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,
                                  const double* gravity, int32_t* model_status, int32_t* model_rule);
 
+/* The reference's per-chain operator builders on the device, in its dense
+ * representation. Host buffers,
+ * blocks row-major, arrays problem-major; each call blocks until done.
+ *
+ *   pd_assemble_kinematics   <- assemble_kinematics(chain, q) (model.hpp:51-58,
+ *                               src/model.cpp:117-146) against the current
+ *                               models: rel [b][n][12] (R 9, p 3),
+ *                               base_transport [b][36], transport [b][n-1][36]
+ *                               (Ad of rel[i+1]), screw [b][n][6]
+ *   pd_link_inertias         <- link_inertias(chain) (model.hpp:60-61,
+ *                               src/model.cpp:148-155): [models][n][36]; a
+ *                               model that failed validation fails the call
+ *                               with the spatial_inertia_from message
+ *   pd_articulated_body_inertias
+ *                            <- articulated_body_inertias(kin, inertia)
+ *                               (forward_dynamics.hpp:48-56,
+ *                               src/forward_dynamics.cpp:120-163): inputs
+ *                               transport [b][n-1][36], inertia [b][n][36]
+ *                               ([n][36] for all if shared_inertia), screw
+ *                               [b][n][6]; outputs abi [b][n][36],
+ *                               joint_inertia [b][n], gain [b][n][6]; per
+ *                               problem PD_SLOT_OK or
+ *                               PD_SLOT_DEGENERATE_ARTICULATION (index = joint)
+ *   pd_constraint_basis      <- build_constraint_basis(chain)
+ *                               (forward_dynamics.hpp:64-71,
+ *                               src/forward_dynamics.cpp:245-259): screw
+ *                               [k][6] -> basis [k][30] (6x5)
+ *   pd_cfa_operators         <- build_cfa_operators(chain, kin, basis)
+ *                               (forward_dynamics.hpp:73-96,
+ *                               src/forward_dynamics.cpp:261-357): inputs as
+ *                               above plus basis [b][n][30]; outputs
+ *                               constraint diag [b][n][25] / upper
+ *                               [b][n-1][25], cross_sub / cross_super
+ *                               [b][n-1][5], cross_diag [b][n][5],
+ *                               joint_diag [b][n], joint_off [b][n-1]; per
+ *                               problem PD_SLOT_OK or
+ *                               PD_SLOT_LINK_INERTIA_NOT_PD (index = link)
+ *   pd_cfa_apply             <- CfaOperators::apply_cross / apply_cross_transpose
+ *                               / apply_joint (forward_dynamics.cpp:359-416):
+ *                               in [b][n] -> out [b][n][5] (PD_APPLY_CROSS),
+ *                               in [b][n][5] -> out [b][n] (PD_APPLY_CROSS_TRANSPOSE),
+ *                               in [b][n] -> out [b][n] (PD_APPLY_JOINT) */
+typedef enum pd_apply_op { PD_APPLY_CROSS = 0, PD_APPLY_CROSS_TRANSPOSE = 1, PD_APPLY_JOINT = 2 } pd_apply_op;
+
+pd_status pd_assemble_kinematics(pd_ctx* ctx, int64_t batch, const double* q, double* rel, double* base_transport,
+                                 double* transport, double* screw);
+pd_status pd_link_inertias(pd_ctx* ctx, double* inertia);
+pd_status pd_articulated_body_inertias(pd_ctx* ctx, int64_t batch, int32_t n, const double* transport,
+                                       const double* inertia, int32_t shared_inertia, const double* screw,
+                                       double* abi, double* joint_inertia, double* gain, int32_t* slot_status,
+                                       int32_t* slot_index);
+pd_status pd_constraint_basis(pd_ctx* ctx, int64_t count, const double* screw, double* basis);
+pd_status pd_cfa_operators(pd_ctx* ctx, int64_t batch, int32_t n, const double* inertia, int32_t shared_inertia,
+                           const double* transport, const double* screw, const double* basis, double* constraint_diag,
+                           double* constraint_upper, double* cross_sub, double* cross_diag, double* cross_super,
+                           double* joint_diag, double* joint_off, int32_t* slot_status, int32_t* slot_index);
+pd_status pd_cfa_apply(pd_ctx* ctx, int32_t op, int64_t batch, int32_t n, const double* cross_sub,
+                       const double* cross_diag, const double* cross_super, const double* joint_diag,
+                       const double* joint_off, const double* in, double* out);
+
 /* Diagnostic: measured dense FP64 FMA throughput of this device (TFLOP/s),
  * the FP64 roofline denominator (no FP64 figure in MEASURED_PEAKS.json). */
 pd_status pd_probe_fp64_peak(pd_ctx* ctx, double* tflops, double* elapsed_ms);

@@ -6,7 +6,17 @@ mirror of the reference's C++ API (proj/core/include/pardyn/*.hpp); the C++
 drop-in lives in include/pardyn/ + paper_1609_06779_b200/cpp/.
 """
 from .api import (  # noqa: F401
+    ArticulatedBodyInertias,
+    CfaOperators,
+    ChainKinematics,
+    ConstraintBasis,
     Context,
+    SE3Transform,
+    articulated_body_inertias,
+    assemble_kinematics,
+    build_cfa_operators,
+    build_constraint_basis,
+    link_inertias,
     CudaError,
     DynamicsError,
     ExecTrace,

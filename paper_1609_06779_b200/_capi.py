@@ -29,7 +29,10 @@ EXPORTS = (
     "pd_inverse_dynamics_device", "pd_bias_torque", "pd_link_states", "pd_joint_space_inertia",
     "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5", "pd_block_bidiag_solve6",
     "pd_forward_dynamics_traced", "pd_last_variant", "pd_last_trace", "pd_set_selection_batch",
+    "pd_assemble_kinematics", "pd_link_inertias", "pd_articulated_body_inertias", "pd_constraint_basis",
+    "pd_cfa_operators", "pd_cfa_apply",
 )
+PD_APPLY_CROSS, PD_APPLY_CROSS_TRANSPOSE, PD_APPLY_JOINT = range(3)
 
 
 class IdOptions(C.Structure):
@@ -130,6 +133,20 @@ def load():
     L.pd_last_trace.restype = C.c_int
     L.pd_set_selection_batch.argtypes = [C.c_void_p, C.c_int64]
     L.pd_set_selection_batch.restype = C.c_int
+    L.pd_assemble_kinematics.argtypes = [C.c_void_p, C.c_int64, _D, _D, _D, _D, _D]
+    L.pd_assemble_kinematics.restype = C.c_int
+    L.pd_link_inertias.argtypes = [C.c_void_p, _D]
+    L.pd_link_inertias.restype = C.c_int
+    L.pd_articulated_body_inertias.argtypes = [C.c_void_p, C.c_int64, C.c_int32, _D, _D, C.c_int32, _D, _D, _D, _D,
+                                               _I32, _I32]
+    L.pd_articulated_body_inertias.restype = C.c_int
+    L.pd_constraint_basis.argtypes = [C.c_void_p, C.c_int64, _D, _D]
+    L.pd_constraint_basis.restype = C.c_int
+    L.pd_cfa_operators.argtypes = [C.c_void_p, C.c_int64, C.c_int32, _D, C.c_int32, _D, _D, _D, _D, _D, _D, _D, _D,
+                                   _D, _D, _I32, _I32]
+    L.pd_cfa_operators.restype = C.c_int
+    L.pd_cfa_apply.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, _D, _D, _D, _D, _D, _D, _D]
+    L.pd_cfa_apply.restype = C.c_int
     _lib = L
     return L
 

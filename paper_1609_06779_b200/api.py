@@ -70,24 +70,32 @@ class FdAlgo(enum.IntEnum):
 
 
 @dataclass
+class SE3Transform:
+    """spatial.hpp:75-97: x_target = rotation @ x_source + translation."""
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+
+@dataclass
 class LinkSpec:
-    """model.hpp:17-23 (defaults match the reference)."""
+    """model.hpp:17-23 (defaults match the reference). joint_screw stacks
+    (angular, linear) -- Twist::stacked() of the reference."""
     mass: float = 1.0
     com: np.ndarray = field(default_factory=lambda: np.zeros(3))
     inertia_rot: np.ndarray = field(default_factory=lambda: np.eye(3))
     joint_screw: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, 1.0, 0.0, 0.0, 0.0]))
-    home_rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
-    home_translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    home_transform: SE3Transform = field(default_factory=SE3Transform)
 
     def to_record(self) -> np.ndarray:
+        h = self.home_transform
         return np.concatenate([[self.mass], np.ravel(self.com), np.ravel(self.inertia_rot), np.ravel(self.joint_screw),
-                               np.ravel(self.home_rotation), np.ravel(self.home_translation)]).astype(np.float64)
+                               np.ravel(h.rotation), np.ravel(h.translation)]).astype(np.float64)
 
     @staticmethod
     def from_record(r) -> "LinkSpec":
         r = np.asarray(r, dtype=np.float64)
         return LinkSpec(float(r[0]), r[1:4].copy(), r[4:13].reshape(3, 3).copy(), r[13:19].copy(),
-                        r[19:28].reshape(3, 3).copy(), r[28:31].copy())
+                        SE3Transform(r[19:28].reshape(3, 3).copy(), r[28:31].copy()))
 
 
 @dataclass
@@ -346,6 +354,81 @@ class Context:
         self._check(self._L.pd_joint_space_inertia(self._h, B, _capi.dptr(q), _capi.dptr(M)))
         return M
 
+    # ---- the reference's operator builders, batched (pd_assemble_kinematics ... pd_cfa_apply)
+    def assemble_kinematics(self, q):
+        """q (B, n) against the current models -> rel (B, n, 12) [R row-major, p],
+        base_transport (B, 6, 6), transport (B, n-1, 6, 6), screw (B, n, 6)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        B, n = q.shape
+        rel, base = np.empty((B, n, 12)), np.empty((B, 6, 6))
+        tr, sc = np.empty((B, max(n - 1, 0), 6, 6)), np.empty((B, n, 6))
+        self._check(self._L.pd_assemble_kinematics(self._h, B, _capi.dptr(q), _capi.dptr(rel), _capi.dptr(base),
+                                                   _capi.dptr(tr), _capi.dptr(sc)))
+        return rel, base, tr, sc
+
+    def link_inertias(self):
+        """Spatial inertias of the current models -> (M, n, 6, 6)."""
+        out = np.empty((max(self.n_models, 1), self.n_links, 6, 6))
+        self._check(self._L.pd_link_inertias(self._h, _capi.dptr(out)))
+        return out
+
+    def articulated_body_inertias(self, transport, inertia, screw):
+        """transport (B, n-1, 6, 6), inertia (B, n, 6, 6) or (n, 6, 6) shared,
+        screw (B, n, 6) -> abi (B, n, 6, 6), joint_inertia (B, n), gain (B, n, 6),
+        status (B,), index (B,)."""
+        screw = np.ascontiguousarray(screw, dtype=np.float64)
+        B, n = screw.shape[:2]
+        inertia = np.ascontiguousarray(inertia, dtype=np.float64)
+        shared = inertia.ndim == 3
+        transport = np.ascontiguousarray(transport, dtype=np.float64).reshape(B, max(n - 1, 0), 6, 6)
+        abi, lam, gain = np.empty((B, n, 6, 6)), np.empty((B, n)), np.empty((B, n, 6))
+        st, ix = np.empty(B, np.int32), np.empty(B, np.int32)
+        self._check(self._L.pd_articulated_body_inertias(
+            self._h, B, n, _capi.dptr(transport), _capi.dptr(inertia), int(shared), _capi.dptr(screw),
+            _capi.dptr(abi), _capi.dptr(lam), _capi.dptr(gain), _capi.iptr(st), _capi.iptr(ix)))
+        return abi, lam, gain, st, ix
+
+    def constraint_basis(self, screw):
+        """screw (K, 6) -> basis (K, 6, 5)."""
+        screw = np.ascontiguousarray(screw, dtype=np.float64).reshape(-1, 6)
+        out = np.empty((screw.shape[0], 6, 5))
+        self._check(self._L.pd_constraint_basis(self._h, screw.shape[0], _capi.dptr(screw), _capi.dptr(out)))
+        return out
+
+    def cfa_operators(self, inertia, transport, screw, basis):
+        """-> dict of constraint diag (B, n, 5, 5) / upper (B, n-1, 5, 5),
+        cross_sub / cross_super (B, n-1, 5), cross_diag (B, n, 5), joint_diag
+        (B, n), joint_off (B, n-1), plus status / index (B,)."""
+        screw = np.ascontiguousarray(screw, dtype=np.float64)
+        B, n = screw.shape[:2]
+        e = max(n - 1, 0)
+        inertia = np.ascontiguousarray(inertia, dtype=np.float64)
+        shared = inertia.ndim == 3
+        transport = np.ascontiguousarray(transport, dtype=np.float64).reshape(B, e, 6, 6)
+        basis = np.ascontiguousarray(basis, dtype=np.float64).reshape(B, n, 6, 5)
+        o = {"diag": np.empty((B, n, 5, 5)), "upper": np.empty((B, e, 5, 5)), "cross_sub": np.empty((B, e, 5)),
+             "cross_diag": np.empty((B, n, 5)), "cross_super": np.empty((B, e, 5)), "joint_diag": np.empty((B, n)),
+             "joint_off": np.empty((B, e)), "status": np.empty(B, np.int32), "index": np.empty(B, np.int32)}
+        self._check(self._L.pd_cfa_operators(
+            self._h, B, n, _capi.dptr(inertia), int(shared), _capi.dptr(transport), _capi.dptr(screw),
+            _capi.dptr(basis), *(_capi.dptr(o[k]) for k in ("diag", "upper", "cross_sub", "cross_diag",
+                                                            "cross_super", "joint_diag", "joint_off")),
+            _capi.iptr(o["status"]), _capi.iptr(o["index"])))
+        return o
+
+    def cfa_apply(self, op, ops, x):
+        """CfaOperators::apply_* on the device: op PD_APPLY_CROSS (x (B, n) ->
+        (B, n, 5)), PD_APPLY_CROSS_TRANSPOSE ((B, n, 5) -> (B, n)),
+        PD_APPLY_JOINT ((B, n) -> (B, n))."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        B, n = x.shape[:2]
+        out = np.empty((B, n, 5) if op == _capi.PD_APPLY_CROSS else (B, n))
+        f = {k: np.ascontiguousarray(ops[k], dtype=np.float64)
+             for k in ("cross_sub", "cross_diag", "cross_super", "joint_diag", "joint_off")}
+        self._check(self._L.pd_cfa_apply(self._h, int(op), B, n, *(_capi.dptr(f[k]) for k in (
+            "cross_sub", "cross_diag", "cross_super", "joint_diag", "joint_off")), _capi.dptr(x), _capi.dptr(out)))
+        return out
+
     def block_bidiag_solve6(self, coupling, rhs, upper=False):
         """Batched scan solve of BlockBiDiagSystem<6>: coupling (B, n-1, 6, 6),
         rhs (B, n, 6) -> x (B, n, 6) (scan.hpp:100-168)."""
@@ -479,9 +562,13 @@ def cfa_forward_dynamics(chain, q, qdot, tau, trace=None, ctx=None):
     return forward_dynamics(chain, q, qdot, tau, FdAlgo.cfa, trace, ctx)
 
 
-def batch_forward_dynamics(problems: Sequence[FdProblem], algo: FdAlgo, ctx: Optional[Context] = None) -> List[FdResult]:
+def batch_forward_dynamics(problems: Sequence[FdProblem], algo: FdAlgo, ctx: Optional[Context] = None,
+                           devices: Optional[Sequence[int]] = None) -> List[FdResult]:
     """forward_dynamics.cpp:466-481: independent problems, per-slot errors,
-    never raises per problem. Problems are bucketed by link count."""
+    never raises per problem. Problems are bucketed by link count; with a
+    device list each bucket is split into contiguous slices, one thread and
+    one context per device, every slice selecting kernels for the whole
+    bucket -- the result is bit-identical to the one-device call."""
     algo = FdAlgo(int(algo))
     out = [FdResult() for _ in problems]
     buckets = {}
@@ -494,21 +581,59 @@ def batch_forward_dynamics(problems: Sequence[FdProblem], algo: FdAlgo, ctx: Opt
         buckets.setdefault(p.chain.size(), []).append(k)
     if not buckets:
         return out
-    ctx = ctx or default_context()
+    devices = list(devices) if devices else None
     for n, idx in buckets.items():
         links = np.stack([problems[k].chain.to_records() for k in idx])
         grav = np.stack([np.asarray(problems[k].chain.gravity, np.float64) for k in idx])
-        ctx.set_models(links, grav)
         q = np.stack([np.asarray(problems[k].q, np.float64) for k in idx])
         qd = np.stack([np.asarray(problems[k].qdot, np.float64) for k in idx])
         tau = np.stack([np.asarray(problems[k].tau, np.float64) for k in idx])
-        qdd, st, rd, ix = ctx.solve(algo, q, qd, tau)
+        B = len(idx)
+        qdd, st = np.empty((B, n)), np.empty(B, np.int32)
+        rd, ix = np.empty(B, np.int32), np.empty(B, np.int32)
+
+        def run(c, lo, hi):
+            c.set_selection_batch(B)
+            try:
+                c.set_models(links[lo:hi], grav[lo:hi])
+                qdd[lo:hi], st[lo:hi], rd[lo:hi], ix[lo:hi] = c.solve(algo, q[lo:hi], qd[lo:hi], tau[lo:hi])
+            finally:
+                c.set_selection_batch(0)
+
+        G = min(len(devices), B) if devices else 1
+        if G <= 1:
+            run(ctx or (default_context() if not devices else _device_context(devices[0])), 0, B)
+        else:
+            errors = []
+
+            def worker(g):
+                try:
+                    run(_device_context(devices[g]), B * g // G, B * (g + 1) // G)
+                except Exception as e:  # re-raised on the calling thread
+                    errors.append(e)
+            threads = [threading.Thread(target=worker, args=(g,)) for g in range(G)]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+            if errors:
+                raise errors[0]
         for j, k in enumerate(idx):
             if st[j] == _capi.SLOT_OK:
                 out[k].qddot = qdd[j].copy()
             else:
                 out[k].error = _capi.slot_message(st[j], rd[j], ix[j], n)
     return out
+
+
+def _device_context(device: int) -> Context:
+    """The calling thread's context on `device` (sharded batch calls)."""
+    ctxs = getattr(_tls, "by_device", None)
+    if ctxs is None:
+        ctxs = _tls.by_device = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
 
 
 def _id_sizes(chain: RobotChain, **vecs):
@@ -575,6 +700,128 @@ def joint_space_inertia(chain: RobotChain, q, ctx: Optional[Context] = None) -> 
         return np.zeros((0, 0))
     ctx = _one_model(chain, q, ctx)
     return ctx.joint_space_inertia(np.asarray(q, np.float64)[None])[0]
+
+
+# --------------------------------------------------------------------------- chain operators
+@dataclass
+class ChainKinematics:
+    """model.hpp:37-49: rel[i] maps link-(i-1) into link-i coordinates
+    (rotation (n, 3, 3), translation (n, 3)); transport[i] = Ad(rel[i+1])."""
+    rotation: np.ndarray
+    translation: np.ndarray
+    base_transport: np.ndarray
+    transport: np.ndarray
+    screw: np.ndarray
+
+    def size(self) -> int:
+        return self.screw.shape[0]
+
+
+@dataclass
+class ArticulatedBodyInertias:
+    """forward_dynamics.hpp:44-52."""
+    inertia: np.ndarray        # (n, 6, 6)
+    joint_inertia: np.ndarray  # (n,)
+    gain: np.ndarray           # (n, 6)
+
+
+@dataclass
+class ConstraintBasis:
+    """forward_dynamics.hpp:64-69: basis (n, 6, 5)."""
+    basis: np.ndarray
+
+
+@dataclass
+class CfaOperators:
+    """forward_dynamics.hpp:73-91; apply_* run on the device."""
+    diag: np.ndarray
+    upper: np.ndarray
+    cross_sub: np.ndarray
+    cross_diag: np.ndarray
+    cross_super: np.ndarray
+    joint_diag: np.ndarray
+    joint_off: np.ndarray
+
+    def _blocks(self):
+        return {k: getattr(self, k)[None] for k in ("cross_sub", "cross_diag", "cross_super", "joint_diag",
+                                                    "joint_off")}
+
+    def apply_cross(self, v, ctx: Optional[Context] = None):
+        """forward_dynamics.cpp:359-376: v (n,) -> (n, 5)."""
+        v = np.asarray(v, np.float64)
+        if len(v) != len(self.cross_diag):
+            raise InvalidArgument("apply_cross: one entry per link expected")
+        return (ctx or default_context()).cfa_apply(_capi.PD_APPLY_CROSS, self._blocks(), v[None])[0]
+
+    def apply_cross_transpose(self, f, ctx: Optional[Context] = None):
+        """forward_dynamics.cpp:378-399: f (n, 5) -> (n,)."""
+        f = np.asarray(f, np.float64).reshape(-1, 5)
+        if f.shape[0] != len(self.cross_diag):
+            raise InvalidArgument("apply_cross_transpose: one constraint block per link expected")
+        return (ctx or default_context()).cfa_apply(_capi.PD_APPLY_CROSS_TRANSPOSE, self._blocks(), f[None])[0]
+
+    def apply_joint(self, v, ctx: Optional[Context] = None):
+        """forward_dynamics.cpp:401-416: v (n,) -> (n,)."""
+        v = np.asarray(v, np.float64)
+        if len(v) != len(self.joint_diag):
+            raise InvalidArgument("apply_joint: one entry per link expected")
+        return (ctx or default_context()).cfa_apply(_capi.PD_APPLY_JOINT, self._blocks(), v[None])[0]
+
+
+def assemble_kinematics(chain: RobotChain, q, ctx: Optional[Context] = None) -> ChainKinematics:
+    """model.cpp:117-146 on the device."""
+    ctx = _one_model(chain, q, ctx)
+    rel, base, tr, sc = ctx.assemble_kinematics(np.asarray(q, np.float64)[None])
+    return ChainKinematics(rel[0, :, :9].reshape(-1, 3, 3), rel[0, :, 9:], base[0], tr[0], sc[0])
+
+
+def link_inertias(chain: RobotChain, ctx: Optional[Context] = None) -> np.ndarray:
+    """model.cpp:148-155 on the device: (n, 6, 6); a bad link raises the
+    spatial_inertia_from message."""
+    ctx = _one_model(chain, np.zeros(chain.size()), ctx)
+    return ctx.link_inertias()[0]
+
+
+def articulated_body_inertias(kin: ChainKinematics, inertia, trace: Optional[ExecTrace] = None,
+                              ctx: Optional[Context] = None) -> ArticulatedBodyInertias:
+    """forward_dynamics.cpp:120-163 on the device (the n-link tip-to-base walk)."""
+    n = kin.size()
+    inertia = np.asarray(inertia, np.float64).reshape(n, 6, 6)
+    abi, lam, gain, st, ix = (ctx or default_context()).articulated_body_inertias(
+        kin.transport[None], inertia[None], kin.screw[None])
+    if st[0] != _capi.SLOT_OK:
+        _raise_slot(st[0], 0, ix[0], n)
+    if trace is not None:
+        trace.longest_sequential_link_chain = max(trace.longest_sequential_link_chain, n)
+    return ArticulatedBodyInertias(abi[0], lam[0], gain[0])
+
+
+def build_constraint_basis(chain: RobotChain, ctx: Optional[Context] = None) -> ConstraintBasis:
+    """forward_dynamics.cpp:245-259 on the device (Householder complement)."""
+    screws = np.stack([np.asarray(l.joint_screw, np.float64) for l in chain.links]) if chain.links else \
+        np.zeros((0, 6))
+    if not chain.links:
+        return ConstraintBasis(np.zeros((0, 6, 5)))
+    return ConstraintBasis((ctx or default_context()).constraint_basis(screws))
+
+
+def build_cfa_operators(chain: RobotChain, kin: ChainKinematics, basis: ConstraintBasis,
+                        trace: Optional[ExecTrace] = None, ctx: Optional[Context] = None) -> CfaOperators:
+    """forward_dynamics.cpp:261-357 on the device."""
+    n = chain.size()
+    if n == 0:
+        raise InvalidArgument("build_cfa_operators: chain has no links")
+    if basis.basis.shape[0] != n or kin.size() != n:
+        raise InvalidArgument("build_cfa_operators: kinematics and basis must match the chain")
+    ctx = ctx or default_context()
+    J = link_inertias(chain, ctx)
+    o = ctx.cfa_operators(J[None], kin.transport[None], kin.screw[None], basis.basis[None])
+    if o["status"][0] != _capi.SLOT_OK:
+        _raise_slot(o["status"][0], 0, o["index"][0], n)
+    if trace is not None:
+        trace.parallel_link_stages += 2
+    return CfaOperators(*(o[k][0] for k in ("diag", "upper", "cross_sub", "cross_diag", "cross_super",
+                                            "joint_diag", "joint_off")))
 
 
 # --------------------------------------------------------------------------- model files
@@ -663,8 +910,8 @@ def validate_chain(chain: RobotChain) -> None:
         nrm = float(np.linalg.norm(s))
         if abs(nrm - 1.0) > 1e-9:
             raise ModelError(f"{_link_prefix(k)}: joint_screw must have unit norm (got {nrm:.6f})")
-        R = np.asarray(l.home_rotation, np.float64).reshape(3, 3)
-        ok = np.all(np.isfinite(R)) and np.all(np.isfinite(l.home_translation))
+        R = np.asarray(l.home_transform.rotation, np.float64).reshape(3, 3)
+        ok = np.all(np.isfinite(R)) and np.all(np.isfinite(l.home_transform.translation))
         ok = ok and np.abs(R.T @ R - np.eye(3)).max() <= 1e-9 and np.linalg.det(R) > 0.0
         if not ok:
             raise ModelError(f"{_link_prefix(k)}: home_transform rotation must be orthonormal with determinant +1")
@@ -725,8 +972,8 @@ def load_chain(path: str) -> RobotChain:
         screw = array(j, "joint_screw", 6, w)
         if not isinstance(home, dict):
             raise ModelError(f"{w}: field 'home_transform' must be an object")
-        out.append(LinkSpec(mass, com, Ir.reshape(3, 3), screw, array(home, "rotation", 9, w).reshape(3, 3),
-                            array(home, "translation", 3, w)))
+        out.append(LinkSpec(mass, com, Ir.reshape(3, 3), screw,
+                            SE3Transform(array(home, "rotation", 9, w).reshape(3, 3), array(home, "translation", 3, w))))
     chain = RobotChain(out, gravity)
     validate_chain(chain)
     return chain
@@ -740,8 +987,8 @@ def save_chain(chain: RobotChain, path: str) -> None:
         {"mass": float(l.mass), "com": [float(x) for x in np.ravel(l.com)],
          "inertia_rot": [float(x) for x in np.ravel(l.inertia_rot)],
          "joint_screw": [float(x) for x in np.ravel(l.joint_screw)],
-         "home_transform": {"rotation": [float(x) for x in np.ravel(l.home_rotation)],
-                            "translation": [float(x) for x in np.ravel(l.home_translation)]}}
+         "home_transform": {"rotation": [float(x) for x in np.ravel(l.home_transform.rotation)],
+                            "translation": [float(x) for x in np.ravel(l.home_transform.translation)]}}
         for l in chain.links]}
     try:
         with open(path, "w") as f:

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/pardyn/pardyn.hpp"
+#include "records.hpp"
 
 namespace pardyn {
 
@@ -31,12 +32,14 @@ std::string link_prefix(int k) { return "link " + std::to_string(k); }
 
 bool finite3(const Vec3& v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
 
+}  // namespace
+
 // Smallest eigenvalue of a symmetric 3x3 (cyclic Jacobi), the
-// SelfAdjointEigenSolver minCoeff of model.cpp:96.
-double sym3_min_eig(const Mat3& a) {
+// SelfAdjointEigenSolver minCoeff of model.cpp:96 and spatial.cpp:83.
+double detail::sym3_min_eig(const Mat3& a) {
   double m[3][3];
   for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) m[r][c] = 0.5 * (a[3 * r + c] + a[3 * c + r]);
+    for (int c = 0; c < 3; ++c) m[r][c] = 0.5 * (a(r, c) + a(c, r));
   for (int sweep = 0; sweep < 64; ++sweep) {
     const double off = m[0][1] * m[0][1] + m[0][2] * m[0][2] + m[1][2] * m[1][2];
     if (off < 1e-300) break;
@@ -62,20 +65,20 @@ double sym3_min_eig(const Mat3& a) {
 }
 
 // SE3Transform::is_valid (spatial.cpp:36-41)
-bool home_is_valid(const Mat3& R, const Vec3& p, double tol) {
-  for (double v : R)
-    if (!std::isfinite(v)) return false;
-  if (!finite3(p)) return false;
+bool SE3Transform::is_valid(double tol) const {
+  if (!rotation.allFinite() || !translation.allFinite()) return false;
+  const Mat3 gram = rotation.transpose() * rotation;
   for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) {
-      double g = 0.0;
-      for (int k = 0; k < 3; ++k) g += R[3 * k + r] * R[3 * k + c];
-      if (std::fabs(g - (r == c ? 1.0 : 0.0)) > tol) return false;
-    }
-  const double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
-                     R[2] * (R[3] * R[7] - R[4] * R[6]);
+    for (int c = 0; c < 3; ++c)
+      if (std::fabs(gram(r, c) - (r == c ? 1.0 : 0.0)) > tol) return false;
+  const Mat3& R = rotation;
+  const double det = R(0, 0) * (R(1, 1) * R(2, 2) - R(1, 2) * R(2, 1)) -
+                     R(0, 1) * (R(1, 0) * R(2, 2) - R(1, 2) * R(2, 0)) +
+                     R(0, 2) * (R(1, 0) * R(2, 1) - R(1, 1) * R(2, 0));
   return det > 0.0;
 }
+
+namespace {
 
 // ---------------------------------------------------------------- JSON reader
 struct Json {
@@ -292,17 +295,17 @@ void validate_chain(const RobotChain& chain) {
     double asym = 0.0, scale = 0.0;
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < 3; ++c) {
-        fin = fin && std::isfinite(link.inertia_rot[3 * r + c]);
-        asym = std::max(asym, std::fabs(link.inertia_rot[3 * r + c] - link.inertia_rot[3 * c + r]));
-        scale = std::max(scale, std::fabs(link.inertia_rot[3 * r + c]));
+        fin = fin && std::isfinite(link.inertia_rot(r, c));
+        asym = std::max(asym, std::fabs(link.inertia_rot(r, c) - link.inertia_rot(c, r)));
+        scale = std::max(scale, std::fabs(link.inertia_rot(r, c)));
       }
     if (!fin || asym > 1e-9 * std::max(1.0, scale))
       throw ModelError(link_prefix(k) + ": rotational inertia must be symmetric");
-    if (!(sym3_min_eig(link.inertia_rot) > 0.0))
+    if (!(detail::sym3_min_eig(link.inertia_rot) > 0.0))
       throw ModelError(link_prefix(k) + ": rotational inertia must be positive definite");
     bool sfin = true;
     double norm = 0.0;
-    for (double v : link.joint_screw) {
+    for (double v : link.joint_screw.stacked()) {
       sfin = sfin && std::isfinite(v);
       norm += v * v;
     }
@@ -310,7 +313,7 @@ void validate_chain(const RobotChain& chain) {
     norm = std::sqrt(norm);
     if (std::fabs(norm - 1.0) > 1e-9)
       throw ModelError(link_prefix(k) + ": joint_screw must have unit norm (got " + std::to_string(norm) + ")");
-    if (!home_is_valid(link.home_rotation, link.home_translation, 1e-9))
+    if (!link.home_transform.is_valid(1e-9))
       throw ModelError(link_prefix(k) + ": home_transform rotation must be orthonormal with determinant +1");
   }
 }
@@ -333,7 +336,7 @@ RobotChain load_chain(const std::string& path) {
   const int n = static_cast<int>(n_field.num);
   RobotChain chain;
   const std::vector<double> g = need_array(doc, "gravity", 3, where);
-  chain.gravity = {g[0], g[1], g[2]};
+  chain.gravity = Vec3(g[0], g[1], g[2]);
   const Json& links = need(doc, "links", where);
   if (links.kind != Json::kArray) throw ModelError(where + ": field 'links' must be an array");
   if (static_cast<int>(links.arr.size()) != n)
@@ -349,15 +352,15 @@ RobotChain load_chain(const std::string& path) {
     const std::vector<double> com = need_array(j, "com", 3, lw);
     const std::vector<double> ir = need_array(j, "inertia_rot", 9, lw);
     const std::vector<double> sc = need_array(j, "joint_screw", 6, lw);
-    for (int i = 0; i < 3; ++i) l.com[i] = com[i];
-    for (int i = 0; i < 9; ++i) l.inertia_rot[i] = ir[i];
-    for (int i = 0; i < 6; ++i) l.joint_screw[i] = sc[i];
+    l.com = Vec3(com[0], com[1], com[2]);
+    l.inertia_rot = Mat3::FromRowMajor(ir.data());
+    l.joint_screw = Twist(Vec3(sc[0], sc[1], sc[2]), Vec3(sc[3], sc[4], sc[5]));
     const Json& home = need(j, "home_transform", lw);
     if (home.kind != Json::kObject) throw ModelError(lw + ": field 'home_transform' must be an object");
     const std::vector<double> hr = need_array(home, "rotation", 9, lw);
     const std::vector<double> ht = need_array(home, "translation", 3, lw);
-    for (int i = 0; i < 9; ++i) l.home_rotation[i] = hr[i];
-    for (int i = 0; i < 3; ++i) l.home_translation[i] = ht[i];
+    l.home_transform.rotation = Mat3::FromRowMajor(hr.data());
+    l.home_transform.translation = Vec3(ht[0], ht[1], ht[2]);
   }
   validate_chain(chain);
   return chain;
@@ -372,15 +375,17 @@ void save_chain(const RobotChain& chain, const std::string& path) {
     const LinkSpec& l = chain.links[k];
     const std::string ind = "      ";
     o << (k ? ",\n" : "\n") << "    {\n" << ind << "\"mass\": " << num(l.mass) << ",\n" << ind << "\"com\": ";
-    put_array(o, l.com.data(), 3, ind);
+    double rec[PD_LINK_FIELDS];
+    detail::to_record(l, rec);  // row-major fields, the file's order
+    put_array(o, rec + 1, 3, ind);
     o << ",\n" << ind << "\"inertia_rot\": ";
-    put_array(o, l.inertia_rot.data(), 9, ind);
+    put_array(o, rec + 4, 9, ind);
     o << ",\n" << ind << "\"joint_screw\": ";
-    put_array(o, l.joint_screw.data(), 6, ind);
+    put_array(o, rec + 13, 6, ind);
     o << ",\n" << ind << "\"home_transform\": {\n" << ind << "  \"rotation\": ";
-    put_array(o, l.home_rotation.data(), 9, ind + "  ");
+    put_array(o, rec + 19, 9, ind + "  ");
     o << ",\n" << ind << "  \"translation\": ";
-    put_array(o, l.home_translation.data(), 3, ind + "  ");
+    put_array(o, rec + 28, 3, ind + "  ");
     o << "\n" << ind << "}\n    }";
   }
   o << (chain.links.empty() ? "]\n}\n" : "\n  ]\n}\n");

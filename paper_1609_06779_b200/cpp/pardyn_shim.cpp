@@ -1,23 +1,29 @@
 // Implementation of the pardyn drop-in C++ API (include/pardyn/pardyn.hpp)
-// over the C-ABI. Host side only: size checks, packing into the C-ABI
-// layouts, bucketing batches by link count, and rebuilding the reference's
-// exceptions / error strings from per-slot codes. No arithmetic of the
-// dynamics happens here -- every solve is a pd_forward_dynamics call.
+// over the C-ABI. Host side: size checks, packing into the C-ABI layouts,
+// bucketing batches by link count, sharding buckets across devices, and
+// rebuilding the reference's exceptions / error strings from per-slot codes.
+// The dynamics, the chain operators and the building-block solves all run on
+// the device; the only host arithmetic is the 3x3 / 6x6 value algebra of
+// spatial.hpp (skew, adjoint_of, screw_exp, spatial_inertia_from).
 #include "../../include/pardyn/pardyn.hpp"
 
+#include <algorithm>
 #include <map>
 #include <memory>
-#include <mutex>
+#include <thread>
 
 #include "../../include/pardyn_c.h"
+#include "records.hpp"
 
 namespace pardyn {
 
 namespace {
 
 thread_local int t_device = 0;
+thread_local std::vector<int> t_devices;  // empty: {t_device}
 
-// One pd_ctx per (thread, device): contexts are single-threaded objects.
+// One pd_ctx per (thread, device) -- contexts are single-threaded objects.
+// A sharded batch call opens one per worker thread as well.
 struct CtxHolder {
   std::map<int, pd_ctx*> by_dev;
   ~CtxHolder() {
@@ -26,32 +32,24 @@ struct CtxHolder {
 };
 thread_local CtxHolder t_ctx;
 
-pd_ctx* ctx() {
-  auto it = t_ctx.by_dev.find(t_device);
+pd_ctx* ctx_on(int device) {
+  auto it = t_ctx.by_dev.find(device);
   if (it != t_ctx.by_dev.end()) return it->second;
   pd_ctx* c = nullptr;
-  const pd_status st = pd_create(&c, t_device);
+  const pd_status st = pd_create(&c, device);
   if (st != PD_OK)
-    throw DeviceError(std::string("pardyn: cannot open CUDA device ") + std::to_string(t_device) + ": " +
+    throw DeviceError(std::string("pardyn: cannot open CUDA device ") + std::to_string(device) + ": " +
                       pd_status_string(st));
-  t_ctx.by_dev[t_device] = c;
+  t_ctx.by_dev[device] = c;
   return c;
 }
+pd_ctx* ctx() { return ctx_on(t_device); }
 
 void check_call(pd_ctx* c, pd_status st) {
   if (st == PD_OK) return;
   const std::string msg = pd_last_error(c);
   if (st == PD_INVALID_ARGUMENT) throw std::invalid_argument(msg);
   throw DeviceError(std::string(pd_status_string(st)) + ": " + msg);
-}
-
-void append_link(const LinkSpec& l, std::vector<double>& out) {
-  out.push_back(l.mass);
-  out.insert(out.end(), l.com.begin(), l.com.end());
-  out.insert(out.end(), l.inertia_rot.begin(), l.inertia_rot.end());
-  out.insert(out.end(), l.joint_screw.begin(), l.joint_screw.end());
-  out.insert(out.end(), l.home_rotation.begin(), l.home_rotation.end());
-  out.insert(out.end(), l.home_translation.begin(), l.home_translation.end());
 }
 
 // forward_dynamics.cpp:19-31
@@ -76,25 +74,6 @@ std::string slot_message(int code, int round, int index, int n) {
   throw DynamicsError(m);
 }
 
-void fill_trace(ExecTrace* t, FdAlgo algo, int n) {
-  if (!t) return;
-  const int L = ceil_log2(static_cast<std::size_t>(n));
-  t->scan_rounds_max = std::max(t->scan_rounds_max, L);
-  switch (algo) {
-    case FdAlgo::jsiia:
-      t->parallel_link_stages += 6;
-      break;
-    case FdAlgo::abia:
-      t->parallel_link_stages += 6;
-      t->longest_sequential_link_chain = std::max(t->longest_sequential_link_chain, n);
-      break;
-    case FdAlgo::cfa:
-      t->parallel_link_stages += 9;
-      t->oee_rounds = L;
-      break;
-  }
-}
-
 pd_algo to_c(FdAlgo a) {
   switch (a) {
     case FdAlgo::jsiia: return PD_JSIIA;
@@ -104,47 +83,335 @@ pd_algo to_c(FdAlgo a) {
   throw std::invalid_argument("forward_dynamics: unknown algorithm");
 }
 
+// Merge the trace of the variant that ran into *t (trace.hpp:24-39 semantics:
+// stages add up, the longest chain and deepest scan are maxima).
+void merge_trace(ExecTrace* t, const pd_exec_trace& r) {
+  if (!t) return;
+  t->parallel_link_stages += r.parallel_link_stages;
+  t->note_sequential_chain(r.longest_sequential_link_chain);
+  t->note_scan(ScanTrace{r.scan_rounds_max});
+  if (r.oee_rounds) t->note_oee(OeeTrace{r.oee_rounds});
+}
+
+void merge_last_trace(ExecTrace* t, pd_ctx* c) {
+  if (!t) return;
+  pd_exec_trace r{};
+  check_call(c, pd_last_trace(c, &r));
+  merge_trace(t, r);
+}
+
+// Upload one chain as the context's shared model; a bad link throws the way
+// link_inertias -> spatial_inertia_from does (spatial.cpp:72-87).
+pd_ctx* one_model(const RobotChain& chain) {
+  std::vector<double> rec;
+  detail::append_records(chain, rec);
+  pd_ctx* c = ctx();
+  int32_t ms = 0, mr = 0;
+  const int n = chain.size();
+  check_call(c, pd_set_models(c, 1, n, rec.data(), chain.gravity.data(), &ms, &mr));
+  if (ms != PD_SLOT_OK) throw std::invalid_argument(slot_message(ms, 0, mr, n));
+  return c;
+}
+
+template <int R, int C>
+void put_block(const Matrix<R, C>& m, double* out) {
+  m.toRowMajor(out);
+}
+template <int R, int C>
+Matrix<R, C> get_block(const double* in) {
+  return Matrix<R, C>::FromRowMajor(in);
+}
+
 }  // namespace
 
 namespace gpu {
 void set_device(int device) { t_device = device; }
 int device() { return t_device; }
+void set_devices(const std::vector<int>& devices) { t_devices = devices; }
+std::vector<int> devices() { return t_devices.empty() ? std::vector<int>{t_device} : t_devices; }
 }  // namespace gpu
 
+// ----------------------------------------------------------------- spatial algebra (spatial.cpp:10-100)
+Mat3 skew(const Vec3& a) { return Mat3::FromRowMajor({0.0, -a(2), a(1), a(2), 0.0, -a(0), -a(1), a(0), 0.0}); }
+
+namespace {
+void set3(Mat6& m, int r0, int c0, const Mat3& b) {
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) m(r0 + r, c0 + c) = b(r, c);
+}
+}  // namespace
+
+Mat6 small_adjoint(const Twist& v) {
+  Mat6 ad;
+  const Mat3 wx = skew(v.angular);
+  set3(ad, 0, 0, wx);
+  set3(ad, 3, 3, wx);
+  set3(ad, 3, 0, skew(v.linear));
+  return ad;
+}
+
+AdjointMap adjoint_of(const SE3Transform& t) {
+  AdjointMap a;
+  a.mat.setZero();
+  set3(a.mat, 0, 0, t.rotation);
+  set3(a.mat, 3, 3, t.rotation);
+  set3(a.mat, 3, 0, skew(t.translation) * t.rotation);
+  return a;
+}
+
+SE3Transform screw_exp(const Twist& s, double q) {
+  const Vec3& w = s.angular;
+  const Vec3& v = s.linear;
+  const double wn = w.norm();
+  SE3Transform t;
+  if (wn < 1e-12) {  // pure translation along the linear part
+    t.translation = q * v;
+    return t;
+  }
+  const Mat3 wx = skew(w), wx2 = wx * wx;
+  const double st = std::sin(wn * q), ct = std::cos(wn * q);
+  t.rotation = Mat3::Identity() + (st / wn) * wx + ((1.0 - ct) / (wn * wn)) * wx2;
+  t.translation = (q * Mat3::Identity() + ((1.0 - ct) / (wn * wn)) * wx + ((q - st / wn) / (wn * wn)) * wx2) * v;
+  return t;
+}
+
+SpatialInertia spatial_inertia_from(double mass, const Vec3& com, const Mat3& inertia_rot) {
+  if (!(mass > 0.0) || !std::isfinite(mass)) throw std::invalid_argument("spatial inertia: mass must be positive");
+  if (!com.allFinite() || !inertia_rot.allFinite())
+    throw std::invalid_argument("spatial inertia: parameters must be finite");
+  double scale = 0.0, asym = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      scale = std::max(scale, std::fabs(inertia_rot(r, c)));
+      asym = std::max(asym, std::fabs(inertia_rot(r, c) - inertia_rot(c, r)));
+    }
+  if (asym > 1e-9 * std::max(scale, 1.0))
+    throw std::invalid_argument("spatial inertia: rotational inertia must be symmetric");
+  if (!(detail::sym3_min_eig(inertia_rot) > 0.0))
+    throw std::invalid_argument("spatial inertia: rotational inertia must be positive definite");
+  const Mat3 cx = skew(com);
+  Mat6 m;
+  set3(m, 0, 0, inertia_rot + mass * (cx * cx.transpose()));
+  set3(m, 0, 3, mass * cx);
+  set3(m, 3, 0, mass * cx.transpose());
+  set3(m, 3, 3, mass * Mat3::Identity());
+  return SpatialInertia(m);
+}
+
+bool operator==(const LinkSpec& a, const LinkSpec& b) {
+  return a.mass == b.mass && a.com == b.com && a.inertia_rot == b.inertia_rot &&
+         a.joint_screw.angular == b.joint_screw.angular && a.joint_screw.linear == b.joint_screw.linear &&
+         a.home_transform.rotation == b.home_transform.rotation &&
+         a.home_transform.translation == b.home_transform.translation;
+}
+bool operator==(const RobotChain& a, const RobotChain& b) { return a.gravity == b.gravity && a.links == b.links; }
+
+// ----------------------------------------------------------------- model (device)
 RobotChain random_chain(int n, std::uint64_t seed) {
   if (n < 1) throw std::invalid_argument("random_chain: n must be at least 1");
   std::vector<double> rec(static_cast<std::size_t>(n) * PD_LINK_FIELDS);
   pd_random_chain(n, seed, rec.data());
-  RobotChain c;
-  c.links.resize(n);
-  for (int i = 0; i < n; ++i) {
-    const double* f = rec.data() + static_cast<std::size_t>(i) * PD_LINK_FIELDS;
-    LinkSpec& l = c.links[i];
-    l.mass = f[0];
-    for (int k = 0; k < 3; ++k) l.com[k] = f[1 + k];
-    for (int k = 0; k < 9; ++k) l.inertia_rot[k] = f[4 + k];
-    for (int k = 0; k < 6; ++k) l.joint_screw[k] = f[13 + k];
-    for (int k = 0; k < 9; ++k) l.home_rotation[k] = f[19 + k];
-    for (int k = 0; k < 3; ++k) l.home_translation[k] = f[28 + k];
-  }
-  return c;
+  return detail::chain_from_records(rec.data(), n);
 }
 
+ChainKinematics assemble_kinematics(const RobotChain& chain, const JointVector& q) {
+  const int n = chain.size();
+  if (static_cast<int>(q.size()) != n)  // model.cpp:120-124
+    throw std::invalid_argument("assemble_kinematics: q has length " + std::to_string(q.size()) +
+                                " but the chain has " + std::to_string(n) + " joints");
+  ChainKinematics kin;
+  if (n == 0) return kin;
+  pd_ctx* c = one_model(chain);
+  std::vector<double> rel(12 * n), base(36), tr(36 * (n - 1)), sc(6 * n);
+  check_call(c, pd_assemble_kinematics(c, 1, q.data(), rel.data(), base.data(), tr.data(), sc.data()));
+  kin.rel.resize(n);
+  kin.screw.resize(n);
+  kin.transport.resize(n - 1);
+  for (int i = 0; i < n; ++i) {
+    kin.rel[i].rotation = get_block<3, 3>(&rel[12 * i]);
+    kin.rel[i].translation = Vec3(rel[12 * i + 9], rel[12 * i + 10], rel[12 * i + 11]);
+    kin.screw[i] = Twist::from_stacked(get_block<6, 1>(&sc[6 * i]));
+  }
+  kin.base_transport.mat = get_block<6, 6>(base.data());
+  for (int i = 0; i + 1 < n; ++i) kin.transport[i].mat = get_block<6, 6>(&tr[36 * i]);
+  return kin;
+}
+
+std::vector<SpatialInertia> link_inertias(const RobotChain& chain) {
+  const int n = chain.size();
+  std::vector<SpatialInertia> out(static_cast<std::size_t>(n));
+  if (n == 0) return out;
+  pd_ctx* c = one_model(chain);
+  std::vector<double> J(36 * static_cast<std::size_t>(n));
+  check_call(c, pd_link_inertias(c, J.data()));
+  for (int i = 0; i < n; ++i) out[i] = SpatialInertia(get_block<6, 6>(&J[36 * i]));
+  return out;
+}
+
+// ----------------------------------------------------------------- operators (device)
+namespace {
+void kin_arrays(const ChainKinematics& kin, std::vector<double>& tr, std::vector<double>& sc) {
+  const int n = kin.size();
+  tr.assign(36 * static_cast<std::size_t>(std::max(n - 1, 0)), 0.0);
+  sc.assign(6 * static_cast<std::size_t>(n), 0.0);
+  for (int i = 0; i + 1 < n; ++i) put_block(kin.transport[i].mat, &tr[36 * i]);
+  for (int i = 0; i < n; ++i) put_block(kin.screw[i].stacked(), &sc[6 * i]);
+}
+}  // namespace
+
+ArticulatedBodyInertias articulated_body_inertias(const ChainKinematics& kin, std::span<const SpatialInertia> inertia,
+                                                  ExecTrace* trace) {
+  const int n = kin.size();
+  ArticulatedBodyInertias out;
+  if (n == 0) return out;
+  if (static_cast<int>(inertia.size()) != n || static_cast<int>(kin.transport.size()) != n - 1 ||
+      static_cast<int>(kin.screw.size()) != n)
+    throw std::invalid_argument("articulated_body_inertias: kinematics and inertias must match");
+  std::vector<double> tr, sc, J(36 * static_cast<std::size_t>(n)), abi(36 * n), lam(n), gain(6 * n);
+  kin_arrays(kin, tr, sc);
+  for (int i = 0; i < n; ++i) put_block(inertia[i].matrix(), &J[36 * i]);
+  pd_ctx* c = ctx();
+  int32_t st = 0, ix = 0;
+  check_call(c, pd_articulated_body_inertias(c, 1, n, tr.data(), J.data(), 0, sc.data(), abi.data(), lam.data(),
+                                             gain.data(), &st, &ix));
+  if (st != PD_SLOT_OK) throw_slot(st, 0, ix, n);
+  out.inertia.resize(n);
+  out.gain.resize(n);
+  out.joint_inertia = JointVector(n);
+  for (int i = 0; i < n; ++i) {
+    out.inertia[i] = get_block<6, 6>(&abi[36 * i]);
+    out.gain[i] = get_block<6, 1>(&gain[6 * i]);
+    out.joint_inertia[i] = lam[i];
+  }
+  if (trace) trace->note_sequential_chain(n);  // the tip-to-base walk (forward_dynamics.cpp:160)
+  return out;
+}
+
+ConstraintBasis build_constraint_basis(const RobotChain& chain) {
+  const int n = chain.size();
+  ConstraintBasis out;
+  out.basis.resize(n);
+  if (n == 0) return out;
+  std::vector<double> sc(6 * static_cast<std::size_t>(n)), W(30 * static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) put_block(chain.links[i].joint_screw.stacked(), &sc[6 * i]);
+  pd_ctx* c = ctx();
+  check_call(c, pd_constraint_basis(c, n, sc.data(), W.data()));
+  for (int i = 0; i < n; ++i) out.basis[i] = get_block<6, 5>(&W[30 * i]);
+  return out;
+}
+
+CfaOperators build_cfa_operators(const RobotChain& chain, const ChainKinematics& kin, const ConstraintBasis& basis,
+                                 ExecTrace* trace) {
+  const int n = chain.size();
+  if (n == 0) throw std::invalid_argument("build_cfa_operators: chain has no links");
+  if (static_cast<int>(basis.basis.size()) != n || kin.size() != n)
+    throw std::invalid_argument("build_cfa_operators: kinematics and basis must match the chain");
+  const std::vector<SpatialInertia> inertia = link_inertias(chain);  // validates like the reference (:273)
+  std::vector<double> tr, sc, J(36 * static_cast<std::size_t>(n)), W(30 * static_cast<std::size_t>(n));
+  kin_arrays(kin, tr, sc);
+  for (int i = 0; i < n; ++i) {
+    put_block(inertia[i].matrix(), &J[36 * i]);
+    put_block(basis.basis[i], &W[30 * i]);
+  }
+  const std::size_t e = static_cast<std::size_t>(n - 1);
+  std::vector<double> D(25 * n), U(25 * e), bs(5 * e), bd(5 * n), bp(5 * e), cd(n), co(e);
+  pd_ctx* c = ctx();
+  int32_t st = 0, ix = 0;
+  check_call(c, pd_cfa_operators(c, 1, n, J.data(), 0, tr.data(), sc.data(), W.data(), D.data(), U.data(), bs.data(),
+                                 bd.data(), bp.data(), cd.data(), co.data(), &st, &ix));
+  if (st != PD_SLOT_OK) throw_slot(st, 0, ix, n);
+  CfaOperators ops;
+  ops.constraint_op.diag.resize(n);
+  ops.constraint_op.upper.resize(e);
+  ops.cross_diag.resize(n);
+  ops.cross_sub.resize(e);
+  ops.cross_super.resize(e);
+  ops.joint_diag = JointVector(n);
+  ops.joint_off = JointVector(e);
+  for (int i = 0; i < n; ++i) {
+    ops.constraint_op.diag[i] = get_block<5, 5>(&D[25 * i]);
+    ops.cross_diag[i] = get_block<5, 1>(&bd[5 * i]);
+    ops.joint_diag[i] = cd[i];
+  }
+  for (std::size_t i = 0; i < e; ++i) {
+    ops.constraint_op.upper[i] = get_block<5, 5>(&U[25 * i]);
+    ops.cross_sub[i] = get_block<5, 1>(&bs[5 * i]);
+    ops.cross_super[i] = get_block<5, 1>(&bp[5 * i]);
+    ops.joint_off[i] = co[i];
+  }
+  if (trace) {  // per-link factor-solves, then per-row projections (forward_dynamics.cpp:322,354)
+    trace->note_parallel_stage();
+    trace->note_parallel_stage();
+  }
+  return ops;
+}
+
+namespace {
+std::vector<double> flat5(const std::vector<Vec5>& v) {
+  std::vector<double> out(5 * v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) put_block(v[i], &out[5 * i]);
+  return out;
+}
+}  // namespace
+
+std::vector<Vec5> CfaOperators::apply_cross(const JointVector& v) const {
+  const std::size_t n = cross_diag.size();
+  if (v.size() != n) throw std::invalid_argument("apply_cross: one entry per link expected");
+  std::vector<Vec5> out(n);
+  if (n == 0) return out;
+  const std::vector<double> bs = flat5(cross_sub), bd = flat5(cross_diag), bp = flat5(cross_super);
+  std::vector<double> r(5 * n);
+  pd_ctx* c = ctx();
+  check_call(c, pd_cfa_apply(c, PD_APPLY_CROSS, 1, static_cast<int32_t>(n), bs.data(), bd.data(), bp.data(), nullptr,
+                             nullptr, v.data(), r.data()));
+  for (std::size_t i = 0; i < n; ++i) out[i] = get_block<5, 1>(&r[5 * i]);
+  return out;
+}
+
+JointVector CfaOperators::apply_cross_transpose(std::span<const Vec5> f) const {
+  const std::size_t n = cross_diag.size();
+  if (f.size() != n) throw std::invalid_argument("apply_cross_transpose: one constraint block per link expected");
+  JointVector out(n);
+  if (n == 0) return out;
+  const std::vector<double> bs = flat5(cross_sub), bd = flat5(cross_diag), bp = flat5(cross_super),
+                            ff = flat5(std::vector<Vec5>(f.begin(), f.end()));
+  pd_ctx* c = ctx();
+  check_call(c, pd_cfa_apply(c, PD_APPLY_CROSS_TRANSPOSE, 1, static_cast<int32_t>(n), bs.data(), bd.data(), bp.data(),
+                             nullptr, nullptr, ff.data(), out.data()));
+  return out;
+}
+
+JointVector CfaOperators::apply_joint(const JointVector& v) const {
+  const std::size_t n = joint_diag.size();
+  if (v.size() != n) throw std::invalid_argument("apply_joint: one entry per link expected");
+  JointVector out(n);
+  if (n == 0) return out;
+  pd_ctx* c = ctx();
+  check_call(c, pd_cfa_apply(c, PD_APPLY_JOINT, 1, static_cast<int32_t>(n), nullptr, nullptr, nullptr,
+                             joint_diag.data(), joint_off.data(), v.data(), out.data()));
+  return out;
+}
+
+// ----------------------------------------------------------------- forward dynamics (device)
 JointVector forward_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
                              const JointVector& tau, FdAlgo algo, ExecTrace* trace) {
   const pd_algo a = to_c(algo);
   check_sizes(chain, q, qdot, tau);
   const int n = chain.size();
-  std::vector<double> links;
-  links.reserve(static_cast<std::size_t>(n) * PD_LINK_FIELDS);
-  for (const LinkSpec& l : chain.links) append_link(l, links);
-  pd_ctx* c = ctx();
-  check_call(c, pd_set_models(c, 1, n, links.data(), chain.gravity.data(), nullptr, nullptr));
+  pd_ctx* c = one_model(chain);
   JointVector out(n);
   int32_t st = 0, rd = 0, ix = 0;
+  if (trace) {
+    // log-depth (CTA) variants; the trace describes the variant that ran
+    pd_exec_trace r{};
+    check_call(c, pd_forward_dynamics_traced(c, a, 1, q.data(), qdot.data(), tau.data(), out.data(), &st, &rd, &ix,
+                                             &r));
+    if (st != PD_SLOT_OK) throw_slot(st, rd, ix, n);
+    merge_trace(trace, r);
+    return out;
+  }
   check_call(c, pd_forward_dynamics(c, a, 1, q.data(), qdot.data(), tau.data(), out.data(), &st, &rd, &ix));
   if (st != PD_SLOT_OK) throw_slot(st, rd, ix, n);
-  fill_trace(trace, algo, n);
   return out;
 }
 
@@ -161,56 +428,106 @@ JointVector cfa_forward_dynamics(const RobotChain& chain, const JointVector& q, 
   return forward_dynamics(chain, q, qdot, tau, FdAlgo::cfa, trace);
 }
 
+namespace {
+
+// One bucket (equal n) packed for the C-ABI: models, gravities, states.
+struct Bucket {
+  int n = 0;
+  std::vector<std::size_t> idx;
+  std::vector<double> links, grav, q, qd, tau, qdd;
+  std::vector<int32_t> st, rd, ix;
+};
+
+// Solve slots [lo, hi) of a packed bucket on one device; every slice selects
+// kernels for the whole bucket (pd_set_selection_batch), so the result does
+// not depend on how the bucket was split.
+void solve_slice(pd_ctx* c, pd_algo a, Bucket& b, std::size_t lo, std::size_t hi) {
+  const std::size_t cnt = hi - lo, n = static_cast<std::size_t>(b.n);
+  if (cnt == 0) return;
+  check_call(c, pd_set_selection_batch(c, static_cast<int64_t>(b.idx.size())));
+  check_call(c, pd_set_models(c, static_cast<int64_t>(cnt), b.n, b.links.data() + lo * n * PD_LINK_FIELDS,
+                              b.grav.data() + 3 * lo, nullptr, nullptr));
+  const pd_status s = pd_forward_dynamics(c, a, static_cast<int64_t>(cnt), b.q.data() + lo * n, b.qd.data() + lo * n,
+                                          b.tau.data() + lo * n, b.qdd.data() + lo * n, b.st.data() + lo,
+                                          b.rd.data() + lo, b.ix.data() + lo);
+  pd_set_selection_batch(c, 0);
+  check_call(c, s);
+}
+
+}  // namespace
+
 // forward_dynamics.cpp:466-481: never throws per problem. Problems are
-// bucketed by link count; each bucket is one pd_forward_dynamics call.
+// bucketed by link count; a bucket is split into contiguous slices over
+// gpu::devices(), one host thread and one context per device.
 std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems, FdAlgo algo) {
   const pd_algo a = to_c(algo);
   std::vector<FdResult> out(problems.size());
-  std::map<int, std::vector<std::size_t>> buckets;
+  std::map<int, Bucket> buckets;
   for (std::size_t k = 0; k < problems.size(); ++k) {
     const FdProblem& p = problems[k];
     try {
       check_sizes(p.chain, p.q, p.qdot, p.tau);
-      buckets[p.chain.size()].push_back(k);
+      buckets[p.chain.size()].idx.push_back(k);
     } catch (const std::exception& e) {
       out[k].error = e.what();
     }
   }
-  if (buckets.empty()) return out;
-  pd_ctx* c = ctx();
-  for (const auto& [n, idx] : buckets) {
-    const std::size_t B = idx.size();
-    std::vector<double> links, grav, q, qd, tau;
-    links.reserve(B * n * PD_LINK_FIELDS);
-    q.reserve(B * n);
-    qd.reserve(B * n);
-    tau.reserve(B * n);
-    for (std::size_t k : idx) {
+  const std::vector<int> devs = gpu::devices();
+  for (auto& [n, b] : buckets) {
+    b.n = n;
+    const std::size_t B = b.idx.size();
+    b.links.reserve(B * n * PD_LINK_FIELDS);
+    b.grav.reserve(3 * B);
+    for (std::vector<double>* v : {&b.q, &b.qd, &b.tau}) v->reserve(B * n);
+    for (std::size_t k : b.idx) {
       const FdProblem& p = problems[k];
-      for (const LinkSpec& l : p.chain.links) append_link(l, links);
-      grav.insert(grav.end(), p.chain.gravity.begin(), p.chain.gravity.end());
-      q.insert(q.end(), p.q.data(), p.q.data() + n);
-      qd.insert(qd.end(), p.qdot.data(), p.qdot.data() + n);
-      tau.insert(tau.end(), p.tau.data(), p.tau.data() + n);
+      detail::append_records(p.chain, b.links);
+      b.grav.insert(b.grav.end(), p.chain.gravity.begin(), p.chain.gravity.end());
+      b.q.insert(b.q.end(), p.q.begin(), p.q.end());
+      b.qd.insert(b.qd.end(), p.qdot.begin(), p.qdot.end());
+      b.tau.insert(b.tau.end(), p.tau.begin(), p.tau.end());
     }
-    check_call(c, pd_set_models(c, static_cast<int64_t>(B), n, links.data(), grav.data(), nullptr, nullptr));
-    std::vector<double> qdd(B * n);
-    std::vector<int32_t> st(B), rd(B), ix(B);
-    check_call(c, pd_forward_dynamics(c, a, static_cast<int64_t>(B), q.data(), qd.data(), tau.data(), qdd.data(),
-                                      st.data(), rd.data(), ix.data()));
-    for (std::size_t j = 0; j < B; ++j) {
-      FdResult& r = out[idx[j]];
-      if (st[j] == PD_SLOT_OK) {
-        r.qddot = JointVector(n);
-        for (int i = 0; i < n; ++i) r.qddot[i] = qdd[j * n + i];
-      } else {
-        r.error = slot_message(st[j], rd[j], ix[j], n);
+    b.qdd.resize(B * n);
+    b.st.resize(B);
+    b.rd.resize(B);
+    b.ix.resize(B);
+    const std::size_t G = std::min<std::size_t>(devs.size(), B);
+    if (G <= 1) {
+      solve_slice(ctx_on(devs[0]), a, b, 0, B);
+    } else {
+      std::vector<std::thread> workers;
+      std::vector<std::string> errors(G);
+      std::vector<int> kinds(G, 0);
+      for (std::size_t g = 0; g < G; ++g)
+        workers.emplace_back([&, g] {
+          try {
+            solve_slice(ctx_on(devs[g]), a, b, B * g / G, B * (g + 1) / G);
+          } catch (const std::invalid_argument& e) {
+            errors[g] = e.what();
+            kinds[g] = 1;
+          } catch (const std::exception& e) {
+            errors[g] = e.what();
+            kinds[g] = 2;
+          }
+        });
+      for (std::thread& w : workers) w.join();
+      for (std::size_t g = 0; g < G; ++g) {
+        if (kinds[g] == 1) throw std::invalid_argument(errors[g]);
+        if (kinds[g] == 2) throw DeviceError(errors[g]);
       }
+    }
+    for (std::size_t j = 0; j < B; ++j) {
+      FdResult& r = out[b.idx[j]];
+      if (b.st[j] == PD_SLOT_OK)
+        r.qddot = JointVector(b.qdd.begin() + j * n, b.qdd.begin() + (j + 1) * n);
+      else
+        r.error = slot_message(b.st[j], b.rd[j], b.ix[j], n);
     }
   }
   return out;
 }
 
+// ----------------------------------------------------------------- inverse dynamics (device)
 namespace {
 
 void id_sizes(const RobotChain& chain, std::initializer_list<std::pair<const char*, const JointVector*>> args) {
@@ -221,17 +538,11 @@ void id_sizes(const RobotChain& chain, std::initializer_list<std::pair<const cha
                                   " but the chain has " + std::to_string(n) + " joints");
 }
 
-// One shared model on this thread's context; a bad link throws as
-// link_inertias -> spatial_inertia_from does (spatial.cpp:72-87).
-pd_ctx* one_model(const RobotChain& chain) {
-  const std::size_t n = chain.links.size();
-  std::vector<double> links;
-  for (const LinkSpec& l : chain.links) append_link(l, links);
-  pd_ctx* c = ctx();
-  int32_t ms = 0, mr = 0;
-  check_call(c, pd_set_models(c, 1, static_cast<int32_t>(n), links.data(), chain.gravity.data(), &ms, &mr));
-  if (ms != PD_SLOT_OK) throw std::invalid_argument(slot_message(ms, 0, mr, static_cast<int>(n)));
-  return c;
+// model.cpp:120-124 (assemble_kinematics runs first in the reference)
+void q_size(const RobotChain& chain, const JointVector& q) {
+  if (q.size() != chain.links.size())
+    throw std::invalid_argument("assemble_kinematics: q has length " + std::to_string(q.size()) +
+                                " but the chain has " + std::to_string(chain.links.size()) + " joints");
 }
 
 pd_id_options to_c(const IdOptions& o) {
@@ -249,109 +560,103 @@ pd_id_options to_c(const IdOptions& o) {
 }  // namespace
 
 JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
-                             const JointVector& qddot, const IdOptions& opts) {
-  id_sizes(chain, {{"q", &q}, {"qdot", &qdot}, {"qddot", &qddot}});
+                             const JointVector& qddot, const IdOptions& opts, ExecTrace* trace) {
+  q_size(chain, q);
   const std::size_t n = chain.links.size();
   if (n == 0) return JointVector();
-  pd_ctx* c = one_model(chain);
+  pd_ctx* c = one_model(chain);  // link_inertias validates before the rates are checked
+  id_sizes(chain, {{"qdot", &qdot}, {"qddot", &qddot}});
   JointVector tau(n);
   const pd_id_options o = to_c(opts);
   check_call(c, pd_inverse_dynamics_opts(c, 1, q.data(), qdot.data(), qddot.data(), &o, tau.data()));
+  merge_last_trace(trace, c);
   return tau;
 }
 
-JointVector bias_torque(const RobotChain& chain, const JointVector& q, const JointVector& qdot) {
-  id_sizes(chain, {{"q", &q}, {"qdot", &qdot}});
-  const std::size_t n = chain.links.size();
-  if (n == 0) return JointVector();
-  pd_ctx* c = one_model(chain);
-  JointVector tau(n);
-  check_call(c, pd_bias_torque(c, 1, q.data(), qdot.data(), tau.data()));
-  return tau;
+JointVector bias_torque(const RobotChain& chain, const JointVector& q, const JointVector& qdot, ExecTrace* trace) {
+  return inverse_dynamics(chain, q, qdot, JointVector::Zero(chain.links.size()), {}, trace);
 }
 
 LinkStates link_states(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
                        const JointVector& qddot, const IdOptions& opts) {
-  id_sizes(chain, {{"q", &q}, {"qdot", &qdot}, {"qddot", &qddot}});
+  q_size(chain, q);
   const std::size_t n = chain.links.size();
   LinkStates out;
   if (n == 0) return out;
   pd_ctx* c = one_model(chain);
+  id_sizes(chain, {{"qdot", &qdot}, {"qddot", &qddot}});
   std::vector<double> v(6 * n), a(6 * n), f(6 * n);
   const pd_id_options o = to_c(opts);
   check_call(c, pd_link_states(c, 1, q.data(), qdot.data(), qddot.data(), &o, v.data(), a.data(), f.data()));
-  auto six = [](const std::vector<double>& x, std::size_t i) {
-    Vec6 r;
-    for (int k = 0; k < 6; ++k) r[k] = x[6 * i + k];
-    return r;
-  };
   for (std::size_t i = 0; i < n; ++i) {
-    out.velocity.push_back(Twist::from_stacked(six(v, i)));
-    out.acceleration.push_back(Twist::from_stacked(six(a, i)));
-    out.force.push_back(Wrench::from_stacked(six(f, i)));
+    out.velocity.push_back(Twist::from_stacked(get_block<6, 1>(&v[6 * i])));
+    out.acceleration.push_back(Twist::from_stacked(get_block<6, 1>(&a[6 * i])));
+    out.force.push_back(Wrench::from_stacked(get_block<6, 1>(&f[6 * i])));
   }
   return out;
 }
 
-MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q) {
+MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q, ExecTrace* trace) {
   const std::size_t n = chain.links.size();
   if (q.size() != n) throw std::invalid_argument("joint_space_inertia: q must have one entry per joint");
   MatrixXd M(n, n);
   if (n == 0) return M;
   pd_ctx* c = one_model(chain);
   check_call(c, pd_joint_space_inertia(c, 1, q.data(), M.data()));
+  merge_last_trace(trace, c);
   return M;
 }
 
+// ----------------------------------------------------------------- building blocks (device)
 namespace {
 
-std::vector<std::array<double, 6>> bidiag(const BlockBiDiagSystem<6>& sys, bool upper, ScanTrace* trace) {
+std::vector<Vec6> bidiag(const BlockBiDiagSystem<6>& sys, bool upper, ScanTrace* trace) {
   const std::size_t n = sys.rhs.size();
   if (sys.coupling.size() + 1 != n && !(n == 0 && sys.coupling.empty()))
     throw std::invalid_argument("block bi-diagonal solve: need n - 1 coupling blocks for n right-hand sides");
   if (trace) trace->rounds = ceil_log2(n);  // the scan's designed depth (scan.hpp:32-65)
-  std::vector<std::array<double, 6>> x(n);
+  std::vector<Vec6> x(n);
   if (n == 0) return x;
-  std::vector<double> c, r, xo(6 * n);
-  for (const auto& b : sys.coupling) c.insert(c.end(), b.begin(), b.end());
-  for (const auto& b : sys.rhs) r.insert(r.end(), b.begin(), b.end());
+  std::vector<double> c(36 * (n - 1)), r(6 * n), xo(6 * n);
+  for (std::size_t k = 0; k + 1 < n; ++k) put_block(sys.coupling[k], &c[36 * k]);
+  for (std::size_t k = 0; k < n; ++k) put_block(sys.rhs[k], &r[6 * k]);
   pd_ctx* cx = ctx();
   check_call(cx, pd_block_bidiag_solve6(cx, 1, static_cast<int32_t>(n), upper ? 1 : 0, c.empty() ? nullptr : c.data(),
                                        r.data(), xo.data()));
-  for (std::size_t k = 0; k < n; ++k)
-    for (int e = 0; e < 6; ++e) x[k][e] = xo[6 * k + e];
+  for (std::size_t k = 0; k < n; ++k) x[k] = get_block<6, 1>(&xo[6 * k]);
   return x;
 }
 
 }  // namespace
 
-std::vector<std::array<double, 6>> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
+std::vector<Vec6> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
   return bidiag(sys, false, trace);
 }
 
-std::vector<std::array<double, 6>> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
+std::vector<Vec6> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
   return bidiag(sys, true, trace);
 }
 
-std::vector<std::array<double, 5>> oee_solve(const SymBlockTriDiagSystem<5>& sys,
-                                             const std::vector<std::array<double, 5>>& rhs, OeeTrace* trace) {
+std::vector<Vec5> oee_solve(const SymBlockTriDiagSystem<5>& sys, const std::vector<Vec5>& rhs, OeeTrace* trace) {
   const std::size_t n = sys.diag.size();
   if (rhs.size() != n || (n > 0 && sys.upper.size() + 1 != n))
     throw std::invalid_argument("odd-even elimination: inconsistent block counts");
-  if (trace) trace->rounds = ceil_log2(n);
-  std::vector<std::array<double, 5>> x(n);
+  if (trace) trace->rounds = 0;
+  std::vector<Vec5> x(n);
   if (n == 0) return x;
-  std::vector<double> d, u, r, xo(5 * n);
-  for (const auto& b : sys.diag) d.insert(d.end(), b.begin(), b.end());
-  for (const auto& b : sys.upper) u.insert(u.end(), b.begin(), b.end());
-  for (const auto& b : rhs) r.insert(r.end(), b.begin(), b.end());
+  std::vector<double> d(25 * n), u(25 * (n - 1)), r(5 * n), xo(5 * n);
+  for (std::size_t k = 0; k < n; ++k) {
+    put_block(sys.diag[k], &d[25 * k]);
+    put_block(rhs[k], &r[5 * k]);
+  }
+  for (std::size_t k = 0; k + 1 < n; ++k) put_block(sys.upper[k], &u[25 * k]);
   pd_ctx* cx = ctx();
   int32_t st = 0, rd = 0, ix = 0;
   check_call(cx, pd_block_tridiag_solve5(cx, 1, static_cast<int32_t>(n), d.data(), u.empty() ? nullptr : u.data(),
                                          r.data(), xo.data(), &st, &rd, &ix));
   if (st != PD_SLOT_OK) throw SingularBlockError(rd, ix, slot_message(st, rd, ix, static_cast<int>(n)));
-  for (std::size_t k = 0; k < n; ++k)
-    for (int e = 0; e < 5; ++e) x[k][e] = xo[5 * k + e];
+  if (trace) trace->rounds = ceil_log2(n);
+  for (std::size_t k = 0; k < n; ++k) x[k] = get_block<5, 1>(&xo[5 * k]);
   return x;
 }
 

@@ -940,6 +940,8 @@ pd_status run_idyn_host(pd_ctx* ctx, int64_t batch, const double* q, const doubl
   launch_idyn(model_view(ctx), io, id_opts(opts), ctx->raw.as<double>(), sv, sv ? sv + sn : nullptr,
               sv ? sv + 2 * sn : nullptr, ctx->stream);
   ctx->launches++;
+  // lane per chain: the V / A and F recursions walk the n links sequentially
+  note_variant(ctx, "idyn_lane_kernel", 0, n, 0, 0);
   PD_CUDA(cudaGetLastError());
   if (tau) {
     launch_transpose(ctx, stau, stau + half, n, batch, batch, n);
@@ -1011,6 +1013,7 @@ pd_status pd_inverse_dynamics_device(pd_ctx* ctx, int64_t batch, const double* d
   BatchIO io{d_q, d_qdot, d_qddot, d_tau, st, st + batch, st + 2 * batch, batch, batch};
   launch_idyn(model_view(ctx), io, id_opts(opts), ctx->raw.as<double>(), nullptr, nullptr, nullptr, ctx->stream);
   ctx->launches++;
+  note_variant(ctx, "idyn_lane_kernel", 0, ctx->n_links, 0, 0);
   PD_CUDA(cudaGetLastError());
   return PD_OK;
 }
@@ -1047,6 +1050,11 @@ pd_status pd_joint_space_inertia(pd_ctx* ctx, int64_t batch, const double* q, do
   BatchIO io{sq, sq, sq, nullptr, st, st + batch, st + 2 * batch, batch, batch};
   launch_jsi(mv, io, ctx->cta_ws.as<double>(), slots, ctx->sm_count, ctx->io_qdd.as<double>(), ctx->stream);
   ctx->launches += slots ? (batch + slots - 1) / slots : 1;
+  {  // CTA per chain: kinematics, S0 / J0, the composite-inertia suffix scan, the M fill
+    const CtaShape cs = cta_shape(n, 32 * jsiia_warps(n, batch, ctx->sm_count));
+    note_variant(ctx, std::string("jsiia_tiled_kernel<") + (slots ? "global" : "smem") + ", M only>", 4,
+                 cs.lpt > 1 ? cs.lpt : 0, ceil_log2_host(cs.groups), 0);
+  }
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaMemcpyAsync(M, ctx->io_qdd.p, mbytes, cudaMemcpyDeviceToHost, ctx->stream));
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1217,6 +1225,264 @@ pd_status pd_set_models_workload(pd_ctx* ctx, uint64_t cell_seed, int32_t n_link
   ctx->model_ld = model_ld;
   ctx->model_cl_valid = false;
   return PD_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- operator builders (operators.cu)
+namespace pd {
+void launch_kinematics(const double* raw, int n, int64_t n_models, int64_t batch, const double* q, double* rel,
+                       double* base_transport, double* transport, double* screw, cudaStream_t s);
+void launch_link_inertias(const double* raw, int64_t count, double* out, cudaStream_t s);
+void launch_abi(int64_t batch, int n, const double* transport, const double* inertia, int64_t inertia_stride,
+                const double* screw, double* abi, double* joint_inertia, double* gain, int32_t* status,
+                int32_t* index, cudaStream_t s);
+void launch_basis(int64_t count, const double* screw, double* basis, cudaStream_t s);
+void launch_cfa_ops(int64_t batch, int n, const double* inertia, int64_t istride, const double* transport,
+                    const double* screw, const double* basis, double* diag, double* upper, double* cross_sub,
+                    double* cross_diag, double* cross_super, double* joint_diag, double* joint_off, int32_t* bad_link,
+                    cudaStream_t s);
+void launch_cfa_apply(int op, int64_t batch, int n, const double* cross_sub, const double* cross_diag,
+                      const double* cross_super, const double* joint_diag, const double* joint_off, const double* in,
+                      double* out, cudaStream_t s);
+}  // namespace pd
+
+namespace {
+
+// One host-buffer call of an operator builder: inputs are copied into one
+// device arena, the kernel runs, outputs come back; the arena (ctx->states)
+// is reused across calls.
+struct Arena {
+  struct In {
+    const void* host;
+    size_t bytes;
+  };
+  struct Out {
+    void* host;
+    size_t bytes;
+  };
+  std::vector<In> ins;
+  std::vector<Out> outs;
+  std::vector<size_t> in_off, out_off;
+  char* base = nullptr;
+  size_t add_in(const void* h, size_t b) {
+    ins.push_back({h, b});
+    return ins.size() - 1;
+  }
+  size_t add_out(void* h, size_t b) {
+    outs.push_back({h, b});
+    return outs.size() - 1;
+  }
+  pd_status stage(pd_ctx* ctx) {
+    size_t off = 0;
+    auto pad = [](size_t b) { return (b + 255) / 256 * 256; };
+    for (const In& i : ins) {
+      in_off.push_back(off);
+      off += pad(i.bytes);
+    }
+    for (const Out& o : outs) {
+      out_off.push_back(off);
+      off += pad(o.bytes);
+    }
+    PD_CUDA(ctx->states.ensure(off + 256));
+    base = ctx->states.as<char>();
+    for (size_t k = 0; k < ins.size(); ++k)
+      if (ins[k].bytes)
+        PD_CUDA(cudaMemcpyAsync(base + in_off[k], ins[k].host, ins[k].bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return PD_OK;
+  }
+  template <class T>
+  T* in(size_t k) const {
+    return reinterpret_cast<T*>(base + in_off[k]);
+  }
+  template <class T>
+  T* out(size_t k) const {
+    return reinterpret_cast<T*>(base + out_off[k]);
+  }
+  pd_status finish(pd_ctx* ctx) {
+    PD_CUDA(cudaGetLastError());
+    for (size_t k = 0; k < outs.size(); ++k)
+      if (outs[k].bytes && outs[k].host)
+        PD_CUDA(cudaMemcpyAsync(outs[k].host, base + out_off[k], outs[k].bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+  }
+};
+
+bool bad_args(pd_ctx* ctx, bool bad, const char* what) {
+  if (bad) ctx->last_error = what;
+  return bad;
+}
+
+}  // namespace
+
+extern "C" {
+
+pd_status pd_assemble_kinematics(pd_ctx* ctx, int64_t batch, const double* q, double* rel, double* base_transport,
+                                 double* transport, double* screw) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (bad_args(ctx, batch < 0 || (batch > 0 && (!q || !rel || !base_transport || !screw)),
+               "assemble_kinematics: null buffer"))
+    return PD_INVALID_ARGUMENT;
+  if (batch == 0) return PD_OK;
+  if (ctx->n_models <= 0 || (ctx->n_models != 1 && ctx->n_models != batch)) {
+    ctx->last_error = "assemble_kinematics: batch must equal the number of models (or use one shared model)";
+    return PD_INVALID_ARGUMENT;
+  }
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int n = ctx->n_links;
+  Arena a;
+  const size_t iq = a.add_in(q, sizeof(double) * n * batch);
+  const size_t orel = a.add_out(rel, sizeof(double) * 12 * n * batch);
+  const size_t obase = a.add_out(base_transport, sizeof(double) * 36 * batch);
+  const size_t otr = a.add_out(transport, sizeof(double) * 36 * (n - 1) * batch);
+  const size_t osc = a.add_out(screw, sizeof(double) * 6 * n * batch);
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  launch_kinematics(ctx->raw.as<double>(), n, ctx->n_models, batch, a.in<double>(iq), a.out<double>(orel),
+                    a.out<double>(obase), a.out<double>(otr), a.out<double>(osc), ctx->stream);
+  ctx->launches++;
+  return a.finish(ctx);
+}
+
+pd_status pd_link_inertias(pd_ctx* ctx, double* inertia) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (bad_args(ctx, !inertia, "link_inertias: null buffer")) return PD_INVALID_ARGUMENT;
+  if (ctx->n_models <= 0) {
+    ctx->last_error = "link_inertias: no models set (pd_set_models)";
+    return PD_INVALID_ARGUMENT;
+  }
+  pd_status cs = check_models(ctx, ctx->n_models, "link_inertias");
+  if (cs != PD_OK) return cs;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int64_t count = ctx->n_models * ctx->n_links;
+  Arena a;
+  const size_t o = a.add_out(inertia, sizeof(double) * 36 * count);
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  launch_link_inertias(ctx->raw.as<double>(), count, a.out<double>(o), ctx->stream);
+  ctx->launches++;
+  return a.finish(ctx);
+}
+
+pd_status pd_articulated_body_inertias(pd_ctx* ctx, int64_t batch, int32_t n, const double* transport,
+                                       const double* inertia, int32_t shared_inertia, const double* screw,
+                                       double* abi, double* joint_inertia, double* gain, int32_t* slot_status,
+                                       int32_t* slot_index) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (bad_args(ctx, batch < 0 || n < 1 || (batch > 0 && (!inertia || !screw || !abi || !joint_inertia || !gain ||
+                                                          (n > 1 && !transport))),
+               "articulated_body_inertias: need n >= 1 and non-null buffers"))
+    return PD_INVALID_ARGUMENT;
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int64_t ib = shared_inertia ? 1 : batch;
+  Arena a;
+  const size_t itr = a.add_in(transport, sizeof(double) * 36 * (n - 1) * batch);
+  const size_t iin = a.add_in(inertia, sizeof(double) * 36 * n * ib);
+  const size_t isc = a.add_in(screw, sizeof(double) * 6 * n * batch);
+  const size_t oab = a.add_out(abi, sizeof(double) * 36 * n * batch);
+  const size_t oji = a.add_out(joint_inertia, sizeof(double) * n * batch);
+  const size_t oga = a.add_out(gain, sizeof(double) * 6 * n * batch);
+  const size_t ost = a.add_out(slot_status, sizeof(int32_t) * batch);
+  const size_t oix = a.add_out(slot_index, sizeof(int32_t) * batch);
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  launch_abi(batch, n, a.in<double>(itr), a.in<double>(iin), shared_inertia ? 0 : 36 * (int64_t)n, a.in<double>(isc),
+             a.out<double>(oab), a.out<double>(oji), a.out<double>(oga), a.out<int32_t>(ost), a.out<int32_t>(oix),
+             ctx->stream);
+  ctx->launches++;
+  return a.finish(ctx);
+}
+
+pd_status pd_constraint_basis(pd_ctx* ctx, int64_t count, const double* screw, double* basis) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (bad_args(ctx, count < 0 || (count > 0 && (!screw || !basis)), "build_constraint_basis: null buffer"))
+    return PD_INVALID_ARGUMENT;
+  if (count == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  Arena a;
+  const size_t isc = a.add_in(screw, sizeof(double) * 6 * count);
+  const size_t ob = a.add_out(basis, sizeof(double) * 30 * count);
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  launch_basis(count, a.in<double>(isc), a.out<double>(ob), ctx->stream);
+  ctx->launches++;
+  return a.finish(ctx);
+}
+
+pd_status pd_cfa_operators(pd_ctx* ctx, int64_t batch, int32_t n, const double* inertia, int32_t shared_inertia,
+                           const double* transport, const double* screw, const double* basis, double* constraint_diag,
+                           double* constraint_upper, double* cross_sub, double* cross_diag, double* cross_super,
+                           double* joint_diag, double* joint_off, int32_t* slot_status, int32_t* slot_index) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (bad_args(ctx, batch < 0 || n < 1 || (batch > 0 && (!inertia || !screw || !basis || !constraint_diag ||
+                                                          !cross_diag || !joint_diag ||
+                                                          (n > 1 && (!transport || !constraint_upper || !cross_sub ||
+                                                                     !cross_super || !joint_off)))),
+               "build_cfa_operators: need n >= 1 and non-null buffers"))
+    return PD_INVALID_ARGUMENT;
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int64_t ib = shared_inertia ? 1 : batch, e = (int64_t)(n - 1) * batch, r = (int64_t)n * batch;
+  Arena a;
+  const size_t iin = a.add_in(inertia, sizeof(double) * 36 * n * ib);
+  const size_t itr = a.add_in(transport, sizeof(double) * 36 * e);
+  const size_t isc = a.add_in(screw, sizeof(double) * 6 * r);
+  const size_t iba = a.add_in(basis, sizeof(double) * 30 * r);
+  const size_t od = a.add_out(constraint_diag, sizeof(double) * 25 * r);
+  const size_t ou = a.add_out(constraint_upper, sizeof(double) * 25 * e);
+  const size_t obs = a.add_out(cross_sub, sizeof(double) * 5 * e);
+  const size_t obd = a.add_out(cross_diag, sizeof(double) * 5 * r);
+  const size_t obp = a.add_out(cross_super, sizeof(double) * 5 * e);
+  const size_t ocd = a.add_out(joint_diag, sizeof(double) * r);
+  const size_t oco = a.add_out(joint_off, sizeof(double) * e);
+  const size_t obad = a.add_out(nullptr, sizeof(int32_t) * batch);
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  int32_t* bad = a.out<int32_t>(obad);
+  launch_cfa_ops(batch, n, a.in<double>(iin), shared_inertia ? 0 : 36 * (int64_t)n, a.in<double>(itr),
+                 a.in<double>(isc), a.in<double>(iba), a.out<double>(od), a.out<double>(ou), a.out<double>(obs),
+                 a.out<double>(obd), a.out<double>(obp), a.out<double>(ocd), a.out<double>(oco), bad, ctx->stream);
+  ctx->launches += 2;
+  st = a.finish(ctx);
+  if (st != PD_OK) return st;
+  std::vector<int32_t> hb(batch);
+  PD_CUDA(cudaMemcpy(hb.data(), bad, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost));
+  for (int64_t p = 0; p < batch; ++p) {  // a link LLT failure: forward_dynamics.cpp:317-320
+    if (slot_status) slot_status[p] = hb[p] < n ? PD_SLOT_LINK_INERTIA_NOT_PD : PD_SLOT_OK;
+    if (slot_index) slot_index[p] = hb[p] < n ? hb[p] : 0;
+  }
+  return PD_OK;
+}
+
+pd_status pd_cfa_apply(pd_ctx* ctx, int32_t op, int64_t batch, int32_t n, const double* cross_sub,
+                       const double* cross_diag, const double* cross_super, const double* joint_diag,
+                       const double* joint_off, const double* in, double* out) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  const bool joint = op == PD_APPLY_JOINT;
+  if (bad_args(ctx, op < PD_APPLY_CROSS || op > PD_APPLY_JOINT || batch < 0 || n < 1 ||
+                        (batch > 0 && (!in || !out || (joint ? !joint_diag || (n > 1 && !joint_off)
+                                                              : !cross_diag || (n > 1 && (!cross_sub || !cross_super))))),
+               "CfaOperators apply: invalid arguments"))
+    return PD_INVALID_ARGUMENT;
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int64_t e = (int64_t)(n - 1) * batch, r = (int64_t)n * batch;
+  Arena a;
+  const size_t ibs = a.add_in(joint ? nullptr : cross_sub, joint ? 0 : sizeof(double) * 5 * e);
+  const size_t ibd = a.add_in(joint ? nullptr : cross_diag, joint ? 0 : sizeof(double) * 5 * r);
+  const size_t ibp = a.add_in(joint ? nullptr : cross_super, joint ? 0 : sizeof(double) * 5 * e);
+  const size_t icd = a.add_in(joint ? joint_diag : nullptr, joint ? sizeof(double) * r : 0);
+  const size_t ico = a.add_in(joint ? joint_off : nullptr, joint ? sizeof(double) * e : 0);
+  const size_t iv = a.add_in(in, sizeof(double) * r * (op == PD_APPLY_CROSS_TRANSPOSE ? 5 : 1));
+  const size_t ov = a.add_out(out, sizeof(double) * r * (op == PD_APPLY_CROSS ? 5 : 1));
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  launch_cfa_apply(op, batch, n, a.in<double>(ibs), a.in<double>(ibd), a.in<double>(ibp), a.in<double>(icd),
+                   a.in<double>(ico), a.in<double>(iv), a.out<double>(ov), ctx->stream);
+  ctx->launches++;
+  return a.finish(ctx);
 }
 
 }  // extern "C"

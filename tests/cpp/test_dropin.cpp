@@ -40,11 +40,12 @@ oracle::RobotChain to_oracle(const pardyn::RobotChain& c) {
   for (const auto& l : c.links) {
     double f[31];
     f[0] = l.mass;
-    for (int k = 0; k < 3; ++k) f[1 + k] = l.com[k];
-    for (int k = 0; k < 9; ++k) f[4 + k] = l.inertia_rot[k];
-    for (int k = 0; k < 6; ++k) f[13 + k] = l.joint_screw[k];
-    for (int k = 0; k < 9; ++k) f[19 + k] = l.home_rotation[k];
-    for (int k = 0; k < 3; ++k) f[28 + k] = l.home_translation[k];
+    for (int k = 0; k < 3; ++k) f[1 + k] = l.com(k);
+    l.inertia_rot.toRowMajor(f + 4);
+    const pardyn::Vec6 s = l.joint_screw.stacked();
+    for (int k = 0; k < 6; ++k) f[13 + k] = s(k);
+    l.home_transform.rotation.toRowMajor(f + 19);
+    for (int k = 0; k < 3; ++k) f[28 + k] = l.home_transform.translation(k);
     o.links.push_back(oracle::link_from_flat(f));
   }
   return o;
@@ -81,11 +82,11 @@ int main() {
   // closed-form pendulum (test_fwddyn.cpp:105-122)
   {
     pardyn::RobotChain c;
-    c.gravity = {0.0, -9.81, 0.0};
+    c.gravity = pardyn::Vec3(0.0, -9.81, 0.0);
     pardyn::LinkSpec l;
     l.mass = 1.3;
-    l.com = {0.45, 0, 0};
-    l.inertia_rot = {0.11, 0, 0, 0, 0.13, 0, 0, 0, 0.07};
+    l.com = pardyn::Vec3(0.45, 0, 0);
+    l.inertia_rot = pardyn::Mat3::FromRowMajor({0.11, 0, 0, 0, 0.13, 0, 0, 0, 0.07});
     c.links.push_back(l);
     std::mt19937_64 e(111);
     bool ok = true;
@@ -168,9 +169,9 @@ int main() {
     const JointVector q = uniform(e, 11, -3, 3), qd = uniform(e, 11, -2, 2), qdd = uniform(e, 11, -5, 5);
     const JointVector a = uniform(e, 6, -1, 1), b = uniform(e, 6, -2, 2), w = uniform(e, 6, -3, 3);
     pardyn::IdOptions opts;
-    opts.base_velocity = pardyn::Twist::from_stacked({a[0], a[1], a[2], a[3], a[4], a[5]});
-    opts.base_acceleration = pardyn::Twist::from_stacked({b[0], b[1], b[2], b[3], b[4], b[5]});
-    opts.tip_wrench = pardyn::Wrench::from_stacked({w[0], w[1], w[2], w[3], w[4], w[5]});
+    opts.base_velocity = pardyn::Twist::from_stacked(pardyn::Vec6::FromRowMajor(a.data()));
+    opts.base_acceleration = pardyn::Twist::from_stacked(pardyn::Vec6::FromRowMajor(b.data()));
+    opts.tip_wrench = pardyn::Wrench::from_stacked(pardyn::Vec6::FromRowMajor(w.data()));
     opts.apply_gravity = false;
     oracle::IdOptions oo;
     for (int k = 0; k < 6; ++k) {
@@ -208,26 +209,21 @@ int main() {
   // the building blocks: scan and OEE (test_oee.cpp:106-126)
   {
     pardyn::BlockBiDiagSystem<6> sys;
-    std::array<double, 36> two{};
-    for (int k = 0; k < 6; ++k) two[7 * k] = 2.0;
+    const pardyn::Mat6 two = 2.0 * pardyn::Mat6::Identity();
     sys.coupling = {two, two};
-    sys.rhs = {std::array<double, 6>{1, 1, 1, 1, 1, 1}, {}, {}};
+    sys.rhs = {pardyn::Vec6::Constant(1.0), pardyn::Vec6(), pardyn::Vec6()};
     pardyn::ScanTrace tr;
     const auto x = pardyn::solve_lower_bidiag(sys, &tr);
-    check(x[0][0] == 1.0 && x[1][0] == 2.0 && x[2][5] == 4.0 && tr.rounds == 2, "scan known answer [1, 2, 4]");
+    check(x[0](0) == 1.0 && x[1](0) == 2.0 && x[2](5) == 4.0 && tr.rounds == 2, "scan known answer [1, 2, 4]");
     sys.orientation = pardyn::BiDiagOrientation::upper;
-    sys.rhs = {std::array<double, 6>{}, {}, std::array<double, 6>{1, 1, 1, 1, 1, 1}};
+    sys.rhs = {pardyn::Vec6(), pardyn::Vec6(), pardyn::Vec6::Constant(1.0)};
     const auto xu = pardyn::solve_upper_bidiag(sys);
-    check(xu[0][0] == 4.0 && xu[2][0] == 1.0, "upper scan known answer [4, 2, 1]");
+    check(xu[0](0) == 4.0 && xu[2](0) == 1.0, "upper scan known answer [4, 2, 1]");
     pardyn::SymBlockTriDiagSystem<5> t3;
-    std::array<double, 25> eye{}, tenth{};
-    for (int k = 0; k < 5; ++k) {
-      eye[6 * k] = 1.0;
-      tenth[6 * k] = 0.1;
-    }
-    t3.diag = {eye, std::array<double, 25>{}, eye};
+    const pardyn::Mat5 eye = pardyn::Mat5::Identity(), tenth = 0.1 * eye;
+    t3.diag = {eye, pardyn::Mat5(), eye};
     t3.upper = {tenth, tenth};
-    const std::vector<std::array<double, 5>> ones(3, std::array<double, 5>{1, 1, 1, 1, 1});
+    const std::vector<pardyn::Vec5> ones(3, pardyn::Vec5::Constant(1.0));
     int rd = -1, ix = -1;
     try {
       pardyn::oee_solve(t3, ones);
@@ -242,9 +238,9 @@ int main() {
     double res = 0.0;  // (I + 0.1 (shift + shift^T)) x = 1
     for (int k = 0; k < 3; ++k)
       for (int e = 0; e < 5; ++e) {
-        double v = xs[k][e];
-        if (k > 0) v += 0.1 * xs[k - 1][e];
-        if (k < 2) v += 0.1 * xs[k + 1][e];
+        double v = xs[k](e);
+        if (k > 0) v += 0.1 * xs[k - 1](e);
+        if (k < 2) v += 0.1 * xs[k + 1](e);
         res = std::max(res, std::fabs(v - 1.0));
       }
     check(res < 1e-14 && ot.rounds == 2, "OEE solves a 3-block system");

@@ -32,16 +32,7 @@ std::string what_of(const std::function<void()>& f) {
   return "NO THROW";
 }
 
-bool same(const pardyn::RobotChain& a, const pardyn::RobotChain& b) {
-  if (a.links.size() != b.links.size() || a.gravity != b.gravity) return false;
-  for (std::size_t k = 0; k < a.links.size(); ++k) {
-    const auto &x = a.links[k], &y = b.links[k];
-    if (x.mass != y.mass || x.com != y.com || x.inertia_rot != y.inertia_rot || x.joint_screw != y.joint_screw ||
-        x.home_rotation != y.home_rotation || x.home_translation != y.home_translation)
-      return false;
-  }
-  return true;
-}
+bool same(const pardyn::RobotChain& a, const pardyn::RobotChain& b) { return a == b; }
 
 void write(const std::string& path, const std::string& text) { std::ofstream(path) << text; }
 
@@ -56,7 +47,7 @@ int main(int argc, char** argv) {
     pardyn::save_chain(c, dir + "/m7.json");
     check(same(pardyn::load_chain(dir + "/m7.json"), c), "save_chain / load_chain round trip is bit exact");
     pardyn::RobotChain g = c;
-    g.gravity = {0.1, -0.2, 1e-300};
+    g.gravity = pardyn::Vec3(0.1, -0.2, 1e-300);
     pardyn::save_chain(g, dir + "/g.json");
     check(same(pardyn::load_chain(dir + "/g.json"), g), "round trip of extreme doubles");
   }
@@ -75,15 +66,15 @@ int main(int argc, char** argv) {
     check(bad([](auto& c) { c.gravity[1] = 1.0 / 0.0; }) == "gravity must be finite", "gravity finite");
     check(bad([](auto& c) { c.links[1].mass = 0.0; }) == "link 1: mass must be positive", "mass positive");
     check(bad([](auto& c) { c.links[2].com[0] = 0.0 / 0.0; }) == "link 2: com must be finite", "com finite");
-    check(bad([](auto& c) { c.links[0].inertia_rot[1] += 1e-3; }) == "link 0: rotational inertia must be symmetric",
+    check(bad([](auto& c) { c.links[0].inertia_rot(0, 1) += 1e-3; }) == "link 0: rotational inertia must be symmetric",
           "inertia symmetric");
-    check(bad([](auto& c) { c.links[0].inertia_rot = {1, 0, 0, 0, 1, 0, 0, 0, -1}; }) ==
+    check(bad([](auto& c) { c.links[0].inertia_rot = pardyn::Mat3::FromRowMajor({1, 0, 0, 0, 1, 0, 0, 0, -1}); }) ==
               "link 0: rotational inertia must be positive definite",
           "inertia positive definite");
-    check(bad([](auto& c) { c.links[1].joint_screw = {0, 0, 2, 0, 0, 0}; }) ==
+    check(bad([](auto& c) { c.links[1].joint_screw = pardyn::Twist(pardyn::Vec3(0, 0, 2), pardyn::Vec3()); }) ==
               "link 1: joint_screw must have unit norm (got 2.000000)",
           "screw unit norm");
-    check(bad([](auto& c) { c.links[2].home_rotation[0] = 2.0; }) ==
+    check(bad([](auto& c) { c.links[2].home_transform.rotation(0, 0) = 2.0; }) ==
               "link 2: home_transform rotation must be orthonormal with determinant +1",
           "home rotation orthonormal");
   }

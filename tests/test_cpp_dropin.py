@@ -10,9 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1609_06779_b200", "lib")
 
 
-def build(tmp_path):
-    exe = str(tmp_path / "test_dropin")
-    cmd = ["g++", "-O2", "-std=c++20", f"-I{ROOT}/include", os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp"),
+def build(tmp_path, name="test_dropin"):
+    exe = str(tmp_path / name)
+    cmd = ["g++", "-O2", "-std=c++20", f"-I{ROOT}/include", os.path.join(ROOT, "tests", "cpp", name + ".cpp"),
            "-o", exe, f"-L{LIB}", "-lpardyn", "-lpardyn_b200", f"-Wl,-rpath,{LIB}"]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     return exe
@@ -21,6 +21,38 @@ def build(tmp_path):
 def test_dropin_compiles_and_links(tmp_path):
     assert os.path.exists(os.path.join(LIB, "libpardyn.so"))
     build(tmp_path)
+    build(tmp_path, "test_operators")
+
+
+def test_reference_shaped_model_types_compile(tmp_path):
+    """Caller code written against the reference's model types
+    (model.hpp:17-30, spatial.hpp:15-150) compiles against the drop-in."""
+    src = tmp_path / "caller.cpp"
+    src.write_text(r"""
+#include <pardyn/pardyn.hpp>
+using namespace pardyn;
+int main() {
+  RobotChain chain;
+  chain.gravity = Vec3(0.0, -9.81, 0.0);
+  LinkSpec link;
+  link.mass = 1.3;
+  link.com = Vec3(0.45, 0.0, 0.0);
+  link.inertia_rot = Mat3::Identity();
+  link.joint_screw = Twist(Vec3::UnitZ(), Vec3::Zero());
+  link.home_transform.rotation = Mat3::Identity();
+  link.home_transform.translation = Vec3(0.1, 0.0, 0.0);
+  chain.links.push_back(link);
+  const SE3Transform t = screw_exp(link.joint_screw, 0.3) * link.home_transform;
+  const AdjointMap ad = adjoint_of(t);
+  const SpatialInertia J = spatial_inertia_from(link.mass, link.com, link.inertia_rot);
+  const Wrench w = J.apply(ad.apply(Twist(Vec3::UnitX(), Vec3::Zero())));
+  return (t.is_valid() && w.is_finite() && chain.size() == 1 && small_adjoint(Twist()).norm() == 0.0) ? 0 : 1;
+}
+""")
+    exe = str(tmp_path / "caller")
+    subprocess.run(["g++", "-O2", "-std=c++20", f"-I{ROOT}/include", str(src), "-o", exe, f"-L{LIB}", "-lpardyn",
+                    "-lpardyn_b200", f"-Wl,-rpath,{LIB}"], check=True, capture_output=True, text=True)
+    assert subprocess.run([exe]).returncode == 0  # host-side value algebra only: no device needed
 
 
 def test_dropin_without_gpu_fails_loudly(tmp_path):
@@ -32,8 +64,9 @@ def test_dropin_without_gpu_fails_loudly(tmp_path):
 
 
 @pytest.mark.gpu
-def test_dropin_cpp_suite_on_gpu(tmp_path):
-    r = subprocess.run([build(tmp_path)], capture_output=True, text=True, timeout=600)
+@pytest.mark.parametrize("name", ["test_dropin", "test_operators"])
+def test_dropin_cpp_suite_on_gpu(tmp_path, name):
+    r = subprocess.run([build(tmp_path, name)], capture_output=True, text=True, timeout=600)
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "0 failure(s)" in r.stdout

