@@ -195,6 +195,9 @@ def cpu_reference(algo: str, n: int, links, q, qd, tau, budget_s: float, reps: i
     Returns (solves/s, sample size, cores, oracle qdd of the sample)."""
     from oracle import pyoracle as po
     cores = po.lib().orc_num_threads()
+    if isinstance(links, DeviceChains):  # device-generated chains: time a host-generated prefix
+        links = links.host_prefix(8192)
+        q, qd, tau = q[:len(links)], qd[:len(links)], tau[:len(links)]
     probe = min(len(q), 512 if algo != "jsiia" else 128)
     t0 = time.perf_counter()
     po.batch_forward_dynamics(algo, links[:probe], [0, 0, -9.81], q[:probe], qd[:probe], tau[:probe])
@@ -210,15 +213,29 @@ def cpu_reference(algo: str, n: int, links, q, qd, tau, budget_s: float, reps: i
     return S * reps / dt, S, cores, ref
 
 
+class DeviceChains:
+    """A rank's slice [g0, g0 + count) of a cell's chains, generated, validated
+    and packed on the device (pd_set_models_workload): no host model buffer
+    (15.5 GiB at c5). host_prefix() gives the first chains on the host for the
+    CPU baseline / parity sample."""
+
+    def __init__(self, cell: int, n: int, g0: int, count: int):
+        self.cell, self.n, self.g0, self.count = cell, n, g0, count
+        self.shape = (count, n, 31)
+
+    def host_prefix(self, k: int):
+        from paper_1609_06779_b200 import workload as W
+        return W.workload_chains(self.cell, self.n, min(k, self.count), g0=self.g0)
+
+
 def gen_workload(wl: dict, rank: int, world: int = 1):
     from paper_1609_06779_b200 import workload as W
     n, B = wl["n"], wl["batch"]
     cell = W.workload_seed(42, n, B)
     if wl.get("sharded"):
         lo, cnt = local_batch(wl, world, rank)
-        links = W.workload_chains(cell, n, cnt, g0=lo)
         inputs = tuple(np.ascontiguousarray(a[lo:lo + cnt]) for a in W.workload_inputs(cell, n, B, 0))
-        return links, inputs, None
+        return DeviceChains(cell, n, lo, cnt), inputs, None
     if wl["shared"]:
         links = W.workload_chains(cell, n, 1)
         qs = [W.workload_inputs(cell, n, 1, r) for r in range(B)]
@@ -353,7 +370,10 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
     n, algo = wl["n"], wl["algo"]
     links, inp, inp2 = gen_workload(wl, rank, world)
     B = len(inp[0])
-    ms, mr = ctx.set_models(links, None)
+    if isinstance(links, DeviceChains):
+        ms, mr = ctx.set_models_workload(links.cell, n, links.count, g0=links.g0)
+    else:
+        ms, mr = ctx.set_models(links, None)
     assert (ms == 0).all()
     dev = torch.device("cuda", local)
 
@@ -396,6 +416,40 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
 # kernel and config as the bench command): DRAM bytes per launch
 NCU_TRAFFIC = {"c2": "profiles/ncu_c2_r1_s3g.txt", "c3": "profiles/ncu_c3_r1_s3g.txt",
                "c2j": "profiles/ncu_c2j_r1_s3g.txt", "c5j": "profiles/ncu_c5j_r1_s3c.txt"}
+
+
+def dropin_api_timings():
+    """The reference's own call paths timed through the C++ drop-in
+    (libpardyn.so): pardyn_bench --mode link (forward_dynamics on one chain,
+    host vectors in and out, the model re-sent every call as the reference
+    API does) for the c4 chain, and --mode group (batch_forward_dynamics over
+    FdProblem values) for c2. Steady-clock means of the harness
+    (bench.cpp:150-278 semantics)."""
+    import csv
+    import subprocess
+    import tempfile
+    exe = os.path.join(ROOT, "paper_1609_06779_b200", "lib", "pardyn_bench")
+    if not os.path.exists(exe):
+        return None
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        runs = {"c4": ["--mode", "link", "--algos", "abia,cfa,jsiia", "--links", "1024", "--repeats", "100"],
+                "c2": ["--mode", "group", "--algos", "abia,jsiia", "--links", "32", "--groups", "65536",
+                       "--repeats", "5"]}
+        for tag, argv in runs.items():
+            path = os.path.join(d, tag + ".csv")
+            r = subprocess.run([exe, *argv, "--out", path], capture_output=True, text=True, timeout=900)
+            if r.returncode != 0:
+                out[tag] = {"error": (r.stderr or r.stdout)[-300:]}
+                continue
+            for row in csv.DictReader(open(path)):
+                g = int(row["n_groups"])
+                key = f"{tag}_{row['algo']}"
+                out[key] = {"call": "forward_dynamics" if g == 1 else "batch_forward_dynamics",
+                            "n_links": int(row["n_links"]), "problems_per_call": g,
+                            "mean_us": float(row["mean_us"]), "stddev_us": float(row["stddev_us"]),
+                            "solves_per_s": g / (float(row["mean_us"]) * 1e-6), "repeats": int(row["repeats"])}
+    return out
 
 
 def ncu_traffic(workload: str):
@@ -529,17 +583,20 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_extra:
         extra = {}
-        for name in ("c2j", "c3", "c1", "c4a", "c4c", "c4j"):
+        for name in ("c2j", "c3", "c1", "c4a", "c4c", "c4j", "c5a", "c5j", "c5c"):
             if name == args.workload:
                 continue
             w = WORKLOADS[name]
-            steps = 20 if w["batch"] > 1 else 3
+            steps = 3 if w["batch"] == 1 or w.get("sharded") else 20
             r = measure_workload(ctx, name, w, steps, 3, 0, local, stream, False, 0)
             mps = r["ms_total"] / steps
             h, f, b, wk = roofline_entry(w, mps, bw, fp64_peak)
             extra[name] = {"workload": w["desc"], "solves_per_s": w["batch"] * steps / (r["ms_total"] * 1e-3),
                            "ms_per_step": mps, "hbm_frac": h["frac"], "fp64_frac": f["frac"], "binding": b,
                            "roofline_frac_of_binding": wk["roofline_frac"]}
+        dropin = dropin_api_timings()
+        if dropin:
+            extra["dropin_api"] = dropin
         line["extra"] = extra
 
     if rank == 0:

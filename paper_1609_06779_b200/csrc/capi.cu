@@ -88,6 +88,11 @@ struct pd_ctx {
   int64_t model_ld = 0;
   DevBuf model, gravity, mstatus, mrule, raw;
   std::vector<int32_t> h_mstatus, h_mrule;  // host copy of the upload validation
+  // the last host model set (kept when <= 64 MiB): an identical pd_set_models
+  // -- the drop-in's single-chain calls re-send the same chain every call --
+  // skips the upload, validation and packing
+  std::vector<double> last_links, last_grav;
+  bool models_cached = false;
   DevBuf model_cl;        // link-fastest copy [chain][field][link] for warp-per-chain kernels
   bool model_cl_valid = false;
   // scratch
@@ -653,6 +658,13 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   for (int64_t m = 0; m < n_models; ++m)
     for (int k = 0; k < 3; ++k) g[3 * m + k] = gravity ? gravity[3 * m + k] : (k == 2 ? -9.81 : 0.0);
   const size_t raw_bytes = sizeof(double) * PD_LINK_FIELDS * n_links * (size_t)n_models;
+  if (ctx->models_cached && ctx->n_models == n_models && ctx->n_links == n_links && ctx->last_grav == g &&
+      std::memcmp(ctx->last_links.data(), links, raw_bytes) == 0) {
+    if (model_status) std::memcpy(model_status, ctx->h_mstatus.data(), sizeof(int32_t) * n_models);
+    if (model_rule) std::memcpy(model_rule, ctx->h_mrule.data(), sizeof(int32_t) * n_models);
+    return PD_OK;
+  }
+  ctx->models_cached = false;
   PD_CUDA(ctx->raw.ensure(raw_bytes + sizeof(double) * 3 * n_models));
   const int64_t model_ld = (n_models + 31) / 32 * 32;
   PD_CUDA(ctx->model.ensure(sizeof(double) * F_COUNT * n_links * (size_t)model_ld));
@@ -676,7 +688,7 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   dim3 grid((unsigned)((n_models + 127) / 128), (unsigned)n_links);
   pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, model_ld,
                                                      ctx->model.as<double>(), ctx->gravity.as<double>());
-  ctx->launches += 2;
+  ctx->launches += 3;
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
   if (model_status) std::memcpy(model_status, ctx->h_mstatus.data(), sizeof(int32_t) * n_models);
@@ -685,6 +697,11 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   ctx->n_models = n_models;
   ctx->model_ld = model_ld;
   ctx->model_cl_valid = false;
+  if (raw_bytes <= ((size_t)64 << 20)) {
+    ctx->last_links.assign(links, links + raw_bytes / sizeof(double));
+    ctx->last_grav = g;
+    ctx->models_cached = true;
+  }
   return PD_OK;
 }
 
@@ -1190,6 +1207,7 @@ pd_status pd_set_models_workload(pd_ctx* ctx, uint64_t cell_seed, int32_t n_link
     return PD_INVALID_ARGUMENT;
   }
   PD_CUDA(cudaSetDevice(ctx->device));
+  ctx->models_cached = false;
   const int64_t n_models = count;
   const size_t raw_bytes = sizeof(double) * PD_LINK_FIELDS * n_links * (size_t)n_models;
   PD_CUDA(ctx->raw.ensure(raw_bytes + sizeof(double) * 3 * n_models));
@@ -1215,7 +1233,8 @@ pd_status pd_set_models_workload(pd_ctx* ctx, uint64_t cell_seed, int32_t n_link
   dim3 grid((unsigned)((n_models + 127) / 128), (unsigned)n_links);
   pack_models_kernel<<<grid, 128, 0, ctx->stream>>>(raw, graw, n_links, n_models, model_ld, ctx->model.as<double>(),
                                                      ctx->gravity.as<double>());
-  ctx->launches += 3;
+  ctx->launches += 4;
+  ctx->models_cached = false;
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
   if (model_status) std::memcpy(model_status, ctx->h_mstatus.data(), sizeof(int32_t) * n_models);

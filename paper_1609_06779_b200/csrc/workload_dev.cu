@@ -258,27 +258,35 @@ __device__ int link_rule(const double* r) {
   return 0;
 }
 
-__global__ void validate_models_kernel(const double* __restrict__ raw, int n, int64_t M, int32_t* __restrict__ status,
-                                       int32_t* __restrict__ rule) {
+// One thread per (model, link): every link runs spatial_inertia_from's rules
+// at once; the first failing link of a model wins through an atomicMin on
+// key = link * 8 + rule (the reference validates links in order and throws at
+// the first bad one, model.cpp:148-155).
+__global__ void validate_links_kernel(const double* __restrict__ raw, int n, int64_t M, int32_t* __restrict__ key) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M * n) return;
+  const int r = link_rule(raw + (size_t)t * PD_LINK_FIELDS);
+  if (r) {
+    const int64_t m = t / n;
+    atomicMin(key + m, (int32_t)((t - m * n) * 8 + r));
+  }
+}
+
+__global__ void finish_validation_kernel(int64_t M, int32_t* __restrict__ status, int32_t* __restrict__ rule) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
-  int32_t st = PD_SLOT_OK, ru = 0;
-  for (int i = 0; i < n; ++i) {
-    const int r = link_rule(raw + ((size_t)m * n + i) * PD_LINK_FIELDS);
-    if (r) {
-      st = PD_SLOT_BAD_MODEL;
-      ru = r;
-      break;
-    }
-  }
-  status[m] = st;
-  rule[m] = ru;
+  const int32_t k = rule[m];  // 0x7f7f7f7f: no failing link
+  const bool bad = k != 0x7f7f7f7f;
+  status[m] = bad ? PD_SLOT_BAD_MODEL : PD_SLOT_OK;
+  rule[m] = bad ? (k & 7) : 0;
 }
 
 }  // namespace wdev
 
 void launch_validate_models(const double* raw, int n, int64_t M, int32_t* status, int32_t* rule, cudaStream_t s) {
-  wdev::validate_models_kernel<<<(unsigned)((M + 127) / 128), 128, 0, s>>>(raw, n, M, status, rule);
+  cudaMemsetAsync(rule, 0x7f, sizeof(int32_t) * M, s);
+  wdev::validate_links_kernel<<<(unsigned)((M * n + 127) / 128), 128, 0, s>>>(raw, n, M, rule);
+  wdev::finish_validation_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, status, rule);
 }
 
 void launch_workload_chains(uint64_t cell, int n, int64_t g0, int64_t count, double* d_links, cudaStream_t s) {

@@ -253,3 +253,34 @@ def test_batch_trace_reports_the_lane_kernels(oracle, gpu_ctx, c2):
     gpu_ctx.solve(pd.FdAlgo.abia, q[:4096], qd[:4096], tau[:4096])
     tr = gpu_ctx.last_trace()
     assert (tr.longest_sequential_link_chain, tr.scan_rounds_max, tr.oee_rounds) == (32, 0, 0)
+
+
+def test_model_upload_cache_and_first_failing_link(oracle, gpu_ctx):
+    """pd_set_models: an identical model set is not re-uploaded (the drop-in's
+    single-chain calls re-send the chain every call); any changed bit is.
+    Validation runs a thread per link and reports the FIRST failing link's
+    rule, as the reference's in-order link_inertias does (model.cpp:148-155)."""
+    n = 40
+    links, g = oracle.random_chain(n, 77)
+    q, qd, tau = (np.random.default_rng(1).uniform(-1, 1, (1, n)) for _ in range(3))
+    gpu_ctx.set_models(links[None], g[None])
+    a, _, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    l0 = gpu_ctx.kernel_launches()
+    gpu_ctx.set_models(links[None].copy(), g[None])
+    assert gpu_ctx.kernel_launches() == l0  # cached: no upload kernels
+    b, _, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    assert np.array_equal(a, b)
+    changed = links.copy()
+    changed[7, 0] = np.nextafter(changed[7, 0], 2 * changed[7, 0])  # one ulp of one mass
+    gpu_ctx.set_models(changed[None], g[None])
+    assert gpu_ctx.kernel_launches() > l0
+    c, _, _, _ = gpu_ctx.solve(pd.FdAlgo.abia, q, qd, tau)
+    ref, _ = oracle.batch_forward_dynamics("abia", changed[None], g, q, qd, tau)
+    assert np.linalg.norm(c - ref) / max(1.0, np.linalg.norm(ref)) <= TOL
+    bad = np.stack([links] * 3)
+    bad[0, 30, 0] = -1.0           # mass rule at link 30
+    bad[0, 5, 5] += 1e-3           # symmetry rule at link 5 (first)
+    bad[1, 39, 4:13] = np.nan      # finiteness rule at the tip
+    ms, mr = gpu_ctx.set_models(bad, None)
+    assert list(ms) == [pd.api._capi.SLOT_BAD_MODEL, pd.api._capi.SLOT_BAD_MODEL, 0]
+    assert list(mr[:2]) == [3, 2]
