@@ -18,9 +18,11 @@
 //    form M_ij = S0_min(i,j) . FB_max(i,j) (exactly symmetric).
 //  * M block (I,J), I >= J: FB_I (8x6) * S0_J^T (6x8) = 2 DMMA (k = 6 padded
 //    to 8). Padding links carry zero S0/FB and a unit diagonal.
-//  * Blocked right-looking Cholesky over k: the 8x8 diagonal block is factored
-//    and inverted in registers with quad shuffles; panel blocks
-//    L_ik = A_ik L_kk^-T and trailing updates A_ij -= L_ik L_jk^T are DMMAs.
+//  * Blocked Cholesky over k: the 8x8 diagonal block is factored and inverted
+//    in registers with quad shuffles; panel blocks L_ik = A_ik L_kk^-T and the
+//    updates A_ij -= L_ik L_jk^T are DMMAs. NB <= 4: right-looking over the
+//    whole block triangle in registers; NB > 4 (c5): left-looking, so only the
+//    L blocks and one block column are live (no spills).
 //  * Solves L y = b, L^T x = y by block substitution with the diagonal
 //    inverses (vectors ride in column 0 of a DMMA tile).
 //  * Residual (M x)_i = FB_i . P_i + S0_i . Q_i with P = prefix sum of S0_j x_j
@@ -346,49 +348,72 @@ __global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 5 : 3) jsiia_dmma_kern
   }
   __syncwarp();
 
-  // ---- M blocks (lower), DMMA ----------------------------------------------------
-  double C[NBLK][2];
-#pragma unroll
-  for (int I = 0; I < NB; ++I) {
-    const double alo = sm.fb[t][8 * I + g], ahi = t < 2 ? sm.fb[4 + t][8 * I + g] : 0.0;
-#pragma unroll
-    for (int J = 0; J <= I; ++J) {
-      double (&c)[2] = C[bidx(I, J)];
-      c[0] = 0.0;
-      c[1] = 0.0;
-      dmma(c, alo, sm.s0[t][8 * J + g]);
-      dmma(c, ahi, t < 2 ? sm.s0[4 + t][8 * J + g] : 0.0);
-      if (I == J && 8 * I + g >= n) {  // padding: unit diagonal
-        if (g == 2 * t) c[0] = 1.0;
-        if (g == 2 * t + 1) c[1] = 1.0;
-      }
-    }
-  }
-
-  // ---- blocked Cholesky --------------------------------------------------------
+  // ---- M blocks and their blocked Cholesky ---------------------------------------
   // LN[bidx(i,k)]: N-frag of L_ik (i > k) or of L_kk^{-1} (i == k)
   double LN[NBLK][2];
   bool spd = true;
-#pragma unroll
-  for (int k = 0; k < NB; ++k) {
-    double xinv[2];
-    potrf_inv8(C[bidx(k, k)], xinv, spd, g, t);
-    c_to_n(xinv, LN[bidx(k, k)], g, t);
-#pragma unroll
-    for (int i = k + 1; i < NB; ++i) {
-      double a[2], d[2] = {0.0, 0.0};
-      c_to_n(C[bidx(i, k)], a, g, t);
-      dmma(d, a[0], LN[bidx(k, k)][0]);
-      dmma(d, a[1], LN[bidx(k, k)][1]);
-      c_to_n(d, LN[bidx(i, k)], g, t);
+  auto m_block = [&](int I, int J, double (&c)[2]) {  // M_IJ = FB_I S0_J^T: 2 DMMA (k = 6 padded to 8)
+    const double alo = sm.fb[t][8 * I + g], ahi = t < 2 ? sm.fb[4 + t][8 * I + g] : 0.0;
+    c[0] = 0.0;
+    c[1] = 0.0;
+    dmma(c, alo, sm.s0[t][8 * J + g]);
+    dmma(c, ahi, t < 2 ? sm.s0[4 + t][8 * J + g] : 0.0);
+    if (I == J && 8 * I + g >= n) {  // padding: unit diagonal
+      if (g == 2 * t) c[0] = 1.0;
+      if (g == 2 * t + 1) c[1] = 1.0;
     }
+  };
+  auto panel = [&](int k, const double (&a_ik)[2], double (&l_ik)[2]) {  // L_ik = A_ik L_kk^{-T}
+    double a[2], d[2] = {0.0, 0.0};
+    c_to_n(a_ik, a, g, t);
+    dmma(d, a[0], LN[bidx(k, k)][0]);
+    dmma(d, a[1], LN[bidx(k, k)][1]);
+    c_to_n(d, l_ik, g, t);
+  };
+  if constexpr (NB > 4) {
+    // Left-looking: block column k is built when it is factored (M_ik minus
+    // sum_{j<k} L_ij L_kj^T), so only the L blocks and one column are live --
+    // never the whole trailing matrix (the c5 kernel would spill it).
 #pragma unroll
-    for (int i = k + 1; i < NB; ++i) {
-      const double na0 = -LN[bidx(i, k)][0], na1 = -LN[bidx(i, k)][1];
+    for (int k = 0; k < NB; ++k) {
+      double col[NB][2];  // rows i >= k of block column k
 #pragma unroll
-      for (int j = k + 1; j <= i; ++j) {
-        dmma(C[bidx(i, j)], na0, LN[bidx(j, k)][0]);
-        dmma(C[bidx(i, j)], na1, LN[bidx(j, k)][1]);
+      for (int i = k; i < NB; ++i) {
+        m_block(i, k, col[i]);
+#pragma unroll
+        for (int j = 0; j < k; ++j) {
+          dmma(col[i], -LN[bidx(i, j)][0], LN[bidx(k, j)][0]);
+          dmma(col[i], -LN[bidx(i, j)][1], LN[bidx(k, j)][1]);
+        }
+      }
+      double xinv[2];
+      potrf_inv8(col[k], xinv, spd, g, t);
+      c_to_n(xinv, LN[bidx(k, k)], g, t);
+#pragma unroll
+      for (int i = k + 1; i < NB; ++i) panel(k, col[i], LN[bidx(i, k)]);
+    }
+  } else {
+    // Right-looking over the whole lower block triangle (small NB: it fits).
+    double C[NBLK][2];
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J = 0; J <= I; ++J) m_block(I, J, C[bidx(I, J)]);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      double xinv[2];
+      potrf_inv8(C[bidx(k, k)], xinv, spd, g, t);
+      c_to_n(xinv, LN[bidx(k, k)], g, t);
+#pragma unroll
+      for (int i = k + 1; i < NB; ++i) panel(k, C[bidx(i, k)], LN[bidx(i, k)]);
+#pragma unroll
+      for (int i = k + 1; i < NB; ++i) {
+        const double na0 = -LN[bidx(i, k)][0], na1 = -LN[bidx(i, k)][1];
+#pragma unroll
+        for (int j = k + 1; j <= i; ++j) {
+          dmma(C[bidx(i, j)], na0, LN[bidx(j, k)][0]);
+          dmma(C[bidx(i, j)], na1, LN[bidx(j, k)][1]);
+        }
       }
     }
   }
