@@ -468,6 +468,17 @@ def ncu_traffic(workload: str):
     return {"bytes_per_launch": total, "source": NCU_TRAFFIC[workload]} if found == 2 else None
 
 
+def _executed_fp64():
+    try:
+        with open(os.path.join(ROOT, "profiles", "executed_fp64_r2.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+EXECUTED_FP64 = _executed_fp64()
+
+
 def roofline_entry(wl, ms_per_step, bw_gbs, fp64_tflops, traffic=None):
     """Algorithmic work of one step (the whole batch) over the step's device
     time. A step is one launch for the batched kernels; multi-kernel paths
@@ -483,7 +494,13 @@ def roofline_entry(wl, ms_per_step, bw_gbs, fp64_tflops, traffic=None):
     t_fp = flops / (fp64_tflops * 1e12)
     hbm = {"bound": "hbm", "achieved": gbs, "peak": bw_gbs, "unit": "GB/s", "frac": gbs / bw_gbs, "traffic": traffic,
            "algorithmic_bytes": bytes_}
-    fp = {"achieved": tfl, "peak": fp64_tflops, "unit": "TFLOP/s (FP64)", "frac": tfl / fp64_tflops}
+    fp = {"achieved": tfl, "peak": fp64_tflops, "unit": "TFLOP/s (FP64)", "frac": tfl / fp64_tflops,
+          "flops_per_solve_algorithmic": f_alg(algo, n)}
+    ex = EXECUTED_FP64.get(wl.get("name", ""))
+    if ex:  # the FP64 work the kernel actually executes (ncu SASS counts), beside the frozen F_alg
+        fp["flops_per_solve_executed"] = ex["flops_per_solve"]
+        fp["frac_executed"] = ex["flops_per_solve"] * B / t / 1e12 / fp64_tflops
+        fp["executed_source"] = ex["source"]
     binding = "hbm" if t_hbm >= t_fp else "fp64"
     return hbm, fp, binding, {"bytes_per_launch": bytes_, "flops_per_launch": flops,
                               "roofline_frac": (max(t_hbm, t_fp) / t)}
@@ -543,7 +560,8 @@ def main():
     ms_per_step = ms_max / args.steps
     # roofline of this rank's step on its own (local) batch
     tr = ncu_traffic(args.workload) if world == 1 else None
-    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B), res["ms_total"] / args.steps, bw, fp64_peak,
+    hbm, fp, binding, work = roofline_entry(dict(wl, batch=B, name=args.workload), res["ms_total"] / args.steps, bw,
+                                            fp64_peak,
                                             traffic=tr["bytes_per_launch"] if tr else None)
 
     line = {
@@ -590,9 +608,10 @@ def main():
             steps = 3 if w["batch"] == 1 or w.get("sharded") else 20
             r = measure_workload(ctx, name, w, steps, 3, 0, local, stream, False, 0)
             mps = r["ms_total"] / steps
-            h, f, b, wk = roofline_entry(w, mps, bw, fp64_peak)
+            h, f, b, wk = roofline_entry(dict(w, name=name), mps, bw, fp64_peak)
             extra[name] = {"workload": w["desc"], "solves_per_s": w["batch"] * steps / (r["ms_total"] * 1e-3),
-                           "ms_per_step": mps, "hbm_frac": h["frac"], "fp64_frac": f["frac"], "binding": b,
+                           "ms_per_step": mps, "hbm_frac": h["frac"], "fp64_frac": f["frac"],
+                           "fp64_frac_executed": f.get("frac_executed"), "binding": b,
                            "roofline_frac_of_binding": wk["roofline_frac"]}
         dropin = dropin_api_timings()
         if dropin:

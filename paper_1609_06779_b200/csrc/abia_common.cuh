@@ -79,6 +79,13 @@ __device__ __forceinline__ void abia_init(AbiaState& st, Vec3d g) {
   st.F0 = svzero();
   st.Z0 = svzero();
   st.a0 = svzero();
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    st.P0.A[k] = 0.0;
+    st.P0.D[k] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) st.P0.B[k] = 0.0;
   st.code = PD_SLOT_OK;
   st.eidx = 0;
   st.qpoison = 0.0;
@@ -116,16 +123,16 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   st.F0 = neg_advT_acc(st.V0, h, inertia_apply_acc(J0, st.A0, st.F0));
   const double tau_delta = tau - dot(S0, st.F0);
   // articulated inertia                            forward_dynamics.cpp:136-156
+  // P0 is zero at the tip (abia_init), so the carry is added unconditionally:
+  // no branch splits the link step's scheduling region
   Sym6 Ia = inertia_sym6(J0);
-  if (i < n - 1) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      Ia.A[k] += st.P0.A[k];
-      Ia.D[k] += st.P0.D[k];
-    }
-#pragma unroll
-    for (int k = 0; k < 9; ++k) Ia.B[k] += st.P0.B[k];
+  for (int k = 0; k < 6; ++k) {
+    Ia.A[k] += st.P0.A[k];
+    Ia.D[k] += st.P0.D[k];
   }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Ia.B[k] += st.P0.B[k];
   const Sv U = sym6_apply(Ia, S0);
   const double lambda = dot(S0, U);
   // degeneracy test on the link-frame trace (forward_dynamics.cpp:140-144).
@@ -156,7 +163,7 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   rec[10] = S0.l.y;
   rec[11] = S0.l.z;
   rec[12] = u;
-  if (i > 0) {
+  {  // (at i = 0 the carried state is dead: updating it anyway keeps the step branch-free)
     st.Z0 = svfma(u, U, st.Z0);  // forward_dynamics.cpp:186-197
     // projected = I^A - U U^T / lambda = I^A - U g0^T   (:150-156)
     st.P0 = Ia;

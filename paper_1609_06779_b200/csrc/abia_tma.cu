@@ -208,12 +208,14 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
   }
   uint32_t cphys = 0, gk = 0;  // consumer's ring position / step counter (mirror the producer's)
   const int tt = t < KT ? t : 0;
-  auto acquire = [&](uint32_t k) -> const double* {
+  // step k's rows; `ahead` = steps already acquired and not yet released
+  auto acquire = [&](uint32_t k, uint32_t ahead = 0) -> const double* {
     const uint32_t rows = rows_of(k);
     if (cphys + rows > cap_rows) cphys = 0;
     const uint32_t off = cphys;
     cphys += rows;
-    mbar_wait(&full[gk % kSlots], (gk / kSlots) & 1u);
+    const uint32_t g = gk + ahead;
+    mbar_wait(&full[g % kSlots], (g / kSlots) & 1u);
     return ring + (size_t)off * KT + tt;
   };
   auto release = [&]() {
@@ -239,9 +241,8 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
       abia_pass_a(st, row_rel<KT>(f, 0, S, q, sn, cs), S, f[(F_NKIN + 1) * KT]);
       release();
     }
-    for (; k < 2u * n; ++k) {  // pass B
-      const double* f = acquire(k);
-      const int i = 2 * n - 1 - (int)k;
+    auto link_b = [&](const double* f, uint32_t kk) {
+      const int i = 2 * n - 1 - (int)kk;
       const Sv S = row_screw<KT>(f, F_KIN);
       const double q = f[F_COUNT * KT];
       double sn, cs;
@@ -258,7 +259,23 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
 #pragma unroll
         for (int j = 0; j < kRec; ++j) st_hint(scratch + ((int64_t)i * kRec + j) * scr_ld + p, rec[j], pol_last);
       }
-      if (k == 2u * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
+    };
+    // pass B two links per wait: both steps' rows are in shared memory before
+    // either link computes, so the scheduler can overlap link i-1's
+    // independent work (frame, link inertia, wrench) with link i's
+    // articulated-inertia chain
+    for (; k + 1 < 2u * n; k += 2) {
+      const double* fa = acquire(k);
+      const double* fb = acquire(k + 1, 1);
+      link_b(fa, k);
+      link_b(fb, k + 1);
+      if (k + 1 == 2u * n - 1) asm volatile("fence.proxy.async.global;" ::: "memory");  // records -> TMA reads
+      release();
+      release();
+    }
+    for (; k < 2u * n; ++k) {  // odd n: the last pass-B step
+      link_b(acquire(k), k);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       release();
     }
     for (; k < total; ++k) {  // pass C
