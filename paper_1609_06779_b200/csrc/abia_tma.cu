@@ -384,15 +384,22 @@ int sm_count() {
 // resident CTAs, so a tile costs KT * ctas chain-units per wave; with fewer
 // tiles than SMs each tile runs alone and costs KT. The arithmetic per chain
 // is the same for every tile size (abia_common.cuh).
+//
+// `eff` is the measured per-chain throughput of a configuration relative to
+// one 224-chain CTA per SM (7 consumer warps): two 96-chain CTAs (2 x 3
+// consumer warps, two producer warps) run 10 % slower per chain (c5a, 1M x 64:
+// 5.18 ms at 224 x 1, 5.77 ms at 96 x 2; profiles/abia_tile_r2.txt), so they win
+// only where they fill SMs a 224-chain tiling would leave idle.
 int abia_ring_tile(int64_t sel_B) {
-  struct Cfg { int kt, ctas; };
-  const Cfg cfgs[3] = {{224, 1}, {96, 2}, {64, 3}};
+  struct Cfg { int kt, ctas; double eff; };
+  const Cfg cfgs[3] = {{224, 1, 1.0}, {96, 2, 0.9}, {64, 3, 0.85}};
   double best = 1e300;
   int kt = 224;
   for (const Cfg& c : cfgs) {
     const int64_t tiles = (sel_B + c.kt - 1) / c.kt;
     const int64_t slots = (int64_t)sm_count() * c.ctas;
-    const double cost = tiles <= sm_count() ? (double)c.kt : (double)((tiles + slots - 1) / slots) * c.kt * c.ctas;
+    const double cost = (tiles <= sm_count() ? (double)c.kt : (double)((tiles + slots - 1) / slots) * c.kt * c.ctas) /
+                        c.eff;
     if (cost < best) {
       best = cost;
       kt = c.kt;
