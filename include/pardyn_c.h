@@ -336,6 +336,12 @@ pd_status pd_cfa_apply(pd_ctx* ctx, int32_t op, int64_t batch, int32_t n, const 
                        const double* cross_diag, const double* cross_super, const double* joint_diag,
                        const double* joint_off, const double* in, double* out);
 
+/* Page-locked host memory for staging host-buffer calls (copies from it run
+ * at PCIe DMA speed instead of through the driver's pageable bounce buffer).
+ * The C++ drop-in packs its batch calls into such a buffer. */
+pd_status pd_host_alloc(uint64_t bytes, void** out);
+void pd_host_free(void* p);
+
 /* Diagnostic: measured dense FP64 FMA throughput of this device (TFLOP/s),
  * the FP64 roofline denominator (no FP64 figure in MEASURED_PEAKS.json). */
 pd_status pd_probe_fp64_peak(pd_ctx* ctx, double* tflops, double* elapsed_ms);

@@ -30,7 +30,7 @@ EXPORTS = (
     "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5", "pd_block_bidiag_solve6",
     "pd_forward_dynamics_traced", "pd_last_variant", "pd_last_trace", "pd_set_selection_batch",
     "pd_assemble_kinematics", "pd_link_inertias", "pd_articulated_body_inertias", "pd_constraint_basis",
-    "pd_cfa_operators", "pd_cfa_apply",
+    "pd_cfa_operators", "pd_cfa_apply", "pd_host_alloc", "pd_host_free",
 )
 PD_APPLY_CROSS, PD_APPLY_CROSS_TRANSPOSE, PD_APPLY_JOINT = range(3)
 
@@ -147,6 +147,10 @@ def load():
     L.pd_cfa_operators.restype = C.c_int
     L.pd_cfa_apply.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, _D, _D, _D, _D, _D, _D, _D]
     L.pd_cfa_apply.restype = C.c_int
+    L.pd_host_alloc.argtypes = [C.c_uint64, C.POINTER(C.c_void_p)]
+    L.pd_host_alloc.restype = C.c_int
+    L.pd_host_free.argtypes = [C.c_void_p]
+    L.pd_host_free.restype = None
     _lib = L
     return L
 

@@ -430,12 +430,78 @@ JointVector cfa_forward_dynamics(const RobotChain& chain, const JointVector& q, 
 
 namespace {
 
-// One bucket (equal n) packed for the C-ABI: models, gravities, states.
+// Page-locked staging for the batch calls, one per thread, grown on demand:
+// copies from it run at DMA speed (pageable host memory goes through the
+// driver's bounce buffer at ~10 GB/s).
+struct PinnedStage {
+  void* p = nullptr;
+  std::size_t cap = 0;
+  ~PinnedStage() { pd_host_free(p); }
+  double* get(std::size_t doubles) {
+    const std::size_t want = doubles * sizeof(double);
+    if (want > cap) {
+      pd_host_free(p);
+      p = nullptr;
+      cap = 0;
+      if (pd_host_alloc(want + (want >> 3), &p) != PD_OK || !p)
+        throw DeviceError("pardyn: cannot allocate page-locked staging memory");
+      cap = want + (want >> 3);
+    }
+    return static_cast<double*>(p);
+  }
+};
+thread_local PinnedStage t_stage;
+
+// Runs f(lo, hi) over [0, count) on up to hardware_concurrency threads
+// (inline below `grain` items per thread).
+template <class F>
+void parallel_ranges(std::size_t count, std::size_t grain, F&& f) {
+  const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t T = std::min<std::size_t>(hw, std::max<std::size_t>(1, count / std::max<std::size_t>(grain, 1)));
+  if (T <= 1) {
+    f(std::size_t{0}, count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (std::size_t t = 1; t < T; ++t) pool.emplace_back([&, t] { f(count * t / T, count * (t + 1) / T); });
+  f(std::size_t{0}, count / T);
+  for (std::thread& th : pool) th.join();
+}
+
+// One bucket (equal n) packed for the C-ABI into page-locked staging:
+// links [B][n][31], gravity [B][3], q / qd / tau / qdd [B][n], then the slot arrays.
 struct Bucket {
   int n = 0;
   std::vector<std::size_t> idx;
-  std::vector<double> links, grav, q, qd, tau, qdd;
-  std::vector<int32_t> st, rd, ix;
+  double *links = nullptr, *grav = nullptr, *q = nullptr, *qd = nullptr, *tau = nullptr, *qdd = nullptr;
+  int32_t *st = nullptr, *rd = nullptr, *ix = nullptr;
+
+  void pack(std::span<const FdProblem> problems, double* base) {
+    const std::size_t B = idx.size(), nn = static_cast<std::size_t>(n);
+    links = base;
+    grav = links + B * nn * PD_LINK_FIELDS;
+    q = grav + 3 * B;
+    qd = q + B * nn;
+    tau = qd + B * nn;
+    qdd = tau + B * nn;
+    st = reinterpret_cast<int32_t*>(qdd + B * nn);
+    rd = st + B;
+    ix = rd + B;
+    parallel_ranges(B, 1024, [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t j = lo; j < hi; ++j) {
+        const FdProblem& p = problems[idx[j]];
+        double* rec = links + j * nn * PD_LINK_FIELDS;
+        for (std::size_t i = 0; i < nn; ++i) detail::to_record(p.chain.links[i], rec + i * PD_LINK_FIELDS);
+        for (int k = 0; k < 3; ++k) grav[3 * j + k] = p.chain.gravity(k);
+        std::copy(p.q.begin(), p.q.end(), q + j * nn);
+        std::copy(p.qdot.begin(), p.qdot.end(), qd + j * nn);
+        std::copy(p.tau.begin(), p.tau.end(), tau + j * nn);
+      }
+    });
+  }
+  static std::size_t doubles(std::size_t B, int n) {
+    return B * n * PD_LINK_FIELDS + 3 * B + 4 * B * n + (3 * B + 1) / 2;
+  }
 };
 
 // Solve slots [lo, hi) of a packed bucket on one device; every slice selects
@@ -445,11 +511,10 @@ void solve_slice(pd_ctx* c, pd_algo a, Bucket& b, std::size_t lo, std::size_t hi
   const std::size_t cnt = hi - lo, n = static_cast<std::size_t>(b.n);
   if (cnt == 0) return;
   check_call(c, pd_set_selection_batch(c, static_cast<int64_t>(b.idx.size())));
-  check_call(c, pd_set_models(c, static_cast<int64_t>(cnt), b.n, b.links.data() + lo * n * PD_LINK_FIELDS,
-                              b.grav.data() + 3 * lo, nullptr, nullptr));
-  const pd_status s = pd_forward_dynamics(c, a, static_cast<int64_t>(cnt), b.q.data() + lo * n, b.qd.data() + lo * n,
-                                          b.tau.data() + lo * n, b.qdd.data() + lo * n, b.st.data() + lo,
-                                          b.rd.data() + lo, b.ix.data() + lo);
+  check_call(c, pd_set_models(c, static_cast<int64_t>(cnt), b.n, b.links + lo * n * PD_LINK_FIELDS, b.grav + 3 * lo,
+                              nullptr, nullptr));
+  const pd_status s = pd_forward_dynamics(c, a, static_cast<int64_t>(cnt), b.q + lo * n, b.qd + lo * n,
+                                          b.tau + lo * n, b.qdd + lo * n, b.st + lo, b.rd + lo, b.ix + lo);
   pd_set_selection_batch(c, 0);
   check_call(c, s);
 }
@@ -457,8 +522,9 @@ void solve_slice(pd_ctx* c, pd_algo a, Bucket& b, std::size_t lo, std::size_t hi
 }  // namespace
 
 // forward_dynamics.cpp:466-481: never throws per problem. Problems are
-// bucketed by link count; a bucket is split into contiguous slices over
-// gpu::devices(), one host thread and one context per device.
+// bucketed by link count; a bucket is packed (in parallel host threads) into
+// page-locked staging and split into contiguous slices over gpu::devices(),
+// one host thread and one context per device.
 std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems, FdAlgo algo) {
   const pd_algo a = to_c(algo);
   std::vector<FdResult> out(problems.size());
@@ -476,21 +542,7 @@ std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems
   for (auto& [n, b] : buckets) {
     b.n = n;
     const std::size_t B = b.idx.size();
-    b.links.reserve(B * n * PD_LINK_FIELDS);
-    b.grav.reserve(3 * B);
-    for (std::vector<double>* v : {&b.q, &b.qd, &b.tau}) v->reserve(B * n);
-    for (std::size_t k : b.idx) {
-      const FdProblem& p = problems[k];
-      detail::append_records(p.chain, b.links);
-      b.grav.insert(b.grav.end(), p.chain.gravity.begin(), p.chain.gravity.end());
-      b.q.insert(b.q.end(), p.q.begin(), p.q.end());
-      b.qd.insert(b.qd.end(), p.qdot.begin(), p.qdot.end());
-      b.tau.insert(b.tau.end(), p.tau.begin(), p.tau.end());
-    }
-    b.qdd.resize(B * n);
-    b.st.resize(B);
-    b.rd.resize(B);
-    b.ix.resize(B);
+    b.pack(problems, t_stage.get(Bucket::doubles(B, n)));
     const std::size_t G = std::min<std::size_t>(devs.size(), B);
     if (G <= 1) {
       solve_slice(ctx_on(devs[0]), a, b, 0, B);
@@ -516,13 +568,15 @@ std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems
         if (kinds[g] == 2) throw DeviceError(errors[g]);
       }
     }
-    for (std::size_t j = 0; j < B; ++j) {
-      FdResult& r = out[b.idx[j]];
-      if (b.st[j] == PD_SLOT_OK)
-        r.qddot = JointVector(b.qdd.begin() + j * n, b.qdd.begin() + (j + 1) * n);
-      else
-        r.error = slot_message(b.st[j], b.rd[j], b.ix[j], n);
-    }
+    parallel_ranges(B, 4096, [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t j = lo; j < hi; ++j) {
+        FdResult& r = out[b.idx[j]];
+        if (b.st[j] == PD_SLOT_OK)
+          r.qddot = JointVector(b.qdd + j * n, b.qdd + (j + 1) * n);
+        else
+          r.error = slot_message(b.st[j], b.rd[j], b.ix[j], n);
+      }
+    });
   }
   return out;
 }

@@ -1505,3 +1505,18 @@ pd_status pd_cfa_apply(pd_ctx* ctx, int32_t op, int64_t batch, int32_t n, const 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+pd_status pd_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return PD_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (bytes == 0) return PD_OK;
+  return cudaMallocHost(out, (size_t)bytes) == cudaSuccess ? PD_OK : PD_CUDA_ERROR;
+}
+
+void pd_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"
