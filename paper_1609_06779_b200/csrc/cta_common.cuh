@@ -15,7 +15,8 @@
 //   F_i = Ad(rel_{i+1})^T F_{i+1} + f_i (upper, :86-120),
 // becomes V_i = Ad(X_i) * prefix_sum_k(Ad(X_k)^{-1} s_k) and
 // F_i = Ad(X_i)^{-T} * suffix_sum_k(Ad(X_k)^T f_k): one structured SE(3)
-// scan plus cheap 6-vector sums instead of three dense 6x6 affine scans.
+// scan plus cheap 6-vector sums instead of three dense 6x6 affine scans; the
+// velocity and bias-acceleration sums share one scan (PairOp).
 #pragma once
 
 #include "pd_batch.cuh"
@@ -40,6 +41,35 @@ struct AddOp {
     Arr<K> o;
 #pragma unroll
     for (int k = 0; k < K; ++k) o.v[k] = earlier.v[k] + later.v[k];
+    return o;
+  }
+  template <int K>
+  __device__ __forceinline__ Arr<K> identity() const {
+    Arr<K> o;
+#pragma unroll
+    for (int k = 0; k < K; ++k) o.v[k] = 0.0;
+    return o;
+  }
+};
+
+// (V0, A0) pairs: V0 = sum of base-frame rate twists s_k, A0 = sum over
+// j <= k of ad_{s_j}(s_k) -- the base-frame velocity and bias acceleration of
+// inverse_dynamics.cpp:27-84 in ONE scan. Over a segment split into an earlier
+// part E and a later part L, bilinearity of ad gives
+// A(E+L) = A(E) + A(L) + ad_{V(E)}(V(L)) (the j = k terms vanish: ad_s s = 0).
+struct PairOp {
+  __device__ __forceinline__ Arr<12> operator()(const Arr<12>& earlier, const Arr<12>& later) const {
+    const Sv ve = {mk(earlier.v[0], earlier.v[1], earlier.v[2]), mk(earlier.v[3], earlier.v[4], earlier.v[5])};
+    const Sv vl = {mk(later.v[0], later.v[1], later.v[2]), mk(later.v[3], later.v[4], later.v[5])};
+    const Sv cross_term = adv_apply(ve, vl);
+    const double ct[6] = {cross_term.a.x, cross_term.a.y, cross_term.a.z, cross_term.l.x, cross_term.l.y,
+                          cross_term.l.z};
+    Arr<12> o;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      o.v[k] = earlier.v[k] + later.v[k];
+      o.v[6 + k] = earlier.v[6 + k] + later.v[6 + k] + ct[k];
+    }
     return o;
   }
   template <int K>
@@ -251,7 +281,8 @@ __device__ __forceinline__ void cta_kinematics(const ModelView& mv, const BatchI
 }
 
 // Stage: tau_delta = tau - ID(q, qd, qdd = 0) with gravity as base
-// acceleration -g (forward_dynamics.cpp:35-42). Requires rel in ws.
+// acceleration -g (forward_dynamics.cpp:35-42). Requires rel in ws. Fields
+// v and tmp must be adjacent (tmp = v + 6): the (V0, A0) pair scan uses both.
 __device__ inline void cta_bias_torque(const ModelView& mv, const BatchIO& io, int64_t p, int64_t mc, double* ws,
                                 const IdFields& F, int lpt, ScanSmem& sm) {
   const int n = mv.n;
@@ -260,41 +291,26 @@ __device__ inline void cta_bias_torque(const ModelView& mv, const BatchIO& io, i
   __syncthreads();
   ws_scan<12, false>(ws, n, F.x, lpt, ComposeOp{}, sm);
   __syncthreads();
-  // velocities
+  // base-frame rate twists s_i = Ad(X_i)^{-1} S_i qd_i, then one pair scan
+  // gives V0_i and the bias acceleration sum A0_i (PairOp)
   for (int i = i0; i < i1; ++i) {
     const SE3d X = ws_get_se3(ws, n, F.x, i);
-    const Sv rate = io.ld(io.qd, i, p) * mv.screw(i, mc);
-    ws_put_sv(ws, n, F.tmp, i, adinv_apply(X, rate));
+    ws_put_sv(ws, n, F.v, i, adinv_apply(X, io.ld(io.qd, i, p) * mv.screw(i, mc)));
+    ws_put_sv(ws, n, F.v + 6, i, svzero());
   }
   __syncthreads();
-  ws_scan<6, false>(ws, n, F.tmp, lpt, AddOp{}, sm);
-  __syncthreads();
-  for (int i = i0; i < i1; ++i) {
-    const SE3d X = ws_get_se3(ws, n, F.x, i);
-    const Sv V = ad_apply(X, ws_get_sv(ws, n, F.tmp, i));
-    ws_put_sv(ws, n, F.v, i, V);
-  }
-  __syncthreads();
-  // accelerations (qddot = 0): source ad_{V_i}(S_i qd_i)
-  for (int i = i0; i < i1; ++i) {
-    const SE3d X = ws_get_se3(ws, n, F.x, i);
-    const Sv rate = io.ld(io.qd, i, p) * mv.screw(i, mc);
-    const Sv V = ws_get_sv(ws, n, F.v, i);
-    ws_put_sv(ws, n, F.tmp, i, adinv_apply(X, adv_apply(V, rate)));
-  }
-  __syncthreads();
-  ws_scan<6, false>(ws, n, F.tmp, lpt, AddOp{}, sm);
+  ws_scan<12, false>(ws, n, F.v, lpt, PairOp{}, sm);
   __syncthreads();
   const Vec3d g = mv.gravity(mc);
   const Sv Abase = {mk(0, 0, 0), mk(-g.x, -g.y, -g.z)};
   for (int i = i0; i < i1; ++i) {
     const SE3d X = ws_get_se3(ws, n, F.x, i);
-    const Sv A = ad_apply(X, Abase + ws_get_sv(ws, n, F.tmp, i));
-    const Sv V = ws_get_sv(ws, n, F.v, i);
+    const Sv V = ad_apply(X, ws_get_sv(ws, n, F.v, i));
+    const Sv A = ad_apply(X, Abase + ws_get_sv(ws, n, F.v + 6, i));
     const Inertia J = mv.inertia(i, mc);
     const Sv h = inertia_apply(J, V);
     const Sv f = inertia_apply(J, A) + neg_advT_apply(V, h);
-    ws_put_sv(ws, n, F.tmp, i, adT_apply(X, f));
+    ws_put_sv(ws, n, F.tmp, i, adT_apply(X, f));  // tmp = v + 6: this link's pair was read above
   }
   __syncthreads();
   ws_scan<6, true>(ws, n, F.tmp, lpt, AddOp{}, sm);
