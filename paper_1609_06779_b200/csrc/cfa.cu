@@ -811,7 +811,8 @@ constexpr int FIELDS = 70;
 }  // namespace cfr
 
 template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO io, const double* __restrict__ td_pre) {
+__global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO io, const double* __restrict__ td_pre,
+                                                           int pf_stride) {
   extern __shared__ double dyn_smem[];
   __shared__ ScanSmem scan_sm;
   __shared__ int s_bad, s_link_fail;
@@ -932,6 +933,25 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
     ws[cfr::JD * n + i] = jd;
   }
   __syncthreads();  // HH is reused by the published pivots below
+  // ---- warm L2 for the chain the SM will most likely run next: CTAs are
+  // dispatched in order, so the successor of this one is p + pf_stride (the
+  // resident CTAs). Its model (contiguous in the link-fastest copy) and
+  // q / qd / tau rows are prefetched into L2 while this chain runs its OEE
+  // rounds, so that chain's kinematics loads hit L2 instead of DRAM.
+  {
+    const int64_t pn = p + pf_stride;
+    if (pf_stride > 0 && pn < io.B) {
+      const char* base = reinterpret_cast<const char*>(mv.fcl + (int64_t)mv.model_of(pn) * F_COUNT * n);
+      const int bytes = F_COUNT * n * (int)sizeof(double);
+      for (int off = t * 128; off < bytes; off += NT * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+      if (own) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(io.q + (int64_t)i * io.lds + pn));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(io.qd + (int64_t)i * io.lds + pn));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(io.tau + (int64_t)i * io.lds + pn));
+      }
+    }
+  }
   // ---- OEE rounds (oee.hpp:73-145), row state in registers
   const int rounds = ceil_log2_dev(n);
   int h = 1;
@@ -1046,7 +1066,12 @@ void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws
     const size_t rb = (size_t)cfr::FIELDS * n * sizeof(double);
     auto go = [&](auto kernel) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
-      kernel<<<(unsigned)io.B, nt, rb, s>>>(mv, io, td_pre);
+      int per_sm = 0, dev = 0;
+      cudaGetDevice(&dev);
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, rb);
+      kernel<<<(unsigned)io.B, nt, rb, s>>>(mv, io, td_pre, mv.fcl ? sms * (per_sm > 0 ? per_sm : 1) : 0);
     };
     // (a c5 sweep of 4 / 5 / 6 chains per SM: register caps that spill lose more
     // than the extra warps gain; 4 x 64 threads at <= 255 registers is best)
