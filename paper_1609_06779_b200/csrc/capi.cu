@@ -24,6 +24,8 @@ void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
                 const double* td_pre);
 void launch_tau_surplus(const ModelView& mv, const BatchIO& io, double* td, cudaStream_t s);
+void launch_cfa_ws(const ModelView& mv, const BatchIO& io, int sm_count, cudaStream_t s);
+bool cfa_ws_fits(int n);
 void launch_bidiag6(const double* coupling, const double* rhs, double* x, int64_t batch, int n, int upper,
                     cudaStream_t s);
 bool launch_oee5(const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
@@ -430,6 +432,15 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
         ctx->launches += (batch + slots - 1) / slots;
       } else {
         ctx->launches++;
+      }
+      if (route == ROUTE_AUTO && cfa_ws_fits(n) && selB >= 2 * (int64_t)ctx->sm_count &&
+          selB < 128 * (int64_t)ctx->sm_count) {
+        // long chains, enough of them to keep every SM on two: the
+        // warp-specialised kernel overlaps chain k+1's prologue with chain k's OEE
+        launch_cfa_ws(mv, io, ctx->sm_count, ctx->stream);
+        ctx->launches++;
+        note_variant(ctx, "cfa_ws_kernel", 9, cs.lpt > 1 ? cs.lpt : 0, ceil_log2_host(cs.groups), L);
+        break;
       }
       // large batches: tau_delta by a lane-per-chain pass first (sequential
       // recurrences, no CTA-wide scans); small batches keep the CTA scans

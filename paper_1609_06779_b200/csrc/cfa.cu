@@ -810,40 +810,25 @@ constexpr int PL = 18, SG = 28, PY = 30, PR = 55, PI = 60, OR = 65;  // OEE
 constexpr int FIELDS = 70;
 }  // namespace cfr
 
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO io, const double* __restrict__ td_pre,
-                                                           int pf_stride) {
-  extern __shared__ double dyn_smem[];
-  __shared__ ScanSmem scan_sm;
-  __shared__ int s_bad, s_link_fail;
+// The row stages of the CFA kernels after kinematics and tau_delta: operators
+// (rows' own blocks into registers), OEE initial state, the OEE rounds, the
+// final block solves and the extraction, on the thread group `grp` (thread =
+// row). rel_{i+1} is read from relws (field relf), tau_delta from ws (TD).
+// after_ops() runs on every group thread right after the operator stage (the
+// last read of relws). s_bad / s_link_fail are the group's shared flags, set
+// to (n, 0) by the caller before a group barrier.
+template <class G, class AfterOps>
+__device__ __forceinline__ void cfa_rows(const ModelView& mv, const BatchIO& io, int64_t p, int64_t mc, double* ws,
+                                         const double* relws, int relf, int* s_bad, int* s_link_fail, int pf_stride,
+                                         int grp_threads, const G& grp, AfterOps after_ops) {
   const int n = mv.n;
-  const int64_t p = blockIdx.x;
-  const int64_t mc = mv.model_of(p);
-  double* ws = dyn_smem;
-  const int t = threadIdx.x, i = t;
+  const int t = grp.tid(), i = t;
   const bool own = i < n;
-  if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) {
-    if (t == 0) model_rejected(mv, io, p, mc);
-    return;
-  }
-  if (t == 0) {
-    s_bad = n;
-    s_link_fail = 0;
-  }
-  // ---- kinematics + torque surplus
-  const IdFields idf{cfr::REL, cfr::X, cfr::V, cfr::TMP, cfr::TD};
-  cta_kinematics(mv, io, p, mc, ws, idf, 1);
-  if (td_pre) {
-    if (own) ws[cfr::TD * n + i] = __ldg(td_pre + (int64_t)i * io.lds + p);
-    __syncthreads();
-  } else {
-    cta_bias_torque(mv, io, p, mc, ws, idf, 1, scan_sm);  // ends with a barrier
-  }
   // ---- operators (forward_dynamics.cpp:261-357): own blocks into registers
   double D[15], U[25], R[5];
   if (own) {
     double L[21], linv[6];
-    if (!llt_inertia(mv.inertia(i, mc), L, linv)) atomicOr(&s_link_fail, 1);
+    if (!llt_inertia(mv.inertia(i, mc), L, linv)) atomicOr(s_link_fail, 1);
     double G[6][6];
     householder_basis(mv.screw(i, mc), G);
 #pragma unroll
@@ -860,7 +845,7 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
         else ws[cfr::JD * n + i] = sacc;
       }
     if (i + 1 < n) {
-      const SE3d T1 = ws_get_se3(ws, n, cfr::REL, i + 1);
+      const SE3d T1 = ws_get_se3(relws, n, relf, i + 1);
       double Z1[6][6], H[6][6];
       householder_basis(mv.screw(i + 1, mc), Z1);
 #pragma unroll
@@ -891,8 +876,9 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
         }
     }
   }
-  __syncthreads();
-  if (s_link_fail) {  // forward_dynamics.cpp:317-320
+  grp.sync();
+  after_ops();  // REL (and the caller's td copy) are no longer read
+  if (*s_link_fail) {  // forward_dynamics.cpp:317-320
     if (t == 0) {
       io.status[p] = PD_SLOT_LINK_INERTIA_NOT_PD;
       io.eround[p] = 0;
@@ -932,7 +918,7 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
     ws_store<5>(ws, n, cfr::XD, i, xd);
     ws[cfr::JD * n + i] = jd;
   }
-  __syncthreads();  // HH is reused by the published pivots below
+  grp.sync();  // HH is reused by the published pivots below
   // ---- warm L2 for the chain the SM will most likely run next: CTAs are
   // dispatched in order, so the successor of this one is p + pf_stride (the
   // resident CTAs). Its model (contiguous in the link-fastest copy) and
@@ -943,7 +929,7 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
     if (pf_stride > 0 && pn < io.B) {
       const char* base = reinterpret_cast<const char*>(mv.fcl + (int64_t)mv.model_of(pn) * F_COUNT * n);
       const int bytes = F_COUNT * n * (int)sizeof(double);
-      for (int off = t * 128; off < bytes; off += NT * 128)
+      for (int off = t * 128; off < bytes; off += grp_threads * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
       if (own) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(io.q + (int64_t)i * io.lds + pn));
@@ -978,11 +964,11 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
         }
       }
     }
-    __syncthreads();
+    grp.sync();
     if (own) {
       const bool up_bad = (i < n - h) && ws[cfr::SG * n + i + h] != 0.0;
       const bool dn_bad = (i >= h) && ws[cfr::SG * n + i - h] != 0.0;
-      if (up_bad || dn_bad) atomicMin(&s_bad, i);
+      if (up_bad || dn_bad) atomicMin(s_bad, i);
       if (i < n - h) {
         const int k = i + h;
         double Lk[10], il[5], rt[5];
@@ -998,10 +984,10 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
         oee_down(D, R, rt, [&](int r, int c) { return ws[(cfr::PY + r * 5 + c) * n + k]; });
       }
     }
-    __syncthreads();
-    if (s_bad < n) {
+    grp.sync();
+    if (*s_bad < n) {
       if (t == 0) {
-        const int ib = s_bad;
+        const int ib = *s_bad;
         const bool up_bad = (ib < n - h) && ws[cfr::SG * n + ib + h] != 0.0;
         io.status[p] = PD_SLOT_OEE_SINGULAR_PIVOT;
         io.eround[p] = round;
@@ -1012,15 +998,15 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
   }
   // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
   if (own) {
-    if (!oee_final(D, R)) atomicMin(&s_bad, i);
+    if (!oee_final(D, R)) atomicMin(s_bad, i);
     ws_store<5>(ws, n, cfr::OR, i, R);  // constraint force F_c,i
   }
-  __syncthreads();
-  if (s_bad < n) {
+  grp.sync();
+  if (*s_bad < n) {
     if (t == 0) {
       io.status[p] = PD_SLOT_OEE_SINGULAR_FINAL;
       io.eround[p] = rounds;
-      io.eindex[p] = s_bad;
+      io.eindex[p] = *s_bad;
     }
     return;
   }
@@ -1049,6 +1035,117 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
   }
 }
 
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO io, const double* __restrict__ td_pre,
+                                                           int pf_stride) {
+  extern __shared__ double dyn_smem[];
+  __shared__ ScanSmem scan_sm;
+  __shared__ int s_bad, s_link_fail;
+  const int n = mv.n;
+  const int64_t p = blockIdx.x;
+  const int64_t mc = mv.model_of(p);
+  double* ws = dyn_smem;
+  const int t = threadIdx.x, i = t;
+  const bool own = i < n;
+  if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) {
+    if (t == 0) model_rejected(mv, io, p, mc);
+    return;
+  }
+  if (t == 0) {
+    s_bad = n;
+    s_link_fail = 0;
+  }
+  // ---- kinematics + torque surplus
+  const IdFields idf{cfr::REL, cfr::X, cfr::V, cfr::TMP, cfr::TD};
+  cta_kinematics(mv, io, p, mc, ws, idf, 1);
+  if (td_pre) {
+    if (own) ws[cfr::TD * n + i] = __ldg(td_pre + (int64_t)i * io.lds + p);
+    __syncthreads();
+  } else {
+    cta_bias_torque(mv, io, p, mc, ws, idf, 1, scan_sm);  // ends with a barrier
+  }
+  cfa_rows(mv, io, p, mc, ws, ws, cfr::REL, &s_bad, &s_link_fail, pf_stride, NT, CtaGroup{}, [] {});
+}
+
+// Warp-specialised CFA for batches of long chains (128 < n <= 256, c3):
+// persistent CTAs of 384 threads run two chains at once on two thread groups.
+//   rows      threads 0..255 (2 warpgroups, setmaxnreg 200): operators, OEE,
+//             extraction of chain k (cfa_rows, thread = row);
+//   prologue  threads 256..383 (1 warpgroup, setmaxnreg 104): joint
+//             transforms and tau_delta of chain k+1 (cta_kinematics /
+//             cta_bias_torque, 2 links per thread).
+// The one-chain-per-SM row kernel ran the latency-bound CTA scans of the
+// prologue alone (~35 % of c3); here they fill the issue slots the OEE rounds
+// leave idle. Handoff through shared memory (rel: 12 fields, tau_delta: 1) with
+// named barriers: 1 rows, 2 prologue, 3 "chain ready" (prologue arrives, rows
+// wait), 4 "handoff free" (rows arrive once the operators have read rel,
+// prologue waits before writing the next chain). setmaxnreg only moves
+// registers inside the CTA's launch allocation (384 x 168): 256 x 200 +
+// 128 x 104 = 384 x 168.
+namespace cws {
+constexpr int REL = 0, TD = 12, X = 13, V = 25, TMP = 31, FIELDS = 37;  // handoff + prologue scratch
+constexpr int kRows = 256, kPro = 128, kAll = kRows + kPro;
+}  // namespace cws
+
+__global__ void __launch_bounds__(cws::kAll, 1) cfa_ws_kernel(ModelView mv, BatchIO io) {
+  extern __shared__ double dyn_smem[];
+  __shared__ ScanSmem scan_pro;
+  __shared__ int s_bad, s_link_fail;
+  const int n = mv.n;
+  double* ws = dyn_smem;                // cfr::FIELDS x n: the rows' workspace
+  double* hand = ws + cfr::FIELDS * n;  // cws::FIELDS x n: handoff + prologue scratch
+  if (threadIdx.x < cws::kRows) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    const NamedGroup grp{0, cws::kRows, 1};
+    const int t = grp.tid();
+    for (int64_t p = blockIdx.x; p < io.B; p += gridDim.x) {
+      asm volatile("bar.sync 3, %0;" ::"n"(cws::kAll) : "memory");  // chain p's rel / tau_delta are in `hand`
+      const int64_t mc = mv.model_of(p);
+      if (__ldg(mv.mstatus + mc) != PD_SLOT_OK) {
+        if (t == 0) model_rejected(mv, io, p, mc);
+        asm volatile("bar.arrive 4, %0;" ::"n"(cws::kAll) : "memory");
+        continue;
+      }
+      if (t == 0) {
+        s_bad = n;
+        s_link_fail = 0;
+      }
+      if (t < n) ws[cfr::TD * n + t] = hand[cws::TD * n + t];
+      grp.sync();
+      cfa_rows(mv, io, p, mc, ws, hand, cws::REL, &s_bad, &s_link_fail, 0, cws::kRows, grp,
+               [] { asm volatile("bar.arrive 4, %0;" ::"n"(cws::kAll) : "memory"); });
+      grp.sync();  // the flags and the workspace are reused by the next chain
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+    const NamedGroup grp{cws::kRows, cws::kPro, 2};
+    bool first = true;
+    for (int64_t p = blockIdx.x; p < io.B; p += gridDim.x) {
+      if (!first) asm volatile("bar.sync 4, %0;" ::"n"(cws::kAll) : "memory");  // rows done with the previous chain's rel
+      first = false;
+      const int64_t mc = mv.model_of(p);
+      if (__ldg(mv.mstatus + mc) == PD_SLOT_OK) {
+        const IdFields idf{cws::REL, cws::X, cws::V, cws::TMP, cws::TD};
+        cta_kinematics(mv, io, p, mc, hand, idf, 2, grp);
+        cta_bias_torque(mv, io, p, mc, hand, idf, 2, scan_pro, grp);  // ends with a group barrier
+      }
+      __threadfence_block();
+      asm volatile("bar.arrive 3, %0;" ::"n"(cws::kAll) : "memory");
+    }
+    if (!first) asm volatile("bar.sync 4, %0;" ::"n"(cws::kAll) : "memory");  // the last chain's release
+  }
+}
+
+bool cfa_ws_fits(int n) { return n > 128 && n <= 256; }
+
+size_t cfa_ws_smem_bytes(int n) { return (size_t)(cfr::FIELDS + cws::FIELDS) * n * sizeof(double); }
+
+void launch_cfa_ws(const ModelView& mv, const BatchIO& io, int sm_count, cudaStream_t s) {
+  const size_t smem = cfa_ws_smem_bytes(mv.n);
+  cudaFuncSetAttribute(cfa_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)(io.B < sm_count ? io.B : sm_count);
+  cfa_ws_kernel<<<grid, cws::kAll, smem, s>>>(mv, io);
+}
 
 size_t cfa_workspace_bytes(int n) { return (size_t)cfa::FIELDS * n * sizeof(double); }
 

@@ -25,6 +25,23 @@ namespace pd {
 
 constexpr int kMaxWarps = 32;
 
+// The threads a CTA-per-chain stage runs on: the whole CTA (default), or a
+// warp-aligned range of it with its own named barrier (warp-specialised
+// kernels run two stages on two thread groups at once).
+struct CtaGroup {
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct NamedGroup {
+  int first;  // first thread (multiple of 32)
+  int count;  // threads (multiple of 32)
+  int bar;    // named barrier id (1..15; 0 is __syncthreads)
+  __device__ __forceinline__ int tid() const { return (int)threadIdx.x - first; }
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(count) : "memory");
+  }
+};
+
 // Scratch for the cross-warp level of a scan (K <= 12 doubles per warp).
 struct ScanSmem {
   double tot[kMaxWarps][12];
@@ -143,9 +160,9 @@ __device__ __forceinline__ Arr<K> shfl_idx(const Arr<K>& x, int src) {
 // exactly ceil_log2(nact) Hillis-Steele rounds like scan.hpp:46-61 (the
 // rounds ExecTrace reports, cta_scan_rounds). Contains three __syncthreads
 // unless one warp holds every link (then none).
-template <int K, bool REVERSE, class Op>
-__device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm, int nact) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int K, bool REVERSE, class Op, class G = CtaGroup>
+__device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm, int nact, const G& grp = G{}) {
+  const int lane = grp.tid() & 31, warp = grp.tid() >> 5;
   const int span = nact < 32 ? nact : 32;    // lanes of a warp that can hold data
   const int nwa = (nact + 31) >> 5;          // warps holding data
   // warp inclusive scan in (reversed) lane order
@@ -164,7 +181,7 @@ __device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm, int nact
 #pragma unroll
     for (int k = 0; k < K; ++k) sm.tot[warp][k] = inc.v[k];
   }
-  __syncthreads();
+  grp.sync();
   if (warp == 0) {
     // scan of warp totals in (reversed) warp order; lane w holds warp w
     Arr<K> t;
@@ -186,13 +203,13 @@ __device__ Arr<K> block_exclusive(const Arr<K>& x, Op op, ScanSmem& sm, int nact
       for (int k = 0; k < K; ++k) sm.tot[lane][k] = te.v[k];
     }
   }
-  __syncthreads();
+  grp.sync();
   Arr<K> wp = op.template identity<K>();
   if (warp < nwa) {
 #pragma unroll
     for (int k = 0; k < K; ++k) wp.v[k] = sm.tot[warp][k];
   }
-  __syncthreads();  // sm reusable by the next scan
+  grp.sync();  // sm reusable by the next scan
   return op(wp, exc);
 }
 
@@ -205,9 +222,9 @@ __host__ __device__ inline int cta_scan_rounds(int nact) {
 
 // Inclusive scan over the chain's links of a K-field array stored in the
 // workspace (ws[(f0 + k) * n + i]), in place. Links not present use identity.
-template <int K, bool REVERSE, class Op>
-__device__ void ws_scan(double* ws, int n, int f0, int lpt, Op op, ScanSmem& sm) {
-  const int t = threadIdx.x;
+template <int K, bool REVERSE, class Op, class G = CtaGroup>
+__device__ void ws_scan(double* ws, int n, int f0, int lpt, Op op, ScanSmem& sm, const G& grp = G{}) {
+  const int t = grp.tid();
   const int i0 = t * lpt, i1 = min(n, i0 + lpt);
   Arr<K> agg = op.template identity<K>();
   // local inclusive scan of own links
@@ -220,7 +237,7 @@ __device__ void ws_scan(double* ws, int n, int f0, int lpt, Op op, ScanSmem& sm)
 #pragma unroll
     for (int k = 0; k < K; ++k) ws[(f0 + k) * n + i] = agg.v[k];
   }
-  const Arr<K> pre = block_exclusive<K, REVERSE>(agg, op, sm, (n + lpt - 1) / lpt);
+  const Arr<K> pre = block_exclusive<K, REVERSE>(agg, op, sm, (n + lpt - 1) / lpt, grp);
   for (int i = i0; i < i1; ++i) {
     Arr<K> x;
 #pragma unroll
@@ -268,10 +285,11 @@ struct IdFields {
 };
 
 // Stage: joint transforms rel_i into ws (per link, independent).
+template <class G = CtaGroup>
 __device__ __forceinline__ void cta_kinematics(const ModelView& mv, const BatchIO& io, int64_t p, int64_t mc,
-                                               double* ws, const IdFields& F, int lpt) {
+                                               double* ws, const IdFields& F, int lpt, const G& grp = G{}) {
   const int n = mv.n;
-  const int i0 = threadIdx.x * lpt, i1 = min(n, i0 + lpt);
+  const int i0 = grp.tid() * lpt, i1 = min(n, i0 + lpt);
   for (int i = i0; i < i1; ++i) {
     const SE3d T = joint_transform(mv.screw(i, mc), mv.screw_iw(i, mc), mv.home_R(i, mc), mv.home_p(i, mc),
                                    io.ld(io.q, i, p));
@@ -283,14 +301,15 @@ __device__ __forceinline__ void cta_kinematics(const ModelView& mv, const BatchI
 // Stage: tau_delta = tau - ID(q, qd, qdd = 0) with gravity as base
 // acceleration -g (forward_dynamics.cpp:35-42). Requires rel in ws. Fields
 // v and tmp must be adjacent (tmp = v + 6): the (V0, A0) pair scan uses both.
+template <class G = CtaGroup>
 __device__ inline void cta_bias_torque(const ModelView& mv, const BatchIO& io, int64_t p, int64_t mc, double* ws,
-                                const IdFields& F, int lpt, ScanSmem& sm) {
+                                const IdFields& F, int lpt, ScanSmem& sm, const G& grp = G{}) {
   const int n = mv.n;
-  const int i0 = threadIdx.x * lpt, i1 = min(n, i0 + lpt);
+  const int i0 = grp.tid() * lpt, i1 = min(n, i0 + lpt);
   // X_i = rel_i * X_{i-1}
-  __syncthreads();
-  ws_scan<12, false>(ws, n, F.x, lpt, ComposeOp{}, sm);
-  __syncthreads();
+  grp.sync();
+  ws_scan<12, false>(ws, n, F.x, lpt, ComposeOp{}, sm, grp);
+  grp.sync();
   // base-frame rate twists s_i = Ad(X_i)^{-1} S_i qd_i, then one pair scan
   // gives V0_i and the bias acceleration sum A0_i (PairOp)
   for (int i = i0; i < i1; ++i) {
@@ -298,9 +317,9 @@ __device__ inline void cta_bias_torque(const ModelView& mv, const BatchIO& io, i
     ws_put_sv(ws, n, F.v, i, adinv_apply(X, io.ld(io.qd, i, p) * mv.screw(i, mc)));
     ws_put_sv(ws, n, F.v + 6, i, svzero());
   }
-  __syncthreads();
-  ws_scan<12, false>(ws, n, F.v, lpt, PairOp{}, sm);
-  __syncthreads();
+  grp.sync();
+  ws_scan<12, false>(ws, n, F.v, lpt, PairOp{}, sm, grp);
+  grp.sync();
   const Vec3d g = mv.gravity(mc);
   const Sv Abase = {mk(0, 0, 0), mk(-g.x, -g.y, -g.z)};
   for (int i = i0; i < i1; ++i) {
@@ -312,15 +331,15 @@ __device__ inline void cta_bias_torque(const ModelView& mv, const BatchIO& io, i
     const Sv f = inertia_apply(J, A) + neg_advT_apply(V, h);
     ws_put_sv(ws, n, F.tmp, i, adT_apply(X, f));  // tmp = v + 6: this link's pair was read above
   }
-  __syncthreads();
-  ws_scan<6, true>(ws, n, F.tmp, lpt, AddOp{}, sm);
-  __syncthreads();
+  grp.sync();
+  ws_scan<6, true>(ws, n, F.tmp, lpt, AddOp{}, sm, grp);
+  grp.sync();
   for (int i = i0; i < i1; ++i) {
     const SE3d X = ws_get_se3(ws, n, F.x, i);
     const Sv Fi = adinvT_apply(X, ws_get_sv(ws, n, F.tmp, i));
     ws[F.td * n + i] = io.ld(io.tau, i, p) - dot(mv.screw(i, mc), Fi);
   }
-  __syncthreads();
+  grp.sync();
 }
 
 }  // namespace pd

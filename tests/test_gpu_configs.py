@@ -118,7 +118,7 @@ def test_c3_cfa_every_slot(oracle, gpu_ctx):
     q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
     gpu_ctx.set_models(links, None)
     qdd, st = device_solve(gpu_ctx, pd.FdAlgo.cfa, q, qd, tau)
-    assert gpu_ctx.last_variant() == "cfa_row_kernel", gpu_ctx.last_variant()
+    assert gpu_ctx.last_variant() == "cfa_ws_kernel", gpu_ctx.last_variant()
     assert (st == 0).all()
     ref, ost = oracle.batch_forward_dynamics("cfa", links, GRAV, q, qd, tau)
     assert (ost == 0).all()
