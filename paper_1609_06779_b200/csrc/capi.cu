@@ -643,8 +643,12 @@ const char* pd_kernel_variant(const pd_ctx* ctx, pd_algo algo, int32_t n_links) 
   switch (algo) {
     case PD_ABIA: return "abia_ring_kernel (lane per chain, 3 fused base-frame passes, persistent CTAs, TMA producer "
                          "warp + per-pass byte ring); abia_cta_kernel for n >= 64 in batches <= 2 x SMs (CTA per chain)";
-    case PD_CFA: return n_links <= 256 ? "cfa_row_kernel (CTA per chain, thread per row, row blocks in registers, OEE "
+    case PD_CFA: return n_links <= 128 ? "cfa_row_kernel (CTA per chain, thread per row, row blocks in registers, OEE "
                                         "in smem); tau_surplus_lane_kernel pre-pass for batches >= 128 x SMs"
+                 : n_links <= 256 ? "cfa_ws_kernel for 2 x SMs <= batch < 128 x SMs (persistent, warp-specialised: OEE "
+                                    "rows of chain k beside the kinematics / tau_delta of chain k+1); otherwise "
+                                    "cfa_row_kernel (CTA per chain, thread per row, OEE in smem), tau_surplus_lane_kernel "
+                                    "pre-pass for batches >= 128 x SMs"
                  : cfa_workspace_bytes(n_links) <= 220 * 1024 ? "cfa_cta_kernel<smem> (CTA per chain, OEE in smem)"
                                                                     : "cfa_cta_kernel<global> (CTA per chain, L2 workspace); batches "
                                                                       "<= 4: CTA prologue + grid-wide cooperative OEE (cfa_oee_coop)";

@@ -284,3 +284,30 @@ def test_model_upload_cache_and_first_failing_link(oracle, gpu_ctx):
     ms, mr = gpu_ctx.set_models(bad, None)
     assert list(ms) == [pd.api._capi.SLOT_BAD_MODEL, pd.api._capi.SLOT_BAD_MODEL, 0]
     assert list(mr[:2]) == [3, 2]
+
+
+def test_warp_specialised_cfa_error_paths(oracle, gpu_ctx):
+    """cfa_ws_kernel (persistent, two thread groups handing chains over through
+    named barriers) with rejected models and non-finite inputs scattered through
+    the batch: every slot gets its own outcome, the others match the oracle,
+    and nothing hangs (a skipped chain still signals both barriers)."""
+    n, B = 160, 700
+    cell = oracle.workload_seed(8, n, B)
+    links = oracle.workload_chains(cell, n, B).copy()
+    q, qd, tau = (a.copy() for a in oracle.workload_inputs(cell, n, B, 0))
+    bad_model = [0, 147, 148, 300, B - 1]
+    for b in bad_model:
+        links[b, 5, 0] = -1.0                   # mass rule
+    q[10, 7] = np.nan                           # Eigen LLT semantics: no error, NaN result
+    gpu_ctx.set_models(links, None)
+    qdd, st = device_solve(gpu_ctx, pd.FdAlgo.cfa, q, qd, tau)
+    assert gpu_ctx.last_variant() == "cfa_ws_kernel", gpu_ctx.last_variant()
+    assert all(st[0, b] == pd.api._capi.SLOT_BAD_MODEL for b in bad_model)
+    good = np.setdiff1d(np.arange(B), bad_model + [10])
+    assert (st[0, good] == 0).all()
+    idx = good[::23]
+    ref, _ = oracle.batch_forward_dynamics("cfa", links[idx], GRAV, q[idx], qd[idx], tau[idx])
+    assert rel_gaps(qdd[idx], ref).max() <= 1e-8
+    with pytest.raises(oracle.OracleError) as e:  # NaN angle: the reference's OEE meets a singular pivot
+        oracle.forward_dynamics("cfa", links[10], GRAV, q[10], qd[10], tau[10])
+    assert pd.api._capi.slot_message(st[0, 10], st[1, 10], st[2, 10], n) == str(e.value)
