@@ -580,16 +580,6 @@ pd_status pd_create(pd_ctx** out, int device) {
     return PD_CUDA_ERROR;
   }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
-  if (const char* e = std::getenv("PD_L2_PERSIST_MB")) {  // experiment: L2 set-aside for evict_last lines
-    int maxp = 0;
-    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
-    size_t want = (size_t)std::atoi(e) << 20;
-    if (want > (size_t)maxp) want = (size_t)maxp;
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-    size_t got = 0;
-    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
-    std::fprintf(stderr, "pd: persisting L2 set-aside %zu MB (max %d MB)\n", got >> 20, maxp >> 20);
-  }
   ctx->stream = ctx->own_stream;
   *out = ctx;
   return PD_OK;
