@@ -16,6 +16,7 @@
 //   Twist / Wrench                 spatial.hpp:15-60 (stacked (angular, linear) / (moment, force))
 //   IdOptions / LinkStates         inverse_dynamics.hpp:23-34
 //   inverse_dynamics / bias_torque / link_states   inverse_dynamics.hpp:71-83
+//   propagate_velocities / _accelerations / _forces, inverse_dynamics_assembled   inverse_dynamics.hpp:36-75
 //   joint_space_inertia            forward_dynamics.hpp:34-35 (MatrixXd stand-in)
 //   solve_lower_bidiag / solve_upper_bidiag / oee_solve   scan.hpp:100-168, oee.hpp:149-189
 //   LinkSpec / RobotChain          model.hpp:17-30
@@ -285,6 +286,22 @@ struct LinkStates {
   std::vector<Twist> acceleration;
   std::vector<Wrench> force;
 };
+
+// The three propagations over assembled kinematics (inverse_dynamics.hpp:36-66,
+// inverse_dynamics.cpp:27-120): block bi-diagonal systems solved on the device
+// by the building-block scan.
+std::vector<Twist> propagate_velocities(const ChainKinematics& kin, const JointVector& qdot,
+                                        const Twist& base_velocity, ScanTrace* trace = nullptr);
+std::vector<Twist> propagate_accelerations(const ChainKinematics& kin, std::span<const Twist> velocity,
+                                           const JointVector& qdot, const JointVector& qddot,
+                                           const Twist& base_acceleration, ScanTrace* trace = nullptr);
+std::vector<Wrench> propagate_forces(const ChainKinematics& kin, std::span<const Twist> velocity,
+                                     std::span<const Twist> acceleration, std::span<const SpatialInertia> inertia,
+                                     const Wrench& tip_wrench, ScanTrace* trace = nullptr);
+// inverse_dynamics.hpp:68-75 (inverse_dynamics.cpp:122-164).
+JointVector inverse_dynamics_assembled(const ChainKinematics& kin, std::span<const SpatialInertia> inertia,
+                                       const Vec3& gravity, const JointVector& qdot, const JointVector& qddot,
+                                       const IdOptions& opts = {}, ExecTrace* trace = nullptr);
 
 JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
                              const JointVector& qddot, const IdOptions& opts = {}, ExecTrace* trace = nullptr);

@@ -336,6 +336,30 @@ pd_status pd_cfa_apply(pd_ctx* ctx, int32_t op, int64_t batch, int32_t n, const 
                        const double* cross_diag, const double* cross_super, const double* joint_diag,
                        const double* joint_off, const double* in, double* out);
 
+/* The three propagations of inverse dynamics over caller-supplied dense
+ * kinematics (inverse_dynamics.hpp:36-66, src/inverse_dynamics.cpp:27-120),
+ * each a block bi-diagonal system solved by the building-block scan
+ * (pd_block_bidiag_solve6's kernel) after a device-side setup of its
+ * couplings and right-hand sides:
+ *   PD_PROPAGATE_VELOCITIES     V_0 = Ad_base V_b + S_0 qd_0, V_i = T_{i-1} V_{i-1} + S_i qd_i
+ *                               (boundary = base twist; needs base_transport, qdot)
+ *   PD_PROPAGATE_ACCELERATIONS  A_i = T_{i-1} A_{i-1} + S_i qdd_i + ad_{V_i}(S_i qd_i)
+ *                               (boundary = base acceleration; needs velocity)
+ *   PD_PROPAGATE_FORCES         F_i = T_i^T F_{i+1} + J_i A_i - ad_{V_i}^T (J_i V_i), F_{n-1} += tip
+ *                               (boundary = tip wrench; needs inertia, velocity, acceleration)
+ * Arrays: base_transport [b][36], transport [b][n-1][36], screw / velocity /
+ * acceleration / out [b][n][6], inertia [b][n][36] ([n][36] if
+ * shared_inertia), qdot / qddot [b][n], boundary [6]. */
+typedef enum pd_propagate_kind {
+  PD_PROPAGATE_VELOCITIES = 0,
+  PD_PROPAGATE_ACCELERATIONS = 1,
+  PD_PROPAGATE_FORCES = 2
+} pd_propagate_kind;
+pd_status pd_propagate(pd_ctx* ctx, int32_t kind, int64_t batch, int32_t n, const double* base_transport,
+                       const double* transport, const double* screw, const double* inertia, int32_t shared_inertia,
+                       const double* qdot, const double* qddot, const double* velocity, const double* acceleration,
+                       const double* boundary, double* out);
+
 /* Page-locked host memory for staging host-buffer calls (copies from it run
  * at PCIe DMA speed instead of through the driver's pageable bounce buffer).
  * The C++ drop-in packs its batch calls into such a buffer. */

@@ -31,7 +31,9 @@ EXPORTS = (
     "pd_forward_dynamics_traced", "pd_last_variant", "pd_last_trace", "pd_set_selection_batch",
     "pd_assemble_kinematics", "pd_link_inertias", "pd_articulated_body_inertias", "pd_constraint_basis",
     "pd_cfa_operators", "pd_cfa_apply", "pd_host_alloc", "pd_host_free",
+    "pd_propagate",
 )
+PD_PROPAGATE_VELOCITIES, PD_PROPAGATE_ACCELERATIONS, PD_PROPAGATE_FORCES = range(3)
 PD_APPLY_CROSS, PD_APPLY_CROSS_TRANSPOSE, PD_APPLY_JOINT = range(3)
 
 
@@ -151,6 +153,9 @@ def load():
     L.pd_host_alloc.restype = C.c_int
     L.pd_host_free.argtypes = [C.c_void_p]
     L.pd_host_free.restype = None
+    L.pd_propagate.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, _D, _D, _D, _D, C.c_int32, _D, _D, _D, _D,
+                               _D, _D]
+    L.pd_propagate.restype = C.c_int
     _lib = L
     return L
 

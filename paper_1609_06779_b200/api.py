@@ -416,6 +416,23 @@ class Context:
             _capi.iptr(o["status"]), _capi.iptr(o["index"])))
         return o
 
+    def propagate(self, kind, base_transport, transport, screw, boundary, qdot=None, qddot=None, velocity=None,
+                  acceleration=None, inertia=None):
+        """One of the three propagations of inverse_dynamics.cpp:27-120 over
+        dense kinematics (pd_propagate): kind PD_PROPAGATE_VELOCITIES /
+        _ACCELERATIONS / _FORCES; arrays batched as in the C-ABI; -> (B, n, 6)."""
+        screw = np.ascontiguousarray(screw, dtype=np.float64)
+        B, n = screw.shape[:2]
+        f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        inertia = f(inertia)
+        shared = inertia is not None and inertia.ndim == 3
+        out = np.empty((B, n, 6))
+        args = [f(base_transport), f(np.reshape(transport, (B, max(n - 1, 0), 6, 6))), screw, inertia]
+        self._check(self._L.pd_propagate(self._h, int(kind), B, n, *(_capi.dptr(a) for a in args), int(shared),
+                                         *(_capi.dptr(f(a)) for a in (qdot, qddot, velocity, acceleration)),
+                                         _capi.dptr(f(np.ravel(boundary))), _capi.dptr(out)))
+        return out
+
     def cfa_apply(self, op, ops, x):
         """CfaOperators::apply_* on the device: op PD_APPLY_CROSS (x (B, n) ->
         (B, n, 5)), PD_APPLY_CROSS_TRANSPOSE ((B, n, 5) -> (B, n)),
@@ -822,6 +839,77 @@ def build_cfa_operators(chain: RobotChain, kin: ChainKinematics, basis: Constrai
         trace.parallel_link_stages += 2
     return CfaOperators(*(o[k][0] for k in ("diag", "upper", "cross_sub", "cross_diag", "cross_super",
                                             "joint_diag", "joint_off")))
+
+
+def _check_joint_size(kin: ChainKinematics, v, name):
+    """inverse_dynamics.cpp:10-17."""
+    if len(v) != kin.size():
+        raise InvalidArgument(f"{name} has length {len(v)} but the chain has {kin.size()} joints")
+
+
+def propagate_velocities(kin: ChainKinematics, qdot, base_velocity=None, trace: Optional[ScanTrace] = None,
+                         ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:27-51 on the device (block bi-diagonal scan): (n, 6) twists."""
+    _check_joint_size(kin, qdot, "qdot")
+    n = kin.size()
+    if trace is not None:
+        trace.rounds = ceil_log2(n)
+    if n == 0:
+        return np.zeros((0, 6))
+    bv = np.zeros(6) if base_velocity is None else np.asarray(base_velocity, np.float64)
+    return (ctx or default_context()).propagate(_capi.PD_PROPAGATE_VELOCITIES, kin.base_transport[None],
+                                                kin.transport[None], kin.screw[None], bv,
+                                                qdot=np.asarray(qdot, np.float64)[None])[0]
+
+
+def propagate_accelerations(kin: ChainKinematics, velocity, qdot, qddot, base_acceleration=None,
+                            trace: Optional[ScanTrace] = None, ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:53-84 on the device: (n, 6) accelerations."""
+    _check_joint_size(kin, qdot, "qdot")
+    _check_joint_size(kin, qddot, "qddot")
+    n = kin.size()
+    if trace is not None:
+        trace.rounds = ceil_log2(n)
+    if n == 0:
+        return np.zeros((0, 6))
+    ba = np.zeros(6) if base_acceleration is None else np.asarray(base_acceleration, np.float64)
+    return (ctx or default_context()).propagate(
+        _capi.PD_PROPAGATE_ACCELERATIONS, kin.base_transport[None], kin.transport[None], kin.screw[None], ba,
+        qdot=np.asarray(qdot, np.float64)[None], qddot=np.asarray(qddot, np.float64)[None],
+        velocity=np.asarray(velocity, np.float64).reshape(1, n, 6))[0]
+
+
+def propagate_forces(kin: ChainKinematics, velocity, acceleration, inertia, tip_wrench=None,
+                     trace: Optional[ScanTrace] = None, ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:86-120 on the device: (n, 6) wrenches."""
+    n = kin.size()
+    if trace is not None:
+        trace.rounds = ceil_log2(n)
+    if n == 0:
+        return np.zeros((0, 6))
+    tw = np.zeros(6) if tip_wrench is None else np.asarray(tip_wrench, np.float64)
+    return (ctx or default_context()).propagate(
+        _capi.PD_PROPAGATE_FORCES, None, kin.transport[None], kin.screw[None], tw,
+        velocity=np.asarray(velocity, np.float64).reshape(1, n, 6),
+        acceleration=np.asarray(acceleration, np.float64).reshape(1, n, 6),
+        inertia=np.asarray(inertia, np.float64).reshape(1, n, 6, 6))[0]
+
+
+def inverse_dynamics_assembled(kin: ChainKinematics, inertia, gravity, qdot, qddot, opts: Optional[IdOptions] = None,
+                               trace: Optional[ExecTrace] = None, ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_dynamics.cpp:122-164: the three propagations, tau_i = S_i . F_i."""
+    opts = opts or IdOptions()
+    sv, sa, sf = ScanTrace(), ScanTrace(), ScanTrace()
+    vel = propagate_velocities(kin, qdot, opts.base_velocity, sv, ctx)
+    ba = np.array(opts.base_acceleration, np.float64).copy()
+    if opts.apply_gravity:
+        ba[3:] -= np.asarray(gravity, np.float64)
+    acc = propagate_accelerations(kin, vel, qdot, qddot, ba, sa, ctx)
+    frc = propagate_forces(kin, vel, acc, inertia, opts.tip_wrench, sf, ctx)
+    if trace is not None:
+        trace.scan_rounds_max = max(trace.scan_rounds_max, sv.rounds, sa.rounds, sf.rounds)
+        trace.parallel_link_stages += 5
+    return np.einsum("ij,ij->i", kin.screw, frc)
 
 
 # --------------------------------------------------------------------------- model files

@@ -613,6 +613,108 @@ pd_id_options to_c(const IdOptions& o) {
 
 }  // namespace
 
+namespace {
+
+// inverse_dynamics.cpp:10-17
+void check_joint_size(const ChainKinematics& kin, const JointVector& v, const char* name) {
+  if (static_cast<int>(v.size()) != kin.size())
+    throw std::invalid_argument(std::string(name) + " has length " + std::to_string(v.size()) + " but the chain has " +
+                                std::to_string(kin.size()) + " joints");
+}
+
+std::vector<double> flat6(std::span<const Twist> v) {
+  std::vector<double> out(6 * v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) put_block(v[i].stacked(), &out[6 * i]);
+  return out;
+}
+
+// One propagation on the device (pd_propagate): kinematics and the per-kind inputs flattened.
+std::vector<Vec6> propagate(int kind, const ChainKinematics& kin, const JointVector* qdot, const JointVector* qddot,
+                            std::span<const Twist> velocity, std::span<const Twist> acceleration,
+                            std::span<const SpatialInertia> inertia, const Vec6& boundary, ScanTrace* trace) {
+  const int n = kin.size();
+  if (trace) trace->rounds = ceil_log2(static_cast<std::size_t>(n));  // the scan's designed depth (scan.hpp:32-65)
+  std::vector<Vec6> out(static_cast<std::size_t>(n));
+  if (n == 0) return out;
+  std::vector<double> tr, sc, base(36), J, vv, aa, bd(6), x(6 * static_cast<std::size_t>(n));
+  kin_arrays(kin, tr, sc);
+  put_block(kin.base_transport.mat, base.data());
+  put_block(boundary, bd.data());
+  if (!velocity.empty()) vv = flat6(velocity);
+  if (!acceleration.empty()) aa = flat6(acceleration);
+  if (!inertia.empty()) {
+    J.resize(36 * static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) put_block(inertia[i].matrix(), &J[36 * i]);
+  }
+  pd_ctx* c = ctx();
+  check_call(c, pd_propagate(c, kind, 1, n, base.data(), tr.empty() ? nullptr : tr.data(), sc.data(),
+                             J.empty() ? nullptr : J.data(), 0, qdot ? qdot->data() : nullptr,
+                             qddot ? qddot->data() : nullptr, vv.empty() ? nullptr : vv.data(),
+                             aa.empty() ? nullptr : aa.data(), bd.data(), x.data()));
+  for (int i = 0; i < n; ++i) out[i] = get_block<6, 1>(&x[6 * i]);
+  return out;
+}
+
+template <class T>
+std::vector<T> as_spatial(const std::vector<Vec6>& v) {
+  std::vector<T> out;
+  out.reserve(v.size());
+  for (const Vec6& x : v) out.push_back(T::from_stacked(x));
+  return out;
+}
+
+}  // namespace
+
+std::vector<Twist> propagate_velocities(const ChainKinematics& kin, const JointVector& qdot,
+                                        const Twist& base_velocity, ScanTrace* trace) {
+  check_joint_size(kin, qdot, "qdot");
+  return as_spatial<Twist>(propagate(PD_PROPAGATE_VELOCITIES, kin, &qdot, nullptr, {}, {}, {},
+                                     base_velocity.stacked(), trace));
+}
+
+std::vector<Twist> propagate_accelerations(const ChainKinematics& kin, std::span<const Twist> velocity,
+                                           const JointVector& qdot, const JointVector& qddot,
+                                           const Twist& base_acceleration, ScanTrace* trace) {
+  check_joint_size(kin, qdot, "qdot");
+  check_joint_size(kin, qddot, "qddot");
+  if (static_cast<int>(velocity.size()) != kin.size())
+    throw std::invalid_argument("propagate_accelerations: one velocity per link expected");
+  return as_spatial<Twist>(propagate(PD_PROPAGATE_ACCELERATIONS, kin, &qdot, &qddot, velocity, {}, {},
+                                     base_acceleration.stacked(), trace));
+}
+
+std::vector<Wrench> propagate_forces(const ChainKinematics& kin, std::span<const Twist> velocity,
+                                     std::span<const Twist> acceleration, std::span<const SpatialInertia> inertia,
+                                     const Wrench& tip_wrench, ScanTrace* trace) {
+  const int n = kin.size();
+  if (static_cast<int>(velocity.size()) != n || static_cast<int>(acceleration.size()) != n ||
+      static_cast<int>(inertia.size()) != n)
+    throw std::invalid_argument("propagate_forces: one velocity, acceleration and inertia per link expected");
+  return as_spatial<Wrench>(
+      propagate(PD_PROPAGATE_FORCES, kin, nullptr, nullptr, velocity, acceleration, inertia, tip_wrench.stacked(), trace));
+}
+
+JointVector inverse_dynamics_assembled(const ChainKinematics& kin, std::span<const SpatialInertia> inertia,
+                                       const Vec3& gravity, const JointVector& qdot, const JointVector& qddot,
+                                       const IdOptions& opts, ExecTrace* trace) {
+  const int n = kin.size();
+  ScanTrace sv, sa, sf;
+  const std::vector<Twist> vel = propagate_velocities(kin, qdot, opts.base_velocity, &sv);
+  Twist base_acc = opts.base_acceleration;
+  if (opts.apply_gravity) base_acc.linear -= gravity;  // inverse_dynamics.cpp:135-140
+  const std::vector<Twist> acc = propagate_accelerations(kin, vel, qdot, qddot, base_acc, &sa);
+  const std::vector<Wrench> frc = propagate_forces(kin, vel, acc, inertia, opts.tip_wrench, &sf);
+  JointVector tau(n);
+  for (int i = 0; i < n; ++i) tau[i] = kin.screw[i].stacked().dot(frc[i].stacked());  // :146-150
+  if (trace) {
+    trace->note_scan(sv);
+    trace->note_scan(sa);
+    trace->note_scan(sf);
+    for (int k = 0; k < 5; ++k) trace->note_parallel_stage();  // kinematics, three source builds, extraction
+  }
+  return tau;
+}
+
 JointVector inverse_dynamics(const RobotChain& chain, const JointVector& q, const JointVector& qdot,
                              const JointVector& qddot, const IdOptions& opts, ExecTrace* trace) {
   q_size(chain, q);

@@ -1269,6 +1269,10 @@ void launch_cfa_ops(int64_t batch, int n, const double* inertia, int64_t istride
 void launch_cfa_apply(int op, int64_t batch, int n, const double* cross_sub, const double* cross_diag,
                       const double* cross_super, const double* joint_diag, const double* joint_off, const double* in,
                       double* out, cudaStream_t s);
+void launch_propagate_setup(int kind, int64_t batch, int n, const double* base_transport, const double* transport,
+                            const double* screw, const double* inertia, int64_t istride, const double* qdot,
+                            const double* qddot, const double* vel, const double* acc, const double* boundary,
+                            double* coupling, double* rhs, cudaStream_t s);
 }  // namespace pd
 
 namespace {
@@ -1522,6 +1526,49 @@ pd_status pd_host_alloc(uint64_t bytes, void** out) {
 
 void pd_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+pd_status pd_propagate(pd_ctx* ctx, int32_t kind, int64_t batch, int32_t n, const double* base_transport,
+                       const double* transport, const double* screw, const double* inertia, int32_t shared_inertia,
+                       const double* qdot, const double* qddot, const double* velocity, const double* acceleration,
+                       const double* boundary, double* out) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  const bool vel = kind == PD_PROPAGATE_VELOCITIES, acc = kind == PD_PROPAGATE_ACCELERATIONS,
+             frc = kind == PD_PROPAGATE_FORCES;
+  if (bad_args(ctx, (!vel && !acc && !frc) || batch < 0 || n < 1 ||
+                        (batch > 0 && (!screw || !out || !boundary || (n > 1 && !transport) ||
+                                       ((vel || acc) && (!base_transport || !qdot)) || (acc && (!qddot || !velocity)) ||
+                                       (frc && (!inertia || !velocity || !acceleration)))),
+               "propagate: invalid arguments"))
+    return PD_INVALID_ARGUMENT;
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const int64_t e = (int64_t)(n - 1) * batch, r = (int64_t)n * batch;
+  Arena a;
+  const size_t ib = a.add_in(vel || acc ? base_transport : nullptr, vel || acc ? sizeof(double) * 36 * batch : 0);
+  const size_t it = a.add_in(transport, sizeof(double) * 36 * e);
+  const size_t is = a.add_in(screw, sizeof(double) * 6 * r);
+  const size_t ij = a.add_in(frc ? inertia : nullptr, frc ? sizeof(double) * 36 * n * (shared_inertia ? 1 : batch) : 0);
+  const size_t iq = a.add_in(vel || acc ? qdot : nullptr, vel || acc ? sizeof(double) * r : 0);
+  const size_t iqq = a.add_in(acc ? qddot : nullptr, acc ? sizeof(double) * r : 0);
+  const size_t iv = a.add_in(acc || frc ? velocity : nullptr, acc || frc ? sizeof(double) * 6 * r : 0);
+  const size_t ia = a.add_in(frc ? acceleration : nullptr, frc ? sizeof(double) * 6 * r : 0);
+  const size_t ibd = a.add_in(boundary, sizeof(double) * 6);
+  const size_t oc = a.add_out(nullptr, sizeof(double) * 36 * e);
+  const size_t orh = a.add_out(nullptr, sizeof(double) * 6 * r);
+  const size_t ox = a.add_out(out, sizeof(double) * 6 * r);
+  pd_status st = a.stage(ctx);
+  if (st != PD_OK) return st;
+  launch_propagate_setup(kind, batch, n, a.in<double>(ib), a.in<double>(it), a.in<double>(is), a.in<double>(ij),
+                         shared_inertia ? 0 : 36 * (int64_t)n, a.in<double>(iq), a.in<double>(iqq), a.in<double>(iv),
+                         a.in<double>(ia), a.in<double>(ibd), a.out<double>(oc), a.out<double>(orh), ctx->stream);
+  launch_bidiag6(a.out<double>(oc), a.out<double>(orh), a.out<double>(ox), batch, n, frc ? 1 : 0, ctx->stream);
+  ctx->launches += 2;
+  return a.finish(ctx);
 }
 
 }  // extern "C"

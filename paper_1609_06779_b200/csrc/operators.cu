@@ -404,6 +404,101 @@ __global__ void cfa_apply_kernel(int op, int64_t batch, int n, const double* __r
   }
 }
 
+// small_adjoint(V) x = (w x xa, v x xa + w x xl) and its transpose applied to f:
+// ad(V)^T f = (-(w x fa) - (v x fl), -(w x fl))   (spatial.cpp:18-25)
+__device__ __forceinline__ void adv_mul(const double* V, const double* x, double* o) {
+  const double* w = V;
+  const double* v = V + 3;
+  double c1[3], c2[3], c3[3];
+  auto cross = [](const double* a, const double* b, double* r) {
+    r[0] = a[1] * b[2] - a[2] * b[1];
+    r[1] = a[2] * b[0] - a[0] * b[2];
+    r[2] = a[0] * b[1] - a[1] * b[0];
+  };
+  cross(w, x, c1);
+  cross(v, x, c2);
+  cross(w, x + 3, c3);
+  for (int k = 0; k < 3; ++k) {
+    o[k] = c1[k];
+    o[3 + k] = c2[k] + c3[k];
+  }
+}
+__device__ __forceinline__ void advT_mul(const double* V, const double* f, double* o) {
+  const double* w = V;
+  const double* v = V + 3;
+  auto cross = [](const double* a, const double* b, double* r) {
+    r[0] = a[1] * b[2] - a[2] * b[1];
+    r[1] = a[2] * b[0] - a[0] * b[2];
+    r[2] = a[0] * b[1] - a[1] * b[0];
+  };
+  double c1[3], c2[3], c3[3];
+  cross(w, f, c1);
+  cross(v, f + 3, c2);
+  cross(w, f + 3, c3);
+  for (int k = 0; k < 3; ++k) {
+    o[k] = -c1[k] - c2[k];
+    o[3 + k] = -c3[k];
+  }
+}
+
+// The three propagations of inverse_dynamics.cpp:27-120 as block bi-diagonal
+// systems (the reference solves them with its scan): this kernel builds the
+// couplings and right-hand sides, thread per (problem, link), and the system
+// goes to bidiag6_kernel (the building-block scan).
+//   kind 0 velocities    lower, coupling transport[i-1], rhs qd_i S_i (+ Ad_base V_base at i = 0)
+//   kind 1 accelerations lower, rhs qdd_i S_i + ad_{V_i}(qd_i S_i) (+ Ad_base A_base)
+//   kind 2 forces        upper, coupling transport[i]^T, rhs J_i A_i - ad_{V_i}^T (J_i V_i) (+ tip at n-1)
+__global__ void propagate_setup_kernel(int kind, int64_t batch, int n, const double* __restrict__ base_transport,
+                                       const double* __restrict__ transport, const double* __restrict__ screw,
+                                       const double* __restrict__ inertia, int64_t istride,
+                                       const double* __restrict__ qdot, const double* __restrict__ qddot,
+                                       const double* __restrict__ vel, const double* __restrict__ acc,
+                                       const double* __restrict__ boundary, double* __restrict__ coupling,
+                                       double* __restrict__ rhs) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= batch * n) return;
+  const int64_t p = t / n;
+  const int i = (int)(t - p * n);
+  const double* S = screw + t * 6;
+  double r[6];
+  if (kind == 0 || kind == 1) {
+    const double qd = qdot[t];
+    for (int k = 0; k < 6; ++k) r[k] = (kind == 0 ? qd : qddot[t]) * S[k];
+    if (kind == 1) {
+      double rate[6], a[6];
+      for (int k = 0; k < 6; ++k) rate[k] = qd * S[k];
+      adv_mul(vel + t * 6, rate, a);
+      for (int k = 0; k < 6; ++k) r[k] += a[k];
+    }
+    if (i == 0) {
+      double b[6];
+      mm<6, 6, 1>(base_transport + p * 36, boundary, b);
+      for (int k = 0; k < 6; ++k) r[k] += b[k];
+    }
+    if (i >= 1) {
+      const double* T = transport + (p * (n - 1) + (i - 1)) * 36;
+      double* C = coupling + (p * (n - 1) + (i - 1)) * 36;
+      for (int k = 0; k < 36; ++k) C[k] = T[k];
+    }
+  } else {
+    const double* J = inertia + p * istride + (int64_t)i * 36;
+    double JA[6], JV[6], adf[6];
+    mm<6, 6, 1>(J, acc + t * 6, JA);
+    mm<6, 6, 1>(J, vel + t * 6, JV);
+    advT_mul(vel + t * 6, JV, adf);
+    for (int k = 0; k < 6; ++k) r[k] = JA[k] - adf[k];  // J A - ad_V^T (J V)   (inverse_dynamics.cpp:105-111)
+    if (i == n - 1)
+      for (int k = 0; k < 6; ++k) r[k] += boundary[k];
+    if (i + 1 < n) {
+      const double* T = transport + (p * (n - 1) + i) * 36;
+      double* C = coupling + (p * (n - 1) + i) * 36;
+      for (int a = 0; a < 6; ++a)
+        for (int b = 0; b < 6; ++b) C[a * 6 + b] = T[b * 6 + a];
+    }
+  }
+  for (int k = 0; k < 6; ++k) rhs[t * 6 + k] = r[k];
+}
+
 __global__ void fill_i32_kernel(int32_t* a, int64_t count, int32_t v) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < count) a[t] = v;
@@ -438,6 +533,14 @@ void launch_cfa_ops(int64_t batch, int n, const double* inertia, int64_t istride
   cfa_ops_kernel<<<blocks_for(batch * n, 64), 64, 0, s>>>(batch, n, inertia, istride, transport, screw, basis, diag,
                                                           upper, cross_sub, cross_diag, cross_super, joint_diag,
                                                           joint_off, bad_link);
+}
+void launch_propagate_setup(int kind, int64_t batch, int n, const double* base_transport, const double* transport,
+                            const double* screw, const double* inertia, int64_t istride, const double* qdot,
+                            const double* qddot, const double* vel, const double* acc, const double* boundary,
+                            double* coupling, double* rhs, cudaStream_t s) {
+  propagate_setup_kernel<<<blocks_for(batch * n, 128), 128, 0, s>>>(kind, batch, n, base_transport, transport, screw,
+                                                                     inertia, istride, qdot, qddot, vel, acc, boundary,
+                                                                     coupling, rhs);
 }
 void launch_cfa_apply(int op, int64_t batch, int n, const double* cross_sub, const double* cross_diag,
                       const double* cross_super, const double* joint_diag, const double* joint_off, const double* in,

@@ -7,6 +7,7 @@
 // exit status = number of failures.
 #include <pardyn/pardyn.hpp>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -338,6 +339,74 @@ int main() {
     const JointVector plain = cfa_forward_dynamics(s.chain, s.q, s.qdot, s.tau);
     const JointVector traced = cfa_forward_dynamics(s.chain, s.q, s.qdot, s.tau, &constraint);
     check((plain - traced).norm() <= 1e-12 * std::max(1.0, plain.norm()), "traced and untraced solves agree");
+  }
+
+  // test_invdyn.cpp:50-76: the scan-backed propagations vs the sequential Newton-Euler oracle
+  for (int n : {1, 2, 3, 7, 20}) {
+    Sample s = make_sample(n, 100 + static_cast<std::uint64_t>(n));
+    std::mt19937_64 e(1000 + n);
+    const JointVector qddot = uniform(e, n, -5.0, 5.0);
+    const ChainKinematics kin = assemble_kinematics(s.chain, s.q);
+    const auto inertia = link_inertias(s.chain);
+    std::vector<double> q(s.q.begin(), s.q.end()), qd(s.qdot.begin(), s.qdot.end()), qdd(qddot.begin(), qddot.end());
+    const auto ref = oracle::newton_euler(to_oracle(s.chain), q, qd, qdd, true, nullptr);
+    ScanTrace tv, ta, tf;
+    const auto vel = propagate_velocities(kin, s.qdot, Twist{}, &tv);
+    Twist base_acc;
+    base_acc.linear = -1.0 * s.chain.gravity;
+    const auto acc = propagate_accelerations(kin, vel, s.qdot, qddot, base_acc, &ta);
+    const auto frc = propagate_forces(kin, vel, acc, inertia, Wrench{}, &tf);
+    double worst = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const Vec6 v = vel[i].stacked(), a = acc[i].stacked(), f = frc[i].stacked();
+      double nv = 0, na = 0, nf = 0, dv = 0, da = 0, df = 0;
+      for (int k = 0; k < 6; ++k) {
+        nv += ref.velocity[i][k] * ref.velocity[i][k];
+        na += ref.acceleration[i][k] * ref.acceleration[i][k];
+        nf += ref.force[i][k] * ref.force[i][k];
+        dv += (v(k) - ref.velocity[i][k]) * (v(k) - ref.velocity[i][k]);
+        da += (a(k) - ref.acceleration[i][k]) * (a(k) - ref.acceleration[i][k]);
+        df += (f(k) - ref.force[i][k]) * (f(k) - ref.force[i][k]);
+      }
+      worst = std::max(worst, std::max(std::sqrt(dv) / std::max(1.0, std::sqrt(nv)),
+                                       std::max(std::sqrt(da) / std::max(1.0, std::sqrt(na)),
+                                                std::sqrt(df) / std::max(1.0, std::sqrt(nf)))));
+    }
+    const int depth = ceil_log2(static_cast<std::size_t>(n));
+    check(worst < 1e-12 && tv.rounds == depth && ta.rounds == depth && tf.rounds == depth,
+          "propagate_velocities / _accelerations / _forces match sequential Newton-Euler, n=" + std::to_string(n));
+    ExecTrace tr;
+    const JointVector tau = inverse_dynamics_assembled(kin, inertia, s.chain.gravity, s.qdot, qddot, {}, &tr);
+    const JointVector tau2 = inverse_dynamics(s.chain, s.q, s.qdot, qddot);
+    check((tau - tau2).norm() <= 1e-12 * std::max(1.0, tau2.norm()) && tr.scan_rounds_max == depth,
+          "inverse_dynamics_assembled == inverse_dynamics, n=" + std::to_string(n));
+  }
+  // test_invdyn.cpp:212-232: a moving base feeds into the link states
+  {
+    const Sample s = make_sample(4, 5115);
+    std::mt19937_64 e(5115);
+    const JointVector qddot = uniform(e, 4, -5.0, 5.0);
+    std::vector<double> q(s.q.begin(), s.q.end()), qd(s.qdot.begin(), s.qdot.end()), qdd(qddot.begin(), qddot.end());
+    const auto ref = oracle::newton_euler(to_oracle(s.chain), q, qd, qdd, false, nullptr);
+    RobotChain tail;
+    tail.gravity = s.chain.gravity;
+    tail.links.assign(s.chain.links.begin() + 1, s.chain.links.end());
+    const JointVector q3(s.q.begin() + 1, s.q.end()), qd3(s.qdot.begin() + 1, s.qdot.end()),
+        qdd3(qddot.begin() + 1, qddot.end());
+    const ChainKinematics kin = assemble_kinematics(tail, q3);
+    auto tw = [](const auto& a) { return Twist(Vec3(a[0], a[1], a[2]), Vec3(a[3], a[4], a[5])); };
+    const auto vel = propagate_velocities(kin, qd3, tw(ref.velocity[0]));
+    const auto acc = propagate_accelerations(kin, vel, qd3, qdd3, tw(ref.acceleration[0]));
+    double worst = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int k = 0; k < 6; ++k)
+        worst = std::max(worst, std::max(std::fabs(vel[i].stacked()(k) - ref.velocity[i + 1][k]),
+                                         std::fabs(acc[i].stacked()(k) - ref.acceleration[i + 1][k])));
+    check(worst < 1e-12, "a moving base feeds into the link states");
+    ChainKinematics empty;
+    ScanTrace et;
+    check(propagate_velocities(empty, JointVector(0), Twist{}, &et).empty() && et.rounds == 0,
+          "empty kinematics short-circuit cleanly");
   }
 
   // a device list shards the batch call; results equal the single-device call bit for bit

@@ -204,3 +204,28 @@ def test_batch_over_a_device_list_is_bit_identical(oracle):
         p = problems[5]
         ref = oracle.forward_dynamics(algo.name, p.chain.to_records(), p.chain.gravity, p.q, p.qdot, p.tau)
         assert rel(one[5].qddot, ref) <= 1e-9
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 20])
+def test_propagations_match_sequential_newton_euler(oracle, n):
+    """test_invdyn.cpp:50-76: propagate_velocities / _accelerations / _forces
+    (block bi-diagonal scans on the device) against the sequential
+    Newton-Euler oracle at 1e-12, scan rounds ceil_log2(n); and
+    inverse_dynamics_assembled == inverse_dynamics."""
+    chain, links, q, qd, _ = sample(oracle, n, 100 + n)
+    qdd = np.random.default_rng(1000 + n).uniform(-5, 5, n)
+    kin = pd.assemble_kinematics(chain, q)
+    J = pd.link_inertias(chain)
+    ref_v, ref_a, ref_f = oracle.newton_euler(links, chain.gravity, q, qd, qdd, True)[:3]
+    tv, ta, tf = pd.ScanTrace(), pd.ScanTrace(), pd.ScanTrace()
+    v = pd.propagate_velocities(kin, qd, None, tv)
+    a = pd.propagate_accelerations(kin, v, qd, qdd, np.concatenate([np.zeros(3), -chain.gravity]), ta)
+    f = pd.propagate_forces(kin, v, a, J, None, tf)
+    for got, want in ((v, ref_v), (a, ref_a), (f, ref_f)):
+        gaps = np.linalg.norm(got - want, axis=1) / np.maximum(1.0, np.linalg.norm(want, axis=1))
+        assert gaps.max() < 1e-12
+    assert tv.rounds == ta.rounds == tf.rounds == pd.ceil_log2(n)
+    tr = pd.ExecTrace()
+    tau = pd.inverse_dynamics_assembled(kin, J, chain.gravity, qd, qdd, trace=tr)
+    assert rel(tau, pd.inverse_dynamics(chain, q, qd, qdd)) < 1e-12
+    assert tr.scan_rounds_max == pd.ceil_log2(n)
