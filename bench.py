@@ -149,15 +149,29 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One rank per GPU over NCCL. With more ranks than visible GPUs (a
+    multi-process check on a one-GPU box) ranks share devices round-robin and
+    the control collectives (barrier, max of the timings, gather) run on gloo."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ndev = max(1, torch.cuda.device_count())
+        if world <= ndev:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            local = local % ndev
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return world, rank, local
+
+
+def _on_nccl() -> bool:
+    import torch.distributed as dist
+    return dist.get_backend() == "nccl"
 
 
 def dist_max(x: float, world: int, local: int) -> float:
@@ -165,7 +179,7 @@ def dist_max(x: float, world: int, local: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}" if _on_nccl() else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -173,7 +187,10 @@ def dist_max(x: float, world: int, local: int) -> float:
 def dist_barrier(world: int, local: int):
     if world > 1:
         import torch.distributed as dist
-        dist.barrier(device_ids=[local])
+        if _on_nccl():
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
 
 
 # ----------------------------------------------------------------------------- CPU arm
@@ -580,6 +597,10 @@ def main():
         "gpu_launches": res["launches"],
         "clocks": clocks,
     }
+    import torch
+    if world > max(1, torch.cuda.device_count()):
+        line["note"] = (f"{world} ranks share {torch.cuda.device_count()} device(s): a multi-process correctness check "
+                        f"of the sharded path, not a scaling measurement")
     if "e2e_s" in res:
         line["e2e"] = {"value": global_batch * res["e2e_steps"] / e2e_max, "unit": UNIT,
                        "h2d_bytes_per_step": res["h2d"] * world, "d2h_bytes_per_step": res["d2h"] * world,
