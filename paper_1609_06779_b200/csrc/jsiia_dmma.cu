@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 5 : 3) jsiia_dmma_kern
     const Vec3d grav = mv.gravity(mc);
     // link wrenches, suffix sums, bias torque               :86-120, :146-150
     Vk<6> Fw[LPL];
-    Vk<21> Ic[LPL];
+    Vk<10> Ic[LPL];  // composite rigid-body inertia: m, h = m c, rotational inertia about the base origin
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
       const int i = lane * LPL + e;
@@ -311,27 +311,25 @@ __global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 5 : 3) jsiia_dmma_kern
       A0.l = A0.l - grav;  // gravity as base acceleration (inverse_dynamics.cpp:135-140)
       const Sv h = inertia_apply(J0, V0);
       Fw[e] = sv6(on ? neg_advT_acc(V0, h, inertia_apply(J0, A0)) : svzero());
+      // a sum of rigid-body inertias is one: 10 numbers instead of the 21 of a
+      // general symmetric 6x6 ([[A, h^], [h^T, m 1]], spatial.cpp:89-98)
       const Sym6 Js = inertia_sym6(J0);
+      Ic[e].v[0] = J0.m;
+      Ic[e].v[1] = J0.m * J0.c.x;
+      Ic[e].v[2] = J0.m * J0.c.y;
+      Ic[e].v[3] = J0.m * J0.c.z;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) Ic[e].v[k] = Js.A[k];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) Ic[e].v[6 + k] = Js.B[k];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) Ic[e].v[15 + k] = Js.D[k];
+      for (int k = 0; k < 6; ++k) Ic[e].v[4 + k] = Js.A[k];
     }
     link_scan<6, LPL, true, true>(Fw, lane);
-    link_scan<21, LPL, true, true>(Ic, lane);
+    link_scan<10, LPL, true, true>(Ic, lane);
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
       td[e] = tau[e] - dot(S0[e], un6(Fw[e]));
-      Sym6 P;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) P.A[k] = Ic[e].v[k];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) P.B[k] = Ic[e].v[6 + k];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) P.D[k] = Ic[e].v[15 + k];
-      FB[e] = sym6_apply(P, S0[e]);
+      // FB = Ic S0 = (A w + h x v, m v + w x h)
+      const double mt = Ic[e].v[0];
+      const Vec3d h = mk(Ic[e].v[1], Ic[e].v[2], Ic[e].v[3]);
+      FB[e] = {cross_acc(h, S0[e].l, sym3_mul(Ic[e].v + 4, S0[e].a)), cross_acc(S0[e].a, h, mt * S0[e].l)};
     }
   }
 #pragma unroll
