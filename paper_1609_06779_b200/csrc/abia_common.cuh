@@ -56,6 +56,57 @@ __device__ __forceinline__ SE3d step_back(const SE3d& rel, const SE3d& X) {
   return o;
 }
 
+// The link-step algebra below is written as FMA chains where a generic
+// helper would spend a separate multiply or add (one FP64 pipe slot each):
+// the ABIA kernels are FP64-issue bound.
+
+// Compose (a*b) with the translation accumulated in the same FMA chain.
+__device__ __forceinline__ SE3d compose_f(const SE3d& a, const SE3d& b) {
+  return {matmul(a.R, b.R), mul_acc(a.R, b.p, a.p)};
+}
+// J x for J = (m, c, Ic): lin = m (v + w x c), ang = Ic w + c x lin
+__device__ __forceinline__ Sv inertia_apply_f(const Inertia& J, const Sv& x) {
+  const Vec3d lin = J.m * cross_acc(x.a, J.c, x.l);
+  return {cross_acc(J.c, lin, sym3_mul(J.I, x.a)), lin};
+}
+// inertia_sym6(J) + P: J's zero entries add nothing, m c is formed once
+__device__ __forceinline__ Sym6 inertia_plus_sym6(const Inertia& J, const Sym6& P) {
+  Sym6 o;
+  const double m = J.m, cx = J.c.x, cy = J.c.y, cz = J.c.z;
+  const double c2 = fma(cx, cx, fma(cy, cy, cz * cz));
+  const double mx = m * cx, my = m * cy, mz = m * cz;
+  o.A[0] = fma(m, c2 - cx * cx, J.I[0] + P.A[0]);
+  o.A[1] = fma(-mx, cy, J.I[1] + P.A[1]);
+  o.A[2] = fma(-mx, cz, J.I[2] + P.A[2]);
+  o.A[3] = fma(m, c2 - cy * cy, J.I[3] + P.A[3]);
+  o.A[4] = fma(-my, cz, J.I[4] + P.A[4]);
+  o.A[5] = fma(m, c2 - cz * cz, J.I[5] + P.A[5]);
+  o.B[0] = P.B[0];      o.B[1] = P.B[1] - mz; o.B[2] = P.B[2] + my;
+  o.B[3] = P.B[3] + mz; o.B[4] = P.B[4];      o.B[5] = P.B[5] - mx;
+  o.B[6] = P.B[6] - my; o.B[7] = P.B[7] + mx; o.B[8] = P.B[8];
+  o.D[0] = P.D[0] + m; o.D[1] = P.D[1]; o.D[2] = P.D[2];
+  o.D[3] = P.D[3] + m; o.D[4] = P.D[4]; o.D[5] = P.D[5] + m;
+  return o;
+}
+// P x with each component one FMA chain: (A a + B l, B^T a + D l)
+__device__ __forceinline__ Sv sym6_apply_f(const Sym6& P, const Sv& x) {
+  const double* A = P.A;
+  const double* B = P.B;
+  const double* D = P.D;
+  const Vec3d a = x.a, l = x.l;
+  return {mk(fma(A[0], a.x, fma(A[1], a.y, fma(A[2], a.z, fma(B[0], l.x, fma(B[1], l.y, B[2] * l.z))))),
+             fma(A[1], a.x, fma(A[3], a.y, fma(A[4], a.z, fma(B[3], l.x, fma(B[4], l.y, B[5] * l.z))))),
+             fma(A[2], a.x, fma(A[4], a.y, fma(A[5], a.z, fma(B[6], l.x, fma(B[7], l.y, B[8] * l.z)))))),
+          mk(fma(B[0], a.x, fma(B[3], a.y, fma(B[6], a.z, fma(D[0], l.x, fma(D[1], l.y, D[2] * l.z))))),
+             fma(B[1], a.x, fma(B[4], a.y, fma(B[7], a.z, fma(D[1], l.x, fma(D[3], l.y, D[4] * l.z))))),
+             fma(B[2], a.x, fma(B[5], a.y, fma(B[8], a.z, fma(D[2], l.x, fma(D[4], l.y, D[5] * l.z))))))};
+}
+// acc - x . y as one FMA chain
+__device__ __forceinline__ double sub_dot(double acc, const Sv& x, const Sv& y) {
+  return fma(-x.a.x, y.a.x, fma(-x.a.y, y.a.y, fma(-x.a.z, y.a.z, fma(-x.l.x, y.l.x, fma(-x.l.y, y.l.y,
+                                                                                          fma(-x.l.z, y.l.z, acc))))));
+}
+
 // Per-link record between pass B and pass C: base-frame gain g0 = U0/lambda
 // (6), base-frame screw S0 (6), free joint rate u (1).
 constexpr int kRec = 13;
@@ -106,7 +157,7 @@ __device__ __forceinline__ bool abia_degenerate(bool nan_tip, double lambda, dou
 // rel = joint_transform(S, HR, hp, q) is history independent; callers may
 // compute it ahead (software pipelining across links).
 __device__ __forceinline__ void abia_pass_a(AbiaState& st, const SE3d& rel, const Sv& S, double qd) {
-  st.X = compose(rel, st.X);
+  st.X = compose_f(rel, st.X);
   const Sv S0 = adinv_screw(st.X, S);
   st.V0 = svfma(qd, S0, st.V0);
   st.A0 = adv_acc(st.V0, qd * S0, st.A0);
@@ -119,21 +170,14 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   const Sv S0 = adinv_screw(st.X, S);
   const Inertia J0 = inertia_to_base(Jl, st.X);
   // link wrench, bias torque                      inverse_dynamics.cpp:103-112,146-150
-  const Sv h = inertia_apply(J0, st.V0);
+  const Sv h = inertia_apply_f(J0, st.V0);
   st.F0 = neg_advT_acc(st.V0, h, inertia_apply_acc(J0, st.A0, st.F0));
-  const double tau_delta = tau - dot(S0, st.F0);
+  const double tau_delta = sub_dot(tau, S0, st.F0);
   // articulated inertia                            forward_dynamics.cpp:136-156
   // P0 is zero at the tip (abia_init), so the carry is added unconditionally:
   // no branch splits the link step's scheduling region
-  Sym6 Ia = inertia_sym6(J0);
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    Ia.A[k] += st.P0.A[k];
-    Ia.D[k] += st.P0.D[k];
-  }
-#pragma unroll
-  for (int k = 0; k < 9; ++k) Ia.B[k] += st.P0.B[k];
-  const Sv U = sym6_apply(Ia, S0);
+  const Sym6 Ia = inertia_plus_sym6(J0, st.P0);
+  const Sv U = sym6_apply_f(Ia, S0);
   const double lambda = dot(S0, U);
   // degeneracy test on the link-frame trace (forward_dynamics.cpp:140-144).
   // ||Ad(X^-1)|| <= 1 + |p|, so tr_link <= (1 + |p|)^2 tr_base <= 2 (1 + |p|^2)
@@ -148,7 +192,7 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
     }
   }
   const double inv_l = rcp_nr(lambda);
-  const double u = (tau_delta - dot(S0, st.Z0)) * inv_l;  // forward_dynamics.cpp:202-212
+  const double u = sub_dot(tau_delta, S0, st.Z0) * inv_l;  // forward_dynamics.cpp:202-212
   const Sv g0 = inv_l * U;                                 // gain (base frame)
   rec[0] = g0.a.x;
   rec[1] = g0.a.y;
