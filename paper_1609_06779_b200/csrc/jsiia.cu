@@ -458,13 +458,33 @@ void launch_jsiia(const ModelView& mv, const BatchIO& io, double* gws, int64_t g
 // the slot's flag for the MODE-3 solve.
 constexpr int kTs = 34;  // smem tile leading dimension (16-byte rows)
 
-__device__ __forceinline__ void warp_tile_in(double* dst, const double* src, int ld, int lane) {
-#pragma unroll 4
-  for (int e = lane; e < 32 * 16; e += 32) {
-    const int r = e >> 4, c = (e & 15) * 2;
-    *reinterpret_cast<double2*>(dst + r * kTs + c) = __ldcg(reinterpret_cast<const double2*>(src + (size_t)r * ld + c));
-  }
+// NT tiles staged at once: every load is issued before the first shared
+// store, so the warp pays one L2 round trip for all of them (the tiles were
+// written by other SMs just before the grid barrier; a round trip is ~1 us).
+template <int NT>
+__device__ __forceinline__ void warp_tiles_in(double* const (&dst)[NT], const double* const (&src)[NT], int ld,
+                                              int lane) {
+  double2 v[NT][16];
+#pragma unroll
+  for (int k = 0; k < NT; ++k)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int e = lane + 32 * q, r = e >> 4, c = (e & 15) * 2;
+      v[k][q] = __ldcg(reinterpret_cast<const double2*>(src[k] + (size_t)r * ld + c));
+    }
+#pragma unroll
+  for (int k = 0; k < NT; ++k)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int e = lane + 32 * q, r = e >> 4, c = (e & 15) * 2;
+      *reinterpret_cast<double2*>(dst[k] + r * kTs + c) = v[k][q];
+    }
   __syncwarp();
+}
+__device__ __forceinline__ void warp_tile_in(double* dst, const double* src, int ld, int lane) {
+  double* const d[1] = {dst};
+  const double* const s[1] = {src};
+  warp_tiles_in<1>(d, s, ld, lane);
 }
 __device__ __forceinline__ void warp_tile_out(double* dst, int ld, const double* src, int lane, bool lower_only) {
   __syncwarp();
@@ -498,14 +518,19 @@ __global__ void __launch_bounds__(256) jsiia_factor_coop(double* __restrict__ gw
   namespace cgr = cooperative_groups;
   cgr::grid_group grid = cgr::this_grid();
   extern __shared__ __align__(16) double coop_smem[];  // per warp: A, B tiles + 32 reciprocals
-  double (*stile)[2][32 * kTs] = reinterpret_cast<double (*)[2][32 * kTs]>(coop_smem);
-  double (*sinv)[32] = reinterpret_cast<double (*)[32]>(coop_smem + 8 * 2 * 32 * kTs);
+  double (*stile)[3][32 * kTs] = reinterpret_cast<double (*)[3][32 * kTs]>(coop_smem);
+  double (*sinv)[32] = reinterpret_cast<double (*)[32]>(coop_smem + 8 * 3 * 32 * kTs);
   const JstLayout L = jst_layout(n);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  // task slot of this warp: consecutive slots on different SMs (warp 0 of every
+  // CTA first), so the few tasks of the late panels -- the critical path --
+  // each get an SM to themselves instead of sharing CTA 0's
+  const int gw = wl * (int)gridDim.x + (int)blockIdx.x;
   const int np = L.np, npad = L.npad, ld = L.ld;
   double* sA = stile[wl][0];
   double* sB = stile[wl][1];
+  double* sC = stile[wl][2];
   for (int c = 0; c < count; ++c) {
     double* ws = gws + (size_t)c * L.total;
     double* Mb = ws + L.m_off;
@@ -563,11 +588,17 @@ __global__ void __launch_bounds__(256) jsiia_factor_coop(double* __restrict__ gw
     for (int K = 0; K < np; ++K) {
       if (__ldcg(flag) != 0.0) break;  // grid-uniform: forward_dynamics.cpp:93-98
       if (K + 1 + gw < np) {
-        warp_tile_in(sA, tile(K, K), ld, lane);
         sinv[wl][lane] = __ldcg(invd + 32 * K + lane);
-        __syncwarp();
+        bool first = true;
         for (int I = K + 1 + gw; I < np; I += nwarps) {
-          warp_tile_in(sB, tile(I, K), ld, lane);
+          if (first) {  // L_KK and the first panel tile in one round trip
+            double* const d[2] = {sA, sB};
+            const double* const src[2] = {tile(K, K), tile(I, K)};
+            warp_tiles_in<2>(d, src, ld, lane);
+            first = false;
+          } else {
+            warp_tile_in(sB, tile(I, K), ld, lane);
+          }
           tile_trsm(sA, kTs, sinv[wl], sB, lane);
           warp_tile_out(tile(I, K), ld, sB, lane, false);
         }
@@ -581,10 +612,13 @@ __global__ void __launch_bounds__(256) jsiia_factor_coop(double* __restrict__ gw
         while (a * (a + 1) / 2 > q) --a;
         const int b = q - a * (a + 1) / 2;
         const int I = K + 1 + a, J = K + 1 + b;
-        warp_tile_in(sA, tile(I, K), ld, lane);
-        warp_tile_in(sB, tile(J, K), ld, lane);
+        {  // L_IK, L_JK and C_IJ in one round trip, all coalesced
+          double* const d[3] = {sA, sB, sC};
+          const double* const src[3] = {tile(I, K), tile(J, K), tile(I, J)};
+          warp_tiles_in<3>(d, src, ld, lane);
+        }
         double r[32];
-        load_row<true>(r, tile(I, J) + (size_t)lane * ld);
+        load_row<false>(r, sC + lane * kTs);
         tile_gemm_rows(r, sA, sB, lane);
         if (q == 0) {  // the next diagonal tile: keep it in smem and factor it right away
           __syncwarp();
@@ -612,77 +646,148 @@ __global__ void __launch_bounds__(256) jsiia_factor_coop(double* __restrict__ gw
 }
 
 // Solve + residual contract (forward_dynamics.cpp:99-116) for the
-// cooperative path: one 1024-thread CTA per chain, warp J owns tile row J of
-// the right-hand side. Triangular solves by tile rows: the owner warp solves
-// its diagonal tile (shuffle recurrence against the tile staged in smem) and
-// publishes the block; after one barrier every later (earlier, for L^T) warp
-// folds it into its own block. The residual td - M x is formed tile by tile
-// from diag(M) and the strict upper triangle the factorization left intact.
-constexpr int kWideWarps = 32;
+// cooperative path: one CTA of kWideWarps warps per chain. Tile rows of the
+// right-hand side are owned round-robin by the warps. An owner folds each
+// earlier block into its own as soon as that block is published (a shared
+// flag per tile row, no CTA barrier per step): the rows of the tile it folds
+// next are loaded before it waits, so a step's critical path is one 32-wide
+// dot product plus the diagonal recurrence against the owner's staged
+// diagonal tile. The residual uses the closed form of M (residual_closed).
+constexpr int kWideWarps = 16;
 
+__device__ __forceinline__ void wait_flag(volatile int* f, int want) {
+  while (*f != want) {
+  }
+  __threadfence_block();
+}
+__device__ __forceinline__ void publish(double* v, int J, int lane, double val, volatile int* ready, int epoch) {
+  v[32 * J + lane] = val;
+  __threadfence_block();
+  __syncwarp();
+  if (lane == 0) ready[J] = epoch;
+}
+__device__ __forceinline__ void stage_diag(const double* Mb, int ld, int J, double* T, int lane) {
+#pragma unroll 8
+  for (int e = lane; e < 32 * 32; e += 32)
+    T[(e >> 5) * 33 + (e & 31)] = Mb[(size_t)(32 * J + (e >> 5)) * ld + 32 * J + (e & 31)];
+  __syncwarp();
+}
+__device__ __forceinline__ double dot32(const double (&a)[32], const double* y) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int c = 0; c < 32; c += 4) {
+    s0 = fma(a[c], y[c], s0);
+    s1 = fma(a[c + 1], y[c + 1], s1);
+    s2 = fma(a[c + 2], y[c + 2], s2);
+    s3 = fma(a[c + 3], y[c + 3], s3);
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+// (L L^T) v = v in place; flags `ready` take the values epoch (forward) and
+// epoch + 1 (backward), so they never need resetting between solves.
 __device__ void wide_llt_solve(const double* Mb, int ld, int np, const double* invd, double* v, double* sT,
-                               int warp, int lane) {
-  // forward: L y = v
-  for (int I = 0; I < np; ++I) {
-    if (warp == I % kWideWarps) {
-      for (int e = lane; e < 32 * 32; e += 32) sT[(e >> 5) * 33 + (e & 31)] = Mb[(size_t)(32 * I + (e >> 5)) * ld + 32 * I + (e & 31)];
-      __syncwarp();
-      double acc = v[32 * I + lane], yo = 0.0;
-      const double id = invd[32 * I + lane];
-#pragma unroll 8
-      for (int m = 0; m < 32; ++m) {
-        const double ym = __shfl_sync(0xffffffffu, acc * id, m);
-        yo = (lane == m) ? ym : yo;
-        acc = (lane > m) ? fma(-sT[lane * 33 + m], ym, acc) : acc;
-      }
-      v[32 * I + lane] = yo;
-    }
-    __syncthreads();
-    for (int J = I + 1 + ((warp - I - 1) % kWideWarps + kWideWarps) % kWideWarps; J < np; J += kWideWarps) {
-      const double* row = Mb + (size_t)(32 * J + lane) * ld + 32 * I;
-      const double* y = v + 32 * I;
-      double acc = 0.0;
-#pragma unroll 8
+                               volatile int* ready, int epoch, int warp, int lane) {
+  double* T = sT + warp * 32 * 33;
+  // forward: L y = v, tile rows ascending
+  for (int J = warp; J < np; J += kWideWarps) {
+    stage_diag(Mb, ld, J, T, lane);
+    double acc = v[32 * J + lane];
+    const double* rowJ = Mb + (size_t)(32 * J + lane) * ld;
+    for (int I = 0; I < J; ++I) {
+      double a[32];  // row `lane` of L_JI, loaded before the wait
+#pragma unroll
       for (int c = 0; c < 32; c += 2) {
-        const double2 a = *reinterpret_cast<const double2*>(row + c);
-        acc = fma(a.x, y[c], fma(a.y, y[c + 1], acc));
+        const double2 t = *reinterpret_cast<const double2*>(rowJ + 32 * I + c);
+        a[c] = t.x;
+        a[c + 1] = t.y;
       }
-      v[32 * J + lane] -= acc;
+      wait_flag(ready + I, epoch);
+      acc -= dot32(a, v + 32 * I);
     }
+    const double id = invd[32 * J + lane];
+    double yo = 0.0;
+#pragma unroll 8
+    for (int m = 0; m < 32; ++m) {
+      const double ym = __shfl_sync(0xffffffffu, acc * id, m);
+      yo = (lane == m) ? ym : yo;
+      acc = (lane > m) ? fma(-T[lane * 33 + m], ym, acc) : acc;
+    }
+    publish(v, J, lane, yo, ready, epoch);
   }
   __syncthreads();
-  // backward: L^T x = y
-  for (int I = np - 1; I >= 0; --I) {
-    if (warp == I % kWideWarps) {
-      for (int e = lane; e < 32 * 32; e += 32) sT[(e >> 5) * 33 + (e & 31)] = Mb[(size_t)(32 * I + (e >> 5)) * ld + 32 * I + (e & 31)];
-      __syncwarp();
-      double acc = v[32 * I + lane], xo = 0.0;
-      const double id = invd[32 * I + lane];
-#pragma unroll 8
-      for (int m = 31; m >= 0; --m) {
-        const double xm = __shfl_sync(0xffffffffu, acc * id, m);
-        xo = (lane == m) ? xm : xo;
-        acc = (lane < m) ? fma(-sT[m * 33 + lane], xm, acc) : acc;
-      }
-      v[32 * I + lane] = xo;
+  // backward: L^T x = y, tile rows descending
+  const int last = warp + ((np - 1 - warp) / kWideWarps) * kWideWarps;
+  for (int J = last; J >= 0 && warp < np; J -= kWideWarps) {
+    stage_diag(Mb, ld, J, T, lane);
+    double acc = v[32 * J + lane];
+    for (int I = np - 1; I > J; --I) {
+      double a[32];  // column `lane` of L_IJ (coalesced), loaded before the wait
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a[c] = Mb[(size_t)(32 * I + c) * ld + 32 * J + lane];
+      wait_flag(ready + I, epoch + 1);
+      acc -= dot32(a, v + 32 * I);
     }
-    __syncthreads();
-    // y_K -= L_IK^T x_I for K < I: lane = row k of tile K, column reads of L_IK (coalesced)
-    for (int K = warp; K < I; K += kWideWarps) {
-      const double* col = Mb + (size_t)(32 * I) * ld + 32 * K + lane;
-      const double* x = v + 32 * I;
-      double acc = 0.0;
+    const double id = invd[32 * J + lane];
+    double xo = 0.0;
 #pragma unroll 8
-      for (int c = 0; c < 32; ++c) acc = fma(col[(size_t)c * ld], x[c], acc);
-      v[32 * K + lane] -= acc;
+    for (int m = 31; m >= 0; --m) {
+      const double xm = __shfl_sync(0xffffffffu, acc * id, m);
+      xo = (lane == m) ? xm : xo;
+      acc = (lane < m) ? fma(-T[m * 33 + lane], xm, acc) : acc;
     }
+    publish(v, J, lane, xo, ready, epoch + 1);
   }
   __syncthreads();
 }
 
+// r = td - M x from the closed form of M (M_ij = S0_min(i,j) . FB_max(i,j), the
+// same dot products the factorization's M holds): (M x)_i = FB_i . P_i +
+// S0_i . Q_i with P_i = sum_{j<=i} S0_j x_j and Q_i = sum_{j>i} FB_j x_j. Two
+// CTA scans of 6-vectors instead of reading all n^2 entries of M through one
+// SM. Returns sum r_i^2 (every thread).
+__device__ double residual_closed(const double* ws, int n, const double* x, double* r, ScanSmem& sm,
+                                  BlockReduce& br) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int lpt = (n + nt - 1) / nt;
+  const int i0 = t * lpt, i1 = min(n, i0 + lpt), nact = (n + lpt - 1) / lpt;
+  const double* td = ws + (size_t)jst::TD * n;
+  auto s0 = [&](int i) { return ws_get_sv(ws, n, jst::S0, i); };
+  auto fb = [&](int i) { return ws_get_sv(ws, n, jst::FB, i); };
+  auto arr = [](const Sv& v) { return Arr<6>{{v.a.x, v.a.y, v.a.z, v.l.x, v.l.y, v.l.z}}; };
+  auto sv = [](const Arr<6>& a) { return Sv{mk(a.v[0], a.v[1], a.v[2]), mk(a.v[3], a.v[4], a.v[5])}; };
+  Sv lp = svzero(), lq = svzero();
+  for (int i = i0; i < i1; ++i) {
+    lp = svfma(x[i], s0(i), lp);
+    lq = svfma(x[i], fb(i), lq);
+  }
+  const Sv P0 = sv(block_exclusive<6, false>(arr(lp), AddOp{}, sm, nact));
+  const Sv Q0 = sv(block_exclusive<6, true>(arr(lq), AddOp{}, sm, nact));
+  // P inclusive walking up, Q exclusive walking down; r_i = td_i - FB_i.P_i - S0_i.Q_i
+  Sv P = P0;
+  for (int i = i0; i < i1; ++i) {
+    P = svfma(x[i], s0(i), P);
+    r[i] = td[i] - dot(fb(i), P);
+  }
+  Sv Q = Q0;
+  double rr = 0.0;
+  for (int i = i1 - 1; i >= i0; --i) {
+    const double ri = r[i] - dot(s0(i), Q);
+    r[i] = ri;
+    rr = fma(ri, ri, rr);
+    Q = svfma(x[i], fb(i), Q);
+  }
+  return block_sum(rr, br);
+}
+
+size_t wide_solve_smem(int np) { return sizeof(double) * kWideWarps * 32 * 33 + sizeof(int) * np; }
+
 __global__ void __launch_bounds__(32 * kWideWarps) jsiia_solve_wide(BatchIO io, double* __restrict__ gws, int n) {
-  __shared__ double sT[32 * 33];
+  extern __shared__ double wide_smem[];
   __shared__ BlockReduce br;
+  __shared__ ScanSmem scan_sm;
+  double* sT = wide_smem;
+  volatile int* ready = reinterpret_cast<volatile int*>(wide_smem + kWideWarps * 32 * 33);
   const JstLayout L = jst_layout(n);
   const int64_t p = blockIdx.x;
   const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
@@ -691,8 +796,9 @@ __global__ void __launch_bounds__(32 * kWideWarps) jsiia_solve_wide(BatchIO io, 
   const double* Mb = ws + L.m_off;
   double* vx = ws + L.v_off;
   double* vw = vx + npad;
-  const double* dg = vx + 2 * (size_t)npad;
   const double* invd = vx + 3 * (size_t)npad;
+  for (int k = t; k < np; k += nt) ready[k] = 0;
+  __syncthreads();
   if (ws[L.total - 1] != 0.0) {  // forward_dynamics.cpp:93-98
     if (t == 0) {
       io.status[p] = PD_SLOT_JSI_NOT_SPD;
@@ -702,46 +808,21 @@ __global__ void __launch_bounds__(32 * kWideWarps) jsiia_solve_wide(BatchIO io, 
     return;
   }
   const double* td = ws + (size_t)jst::TD * n;
-  wide_llt_solve(Mb, ld, np, invd, vx, sT, warp, lane);
+  wide_llt_solve(Mb, ld, np, invd, vx, sT, ready, 1, warp, lane);
   double sq = 0.0;
   for (int i = t; i < n; i += nt) sq = fma(td[i], td[i], sq);
   const double scale = fmax(sqrt(block_sum(sq, br)), 2.2250738585072014e-308);
   int code = PD_SLOT_OK;
   for (int pass = 0; pass < 2; ++pass) {
-    // r = td - M x, tile row I per warp: lane = row
-    double rr = 0.0;
-    for (int I = warp; I < np; I += kWideWarps) {
-      const int i = 32 * I + lane;
-      double s = (i < n) ? td[i] : 0.0;
-      s = fma(-dg[i], vx[i], s);
-      for (int J = 0; J < np; ++J) {
-        const double* x = vx + 32 * J;
-        if (J > I) {  // upper tile: row i
-          const double* row = Mb + (size_t)i * ld + 32 * J;
-#pragma unroll 8
-          for (int c = 0; c < 32; ++c) s = fma(-row[c], x[c], s);
-        } else if (J < I) {  // lower tile = (upper tile (J, I))^T: column i
-          const double* col = Mb + (size_t)(32 * J) * ld + i;
-#pragma unroll 8
-          for (int c = 0; c < 32; ++c) s = fma(-col[(size_t)c * ld], x[c], s);
-        } else {  // diagonal tile: strict upper part, both ways
-          for (int c = 0; c < 32; ++c) {
-            const int j = 32 * J + c;
-            if (j > i) s = fma(-Mb[(size_t)i * ld + j], x[c], s);
-            else if (j < i) s = fma(-Mb[(size_t)j * ld + i], x[c], s);
-          }
-        }
-      }
-      vw[i] = s;
-      rr = fma(s, s, rr);
-    }
-    const double rn = sqrt(block_sum(rr, br));  // syncs
+    __syncthreads();  // x complete
+    for (int i = n + t; i < npad; i += nt) vw[i] = 0.0;
+    const double rn = sqrt(residual_closed(ws, n, vx, vw, scan_sm, br));  // syncs
     if (!(rn > 1e-9 * scale)) break;
     if (pass == 1) {
       code = PD_SLOT_JSI_REFINE_FAILED;
       break;
     }
-    wide_llt_solve(Mb, ld, np, invd, vw, sT, warp, lane);
+    wide_llt_solve(Mb, ld, np, invd, vw, sT, ready, 3, warp, lane);
     for (int i = t; i < npad; i += nt) vx[i] += vw[i];
     __syncthreads();
   }
@@ -764,10 +845,12 @@ void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int 
   jsiia_tiled_kernel<false, 2><<<(unsigned)io.B, nt, 0, s>>>(mv, io, gws, 0);
   int count = (int)io.B;
   void* args[] = {&gws, (void*)&n, &count};
-  const size_t smem = sizeof(double) * 8 * (2 * 32 * kTs + 32);
+  const size_t smem = sizeof(double) * 8 * (3 * 32 * kTs + 32);
   cudaFuncSetAttribute(jsiia_factor_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchCooperativeKernel((const void*)jsiia_factor_coop, dim3((unsigned)sm_count), dim3(256), args, smem, s);
-  jsiia_solve_wide<<<(unsigned)io.B, 32 * kWideWarps, 0, s>>>(io, gws, n);
+  const size_t wsm = wide_solve_smem(jst_layout(n).np);
+  cudaFuncSetAttribute(jsiia_solve_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+  jsiia_solve_wide<<<(unsigned)io.B, 32 * kWideWarps, wsm, s>>>(io, gws, n);
 }
 
 // Joint-space inertia of every problem into d_M[p][i][j] (same build as the
