@@ -292,3 +292,32 @@ def test_degenerate_articulation(oracle, gpu_ctx, n):
     for b in (0, 2):
         assert st[b] == 0
         assert rel_gap(qdd[b], oracle.forward_dynamics("abia", links[b], [0, 0, -9.81], q[b], qd[b], tau[b])) <= TOL
+
+
+@pytest.mark.parametrize("n,B", [(8, 3), (40, 3), (100, 3), (300, 1)])
+def test_zero_screw_joint_error_paths(oracle, gpu_ctx, n, B):
+    """A joint whose screw is zero leaves M singular and the articulation
+    degenerate: the reference's JSIIA throws 'not positive definite' from its
+    LLT (forward_dynamics.cpp:93-98) and ABIA 'degenerate articulation'
+    (:140-144); CFA follows its own rank tests. Every algorithm and kernel
+    family (warp DMMA n <= 64, CTA-tiled, grid-wide for one long chain)
+    reports the reference's message for that problem only."""
+    cell = oracle.workload_seed(11, n, B)
+    links = oracle.workload_chains(cell, n, B).copy()
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    bad = B // 2
+    links[bad, n // 3, 13:19] = 0.0
+    ms, _ = gpu_ctx.set_models(links, None)
+    assert (ms == 0).all()
+    for algo in ALGOS:
+        qdd, st, rd, ix = gpu_ctx.solve(algo, q, qd, tau)
+        for b in range(B):
+            try:
+                ref = oracle.forward_dynamics(ONAME[algo], links[b], [0, 0, -9.81], q[b], qd[b], tau[b])
+                msg = ""
+            except oracle.OracleError as e:
+                ref, msg = None, str(e)
+            got = pd.api._capi.slot_message(st[b], rd[b], ix[b], n) if st[b] else ""
+            assert got == msg, (algo, n, b, got, msg)
+            if not msg:
+                assert rel_gap(qdd[b], ref) <= TOL, (algo, n, b, rel_gap(qdd[b], ref))
