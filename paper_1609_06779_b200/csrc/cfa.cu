@@ -628,10 +628,6 @@ __global__ void __launch_bounds__(256) cfa_cta_kernel(ModelView mv, BatchIO io, 
 // (ld.global.cg), a grid barrier where the CTA kernel has __syncthreads.
 // Chains one after the other; cfa_cta_kernel<false, 2> left each chain's
 // joint transforms and tau_delta in workspace slot c.
-__device__ __forceinline__ void cg_load(const double* ws, int n, int f0, int i, double* out, int K) {
-  for (int k = 0; k < K; ++k) out[k] = __ldcg(ws + (size_t)(f0 + k) * n + i);
-}
-
 __global__ void __launch_bounds__(128) cfa_oee_coop(ModelView mv, BatchIO io, double* __restrict__ gws, int n,
                                                     int count, int* __restrict__ bad) {
   namespace cgr = cooperative_groups;
@@ -701,20 +697,29 @@ __global__ void __launch_bounds__(128) cfa_oee_coop(ModelView mv, BatchIO io, do
         const bool up_bad = (i < n - h) && __ldcg(ws + (size_t)cfa::SG * n + i + h) != 0.0;
         const bool dn_bad = (i >= h) && __ldcg(ws + (size_t)cfa::SG * n + i - h) != 0.0;
         if (up_bad || dn_bad) atomicMin(bad, i);
+        // each neighbour's published data is requested in one batch (one L2
+        // round trip) before the elimination uses any of it
         if (i < n - h) {
           const int k = i + h;
-          double Lk[10], il[5], rt[5];
-          cg_load(ws, n, cfa::PL, k, Lk, 10);
-          cg_load(ws, n, cfa::PI, k, il, 5);
-          cg_load(ws, n, cfa::PR, k, rt, 5);
-          oee_up(D, R, U, Lk, il, rt, i < n - 2 * h,
-                 [&](int r, int c) { return __ldcg(ws + (size_t)(cfa::PY + r * 5 + c) * n + k); });
+          double Lk[10], il[5], rt[5], Y[25];
+#pragma unroll
+          for (int q = 0; q < 10; ++q) Lk[q] = __ldcg(ws + (size_t)(cfa::PL + q) * n + k);
+#pragma unroll
+          for (int q = 0; q < 5; ++q) il[q] = __ldcg(ws + (size_t)(cfa::PI + q) * n + k);
+#pragma unroll
+          for (int q = 0; q < 5; ++q) rt[q] = __ldcg(ws + (size_t)(cfa::PR + q) * n + k);
+#pragma unroll
+          for (int q = 0; q < 25; ++q) Y[q] = __ldcg(ws + (size_t)(cfa::PY + q) * n + k);
+          oee_up(D, R, U, Lk, il, rt, i < n - 2 * h, [&](int r, int c) { return Y[r * 5 + c]; });
         }
         if (i >= h) {
           const int k = i - h;
-          double rt[5];
-          cg_load(ws, n, cfa::PR, k, rt, 5);
-          oee_down(D, R, rt, [&](int r, int c) { return __ldcg(ws + (size_t)(cfa::PY + r * 5 + c) * n + k); });
+          double rt[5], Y[25];
+#pragma unroll
+          for (int q = 0; q < 5; ++q) rt[q] = __ldcg(ws + (size_t)(cfa::PR + q) * n + k);
+#pragma unroll
+          for (int q = 0; q < 25; ++q) Y[q] = __ldcg(ws + (size_t)(cfa::PY + q) * n + k);
+          oee_down(D, R, rt, [&](int r, int c) { return Y[r * 5 + c]; });
         }
       }
       grid.sync();
