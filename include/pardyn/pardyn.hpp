@@ -243,10 +243,11 @@ struct ExecTrace {
 };
 
 // ----------------------------------------------------------------- building blocks (scan.hpp, oee.hpp)
-// The paper's two solvers on their own, on the GPU: 6x6 block bi-diagonal
-// systems by the affine scan (scan.hpp:100-168), symmetric 5x5 block
-// tri-diagonal systems by odd-even elimination (oee.hpp:28-32, 149-189) --
-// the block sizes the dynamics use.
+// The paper's two solvers on their own, on the GPU: block bi-diagonal
+// systems by the affine scan (scan.hpp:100-168), symmetric block
+// tri-diagonal systems by odd-even elimination (oee.hpp:28-32, 149-189), at
+// the block sizes the reference's templates take (the dynamics use D = 6,
+// B = 5).
 enum class BiDiagOrientation { lower, upper };
 
 // lower: x[0] = rhs[0], x[k] = coupling[k-1] x[k-1] + rhs[k];
@@ -265,11 +266,63 @@ struct SymBlockTriDiagSystem {
   std::vector<Matrix<B, B>> upper;  // n - 1 blocks
 };
 
-std::vector<Vec6> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
-std::vector<Vec6> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace = nullptr);
-// Exactly ceil_log2(n) rounds; throws SingularBlockError(round, index) like the reference.
-std::vector<Vec5> oee_solve(const SymBlockTriDiagSystem<5>& sys, const std::vector<Vec5>& rhs,
-                            OeeTrace* trace = nullptr);
+namespace detail {
+// Row-major packed blocks through the C-ABI (pd_block_bidiag_solve /
+// pd_block_tridiag_solve); D, B in 1..6, M in 1..4. Throw the reference's
+// exceptions (std::invalid_argument, SingularBlockError).
+void bidiag_solve_rm(int dim, bool upper, std::size_t n, const double* coupling, const double* rhs, double* x);
+void oee_solve_rm(int block, int cols, std::size_t n, const double* diag, const double* upper, const double* rhs,
+                  double* x);
+
+template <int D>
+std::vector<Matrix<D, 1>> bidiag(const BlockBiDiagSystem<D>& sys, bool upper, ScanTrace* trace) {
+  static_assert(D >= 1 && D <= 6, "block bi-diagonal solve: block size 1..6");
+  const std::size_t n = sys.rhs.size();
+  if (sys.coupling.size() + 1 != n && !(n == 0 && sys.coupling.empty()))
+    throw std::invalid_argument("block bi-diagonal solve: need n - 1 coupling blocks for n right-hand sides");
+  if (trace) trace->rounds = ceil_log2(n);  // the scan's designed depth (scan.hpp:32-65)
+  std::vector<Matrix<D, 1>> x(n);
+  if (n == 0) return x;
+  std::vector<double> c(D * D * (n - 1)), r(D * n), xo(D * n);
+  for (std::size_t k = 0; k + 1 < n; ++k) sys.coupling[k].toRowMajor(&c[D * D * k]);
+  for (std::size_t k = 0; k < n; ++k) sys.rhs[k].toRowMajor(&r[D * k]);
+  bidiag_solve_rm(D, upper, n, c.empty() ? nullptr : c.data(), r.data(), xo.data());
+  for (std::size_t k = 0; k < n; ++k) x[k] = Matrix<D, 1>::FromRowMajor(&xo[D * k]);
+  return x;
+}
+}  // namespace detail
+
+template <int D>
+std::vector<Matrix<D, 1>> solve_lower_bidiag(const BlockBiDiagSystem<D>& sys, ScanTrace* trace = nullptr) {
+  return detail::bidiag<D>(sys, false, trace);
+}
+template <int D>
+std::vector<Matrix<D, 1>> solve_upper_bidiag(const BlockBiDiagSystem<D>& sys, ScanTrace* trace = nullptr) {
+  return detail::bidiag<D>(sys, true, trace);
+}
+// Exactly ceil_log2(n) rounds; throws SingularBlockError(round, index) like
+// the reference (oee.hpp:149-189). B in 1..6, M in 1..4 right-hand-side columns.
+template <int B, int M = 1>
+std::vector<Matrix<B, M>> oee_solve(const SymBlockTriDiagSystem<B>& sys, const std::vector<Matrix<B, M>>& rhs,
+                                    OeeTrace* trace = nullptr) {
+  static_assert(B >= 1 && B <= 6 && M >= 1 && M <= 4, "odd-even elimination: B in 1..6, M in 1..4");
+  const std::size_t n = sys.diag.size();
+  if (rhs.size() != n || (n > 0 && sys.upper.size() + 1 != n))
+    throw std::invalid_argument("odd-even elimination: inconsistent block counts");
+  if (trace) trace->rounds = 0;
+  std::vector<Matrix<B, M>> x(n);
+  if (n == 0) return x;
+  std::vector<double> d(B * B * n), u(B * B * (n - 1)), r(B * M * n), xo(B * M * n);
+  for (std::size_t k = 0; k < n; ++k) {
+    sys.diag[k].toRowMajor(&d[B * B * k]);
+    rhs[k].toRowMajor(&r[B * M * k]);
+  }
+  for (std::size_t k = 0; k + 1 < n; ++k) sys.upper[k].toRowMajor(&u[B * B * k]);
+  detail::oee_solve_rm(B, M, n, d.data(), u.empty() ? nullptr : u.data(), r.data(), xo.data());
+  if (trace) trace->rounds = ceil_log2(n);
+  for (std::size_t k = 0; k < n; ++k) x[k] = Matrix<B, M>::FromRowMajor(&xo[B * M * k]);
+  return x;
+}
 
 // ----------------------------------------------------------------- inverse dynamics (inverse_dynamics.hpp)
 // inverse_dynamics.hpp:23-28

@@ -32,9 +32,11 @@
  *                               src/inverse_dynamics.cpp:175-179)
  *   pd_link_states           <- link_states (inverse_dynamics.hpp:81-83,
  *                               src/inverse_dynamics.cpp:181-196)
- *   pd_block_bidiag_solve6   <- solve_lower_bidiag / solve_upper_bidiag
+ *   pd_block_bidiag_solve    <- solve_lower_bidiag<D> / solve_upper_bidiag<D> (D <= 6)
+ *   pd_block_bidiag_solve6   <- the D = 6 case
  *                               (include/pardyn/scan.hpp:100-168)
- *   pd_block_tridiag_solve5  <- oee_solve<5,1> / SymBlockTriDiagSystem
+ *   pd_block_tridiag_solve   <- oee_solve<B,M> / SymBlockTriDiagSystem<B> (B <= 6, M <= 4)
+ *   pd_block_tridiag_solve5  <- the oee_solve<5,1> case
  *                               (include/pardyn/oee.hpp:28-32,149-189)
  *   pd_workload_chains_device, pd_set_models_workload
  *                            <- workload_chains / random_chain on the device
@@ -239,11 +241,16 @@ void pd_workload_inputs(uint64_t cell_seed, int32_t n_links, int64_t n_groups, i
                         double* qdot, double* drive);
 
 /* The paper's building block 1 on its own: `batch` block bi-diagonal
- * systems with 6x6 blocks and implicit identity diagonal (BlockBiDiagSystem<6>,
- * include/pardyn/scan.hpp:100-168), solved by an all-prefix scan of affine
- * elements: lower (upper = 0): x[0] = rhs[0], x[k] = coupling[k-1] x[k-1] +
- * rhs[k]; upper: x[n-1] = rhs[n-1], x[k] = coupling[k] x[k+1] + rhs[k].
- * coupling [batch][n-1][36] row-major, rhs / x [batch][n][6], host buffers. */
+ * systems with dim x dim blocks (1 <= dim <= 6) and implicit identity diagonal
+ * (BlockBiDiagSystem<D>, include/pardyn/scan.hpp:100-168), solved by an
+ * all-prefix scan of affine elements: lower (upper = 0): x[0] = rhs[0],
+ * x[k] = coupling[k-1] x[k-1] + rhs[k]; upper: x[n-1] = rhs[n-1],
+ * x[k] = coupling[k] x[k+1] + rhs[k]. coupling [batch][n-1][dim*dim]
+ * row-major, rhs / x [batch][n][dim], host buffers.
+ *   pd_block_bidiag_solve   <- solve_lower_bidiag<D> / solve_upper_bidiag<D>
+ *   pd_block_bidiag_solve6  the dim = 6 case (the dynamics' recurrences) */
+pd_status pd_block_bidiag_solve(pd_ctx* ctx, int32_t dim, int64_t batch, int32_t n, int32_t upper,
+                                const double* coupling, const double* rhs, double* x);
 pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t upper, const double* coupling,
                                  const double* rhs, double* x);
 
@@ -258,6 +265,14 @@ pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t 
 pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const double* diag, const double* upper,
                                   const double* rhs, double* x, int32_t* slot_status, int32_t* slot_round,
                                   int32_t* slot_index);
+/* The same for block size `block` (1..6) and `cols` (1..4) right-hand-side
+ * columns, oee_solve<B, M> (oee.hpp:149-189): diag / upper [..][block*block],
+ * rhs / x [batch][n][block*cols] with each block row-major (element (r, c) at
+ * r * cols + c). The singularity test is FullPivLU::isInvertible's with
+ * threshold block * eps (oee.hpp:40-51). */
+pd_status pd_block_tridiag_solve(pd_ctx* ctx, int32_t block, int32_t cols, int64_t batch, int32_t n,
+                                 const double* diag, const double* upper, const double* rhs, double* x,
+                                 int32_t* slot_status, int32_t* slot_round, int32_t* slot_index);
 
 /* The same chains generated on the device (§8f row 3), one thread per chain:
  *   pd_workload_chains_device  chains [g0, g0+count) into device memory,

@@ -446,30 +446,40 @@ class Context:
             "cross_sub", "cross_diag", "cross_super", "joint_diag", "joint_off")), _capi.dptr(x), _capi.dptr(out)))
         return out
 
-    def block_bidiag_solve6(self, coupling, rhs, upper=False):
-        """Batched scan solve of BlockBiDiagSystem<6>: coupling (B, n-1, 6, 6),
-        rhs (B, n, 6) -> x (B, n, 6) (scan.hpp:100-168)."""
+    def block_bidiag_solve(self, coupling, rhs, upper=False):
+        """Batched scan solve of BlockBiDiagSystem<D> (D = 1..6): coupling
+        (B, n-1, D, D), rhs (B, n, D) -> x (B, n, D) (scan.hpp:100-168)."""
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
-        B, n = rhs.shape[0], rhs.shape[1]
-        coupling = np.ascontiguousarray(coupling, dtype=np.float64) if n > 1 else np.zeros((B, 0, 6, 6))
+        B, n, d = rhs.shape
+        coupling = np.ascontiguousarray(coupling, dtype=np.float64) if n > 1 else np.zeros((B, 0, d, d))
         x = np.empty_like(rhs)
-        self._check(self._L.pd_block_bidiag_solve6(self._h, B, n, 1 if upper else 0, _capi.dptr(coupling),
-                                                   _capi.dptr(rhs), _capi.dptr(x)))
+        self._check(self._L.pd_block_bidiag_solve(self._h, d, B, n, 1 if upper else 0, _capi.dptr(coupling),
+                                                  _capi.dptr(rhs), _capi.dptr(x)))
         return x
 
-    def block_tridiag_solve5(self, diag, upper, rhs):
-        """Batched OEE (oee_solve<5,1>): diag (B, n, 5, 5), upper (B, n-1, 5, 5),
-        rhs (B, n, 5) -> (x (B, n, 5), status, round, index)."""
+    def block_bidiag_solve6(self, coupling, rhs, upper=False):
+        """block_bidiag_solve for the dynamics' 6x6 blocks."""
+        return self.block_bidiag_solve(coupling, rhs, upper)
+
+    def block_tridiag_solve(self, diag, upper, rhs):
+        """Batched OEE (oee_solve<B, M>, B = 1..6, M = 1..4): diag (S, n, B, B),
+        upper (S, n-1, B, B), rhs (S, n, B) or (S, n, B, M) -> (x shaped like
+        rhs, status, round, index) per system."""
         diag = np.ascontiguousarray(diag, dtype=np.float64)
-        B, n = diag.shape[0], diag.shape[1]
-        upper = np.ascontiguousarray(upper, dtype=np.float64) if n > 1 else np.zeros((B, 0, 5, 5))
+        S, n, b = diag.shape[0], diag.shape[1], diag.shape[2]
+        upper = np.ascontiguousarray(upper, dtype=np.float64) if n > 1 else np.zeros((S, 0, b, b))
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
-        x = np.empty((B, n, 5))
-        st, rd, ix = (np.zeros(B, np.int32) for _ in range(3))
-        self._check(self._L.pd_block_tridiag_solve5(self._h, B, n, _capi.dptr(diag), _capi.dptr(upper),
-                                                    _capi.dptr(rhs), _capi.dptr(x), _capi.iptr(st), _capi.iptr(rd),
-                                                    _capi.iptr(ix)))
+        m = 1 if rhs.ndim == 3 else rhs.shape[3]
+        x = np.empty_like(rhs)
+        st, rd, ix = (np.zeros(S, np.int32) for _ in range(3))
+        self._check(self._L.pd_block_tridiag_solve(self._h, b, m, S, n, _capi.dptr(diag), _capi.dptr(upper),
+                                                   _capi.dptr(rhs), _capi.dptr(x), _capi.iptr(st), _capi.iptr(rd),
+                                                   _capi.iptr(ix)))
         return x, st, rd, ix
+
+    def block_tridiag_solve5(self, diag, upper, rhs):
+        """block_tridiag_solve for the constraint operator's 5x5 blocks."""
+        return self.block_tridiag_solve(diag, upper, rhs)
 
     def set_stream(self, stream_ptr):
         """Run on a CUDA stream (cudaStream_t as int). 0 = the legacy default
@@ -928,45 +938,53 @@ class OeeTrace:
 
 def _bidiag(coupling, rhs, upper, trace, ctx):
     rhs = np.asarray(rhs, dtype=np.float64)
-    n = rhs.shape[0]
-    if rhs.ndim != 2 or rhs.shape[1] != 6:
-        raise InvalidArgument("block bi-diagonal solve: rhs must be (n, 6)")
-    coupling = np.asarray(coupling, dtype=np.float64).reshape(-1, 6, 6)
+    if rhs.ndim != 2 or not 1 <= rhs.shape[1] <= 6:
+        raise InvalidArgument("block bi-diagonal solve: rhs must be (n, D) with 1 <= D <= 6")
+    n, d = rhs.shape
+    coupling = np.asarray(coupling, dtype=np.float64)
+    if coupling.size and coupling.shape[-2:] != (d, d):
+        raise InvalidArgument("block bi-diagonal solve: coupling blocks must be D x D")
+    coupling = coupling.reshape(-1, d, d)
     if n > 0 and coupling.shape[0] != n - 1:
         raise InvalidArgument("block bi-diagonal solve: need n - 1 coupling blocks for n right-hand sides")
     if trace is not None:
         trace.rounds = ceil_log2(n)
     if n == 0:
-        return np.zeros((0, 6))
-    return (ctx or default_context()).block_bidiag_solve6(coupling[None], rhs[None], upper=upper)[0]
+        return np.zeros((0, d))
+    return (ctx or default_context()).block_bidiag_solve(coupling[None], rhs[None], upper=upper)[0]
 
 
 def solve_lower_bidiag(coupling, rhs, trace: Optional[ScanTrace] = None, ctx: Optional[Context] = None):
-    """solve_lower_bidiag (scan.hpp:115-140) of one BlockBiDiagSystem<6>:
-    x_0 = r_0, x_i = C_i x_{i-1} + r_i; coupling (n-1, 6, 6), rhs (n, 6)."""
+    """solve_lower_bidiag<D> (scan.hpp:115-140) of one BlockBiDiagSystem<D>:
+    x_0 = r_0, x_i = C_i x_{i-1} + r_i; coupling (n-1, D, D), rhs (n, D)."""
     return _bidiag(coupling, rhs, False, trace, ctx)
 
 
 def solve_upper_bidiag(coupling, rhs, trace: Optional[ScanTrace] = None, ctx: Optional[Context] = None):
-    """solve_upper_bidiag (scan.hpp:143-168): the reversed index order."""
+    """solve_upper_bidiag<D> (scan.hpp:143-168): the reversed index order."""
     return _bidiag(coupling, rhs, True, trace, ctx)
 
 
 def oee_solve(diag, upper, rhs, trace: Optional[OeeTrace] = None, ctx: Optional[Context] = None):
-    """oee_solve<5,1> (oee.hpp:149-189) of one SymBlockTriDiagSystem<5>:
-    diag (n, 5, 5), upper (n-1, 5, 5), rhs (n, 5) -> x (n, 5). Raises
-    SingularBlockError(round, index) with the reference's message."""
-    diag = np.asarray(diag, dtype=np.float64).reshape(-1, 5, 5)
-    n = diag.shape[0]
-    rhs = np.asarray(rhs, dtype=np.float64).reshape(-1, 5)
-    upper = np.asarray(upper, dtype=np.float64).reshape(-1, 5, 5)
-    if rhs.shape[0] != n or (n > 0 and upper.shape[0] != n - 1):
+    """oee_solve<B, M> (oee.hpp:149-189) of one SymBlockTriDiagSystem<B>:
+    diag (n, B, B), upper (n-1, B, B), rhs (n, B) or (n, B, M) -> x shaped
+    like rhs (B <= 6, M <= 4). Raises SingularBlockError(round, index) with
+    the reference's message."""
+    diag = np.asarray(diag, dtype=np.float64)
+    if diag.ndim != 3 or diag.shape[1] != diag.shape[2] or not 1 <= diag.shape[1] <= 6:
+        raise InvalidArgument("odd-even elimination: diag must be (n, B, B) with 1 <= B <= 6")
+    n, b = diag.shape[0], diag.shape[1]
+    rhs = np.asarray(rhs, dtype=np.float64)
+    upper = np.asarray(upper, dtype=np.float64).reshape(-1, b, b)
+    if rhs.ndim not in (2, 3) or rhs.shape[0] != n or rhs.shape[1] != b or (n > 0 and upper.shape[0] != n - 1):
         raise InvalidArgument("odd-even elimination: inconsistent block counts")
+    if rhs.ndim == 3 and not 1 <= rhs.shape[2] <= 4:
+        raise InvalidArgument("odd-even elimination: 1 to 4 right-hand-side columns")
     if trace is not None:
         trace.rounds = ceil_log2(n)
     if n == 0:
-        return np.zeros((0, 5))
-    x, st, rd, ix = (ctx or default_context()).block_tridiag_solve5(diag[None], upper[None], rhs[None])
+        return np.zeros(rhs.shape)
+    x, st, rd, ix = (ctx or default_context()).block_tridiag_solve(diag[None], upper[None], rhs[None])
     if st[0] != 0:
         _raise_slot(int(st[0]), int(rd[0]), int(ix[0]), n)
     return x[0]

@@ -764,56 +764,22 @@ MatrixXd joint_space_inertia(const RobotChain& chain, const JointVector& q, Exec
 }
 
 // ----------------------------------------------------------------- building blocks (device)
-namespace {
+namespace detail {
 
-std::vector<Vec6> bidiag(const BlockBiDiagSystem<6>& sys, bool upper, ScanTrace* trace) {
-  const std::size_t n = sys.rhs.size();
-  if (sys.coupling.size() + 1 != n && !(n == 0 && sys.coupling.empty()))
-    throw std::invalid_argument("block bi-diagonal solve: need n - 1 coupling blocks for n right-hand sides");
-  if (trace) trace->rounds = ceil_log2(n);  // the scan's designed depth (scan.hpp:32-65)
-  std::vector<Vec6> x(n);
-  if (n == 0) return x;
-  std::vector<double> c(36 * (n - 1)), r(6 * n), xo(6 * n);
-  for (std::size_t k = 0; k + 1 < n; ++k) put_block(sys.coupling[k], &c[36 * k]);
-  for (std::size_t k = 0; k < n; ++k) put_block(sys.rhs[k], &r[6 * k]);
+void bidiag_solve_rm(int dim, bool upper, std::size_t n, const double* coupling, const double* rhs, double* x) {
   pd_ctx* cx = ctx();
-  check_call(cx, pd_block_bidiag_solve6(cx, 1, static_cast<int32_t>(n), upper ? 1 : 0, c.empty() ? nullptr : c.data(),
-                                       r.data(), xo.data()));
-  for (std::size_t k = 0; k < n; ++k) x[k] = get_block<6, 1>(&xo[6 * k]);
-  return x;
+  check_call(cx, pd_block_bidiag_solve(cx, dim, 1, static_cast<int32_t>(n), upper ? 1 : 0, coupling, rhs, x));
 }
 
-}  // namespace
-
-std::vector<Vec6> solve_lower_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
-  return bidiag(sys, false, trace);
-}
-
-std::vector<Vec6> solve_upper_bidiag(const BlockBiDiagSystem<6>& sys, ScanTrace* trace) {
-  return bidiag(sys, true, trace);
-}
-
-std::vector<Vec5> oee_solve(const SymBlockTriDiagSystem<5>& sys, const std::vector<Vec5>& rhs, OeeTrace* trace) {
-  const std::size_t n = sys.diag.size();
-  if (rhs.size() != n || (n > 0 && sys.upper.size() + 1 != n))
-    throw std::invalid_argument("odd-even elimination: inconsistent block counts");
-  if (trace) trace->rounds = 0;
-  std::vector<Vec5> x(n);
-  if (n == 0) return x;
-  std::vector<double> d(25 * n), u(25 * (n - 1)), r(5 * n), xo(5 * n);
-  for (std::size_t k = 0; k < n; ++k) {
-    put_block(sys.diag[k], &d[25 * k]);
-    put_block(rhs[k], &r[5 * k]);
-  }
-  for (std::size_t k = 0; k + 1 < n; ++k) put_block(sys.upper[k], &u[25 * k]);
+void oee_solve_rm(int block, int cols, std::size_t n, const double* diag, const double* upper, const double* rhs,
+                  double* x) {
   pd_ctx* cx = ctx();
   int32_t st = 0, rd = 0, ix = 0;
-  check_call(cx, pd_block_tridiag_solve5(cx, 1, static_cast<int32_t>(n), d.data(), u.empty() ? nullptr : u.data(),
-                                         r.data(), xo.data(), &st, &rd, &ix));
+  check_call(cx, pd_block_tridiag_solve(cx, block, cols, 1, static_cast<int32_t>(n), diag, upper, rhs, x, &st, &rd,
+                                        &ix));
   if (st != PD_SLOT_OK) throw SingularBlockError(rd, ix, slot_message(st, rd, ix, static_cast<int>(n)));
-  if (trace) trace->rounds = ceil_log2(n);
-  for (std::size_t k = 0; k < n; ++k) x[k] = get_block<5, 1>(&xo[5 * k]);
-  return x;
 }
+
+}  // namespace detail
 
 }  // namespace pardyn

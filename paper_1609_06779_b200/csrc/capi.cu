@@ -28,8 +28,10 @@ void launch_cfa_ws(const ModelView& mv, const BatchIO& io, int sm_count, cudaStr
 bool cfa_ws_fits(int n);
 void launch_bidiag6(const double* coupling, const double* rhs, double* x, int64_t batch, int n, int upper,
                     cudaStream_t s);
-bool launch_oee5(const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
-                 int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s);
+bool launch_bidiag(int dim, const double* coupling, const double* rhs, double* x, int64_t batch, int n, int upper,
+                   cudaStream_t s);
+bool launch_oee_block(int b, int m, const double* diag, const double* upper, const double* rhs, double* x,
+                      int64_t batch, int n, int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s);
 bool cfa_coop_path(int n, int64_t batch);
 void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
@@ -1132,23 +1134,27 @@ void pd_slot_message(int32_t code, int32_t round, int32_t index, int32_t n_links
 // ---------------------------------------------------------------- device workloads
 extern "C" {
 
-pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t upper, const double* coupling,
-                                 const double* rhs, double* x) {
+pd_status pd_block_bidiag_solve(pd_ctx* ctx, int32_t dim, int64_t batch, int32_t n, int32_t upper,
+                                const double* coupling, const double* rhs, double* x) {
   if (!ctx) return PD_INVALID_ARGUMENT;
+  if (dim < 1 || dim > 6) {
+    ctx->last_error = "block bi-diagonal solve: block size must be 1..6";
+    return PD_INVALID_ARGUMENT;
+  }
   if (batch < 0 || n < 0 || (batch > 0 && n > 0 && (!rhs || !x || (n > 1 && !coupling)))) {
     ctx->last_error = "block bi-diagonal solve: null buffer";
     return PD_INVALID_ARGUMENT;
   }
   if (batch == 0 || n == 0) return PD_OK;
   PD_CUDA(cudaSetDevice(ctx->device));
-  const size_t nc = (size_t)batch * (n - 1) * 36, nr = (size_t)batch * n * 6;
+  const size_t nc = (size_t)batch * (n - 1) * dim * dim, nr = (size_t)batch * n * dim;
   PD_CUDA(ctx->states.ensure(sizeof(double) * (nc + 2 * nr)));
   double* c = ctx->states.as<double>();
   double* r = c + nc;
   double* xo = r + nr;
   if (nc) PD_CUDA(cudaMemcpyAsync(c, coupling, sizeof(double) * nc, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * nr, cudaMemcpyHostToDevice, ctx->stream));
-  launch_bidiag6(c, r, xo, batch, n, upper ? 1 : 0, ctx->stream);
+  launch_bidiag(dim, c, r, xo, batch, n, upper ? 1 : 0, ctx->stream);
   ctx->launches++;
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaMemcpyAsync(x, xo, sizeof(double) * nr, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1156,17 +1162,27 @@ pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t 
   return PD_OK;
 }
 
-pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const double* diag, const double* upper,
-                                  const double* rhs, double* x, int32_t* slot_status, int32_t* slot_round,
-                                  int32_t* slot_index) {
+pd_status pd_block_bidiag_solve6(pd_ctx* ctx, int64_t batch, int32_t n, int32_t upper, const double* coupling,
+                                 const double* rhs, double* x) {
+  return pd_block_bidiag_solve(ctx, 6, batch, n, upper, coupling, rhs, x);
+}
+
+pd_status pd_block_tridiag_solve(pd_ctx* ctx, int32_t block, int32_t cols, int64_t batch, int32_t n,
+                                 const double* diag, const double* upper, const double* rhs, double* x,
+                                 int32_t* slot_status, int32_t* slot_round, int32_t* slot_index) {
   if (!ctx) return PD_INVALID_ARGUMENT;
+  if (block < 1 || block > 6 || cols < 1 || cols > 4) {
+    ctx->last_error = "block tri-diagonal solve: block size must be 1..6 and right-hand-side columns 1..4";
+    return PD_INVALID_ARGUMENT;
+  }
   if (batch < 0 || n < 1 || n > 256 || (batch > 0 && (!diag || !rhs || !x || (n > 1 && !upper)))) {
     ctx->last_error = "block tri-diagonal solve: need 1 <= n <= 256 rows and non-null buffers";
     return PD_INVALID_ARGUMENT;
   }
   if (batch == 0) return PD_OK;
   PD_CUDA(cudaSetDevice(ctx->device));
-  const size_t nd = (size_t)batch * n * 25, nu = (size_t)batch * (n - 1) * 25, nr = (size_t)batch * n * 5;
+  const size_t bb = (size_t)block * block, bm = (size_t)block * cols;
+  const size_t nd = (size_t)batch * n * bb, nu = (size_t)batch * (n - 1) * bb, nr = (size_t)batch * n * bm;
   PD_CUDA(ctx->states.ensure(sizeof(double) * (nd + nu + 2 * nr) + sizeof(int32_t) * 3 * batch));
   double* d = ctx->states.as<double>();
   double* u = d + nd;
@@ -1176,7 +1192,7 @@ pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const d
   PD_CUDA(cudaMemcpyAsync(d, diag, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
   if (nu) PD_CUDA(cudaMemcpyAsync(u, upper, sizeof(double) * nu, cudaMemcpyHostToDevice, ctx->stream));
   PD_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * nr, cudaMemcpyHostToDevice, ctx->stream));
-  launch_oee5(d, u, r, xo, batch, n, st, st + batch, st + 2 * batch, ctx->stream);
+  launch_oee_block(block, cols, d, u, r, xo, batch, n, st, st + batch, st + 2 * batch, ctx->stream);
   ctx->launches++;
   PD_CUDA(cudaGetLastError());
   PD_CUDA(cudaMemcpyAsync(x, xo, sizeof(double) * nr, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1187,6 +1203,12 @@ pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const d
   if (slot_round) std::memcpy(slot_round, hs.data() + batch, sizeof(int32_t) * batch);
   if (slot_index) std::memcpy(slot_index, hs.data() + 2 * batch, sizeof(int32_t) * batch);
   return PD_OK;
+}
+
+pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const double* diag, const double* upper,
+                                  const double* rhs, double* x, int32_t* slot_status, int32_t* slot_round,
+                                  int32_t* slot_index) {
+  return pd_block_tridiag_solve(ctx, 5, 1, batch, n, diag, upper, rhs, x, slot_status, slot_round, slot_index);
 }
 
 pd_status pd_workload_chains_device(pd_ctx* ctx, uint64_t cell_seed, int32_t n_links, int64_t g0, int64_t count,

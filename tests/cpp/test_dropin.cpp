@@ -244,6 +244,37 @@ int main() {
         res = std::max(res, std::fabs(v - 1.0));
       }
     check(res < 1e-14 && ot.rounds == 2, "OEE solves a 3-block system");
+    // other block sizes, as the reference's templates take them (test_oee.cpp:106-126, :45-58)
+    pardyn::SymBlockTriDiagSystem<2> t2;
+    t2.diag = {pardyn::Matrix<2, 2>::Identity(), pardyn::Matrix<2, 2>(), pardyn::Matrix<2, 2>::Identity()};
+    t2.upper = {0.1 * pardyn::Matrix<2, 2>::Identity(), 0.1 * pardyn::Matrix<2, 2>::Identity()};
+    rd = ix = -1;
+    try {
+      pardyn::oee_solve<2, 1>(t2, std::vector<pardyn::Matrix<2, 1>>(3, pardyn::Matrix<2, 1>::Constant(1.0)));
+    } catch (const pardyn::SingularBlockError& e) {
+      rd = e.round();
+      ix = e.index();
+    }
+    check(rd == 1 && ix == 1, "OEE<2,1> singular pivot reports (round 1, block 1)");
+    t3.diag = {eye, eye, eye};
+    std::vector<pardyn::Matrix<5, 3>> rhs3(3, pardyn::Matrix<5, 3>::Constant(1.0));
+    rhs3[1](2, 1) = -2.0;
+    const auto x3 = pardyn::oee_solve<5, 3>(t3, rhs3);
+    double res3 = 0.0;
+    for (int k = 0; k < 3; ++k)
+      for (int e = 0; e < 5; ++e)
+        for (int c = 0; c < 3; ++c) {
+          double v = x3[k](e, c);
+          if (k > 0) v += 0.1 * x3[k - 1](e, c);
+          if (k < 2) v += 0.1 * x3[k + 1](e, c);
+          res3 = std::max(res3, std::fabs(v - rhs3[k](e, c)));
+        }
+    check(res3 < 1e-14, "OEE<5,3> carries three right-hand-side columns");
+    pardyn::BlockBiDiagSystem<2> s2;
+    s2.coupling = {pardyn::Matrix<2, 2>::FromRowMajor({0.0, 1.0, -1.0, 0.0})};
+    s2.rhs = {pardyn::Matrix<2, 1>::FromRowMajor({1.0, 2.0}), pardyn::Matrix<2, 1>::FromRowMajor({0.5, 0.5})};
+    const auto x2 = pardyn::solve_lower_bidiag(s2);
+    check(x2[1](0) == 2.5 && x2[1](1) == -0.5, "scan<2>: x1 = C x0 + r1");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
