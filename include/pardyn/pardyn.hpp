@@ -266,13 +266,49 @@ struct SymBlockTriDiagSystem {
   std::vector<Matrix<B, B>> upper;  // n - 1 blocks
 };
 
+// One step of the block recursion x[k] = coeff x[k-1] + offset; composing
+// steps gives the step of the concatenated range (scan.hpp:66-97). The later
+// step's coefficient multiplies from the left. Value algebra only: the scans
+// run on the GPU as solve_lower_bidiag / solve_upper_bidiag.
+template <int D>
+struct AffineElement {
+  Matrix<D, D> coeff = Matrix<D, D>::Identity();
+  Matrix<D, 1> offset = Matrix<D, 1>::Zero();
+  static AffineElement identity() { return {}; }
+  static AffineElement compose(const AffineElement& first, const AffineElement& second) {
+    AffineElement out;
+    out.coeff = second.coeff * first.coeff;
+    out.offset = second.coeff * first.offset + second.offset;
+    return out;
+  }
+};
+
+// Elimination state after `round` rounds: coupling[i] links row i to row
+// i + distance (oee.hpp:57-67).
+template <int B, int M = 1>
+struct OeeState {
+  using PivotBlock = Matrix<B, B>;
+  using RhsBlock = Matrix<B, M>;
+  std::vector<PivotBlock> diag;
+  std::vector<PivotBlock> coupling;
+  std::vector<RhsBlock> rhs;
+  int distance = 1;
+  int round = 0;
+};
+
 namespace detail {
 // Row-major packed blocks through the C-ABI (pd_block_bidiag_solve /
-// pd_block_tridiag_solve); D, B in 1..6, M in 1..4. Throw the reference's
-// exceptions (std::invalid_argument, SingularBlockError).
+// pd_block_tridiag_solve / pd_oee_eliminate_rounds); D, B in 1..6, M in 1..4.
+// Throw the reference's exceptions (std::invalid_argument, SingularBlockError).
 void bidiag_solve_rm(int dim, bool upper, std::size_t n, const double* coupling, const double* rhs, double* x);
 void oee_solve_rm(int block, int cols, std::size_t n, const double* diag, const double* upper, const double* rhs,
                   double* x);
+void oee_rounds_rm(int block, int cols, std::size_t n, int distance, int round, const double* diag,
+                   const double* coupling, const double* rhs, double* diag_out, double* coupling_out,
+                   double* rhs_out);
+// pivot x = rhs for one pivot (n = 1 elimination), SingularBlockError(round, index) if singular
+void coefficient_solve_rm(int block, int cols, const double* pivot, const double* rhs, double* x, int round,
+                          int index);
 
 template <int D>
 std::vector<Matrix<D, 1>> bidiag(const BlockBiDiagSystem<D>& sys, bool upper, ScanTrace* trace) {
@@ -322,6 +358,53 @@ std::vector<Matrix<B, M>> oee_solve(const SymBlockTriDiagSystem<B>& sys, const s
   if (trace) trace->rounds = ceil_log2(n);
   for (std::size_t k = 0; k < n; ++k) x[k] = Matrix<B, M>::FromRowMajor(&xo[B * M * k]);
   return x;
+}
+
+// One elimination round on the GPU (oee.hpp:69-145): distance doubles, the
+// couplings shrink to n - 2h; a singular pivot throws SingularBlockError and
+// leaves the state as it was.
+template <int B, int M>
+void oee_eliminate_round(OeeState<B, M>& state) {
+  static_assert(B >= 1 && B <= 6 && M >= 1 && M <= 4, "odd-even elimination: B in 1..6, M in 1..4");
+  const std::size_t n = state.diag.size();
+  const std::size_t h = static_cast<std::size_t>(state.distance);
+  if (state.rhs.size() != n || state.coupling.size() != (n > h ? n - h : 0))
+    throw std::invalid_argument("odd-even elimination: inconsistent block counts");
+  const std::size_t nu = n > 2 * h ? n - 2 * h : 0;
+  if (n == 0) {
+    state.distance *= 2;
+    state.round += 1;
+    return;
+  }
+  std::vector<double> d(B * B * n), c(B * B * state.coupling.size()), r(B * M * n), d1(B * B * n),
+      c1(B * B * nu), r1(B * M * n);
+  for (std::size_t k = 0; k < n; ++k) {
+    state.diag[k].toRowMajor(&d[B * B * k]);
+    state.rhs[k].toRowMajor(&r[B * M * k]);
+  }
+  for (std::size_t k = 0; k < state.coupling.size(); ++k) state.coupling[k].toRowMajor(&c[B * B * k]);
+  detail::oee_rounds_rm(B, M, n, state.distance, state.round, d.data(), c.empty() ? nullptr : c.data(), r.data(),
+                        d1.data(), c1.empty() ? nullptr : c1.data(), r1.data());
+  state.coupling.resize(nu);
+  for (std::size_t k = 0; k < n; ++k) {
+    state.diag[k] = Matrix<B, B>::FromRowMajor(&d1[B * B * k]);
+    state.rhs[k] = Matrix<B, M>::FromRowMajor(&r1[B * M * k]);
+  }
+  for (std::size_t k = 0; k < nu; ++k) state.coupling[k] = Matrix<B, B>::FromRowMajor(&c1[B * B * k]);
+  state.distance *= 2;
+  state.round += 1;
+}
+
+// pivot x = rhs by full-pivot LU (oee.hpp:34-51); throws
+// SingularBlockError(round, index) when the pivot is rank deficient.
+template <int B, int C>
+Matrix<B, C> coefficient_solve(const Matrix<B, B>& pivot, const Matrix<B, C>& rhs, int round, int index) {
+  static_assert(B >= 1 && B <= 6 && C >= 1, "coefficient_solve: B in 1..6");
+  double p[B * B], r[B * C], x[B * C];
+  pivot.toRowMajor(p);
+  rhs.toRowMajor(r);
+  detail::coefficient_solve_rm(B, C, p, r, x, round, index);
+  return Matrix<B, C>::FromRowMajor(x);
 }
 
 // ----------------------------------------------------------------- inverse dynamics (inverse_dynamics.hpp)

@@ -37,6 +37,7 @@
  *                               (include/pardyn/scan.hpp:100-168)
  *   pd_block_tridiag_solve   <- oee_solve<B,M> / SymBlockTriDiagSystem<B> (B <= 6, M <= 4)
  *   pd_block_tridiag_solve5  <- the oee_solve<5,1> case
+ *   pd_oee_eliminate_rounds  <- oee_eliminate_round / OeeState<B,M> (oee.hpp:57-145)
  *                               (include/pardyn/oee.hpp:28-32,149-189)
  *   pd_workload_chains_device, pd_set_models_workload
  *                            <- workload_chains / random_chain on the device
@@ -273,6 +274,20 @@ pd_status pd_block_tridiag_solve5(pd_ctx* ctx, int64_t batch, int32_t n, const d
 pd_status pd_block_tridiag_solve(pd_ctx* ctx, int32_t block, int32_t cols, int64_t batch, int32_t n,
                                  const double* diag, const double* upper, const double* rhs, double* x,
                                  int32_t* slot_status, int32_t* slot_round, int32_t* slot_index);
+/* Odd-even elimination rounds on a state (OeeState<B, M> + oee_eliminate_round,
+ * oee.hpp:57-145) for `batch` systems: diag [batch][n][block*block], coupling
+ * [batch][max(n - distance, 0)][block*block] (coupling[i] links row i to row
+ * i + distance), rhs [batch][n][block*cols], after `state_round` rounds. Runs
+ * `rounds` more rounds (numbered state_round + 1, ...) and writes the advanced
+ * state to diag_out / rhs_out (same shapes) and coupling_out
+ * [batch][max(n - distance * 2^rounds, 0)][block*block]. A singular pivot
+ * reports PD_SLOT_OEE_SINGULAR_PIVOT (round, block) for that system, whose
+ * outputs are then unspecified. 1 <= n <= 256, block 1..6, cols 1..4. */
+pd_status pd_oee_eliminate_rounds(pd_ctx* ctx, int32_t block, int32_t cols, int64_t batch, int32_t n,
+                                  int32_t distance, int32_t state_round, int32_t rounds, const double* diag,
+                                  const double* coupling, const double* rhs, double* diag_out,
+                                  double* coupling_out, double* rhs_out, int32_t* slot_status, int32_t* slot_round,
+                                  int32_t* slot_index);
 
 /* The same chains generated on the device (§8f row 3), one thread per chain:
  *   pd_workload_chains_device  chains [g0, g0+count) into device memory,

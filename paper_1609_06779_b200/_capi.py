@@ -27,7 +27,7 @@ EXPORTS = (
     "pd_slot_message", "pd_kernel_launches", "pd_kernel_variant", "pd_mix", "pd_workload_seed", "pd_random_chain",
     "pd_workload_chains", "pd_workload_inputs", "pd_probe_fp64_peak", "pd_inverse_dynamics_opts",
     "pd_inverse_dynamics_device", "pd_bias_torque", "pd_link_states", "pd_joint_space_inertia",
-    "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5", "pd_block_bidiag_solve6", "pd_block_tridiag_solve", "pd_block_bidiag_solve",
+    "pd_workload_chains_device", "pd_set_models_workload", "pd_block_tridiag_solve5", "pd_block_bidiag_solve6", "pd_block_tridiag_solve", "pd_block_bidiag_solve", "pd_oee_eliminate_rounds",
     "pd_forward_dynamics_traced", "pd_last_variant", "pd_last_trace", "pd_set_selection_batch",
     "pd_assemble_kinematics", "pd_link_inertias", "pd_articulated_body_inertias", "pd_constraint_basis",
     "pd_cfa_operators", "pd_cfa_apply", "pd_host_alloc", "pd_host_free",
@@ -113,6 +113,9 @@ def load():
     L.pd_block_tridiag_solve.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _D, _D, _D, _D,
                                          _I32, _I32, _I32]
     L.pd_block_tridiag_solve.restype = C.c_int
+    L.pd_oee_eliminate_rounds.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                          C.c_int32, _D, _D, _D, _D, _D, _D, _I32, _I32, _I32]
+    L.pd_oee_eliminate_rounds.restype = C.c_int
     L.pd_slot_message.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int32]
     L.pd_slot_message.restype = None
     L.pd_kernel_launches.argtypes = [C.c_void_p]

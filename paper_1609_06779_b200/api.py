@@ -990,6 +990,65 @@ def oee_solve(diag, upper, rhs, trace: Optional[OeeTrace] = None, ctx: Optional[
     return x[0]
 
 
+@dataclass
+class OeeState:
+    """OeeState<B, M> (oee.hpp:57-67): diag (n, B, B), coupling (n - distance,
+    B, B) linking row i to row i + distance, rhs (n, B) or (n, B, M)."""
+    diag: np.ndarray
+    coupling: np.ndarray
+    rhs: np.ndarray
+    distance: int = 1
+    round: int = 0
+
+
+def oee_eliminate_round(state: OeeState, ctx: Optional[Context] = None) -> None:
+    """oee_eliminate_round (oee.hpp:69-145) on the GPU: advances `state` by
+    one round in place (distance doubles, couplings shrink to n - 2h); a
+    singular pivot raises SingularBlockError(round, block) and leaves the
+    state as it was."""
+    diag = np.ascontiguousarray(state.diag, dtype=np.float64)
+    n, b = diag.shape[0], diag.shape[1]
+    rhs = np.ascontiguousarray(state.rhs, dtype=np.float64)
+    m = 1 if rhs.ndim == 2 else rhs.shape[2]
+    h = int(state.distance)
+    coupling = np.ascontiguousarray(np.asarray(state.coupling, dtype=np.float64).reshape(-1, b, b))
+    if rhs.shape[0] != n or coupling.shape[0] != max(n - h, 0):
+        raise InvalidArgument("odd-even elimination: inconsistent block counts")
+    nu = max(n - 2 * h, 0)
+    if n > 0:
+        c = ctx or default_context()
+        d1, c1, r1 = np.empty_like(diag), np.empty((nu, b, b)), np.empty_like(rhs)
+        st, rd, ix = (np.zeros(1, np.int32) for _ in range(3))
+        c._check(c._L.pd_oee_eliminate_rounds(c._h, b, m, 1, n, h, int(state.round), 1, _capi.dptr(diag),
+                                              _capi.dptr(coupling), _capi.dptr(rhs), _capi.dptr(d1), _capi.dptr(c1),
+                                              _capi.dptr(r1), _capi.iptr(st), _capi.iptr(rd), _capi.iptr(ix)))
+        if st[0] != 0:
+            _raise_slot(int(st[0]), int(rd[0]), int(ix[0]), n)
+        state.diag, state.coupling, state.rhs = d1, c1, r1
+    state.distance = 2 * h
+    state.round = int(state.round) + 1
+
+
+def coefficient_solve(pivot, rhs, round_: int, index: int, ctx: Optional[Context] = None):
+    """coefficient_solve<B> (oee.hpp:34-51): pivot x = rhs by full-pivot LU on
+    the GPU (a one-row elimination); SingularBlockError(round_, index) when
+    the pivot is rank deficient."""
+    pivot = np.asarray(pivot, dtype=np.float64)
+    rhs = np.asarray(rhs, dtype=np.float64)
+    b = pivot.shape[0]
+    cols = rhs.reshape(b, -1)
+    out = np.empty_like(cols)
+    c = ctx or default_context()
+    for c0 in range(0, cols.shape[1], 4):
+        part = np.ascontiguousarray(cols[:, c0:c0 + 4])
+        x, st, _, _ = c.block_tridiag_solve(pivot[None, None], np.zeros((1, 0, b, b)), part[None, None])
+        if st[0] != 0:
+            raise SingularBlockError(round_, index, f"odd-even elimination: singular pivot block (round {round_}, "
+                                                    f"block {index})")
+        out[:, c0:c0 + 4] = x[0, 0]
+    return out.reshape(rhs.shape)
+
+
 def _link_prefix(k: int) -> str:
     return f"link {k}"
 

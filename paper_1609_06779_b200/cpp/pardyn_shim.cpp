@@ -780,6 +780,36 @@ void oee_solve_rm(int block, int cols, std::size_t n, const double* diag, const 
   if (st != PD_SLOT_OK) throw SingularBlockError(rd, ix, slot_message(st, rd, ix, static_cast<int>(n)));
 }
 
+void oee_rounds_rm(int block, int cols, std::size_t n, int distance, int round, const double* diag,
+                   const double* coupling, const double* rhs, double* diag_out, double* coupling_out,
+                   double* rhs_out) {
+  pd_ctx* cx = ctx();
+  int32_t st = 0, rd = 0, ix = 0;
+  check_call(cx, pd_oee_eliminate_rounds(cx, block, cols, 1, static_cast<int32_t>(n), distance, round, 1, diag,
+                                         coupling, rhs, diag_out, coupling_out, rhs_out, &st, &rd, &ix));
+  if (st != PD_SLOT_OK) throw SingularBlockError(rd, ix, slot_message(st, rd, ix, static_cast<int>(n)));
+}
+
+void coefficient_solve_rm(int block, int cols, const double* pivot, const double* rhs, double* x, int round,
+                          int index) {
+  // a one-row system is exactly a pivot solve: no rounds, the final block solve
+  pd_ctx* cx = ctx();
+  std::vector<double> rc(static_cast<std::size_t>(block) * std::min(cols, 4)), xc(rc.size());
+  for (int c0 = 0; c0 < cols; c0 += 4) {  // the kernel carries up to 4 columns at a time
+    const int w = std::min(4, cols - c0);
+    for (int r = 0; r < block; ++r)
+      for (int c = 0; c < w; ++c) rc[r * w + c] = rhs[r * cols + c0 + c];
+    int32_t st = 0, rd = 0, ix = 0;
+    check_call(cx, pd_block_tridiag_solve(cx, block, w, 1, 1, pivot, nullptr, rc.data(), xc.data(), &st, &rd, &ix));
+    if (st != PD_SLOT_OK)
+      throw SingularBlockError(round, index,
+                               "odd-even elimination: singular pivot block (round " + std::to_string(round) +
+                                   ", block " + std::to_string(index) + ")");
+    for (int r = 0; r < block; ++r)
+      for (int c = 0; c < w; ++c) x[r * cols + c0 + c] = xc[r * w + c];
+  }
+}
+
 }  // namespace detail
 
 }  // namespace pardyn

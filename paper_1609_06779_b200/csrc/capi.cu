@@ -32,6 +32,9 @@ bool launch_bidiag(int dim, const double* coupling, const double* rhs, double* x
                    cudaStream_t s);
 bool launch_oee_block(int b, int m, const double* diag, const double* upper, const double* rhs, double* x,
                       int64_t batch, int n, int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s);
+bool launch_oee_rounds(int b, int m, const double* diag, const double* coupling, const double* rhs, int64_t batch,
+                       int n, int distance, int round0, int nrounds, double* diag_out, double* coupling_out,
+                       double* rhs_out, int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s);
 bool cfa_coop_path(int n, int64_t batch);
 void launch_cfa_coop(const ModelView& mv, const BatchIO& io, double* gws, int* bad, int sm_count, cudaStream_t s);
 size_t cfa_workspace_bytes(int n);
@@ -1198,6 +1201,58 @@ pd_status pd_block_tridiag_solve(pd_ctx* ctx, int32_t block, int32_t cols, int64
   PD_CUDA(cudaMemcpyAsync(x, xo, sizeof(double) * nr, cudaMemcpyDeviceToHost, ctx->stream));
   std::vector<int32_t> hs(3 * batch);
   PD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (slot_status) std::memcpy(slot_status, hs.data(), sizeof(int32_t) * batch);
+  if (slot_round) std::memcpy(slot_round, hs.data() + batch, sizeof(int32_t) * batch);
+  if (slot_index) std::memcpy(slot_index, hs.data() + 2 * batch, sizeof(int32_t) * batch);
+  return PD_OK;
+}
+
+pd_status pd_oee_eliminate_rounds(pd_ctx* ctx, int32_t block, int32_t cols, int64_t batch, int32_t n,
+                                  int32_t distance, int32_t state_round, int32_t rounds, const double* diag,
+                                  const double* coupling, const double* rhs, double* diag_out,
+                                  double* coupling_out, double* rhs_out, int32_t* slot_status, int32_t* slot_round,
+                                  int32_t* slot_index) {
+  if (!ctx) return PD_INVALID_ARGUMENT;
+  if (block < 1 || block > 6 || cols < 1 || cols > 4 || n < 1 || n > 256 || distance < 1 || state_round < 0 ||
+      rounds < 0 || rounds > 30) {
+    ctx->last_error = "odd-even elimination rounds: block 1..6, cols 1..4, 1 <= n <= 256, distance >= 1";
+    return PD_INVALID_ARGUMENT;
+  }
+  const int64_t nu0 = n > distance ? n - distance : 0;
+  int64_t hend = distance;
+  for (int r = 0; r < rounds && hend < (1ll << 40); ++r) hend *= 2;
+  const int64_t nu1 = n > hend ? n - hend : 0;
+  if (batch < 0 || (batch > 0 && (!diag || !rhs || !diag_out || !rhs_out || (nu0 > 0 && !coupling) ||
+                                   (nu1 > 0 && !coupling_out)))) {
+    ctx->last_error = "odd-even elimination rounds: null buffer";
+    return PD_INVALID_ARGUMENT;
+  }
+  if (batch == 0) return PD_OK;
+  PD_CUDA(cudaSetDevice(ctx->device));
+  const size_t bb = (size_t)block * block, bm = (size_t)block * cols;
+  const size_t nd = (size_t)batch * n * bb, nc0 = (size_t)batch * nu0 * bb, nc1 = (size_t)batch * nu1 * bb,
+               nr = (size_t)batch * n * bm;
+  PD_CUDA(ctx->states.ensure(sizeof(double) * (2 * nd + nc0 + nc1 + 2 * nr) + sizeof(int32_t) * 3 * batch));
+  double* d = ctx->states.as<double>();
+  double* c = d + nd;
+  double* r = c + nc0;
+  double* dout = r + nr;
+  double* cout = dout + nd;
+  double* rout = cout + nc1;
+  int32_t* st = reinterpret_cast<int32_t*>(rout + nr);
+  PD_CUDA(cudaMemcpyAsync(d, diag, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+  if (nc0) PD_CUDA(cudaMemcpyAsync(c, coupling, sizeof(double) * nc0, cudaMemcpyHostToDevice, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * nr, cudaMemcpyHostToDevice, ctx->stream));
+  launch_oee_rounds(block, cols, d, c, r, batch, n, distance, state_round, rounds, dout, cout, rout, st, st + batch,
+                    st + 2 * batch, ctx->stream);
+  ctx->launches++;
+  PD_CUDA(cudaGetLastError());
+  std::vector<int32_t> hs(3 * batch);
+  PD_CUDA(cudaMemcpyAsync(hs.data(), st, sizeof(int32_t) * 3 * batch, cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(diag_out, dout, sizeof(double) * nd, cudaMemcpyDeviceToHost, ctx->stream));
+  if (nc1) PD_CUDA(cudaMemcpyAsync(coupling_out, cout, sizeof(double) * nc1, cudaMemcpyDeviceToHost, ctx->stream));
+  PD_CUDA(cudaMemcpyAsync(rhs_out, rout, sizeof(double) * nr, cudaMemcpyDeviceToHost, ctx->stream));
   PD_CUDA(cudaStreamSynchronize(ctx->stream));
   if (slot_status) std::memcpy(slot_status, hs.data(), sizeof(int32_t) * batch);
   if (slot_round) std::memcpy(slot_round, hs.data() + batch, sizeof(int32_t) * batch);

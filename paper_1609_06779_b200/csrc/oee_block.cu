@@ -117,12 +117,22 @@ struct Pub {
 }  // namespace
 
 // rhs / x blocks are row-major B x M: element (r, c) at r * M + c.
+// Rounds: the state enters at coupling distance h0 after round0 rounds
+// (OeeState, oee.hpp:57-67; `upper` holds coupling[i] for i < n - h0) and
+// nrounds rounds run. With st == nullptr the final block solves follow (the
+// full oee_solve); otherwise the advanced state (diag, coupling at the new
+// distance, rhs) is written to st_* -- oee_eliminate_round repeated.
+struct OeeRounds {
+  int h0, round0, nrounds;
+  double *st_diag, *st_coupling, *st_rhs;
+};
+
 template <int B, int M>
 __global__ void __launch_bounds__(256) oee_block_kernel(const double* __restrict__ diag,
                                                         const double* __restrict__ upper,
                                                         const double* __restrict__ rhs, double* __restrict__ x, int n,
                                                         int32_t* __restrict__ status, int32_t* __restrict__ eround,
-                                                        int32_t* __restrict__ eindex) {
+                                                        int32_t* __restrict__ eindex, OeeRounds rr) {
   using P = Pub<B, M>;
   extern __shared__ double ws[];                                 // [P::FIELDS][n]
   int* perm = reinterpret_cast<int*>(ws + P::FIELDS * n);         // [2B][n]: rowt, colt
@@ -131,18 +141,19 @@ __global__ void __launch_bounds__(256) oee_block_kernel(const double* __restrict
   const int64_t p = blockIdx.x;
   const int i = threadIdx.x;
   const bool own = i < n;
+  const int h0 = rr.h0, nu0 = n > h0 ? n - h0 : 0;
   const double* Dg = diag + (size_t)p * n * B * B;
-  const double* Ug = upper + (size_t)p * (n > 0 ? n - 1 : 0) * B * B;
+  const double* Ug = upper + (size_t)p * nu0 * B * B;
   const double* Rg = rhs + (size_t)p * n * B * M;
   double D[B * B], U[B * B], R[B * M];
   if (own) {
     for (int k = 0; k < B * B; ++k) D[k] = __ldg(Dg + (size_t)i * B * B + k);
-    for (int k = 0; k < B * B; ++k) U[k] = (i + 1 < n) ? __ldg(Ug + (size_t)i * B * B + k) : 0.0;
+    for (int k = 0; k < B * B; ++k) U[k] = (i + h0 < n) ? __ldg(Ug + (size_t)i * B * B + k) : 0.0;
     for (int k = 0; k < B * M; ++k) R[k] = __ldg(Rg + (size_t)i * B * M + k);
   }
-  const int rounds = ceil_log2_dev(n);
-  int h = 1;
-  for (int round = 1; round <= rounds; ++round, h <<= 1) {
+  const int rounds = rr.round0 + rr.nrounds;
+  int h = h0;
+  for (int round = rr.round0 + 1; round <= rounds; ++round, h <<= 1) {
     if (i == 0) s_bad = n;
     if (own) {  // publish: LU of the pivot, the coupling to i + h, the rhs
       Lu<B> f;
@@ -246,6 +257,21 @@ __global__ void __launch_bounds__(256) oee_block_kernel(const double* __restrict
     }
     __syncthreads();  // published fields are rewritten next round
   }
+  if (rr.st_diag) {  // the advanced state: coupling now at distance h
+    if (own) {
+      for (int k = 0; k < B * B; ++k) rr.st_diag[((size_t)p * n + i) * B * B + k] = D[k];
+      for (int k = 0; k < B * M; ++k) rr.st_rhs[((size_t)p * n + i) * B * M + k] = R[k];
+      const int nu = n > h ? n - h : 0;
+      if (i < nu)
+        for (int k = 0; k < B * B; ++k) rr.st_coupling[((size_t)p * nu + i) * B * B + k] = U[k];
+    }
+    if (i == 0) {
+      status[p] = PD_SLOT_OK;
+      eround[p] = 0;
+      eindex[p] = 0;
+    }
+    return;
+  }
   // final block solves x_i = D_i^{-1} R_i (oee.hpp:168-187)
   if (i == 0) s_bad = n;
   __syncthreads();
@@ -270,22 +296,41 @@ __global__ void __launch_bounds__(256) oee_block_kernel(const double* __restrict
 }
 
 namespace {
+struct OeeArgs {
+  const double *diag, *upper, *rhs;
+  double* x;
+  int64_t batch;
+  int n;
+  int32_t *status, *eround, *eindex;
+  OeeRounds rr;
+};
+
 template <int B, int M>
-void go_oee(const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
-            int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s) {
-  const size_t bytes = (size_t)Pub<B, M>::FIELDS * n * sizeof(double) + (size_t)2 * B * n * sizeof(int) + n;
+void go_oee(const OeeArgs& a, cudaStream_t s) {
+  const size_t bytes = (size_t)Pub<B, M>::FIELDS * a.n * sizeof(double) + (size_t)2 * B * a.n * sizeof(int) + a.n;
   cudaFuncSetAttribute(oee_block_kernel<B, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  oee_block_kernel<B, M><<<(unsigned)batch, ((n + 31) / 32) * 32, bytes, s>>>(diag, upper, rhs, x, n, status, eround,
-                                                                                eindex);
+  oee_block_kernel<B, M><<<(unsigned)a.batch, ((a.n + 31) / 32) * 32, bytes, s>>>(
+      a.diag, a.upper, a.rhs, a.x, a.n, a.status, a.eround, a.eindex, a.rr);
 }
 template <int B>
-bool go_oee_m(int m, const double* diag, const double* upper, const double* rhs, double* x, int64_t batch, int n,
-              int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s) {
+bool go_oee_m(int m, const OeeArgs& a, cudaStream_t s) {
   switch (m) {
-    case 1: go_oee<B, 1>(diag, upper, rhs, x, batch, n, status, eround, eindex, s); return true;
-    case 2: go_oee<B, 2>(diag, upper, rhs, x, batch, n, status, eround, eindex, s); return true;
-    case 3: go_oee<B, 3>(diag, upper, rhs, x, batch, n, status, eround, eindex, s); return true;
-    case 4: go_oee<B, 4>(diag, upper, rhs, x, batch, n, status, eround, eindex, s); return true;
+    case 1: go_oee<B, 1>(a, s); return true;
+    case 2: go_oee<B, 2>(a, s); return true;
+    case 3: go_oee<B, 3>(a, s); return true;
+    case 4: go_oee<B, 4>(a, s); return true;
+    default: return false;
+  }
+}
+bool go_oee_b(int b, int m, const OeeArgs& a, cudaStream_t s) {
+  if (a.n < 1 || a.n > 256) return false;
+  switch (b) {
+    case 1: return go_oee_m<1>(m, a, s);
+    case 2: return go_oee_m<2>(m, a, s);
+    case 3: return go_oee_m<3>(m, a, s);
+    case 4: return go_oee_m<4>(m, a, s);
+    case 5: return go_oee_m<5>(m, a, s);
+    case 6: return go_oee_m<6>(m, a, s);
     default: return false;
   }
 }
@@ -293,16 +338,16 @@ bool go_oee_m(int m, const double* diag, const double* upper, const double* rhs,
 
 bool launch_oee_block(int b, int m, const double* diag, const double* upper, const double* rhs, double* x,
                       int64_t batch, int n, int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s) {
-  if (n < 1 || n > 256) return false;
-  switch (b) {
-    case 1: return go_oee_m<1>(m, diag, upper, rhs, x, batch, n, status, eround, eindex, s);
-    case 2: return go_oee_m<2>(m, diag, upper, rhs, x, batch, n, status, eround, eindex, s);
-    case 3: return go_oee_m<3>(m, diag, upper, rhs, x, batch, n, status, eround, eindex, s);
-    case 4: return go_oee_m<4>(m, diag, upper, rhs, x, batch, n, status, eround, eindex, s);
-    case 5: return go_oee_m<5>(m, diag, upper, rhs, x, batch, n, status, eround, eindex, s);
-    case 6: return go_oee_m<6>(m, diag, upper, rhs, x, batch, n, status, eround, eindex, s);
-    default: return false;
-  }
+  int rounds = 0;
+  while ((1 << rounds) < n) ++rounds;
+  return go_oee_b(b, m, OeeArgs{diag, upper, rhs, x, batch, n, status, eround, eindex, OeeRounds{1, 0, rounds, nullptr, nullptr, nullptr}}, s);
+}
+
+bool launch_oee_rounds(int b, int m, const double* diag, const double* coupling, const double* rhs, int64_t batch,
+                       int n, int distance, int round0, int nrounds, double* diag_out, double* coupling_out,
+                       double* rhs_out, int32_t* status, int32_t* eround, int32_t* eindex, cudaStream_t s) {
+  return go_oee_b(b, m, OeeArgs{diag, coupling, rhs, nullptr, batch, n, status, eround, eindex,
+                                OeeRounds{distance, round0, nrounds, diag_out, coupling_out, rhs_out}}, s);
 }
 
 }  // namespace pd

@@ -275,6 +275,63 @@ int main() {
     s2.rhs = {pardyn::Matrix<2, 1>::FromRowMajor({1.0, 2.0}), pardyn::Matrix<2, 1>::FromRowMajor({0.5, 0.5})};
     const auto x2 = pardyn::solve_lower_bidiag(s2);
     check(x2[1](0) == 2.5 && x2[1](1) == -0.5, "scan<2>: x1 = C x0 + r1");
+    // AffineElement composition order (scan.hpp:66-97)
+    pardyn::AffineElement<2> e1, e2;
+    e1.offset = s2.rhs[0];
+    e2.coeff = s2.coupling[0];
+    e2.offset = s2.rhs[1];
+    const auto e12 = pardyn::AffineElement<2>::compose(e1, e2);
+    check(e12.offset(0) == 2.5 && e12.offset(1) == -0.5, "AffineElement::compose(first, second)");
+    // elimination rounds on a state (test_oee.cpp:60-94): pivots stay
+    // symmetric round to round, couplings shrink by rows, distance doubles
+    for (int n : {5, 16, 33, 100}) {
+      pardyn::OeeState<5, 1> st;
+      for (int k = 0; k < n; ++k) {
+        pardyn::Mat5 a;
+        for (int r = 0; r < 5; ++r)
+          for (int c = 0; c < 5; ++c) a(r, c) = std::sin(1.3 * (k + 1) * (r + 1) + 0.7 * c);
+        st.diag.push_back(a * a.transpose() + 4.0 * pardyn::Mat5::Identity());
+        st.rhs.push_back(pardyn::Vec5::Constant(1.0 + 0.01 * k));
+        if (k + 1 < n) st.coupling.push_back(0.2 * a);
+      }
+      const int rounds = pardyn::ceil_log2(static_cast<std::size_t>(n));
+      double asym = 0.0;
+      for (int j = 0; j < rounds; ++j) {
+        pardyn::oee_eliminate_round(st);
+        for (const auto& d : st.diag)
+          for (int r = 0; r < 5; ++r)
+            for (int c = 0; c < 5; ++c) asym = std::max(asym, std::fabs(d(r, c) - d(c, r)));
+        check(st.distance == (2 << j) && st.coupling.size() == static_cast<std::size_t>(std::max(0, n - (2 << j))),
+              "elimination round: distance doubles, couplings shrink by rows");
+      }
+      check(asym < 1e-10 && st.round == rounds && st.coupling.empty(), "pivots stay symmetric; all couplings gone");
+      // the eliminated system decouples: each row solves alone, and agrees with oee_solve
+      pardyn::SymBlockTriDiagSystem<5> sys;
+      pardyn::OeeState<5, 1> st0;
+      for (int k = 0; k < n; ++k) {
+        pardyn::Mat5 a;
+        for (int r = 0; r < 5; ++r)
+          for (int c = 0; c < 5; ++c) a(r, c) = std::sin(1.3 * (k + 1) * (r + 1) + 0.7 * c);
+        sys.diag.push_back(a * a.transpose() + 4.0 * pardyn::Mat5::Identity());
+        st0.rhs.push_back(pardyn::Vec5::Constant(1.0 + 0.01 * k));
+        if (k + 1 < n) sys.upper.push_back(0.2 * a);
+      }
+      const auto xs = pardyn::oee_solve(sys, st0.rhs);
+      double gap = 0.0;
+      for (int k = 0; k < n; ++k) {
+        const pardyn::Vec5 xk = pardyn::coefficient_solve<5, 1>(st.diag[k], st.rhs[k], st.round, k);
+        for (int e = 0; e < 5; ++e) gap = std::max(gap, std::fabs(xk(e) - xs[k](e)));
+      }
+      check(gap < 1e-12, "rounds + coefficient_solve reproduce oee_solve");
+    }
+    int cs_round = -1, cs_index = -1;
+    try {
+      pardyn::coefficient_solve<2, 1>(pardyn::Matrix<2, 2>(), pardyn::Matrix<2, 1>::Constant(1.0), 3, 7);
+    } catch (const pardyn::SingularBlockError& e) {
+      cs_round = e.round();
+      cs_index = e.index();
+    }
+    check(cs_round == 3 && cs_index == 7, "coefficient_solve: singular pivot names (round, block)");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;

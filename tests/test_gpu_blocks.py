@@ -156,3 +156,41 @@ def test_affine_composition_carries_the_recursion(gpu_ctx):
     assert np.abs(x[0] - want[0]).max() < 1e-14
     assert np.abs(x - want).max() < 1e-12
     assert tr.rounds == 4
+
+
+@pytest.mark.parametrize("b", [2, 5])
+@pytest.mark.parametrize("n", [5, 16, 33, 100])
+def test_elimination_rounds_on_a_state(gpu_ctx, b, n):
+    """test_oee.cpp:60-94: pivots stay symmetric round to round, the
+    couplings shrink by rows and the distance doubles; after the last round
+    every row solves alone (coefficient_solve), bit for bit what oee_solve
+    returns (same kernel arithmetic, state through memory)."""
+    rng = np.random.default_rng(121 + n + b)
+    diag, upper = random_tridiag(rng, n, b)
+    rhs = rng.uniform(-1, 1, (n, b))
+    st = pd.OeeState(diag.copy(), upper.copy(), rhs.copy())
+    rounds = pd.ceil_log2(n)
+    for j in range(rounds):
+        pd.oee_eliminate_round(st, ctx=gpu_ctx)
+        assert np.abs(st.diag - np.transpose(st.diag, (0, 2, 1))).max() < 1e-10
+        assert st.distance == 2 << j and st.coupling.shape[0] == max(0, n - (2 << j))
+    assert st.round == rounds and st.coupling.shape[0] == 0
+    x = pd.oee_solve(diag, upper, rhs, ctx=gpu_ctx)
+    xr = np.stack([pd.coefficient_solve(st.diag[k], st.rhs[k], st.round, k, ctx=gpu_ctx) for k in range(n)])
+    assert np.array_equal(xr, x)
+
+
+def test_elimination_round_singular_pivot_leaves_state(gpu_ctx):
+    """oee.hpp:130-138: a singular pivot throws (round, block) and the state
+    is not advanced."""
+    diag = np.stack([np.eye(2), np.zeros((2, 2)), np.eye(2)])
+    st = pd.OeeState(diag.copy(), np.stack([0.1 * np.eye(2)] * 2), np.ones((3, 2)))
+    with pytest.raises(pd.SingularBlockError) as e:
+        pd.oee_eliminate_round(st, ctx=gpu_ctx)
+    assert (e.value.round(), e.value.index()) == (1, 1)
+    assert st.round == 0 and st.distance == 1 and np.array_equal(st.diag, diag)
+    with pytest.raises(pd.SingularBlockError) as e2:
+        pd.coefficient_solve(np.zeros((3, 3)), np.ones((3, 6)), 4, 9, ctx=gpu_ctx)
+    assert (e2.value.round(), e2.value.index()) == (4, 9)
+    x = pd.coefficient_solve(2.0 * np.eye(3), np.ones((3, 6)), 1, 0, ctx=gpu_ctx)  # > 4 columns: two launches
+    assert np.array_equal(x, 0.5 * np.ones((3, 6)))
