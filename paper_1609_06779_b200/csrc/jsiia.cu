@@ -655,16 +655,22 @@ __global__ void __launch_bounds__(256) jsiia_factor_coop(double* __restrict__ gw
 // diagonal tile. The residual uses the closed form of M (residual_closed).
 constexpr int kWideWarps = 16;
 
-__device__ __forceinline__ void wait_flag(volatile int* f, int want) {
-  while (*f != want) {
-  }
+// Flags are read and written with shared-memory atomics, bracketed by block
+// fences: release (data, fence, flag) on the publishing side, acquire (flag,
+// fence, data) on the waiting side.
+// (one lane polls, so the warp's spin is one atomic at a time)
+__device__ __forceinline__ void wait_flag(int* f, int want, int lane) {
+  if (lane == 0)
+    while (atomicAdd(f, 0) != want) {
+    }
+  __syncwarp();
   __threadfence_block();
 }
-__device__ __forceinline__ void publish(double* v, int J, int lane, double val, volatile int* ready, int epoch) {
+__device__ __forceinline__ void publish(double* v, int J, int lane, double val, int* ready, int epoch) {
   v[32 * J + lane] = val;
   __threadfence_block();
   __syncwarp();
-  if (lane == 0) ready[J] = epoch;
+  if (lane == 0) atomicExch(ready + J, epoch);
 }
 __device__ __forceinline__ void stage_diag(const double* Mb, int ld, int J, double* T, int lane) {
 #pragma unroll 8
@@ -687,7 +693,7 @@ __device__ __forceinline__ double dot32(const double (&a)[32], const double* y) 
 // (L L^T) v = v in place; flags `ready` take the values epoch (forward) and
 // epoch + 1 (backward), so they never need resetting between solves.
 __device__ void wide_llt_solve(const double* Mb, int ld, int np, const double* invd, double* v, double* sT,
-                               volatile int* ready, int epoch, int warp, int lane) {
+                               int* ready, int epoch, int warp, int lane) {
   double* T = sT + warp * 32 * 33;
   // forward: L y = v, tile rows ascending
   for (int J = warp; J < np; J += kWideWarps) {
@@ -702,7 +708,7 @@ __device__ void wide_llt_solve(const double* Mb, int ld, int np, const double* i
         a[c] = t.x;
         a[c + 1] = t.y;
       }
-      wait_flag(ready + I, epoch);
+      wait_flag(ready + I, epoch, lane);
       acc -= dot32(a, v + 32 * I);
     }
     const double id = invd[32 * J + lane];
@@ -725,7 +731,7 @@ __device__ void wide_llt_solve(const double* Mb, int ld, int np, const double* i
       double a[32];  // column `lane` of L_IJ (coalesced), loaded before the wait
 #pragma unroll
       for (int c = 0; c < 32; ++c) a[c] = Mb[(size_t)(32 * I + c) * ld + 32 * J + lane];
-      wait_flag(ready + I, epoch + 1);
+      wait_flag(ready + I, epoch + 1, lane);
       acc -= dot32(a, v + 32 * I);
     }
     const double id = invd[32 * J + lane];
@@ -787,7 +793,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) jsiia_solve_wide(BatchIO io, 
   __shared__ BlockReduce br;
   __shared__ ScanSmem scan_sm;
   double* sT = wide_smem;
-  volatile int* ready = reinterpret_cast<volatile int*>(wide_smem + kWideWarps * 32 * 33);
+  int* ready = reinterpret_cast<int*>(wide_smem + kWideWarps * 32 * 33);
   const JstLayout L = jst_layout(n);
   const int64_t p = blockIdx.x;
   const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;

@@ -36,7 +36,8 @@ run(A, 70, 3)              # abia_cta_kernel
 run(J, 32, 200)            # jsiia_dmma_kernel
 run(J, 64, 100)            # jsiia_dmma_kernel, 8 blocks
 run(J, 100, 6)             # jsiia_tiled_kernel
-run(J, 300, 1)             # cooperative grid Cholesky
+run(J, 300, 1)             # cooperative grid Cholesky + wavefront solves
+run(J, 1050, 1)            # more tile rows (33) than solve warps (16)
 run(C, 40, 100)            # cfa_row_kernel
 run(C, 64, 300, 1 << 20)   # tau_surplus_lane_kernel + cfa_row_kernel
 run(C, 300, 2)             # cfa_cta_kernel / coop OEE
@@ -60,6 +61,12 @@ rng = np.random.default_rng(1)
 ctx.block_bidiag_solve6(rng.standard_normal((4, 9, 6, 6)) * 0.3, rng.standard_normal((4, 10, 6)))
 d = np.tile(np.eye(5) * 4.0, (4, 10, 1, 1))
 ctx.block_tridiag_solve5(d, np.tile(np.eye(5) * 0.5, (4, 9, 1, 1)), rng.standard_normal((4, 10, 5)))
+ctx.block_bidiag_solve(rng.standard_normal((3, 20, 3, 3)) * 0.3, rng.standard_normal((3, 21, 3)), True)
+d2 = np.tile(np.eye(2) * 4.0, (3, 12, 1, 1))
+ctx.block_tridiag_solve(d2, np.tile(np.eye(2) * 0.5, (3, 11, 1, 1)), rng.standard_normal((3, 12, 2, 3)))
+st = pd.OeeState(d2[0].copy(), np.tile(np.eye(2) * 0.5, (11, 1, 1)), rng.standard_normal((12, 2)))
+pd.oee_eliminate_round(st, ctx=ctx)
+pd.oee_eliminate_round(st, ctx=ctx)
 ms, _ = ctx.set_models_workload(W.workload_seed(42, 20, 500), 20, 500)
 print("operators / ID / building blocks / device workload: done", flush=True)
 sys.exit(1 if bad else 0)
