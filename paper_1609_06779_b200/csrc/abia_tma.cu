@@ -134,10 +134,12 @@ __device__ __forceinline__ SE3d row_rel(const double* f, int r0, const Sv& S, do
 
 // MAXREG caps registers per thread (__maxnreg__) so that the wanted number of
 // CTAs fits the SM's 64K registers (e.g. 2 x 160 threads x 200).
-template <int KT, int MAXREG>
-__global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
-    abia_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
-                     int64_t scr_ld, uint32_t cap_rows) {
+// SPLIT: the producer warpgroup gives its registers to the consumers
+// (setmaxnreg inside each role's branch, so ptxas allocates each role's code
+// with its own budget).
+template <int KT, bool SPLIT = false>
+__device__ __forceinline__ void abia_ring_body(const Maps& maps, const ModelView& mv, const BatchIO& io,
+                                               double* __restrict__ scratch, int64_t scr_ld, uint32_t cap_rows) {
   static_assert(KT % 16 == 0, "ring rows must stay 128-byte aligned for TMA");
   extern __shared__ __align__(128) double ring[];  // cap_rows x KT doubles
   __shared__ __align__(8) uint64_t full[kSlots];
@@ -161,8 +163,9 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
   // Persistent CTA: tiles blockIdx.x, blockIdx.x + gridDim.x, ... flow through
   // one ring, so the next tile's pass-A loads stream in during this tile's
   // (memory-light) pass C. Steps are numbered gk across the CTA's tiles.
-  if (t >= NW * 32) {  // ---- producer warp: one elected lane issues every step in order
-    if (lane == 0) {
+  if (t >= NW * 32) {  // ---- producer warp(s): one elected lane issues every step in order
+    if constexpr (SPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+    if (t == NW * 32) {
       uint32_t vpos = 0, phys = 0, old = 0, gk = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int c0 = tile * KT;
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
     }
     return;
   }
+  if constexpr (SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 240;" ::: "memory");
   uint32_t cphys = 0, gk = 0;  // consumer's ring position / step counter (mirror the producer's)
   const int tt = t < KT ? t : 0;
   // step k's rows; `ahead` = steps already acquired and not yet released
@@ -302,6 +306,23 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
   }
 }
 
+template <int KT, int MAXREG>
+__global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
+    abia_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
+                     int64_t scr_ld, uint32_t cap_rows) {
+  abia_ring_body<KT>(maps, mv, io, scratch, scr_ld, cap_rows);
+}
+
+// 256-chain tiles: eight consumer warps (two warpgroups raised to 240
+// registers) and a producer warpgroup lowered to 24 (one working lane), so
+// every SMSP carries two consumer warps within the SM's 64K registers
+// (384 x 168 at launch = 256 x 240 + 128 x 24).
+__global__ void __launch_bounds__(384, 1)
+    abia_ring8_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
+                      int64_t scr_ld, uint32_t cap_rows) {
+  abia_ring_body<256, true>(maps, mv, io, scratch, scr_ld, cap_rows);
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 
@@ -389,10 +410,14 @@ int sm_count() {
 // one 224-chain CTA per SM (7 consumer warps): two 96-chain CTAs (2 x 3
 // consumer warps, two producer warps) run 10 % slower per chain (c5a, 1M x 64:
 // 5.18 ms at 224 x 1, 5.77 ms at 96 x 2; profiles/abia_tile_r2.txt), so they win
-// only where they fill SMs a 224-chain tiling would leave idle.
+// only where they fill SMs a 224-chain tiling would leave idle. One
+// 256-chain CTA (abia_ring8_kernel: 8 consumer warps, two per SMSP, with the
+// producer warpgroup's registers) moves 6 % more chains per unit time (c5a
+// 4.93 -> 4.66 ms; a tile takes 8 % longer for 14 % more chains), which wins
+// once the batch spans enough waves for the larger tile to save one.
 int abia_ring_tile(int64_t sel_B) {
   struct Cfg { int kt, ctas; double eff; };
-  const Cfg cfgs[3] = {{224, 1, 1.0}, {96, 2, 0.9}, {64, 3, 0.85}};
+  const Cfg cfgs[4] = {{224, 1, 1.0}, {256, 1, 1.06}, {96, 2, 0.9}, {64, 3, 0.85}};
   double best = 1e300;
   int kt = 224;
   for (const Cfg& c : cfgs) {
@@ -415,7 +440,7 @@ int launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int
   if (!aligned16(mv.f) || !aligned16(io.q) || !aligned16(io.qd) || !aligned16(io.tau) || !aligned16(scratch)) return 0;
   if (io.B >= (1ll << 31) || (int64_t)mv.n * kRec >= (1ll << 31)) return 0;
   const uint32_t kt = (uint32_t)abia_ring_tile(sel_B);
-  const int ctas = kt == 224 ? 1 : (kt == 96 ? 2 : 3);
+  const int ctas = (kt == 224 || kt == 256) ? 1 : (kt == 96 ? 2 : 3);
   Maps maps;
   if (!encode_maps(maps, mv, io, scratch, scr_ld, kt)) return 0;
   // the ring takes the SM's shared memory
@@ -427,7 +452,10 @@ int launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel<<<grid, (kt + 31) / 32 * 32 + 32, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
   };
-  if (kt == 224)
+  if (kt == 256) {
+    cudaFuncSetAttribute(abia_ring8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    abia_ring8_kernel<<<grid, 384, smem, s>>>(maps, mv, io, scratch, scr_ld, cap_rows);
+  } else if (kt == 224)
     go(abia_ring_kernel<224, 255>);
   else if (kt == 96)
     go(abia_ring_kernel<96, 248>);

@@ -311,3 +311,33 @@ def test_warp_specialised_cfa_error_paths(oracle, gpu_ctx):
     with pytest.raises(oracle.OracleError) as e:  # NaN angle: the reference's OEE meets a singular pivot
         oracle.forward_dynamics("cfa", links[10], GRAV, q[10], qd[10], tau[10])
     assert pd.api._capi.slot_message(st[0, 10], st[1, 10], st[2, 10], n) == str(e.value)
+
+
+def test_abia_256_chain_tiles(oracle, gpu_ctx):
+    """Large batches select 256-chain tiles (abia_ring8_kernel: eight consumer
+    warps, the producer warpgroup's registers moved to them). A selection
+    batch of 1M puts the kernel on 148 x 256 + 78 chains (an even batch: the
+    TMA row stride must stay 16-byte aligned): one CTA runs two tiles through
+    its ring, the second one ragged. Sampled slots (every tile
+    boundary) against the oracle, and bit-identical to the 224-chain tiling
+    of the same chains (same per-chain arithmetic)."""
+    n, B = 32, 148 * 256 + 78
+    cell = oracle.workload_seed(42, n, B)
+    ms, _ = gpu_ctx.set_models_workload(cell, n, B)
+    assert (ms == 0).all()
+    q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
+    gpu_ctx.set_selection_batch(1 << 20)
+    try:
+        qdd, st = device_solve(gpu_ctx, pd.FdAlgo.abia, q, qd, tau)
+        variant = gpu_ctx.last_variant()
+    finally:
+        gpu_ctx.set_selection_batch(0)
+    assert variant.startswith("abia_ring_kernel<256> grid 148 tiles 149"), variant
+    assert (st == 0).all()
+    other, st_other = device_solve(gpu_ctx, pd.FdAlgo.abia, q, qd, tau)  # the batch's own tiling (not 256)
+    assert gpu_ctx.last_variant().startswith("abia_ring_kernel<") and "<256>" not in gpu_ctx.last_variant()
+    assert np.array_equal(qdd, other) and (st_other == 0).all()
+    idx = np.unique(np.concatenate([np.arange(0, B, 4099), np.arange(255, B, 256), np.arange(256, B, 256), [B - 1]]))
+    links = oracle.workload_chains(cell, n, B)
+    ref, _ = oracle.batch_forward_dynamics("abia", links[idx], GRAV, q[idx], qd[idx], tau[idx])
+    assert rel_gaps(qdd[idx], ref).max() <= TOL

@@ -32,6 +32,7 @@ run(A, 16, 300)            # abia_ring_kernel (<64> tiles)
 run(A, 32, 600, 65536)     # abia_ring_kernel<224>, 2 tiles per CTA when the grid is full
 run(A, 8, 40)              # lane / ring, small
 run(A, 8, 148 * 224 + 77)  # abia_ring_kernel<224>: 2 tiles through one CTA's ring, ragged last tile
+run(A, 8, 600, 1 << 20)    # abia_ring8_kernel (256-chain tiles, setmaxnreg register split)
 run(A, 70, 3)              # abia_cta_kernel
 run(J, 32, 200)            # jsiia_dmma_kernel
 run(J, 64, 100)            # jsiia_dmma_kernel, 8 blocks
