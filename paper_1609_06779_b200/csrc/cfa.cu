@@ -1074,9 +1074,9 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
 
 // Warp-specialised CFA for batches of long chains (128 < n <= 256, c3):
 // persistent CTAs of 384 threads run two chains at once on two thread groups.
-//   rows      threads 0..255 (2 warpgroups, setmaxnreg 200): operators, OEE,
+//   rows      threads 0..255 (2 warpgroups, setmaxnreg 208): operators, OEE,
 //             extraction of chain k (cfa_rows, thread = row);
-//   prologue  threads 256..383 (1 warpgroup, setmaxnreg 104): joint
+//   prologue  threads 256..383 (1 warpgroup, setmaxnreg 88): joint
 //             transforms and tau_delta of chain k+1 (cta_kinematics /
 //             cta_bias_torque, 2 links per thread).
 // The one-chain-per-SM row kernel ran the latency-bound CTA scans of the
@@ -1085,8 +1085,9 @@ __global__ void __launch_bounds__(NT, MINB) cfa_row_kernel(ModelView mv, BatchIO
 // named barriers: 1 rows, 2 prologue, 3 "chain ready" (prologue arrives, rows
 // wait), 4 "handoff free" (rows arrive once the operators have read rel,
 // prologue waits before writing the next chain). setmaxnreg only moves
-// registers inside the CTA's launch allocation (384 x 168): 256 x 200 +
-// 128 x 104 = 384 x 168.
+// registers inside the CTA's launch allocation (384 x 168): 256 x 208 +
+// 128 x 88 = 384 x 168 (split sweep on c3: 200/104 0.828, 208/88 0.822,
+// 216/72 0.888, 224/56 0.990 ms -- the prologue's scans spill below 88).
 namespace cws {
 constexpr int REL = 0, TD = 12, X = 13, V = 25, TMP = 31, FIELDS = 37;  // handoff + prologue scratch
 constexpr int kRows = 256, kPro = 128, kAll = kRows + kPro;
@@ -1100,7 +1101,7 @@ __global__ void __launch_bounds__(cws::kAll, 1) cfa_ws_kernel(ModelView mv, Batc
   double* ws = dyn_smem;                // cfr::FIELDS x n: the rows' workspace
   double* hand = ws + cfr::FIELDS * n;  // cws::FIELDS x n: handoff + prologue scratch
   if (threadIdx.x < cws::kRows) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     const NamedGroup grp{0, cws::kRows, 1};
     const int t = grp.tid();
     for (int64_t p = blockIdx.x; p < io.B; p += gridDim.x) {
@@ -1122,7 +1123,7 @@ __global__ void __launch_bounds__(cws::kAll, 1) cfa_ws_kernel(ModelView mv, Batc
       grp.sync();  // the flags and the workspace are reused by the next chain
     }
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
     const NamedGroup grp{cws::kRows, cws::kPro, 2};
     bool first = true;
     for (int64_t p = blockIdx.x; p < io.B; p += gridDim.x) {
