@@ -77,49 +77,58 @@ __device__ __forceinline__ void householder_basis(const Sv& S, double z[6][6]) {
   for (int r = 0; r < 6; ++r) z[5][r] = s[r];
 }
 
-// LLT of the link's spatial inertia (packed lower, 21), Eigen semantics:
-// fails iff a pivot is <= 0 (forward_dynamics.cpp:302-305).
-__device__ __forceinline__ bool llt_inertia(const Inertia& J, double L[21], double inv[6]) {
-  const Sym6 S = inertia_sym6(J);
-  double a[21];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c <= r; ++c) {
-      a[pk(r, c)] = S.A[s3(r, c)];
-      a[pk(r + 3, c + 3)] = S.D[s3(r, c)];
-    }
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) a[pk(r + 3, c)] = S.B[3 * c + r];  // lower-left = B^T
-  bool ok = true;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    double x = a[pk(k, k)];
-#pragma unroll
-    for (int j = 0; j < k; ++j) x = fma(-L[pk(k, j)], L[pk(k, j)], x);
-    ok = ok && !(x <= 0.0);  // Eigen LLT's failure test
-    inv[k] = rsqrt_nr(x);  // one reciprocal square root per pivot
-    L[pk(k, k)] = x * inv[k];
-#pragma unroll
-    for (int i = k + 1; i < 6; ++i) {
-      double s = a[pk(i, k)];
-#pragma unroll
-      for (int j = 0; j < k; ++j) s = fma(-L[pk(i, j)], L[pk(k, j)], s);
-      L[pk(i, k)] = s * inv[k];
-    }
-  }
+// The link's spatial inertia J factored in (linear, angular) block order.
+// The reference takes LLT(J) (forward_dynamics.cpp:302-305) only to apply
+// J^{-1} inside the operator products (G^T G, G^T H, H^T H with G = L^{-1} Z),
+// which any L with L L^T = P J P^T gives the same way. With P swapping the
+// blocks, J = [[Ic + m c^ c^T, m c^], [m c^T, m 1]] (spatial.cpp:88-99)
+// factors in closed form:
+//   L = [[sqrt(m) 1, 0], [sqrt(m) c^, chol(Ic)]]
+// (the Schur complement of m 1 is exactly Ic), so a 3x3 Cholesky replaces the
+// 6x6 one and each solve is a cross product, three scalings and a 3x3
+// triangular solve. J is positive definite iff m > 0 and Ic is, so the
+// failure test is Eigen LLT's (a pivot <= 0) on m and on Ic's pivots.
+struct JFactor {
+  double ism;    // 1 / sqrt(m)
+  Vec3d c;       // centre of mass
+  double Lc[6];  // chol(Ic), packed lower rows: 00 | 10 11 | 20 21 22
+  double il[3];  // 1 / Lc_jj
+};
+__device__ __forceinline__ bool jfactor(const Inertia& J, JFactor& f) {
+  const double* I = J.I;  // xx xy xz yy yz zz (about the com)
+  bool ok = !(J.m <= 0.0);
+  f.ism = rsqrt_nr(J.m);
+  f.c = J.c;
+  double x = I[0];
+  ok = ok && !(x <= 0.0);
+  f.il[0] = rsqrt_nr(x);
+  f.Lc[0] = x * f.il[0];
+  f.Lc[1] = I[1] * f.il[0];
+  f.Lc[3] = I[2] * f.il[0];
+  x = fma(-f.Lc[1], f.Lc[1], I[3]);
+  ok = ok && !(x <= 0.0);
+  f.il[1] = rsqrt_nr(x);
+  f.Lc[2] = x * f.il[1];
+  f.Lc[4] = fma(-f.Lc[3], f.Lc[1], I[4]) * f.il[1];
+  x = fma(-f.Lc[4], f.Lc[4], fma(-f.Lc[3], f.Lc[3], I[5]));
+  ok = ok && !(x <= 0.0);
+  f.il[2] = rsqrt_nr(x);
+  f.Lc[5] = x * f.il[2];
   return ok;
 }
-__device__ __forceinline__ void lower_solve6(const double L[21], const double inv[6], double x[6]) {
-#pragma unroll
-  for (int r = 0; r < 6; ++r) {
-    double s = x[r];
-#pragma unroll
-    for (int c = 0; c < r; ++c) s = fma(-L[pk(r, c)], x[c], s);
-    x[r] = s * inv[r];
-  }
+// x <- L^{-1} P x for x = (angular, linear): (x_lin / sqrt(m), chol(Ic)^{-1} (x_ang - c x x_lin))
+__device__ __forceinline__ void jsolve(const JFactor& f, double x[6]) {
+  const Vec3d xl = mk(x[3], x[4], x[5]);
+  const Vec3d r = mk(x[0], x[1], x[2]) - cross(f.c, xl);
+  const double y0 = r.x * f.il[0];
+  const double y1 = fma(-f.Lc[1], y0, r.y) * f.il[1];
+  const double y2 = fma(-f.Lc[4], y1, fma(-f.Lc[3], y0, r.z)) * f.il[2];
+  x[0] = xl.x * f.ism;
+  x[1] = xl.y * f.ism;
+  x[2] = xl.z * f.ism;
+  x[3] = y0;
+  x[4] = y1;
+  x[5] = y2;
 }
 
 // ---- OEE row algebra on packed 5x5 blocks (Cholesky form) -------------------
@@ -266,12 +275,12 @@ __device__ __forceinline__ void ws_store(double* ws, int n, int f0, int i, const
 // row's carried blocks H^T H (HH). Reads rel_{i+1} from the workspace (HT is
 // this link's scratch). Returns false if J_i is not positive definite.
 __device__ __forceinline__ bool cfa_link_ops(const ModelView& mv, int64_t mc, double* ws, int n, int i) {
-    double L[21], linv[6];
-  const bool ok = llt_inertia(mv.inertia(i, mc), L, linv);
+    JFactor jf;
+  const bool ok = jfactor(mv.inertia(i, mc), jf);
   double G[6][6];
   householder_basis(mv.screw(i, mc), G);
 #pragma unroll
-  for (int c = 0; c < 6; ++c) lower_solve6(L, linv, G[c]);
+  for (int c = 0; c < 6; ++c) jsolve(jf, G[c]);
   {
     double ad[15], xd[5];
 #pragma unroll
@@ -297,7 +306,7 @@ __device__ __forceinline__ bool cfa_link_ops(const ModelView& mv, int64_t mc, do
     for (int c = 0; c < 6; ++c) {
     const Sv col = adT_apply(T1, Sv{mk(Z1[c][0], Z1[c][1], Z1[c][2]), mk(Z1[c][3], Z1[c][4], Z1[c][5])});
     double h[6] = {col.a.x, col.a.y, col.a.z, col.l.x, col.l.y, col.l.z};
-    lower_solve6(L, linv, h);
+    jsolve(jf, h);
     ws_store<6>(ws, n, cfa::HT + 6 * c, i, h);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
@@ -832,12 +841,12 @@ __device__ __forceinline__ void cfa_rows(const ModelView& mv, const BatchIO& io,
   // ---- operators (forward_dynamics.cpp:261-357): own blocks into registers
   double D[15], U[25], R[5];
   if (own) {
-    double L[21], linv[6];
-    if (!llt_inertia(mv.inertia(i, mc), L, linv)) atomicOr(s_link_fail, 1);
+    JFactor jf;
+    if (!jfactor(mv.inertia(i, mc), jf)) atomicOr(s_link_fail, 1);
     double G[6][6];
     householder_basis(mv.screw(i, mc), G);
 #pragma unroll
-    for (int c = 0; c < 6; ++c) lower_solve6(L, linv, G[c]);
+    for (int c = 0; c < 6; ++c) jsolve(jf, G[c]);
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
@@ -858,7 +867,7 @@ __device__ __forceinline__ void cfa_rows(const ModelView& mv, const BatchIO& io,
         const Sv col = adT_apply(T1, Sv{mk(Z1[c][0], Z1[c][1], Z1[c][2]), mk(Z1[c][3], Z1[c][4], Z1[c][5])});
         double* h = H[c];
         h[0] = col.a.x; h[1] = col.a.y; h[2] = col.a.z; h[3] = col.l.x; h[4] = col.l.y; h[5] = col.l.z;
-        lower_solve6(L, linv, h);
+        jsolve(jf, h);
 #pragma unroll
         for (int r = 0; r < 6; ++r) {
           double sacc = 0.0;
