@@ -1136,6 +1136,20 @@ __global__ void __launch_bounds__(cws::kAll, 1) cfa_ws_kernel(ModelView mv, Batc
     const NamedGroup grp{cws::kRows, cws::kPro, 2};
     bool first = true;
     for (int64_t p = blockIdx.x; p < io.B; p += gridDim.x) {
+      {  // warm L2 with the chain after this one (its model rows and states)
+        const int64_t pn = p + gridDim.x;
+        const int t = grp.tid();
+        if (mv.fcl && pn < io.B) {
+          const char* base = reinterpret_cast<const char*>(mv.fcl + (int64_t)mv.model_of(pn) * F_COUNT * n);
+          for (int off = t * 128; off < F_COUNT * n * (int)sizeof(double); off += cws::kPro * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+          for (int i = t; i < n; i += cws::kPro) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(io.q + (int64_t)i * io.lds + pn));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(io.qd + (int64_t)i * io.lds + pn));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(io.tau + (int64_t)i * io.lds + pn));
+          }
+        }
+      }
       if (!first) asm volatile("bar.sync 4, %0;" ::"n"(cws::kAll) : "memory");  // rows done with the previous chain's rel
       first = false;
       const int64_t mc = mv.model_of(p);
