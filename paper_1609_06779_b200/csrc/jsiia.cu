@@ -239,8 +239,8 @@ __device__ void warp_llt_solve(const double* Mb, int ld, int np, const double* i
 //         wide Cholesky (jsiia_factor_coop) runs next, then MODE 3.
 // MODE 3: solve + residual contract on a workspace MODE 2 / the cooperative
 //         factorization left (fail flag in the workspace tail).
-template <bool SMEM, int MODE = 0>
-__global__ void __launch_bounds__(256) jsiia_tiled_kernel(ModelView mv, BatchIO io, double* __restrict__ gws,
+template <bool SMEM, int MODE = 0, int NT = 256>
+__global__ void __launch_bounds__(NT) jsiia_tiled_kernel(ModelView mv, BatchIO io, double* __restrict__ gws,
                                                            int64_t p_off, double* __restrict__ mout = nullptr) {
   constexpr bool MOUT = MODE == 1;
   extern __shared__ __align__(16) double dyn_smem[];
@@ -847,8 +847,11 @@ bool jsiia_coop_path(int n, int64_t batch) { return !jsiia_smem_path(n) && batch
 void launch_jsiia_coop(const ModelView& mv, const BatchIO& io, double* gws, int sm_count, int64_t sel_B,
                        cudaStream_t s) {
   const int n = mv.n;
-  const int nt = 32 * jsiia_warps(n, sel_B, sm_count);
-  jsiia_tiled_kernel<false, 2><<<(unsigned)io.B, nt, 0, s>>>(mv, io, gws, 0);
+  (void)sel_B;
+  // 512 threads, 2 links each (1024-link chain): 256 x 4 0.861 ms, 512 x 2
+  // 0.811, 1024 x 1 0.836 (spills at 64 registers) for c4 JSIIA end to end
+  constexpr int kPrepThreads = 512;
+  jsiia_tiled_kernel<false, 2, kPrepThreads><<<(unsigned)io.B, kPrepThreads, 0, s>>>(mv, io, gws, 0);
   int count = (int)io.B;
   void* args[] = {&gws, (void*)&n, &count};
   const size_t smem = sizeof(double) * 8 * (3 * 32 * kTs + 32);
