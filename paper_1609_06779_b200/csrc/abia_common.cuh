@@ -232,6 +232,24 @@ __device__ __forceinline__ void abia_pass_b(AbiaState& st, int i, int n, const S
   st.qpoison = fma(q, 0.0, st.qpoison);  // NaN / inf angle poisons the links below it
 }
 
+// pass B reduced to the bias (the torque-surplus mode of the ring kernels,
+// CFA's tau_delta pre-pass): link wrench, tau_delta = tau - S0 . F0
+// (forward_dynamics.cpp:35-42, inverse_dynamics.cpp:103-112,146-150), then
+// the step back to link i-1 -- the articulated-inertia part left out.
+__device__ __forceinline__ double abia_pass_b_bias(AbiaState& st, const SE3d& rel, const Sv& S, double qd,
+                                                   const Inertia& Jl, double tau) {
+  const Sv S0 = adinv_screw(st.X, S);
+  const Inertia J0 = inertia_to_base(Jl, st.X);
+  const Sv h = inertia_apply_f(J0, st.V0);
+  st.F0 = neg_advT_acc(st.V0, h, inertia_apply_acc(J0, st.A0, st.F0));
+  const double tau_delta = sub_dot(tau, S0, st.F0);
+  const Sv rate0 = qd * S0;
+  st.A0 = adv_acc(st.V0, -1.0 * rate0, st.A0);
+  st.V0 = svfma(-qd, S0, st.V0);
+  st.X = step_back(rel, st.X);
+  return tau_delta;
+}
+
 // pass C, link i (base -> tip): qdd_i = u_i - g0_i . a0_{i-1}; a0_i = a0_{i-1} + S0_i qdd_i
 //   forward_dynamics.cpp:199-235
 __device__ __forceinline__ double abia_pass_c(AbiaState& st, const double rec[kRec]) {

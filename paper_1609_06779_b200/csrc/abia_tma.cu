@@ -137,7 +137,10 @@ __device__ __forceinline__ SE3d row_rel(const double* f, int r0, const Sv& S, do
 // SPLIT: the producer warpgroup gives its registers to the consumers
 // (setmaxnreg inside each role's branch, so ptxas allocates each role's code
 // with its own budget).
-template <int KT, bool SPLIT = false>
+// BIAS: torque-surplus mode -- passes A and B only, pass B reduced to the
+// link wrenches, tau_delta written to io.qdd's slot ([link][problem]); no
+// records, no pass C, no status.
+template <int KT, bool SPLIT = false, bool BIAS = false>
 __device__ __forceinline__ void abia_ring_body(const Maps& maps, const ModelView& mv, const BatchIO& io,
                                                double* __restrict__ scratch, int64_t scr_ld, uint32_t cap_rows) {
   static_assert(KT % 16 == 0, "ring rows must stay 128-byte aligned for TMA");
@@ -148,7 +151,7 @@ __device__ __forceinline__ void abia_ring_body(const Maps& maps, const ModelView
   constexpr int NW = (KT + 31) / 32;   // consumer warps; warp NW is the producer
   const int t = threadIdx.x, lane = t & 31;
   const int n = mv.n;
-  const uint32_t total = 3u * (uint32_t)n;
+  const uint32_t total = (BIAS ? 2u : 3u) * (uint32_t)n;
   const int ntiles = (int)((io.B + KT - 1) / KT);
   if (t == 0) {
     for (int s = 0; s < kSlots; ++s) {
@@ -256,6 +259,12 @@ __device__ __forceinline__ void abia_ring_body(const Maps& maps, const ModelView
       J.c = mk(f[F_COM * KT], f[(F_COM + 1) * KT], f[(F_COM + 2) * KT]);
 #pragma unroll
       for (int j = 0; j < 6; ++j) J.I[j] = f[(F_IC + j) * KT];
+      if constexpr (BIAS) {
+        const double td = abia_pass_b_bias(st, row_rel<KT>(f, F_KIN, S, q, sn, cs), S, f[(F_COUNT + 1) * KT], J,
+                                           f[(F_COUNT + 2) * KT]);
+        if (live) io.put_qdd(i, p, td);
+        return;
+      }
       double rec[kRec];
       abia_pass_b(st, i, n, row_rel<KT>(f, F_KIN, S, q, sn, cs), S, f[(F_COUNT + 1) * KT], J, f[(F_COUNT + 2) * KT],
                   rec, q);
@@ -282,6 +291,7 @@ __device__ __forceinline__ void abia_ring_body(const Maps& maps, const ModelView
       asm volatile("fence.proxy.async.global;" ::: "memory");
       release();
     }
+    if constexpr (BIAS) continue;
     for (; k < total; ++k) {  // pass C
       const double* f = acquire(k);
       const int i = (int)k - 2 * n;
@@ -311,6 +321,15 @@ __global__ void __launch_bounds__((KT + 31) / 32 * 32 + 32) __maxnreg__(MAXREG)
     abia_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
                      int64_t scr_ld, uint32_t cap_rows) {
   abia_ring_body<KT>(maps, mv, io, scratch, scr_ld, cap_rows);
+}
+
+// The torque surplus tau_delta = tau - ID(q, qd, 0) of every chain through the
+// same TMA ring (passes A and B of the ABIA kernel without its articulated
+// part), into io.qdd's slot: CFA's pre-pass for large batches.
+__global__ void __launch_bounds__(256, 1)
+    bias_ring_kernel(const __grid_constant__ Maps maps, ModelView mv, BatchIO io, double* __restrict__ scratch,
+                     int64_t scr_ld, uint32_t cap_rows) {
+  abia_ring_body<224, false, true>(maps, mv, io, scratch, scr_ld, cap_rows);
 }
 
 // 256-chain tiles: eight consumer warps (two warpgroups raised to 240
@@ -358,7 +377,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 }  // namespace
 
-bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, uint32_t kt) {
+bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scratch, int64_t scr_ld, uint32_t kt,
+                 bool records = true) {
   const int n = mv.n;
   {
     const cuuint64_t dims[3] = {(cuuint64_t)mv.M, (cuuint64_t)n, (cuuint64_t)F_COUNT};
@@ -375,7 +395,7 @@ bool encode_maps(Maps& maps, const ModelView& mv, const BatchIO& io, double* scr
     if (!encode(&maps.qd, io.qd, 2, dims, str, box)) return false;
     if (!encode(&maps.tau, io.tau, 2, dims, str, box)) return false;
   }
-  {
+  if (records) {
     const cuuint64_t dims[2] = {(cuuint64_t)io.B, (cuuint64_t)n * kRec};
     const cuuint64_t str[1] = {(cuuint64_t)scr_ld * 8};
     const cuuint32_t box[2] = {kt, kRec};
@@ -463,6 +483,26 @@ int launch_abia_tma(const ModelView& mv, const BatchIO& io, double* scratch, int
     go(abia_ring_kernel<64, 224>);
   if (grid_out) *grid_out = grid;
   return (int)kt;
+}
+
+// tau_delta of every chain into io.qdd ([link][problem], stride io.lds) by the
+// ring kernel's passes A and B (bias_ring_kernel); false when the batch does
+// not meet TMA's layout rules (the caller then runs the lane pre-pass).
+bool launch_bias_tma(const ModelView& mv, const BatchIO& io, cudaStream_t s) {
+  if (mv.M == 1 || mv.M != io.B) return false;
+  if ((io.lds & 1) || (mv.ld & 1)) return false;
+  if (!aligned16(mv.f) || !aligned16(io.q) || !aligned16(io.qd) || !aligned16(io.tau)) return false;
+  if (io.B >= (1ll << 31)) return false;
+  constexpr uint32_t kt = 224;
+  Maps maps;
+  if (!encode_maps(maps, mv, io, nullptr, 0, kt, false)) return false;
+  const size_t smem = (size_t)(220 * 1024) / (kt * 8) * (kt * 8);
+  const uint32_t cap_rows = (uint32_t)(smem / (kt * 8));
+  const int64_t ntiles = (io.B + kt - 1) / kt;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count());
+  cudaFuncSetAttribute(bias_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bias_ring_kernel<<<grid, 256, smem, s>>>(maps, mv, io, nullptr, 0, cap_rows);
+  return true;
 }
 
 }  // namespace pd

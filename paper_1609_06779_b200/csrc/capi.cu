@@ -24,6 +24,7 @@ void launch_invdyn(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa(const ModelView& mv, const BatchIO& io, double* gws, int64_t gws_slots, cudaStream_t s,
                 const double* td_pre);
 void launch_tau_surplus(const ModelView& mv, const BatchIO& io, double* td, cudaStream_t s);
+bool launch_bias_tma(const ModelView& mv, const BatchIO& io, cudaStream_t s);
 void launch_cfa_ws(const ModelView& mv, const BatchIO& io, int sm_count, cudaStream_t s);
 bool cfa_ws_fits(int n);
 void launch_bidiag6(const double* coupling, const double* rhs, double* x, int64_t batch, int n, int upper,
@@ -450,16 +451,23 @@ pd_status run_device(pd_ctx* ctx, pd_algo algo, int64_t batch, int64_t lds, cons
       // large batches: tau_delta by a lane-per-chain pass first (sequential
       // recurrences, no CTA-wide scans); small batches keep the CTA scans
       const double* td_pre = nullptr;
+      bool td_ring = false;
       if (route == ROUTE_AUTO && selB >= 128 * (int64_t)ctx->sm_count) {  // >= 4 warps of chains per SM
         PD_CUDA(ctx->cfa_td.ensure(sizeof(double) * (size_t)n * io.lds));
-        launch_tau_surplus(model_view(ctx, m0, batch), io, ctx->cfa_td.as<double>(), ctx->stream);
+        // the ABIA ring kernel's passes A and B (TMA-streamed, base frame)
+        // when the layout allows, else the lane pre-pass
+        BatchIO tio = io;
+        tio.qdd = ctx->cfa_td.as<double>();
+        td_ring = launch_bias_tma(model_view(ctx, m0, batch), tio, ctx->stream);
+        if (!td_ring) launch_tau_surplus(model_view(ctx, m0, batch), io, ctx->cfa_td.as<double>(), ctx->stream);
         ctx->launches++;
         td_pre = ctx->cfa_td.as<double>();
       }
       const char* kname = n <= 256 ? "cfa_row_kernel" : (slots ? "cfa_cta_kernel<global>" : "cfa_cta_kernel<smem>");
       launch_cfa(mv, io, ctx->cta_ws.as<double>(), slots, ctx->stream, td_pre);
       if (td_pre)  // tau_delta walked sequentially per chain; operators, OEE and extraction per row
-        note_variant(ctx, std::string("tau_surplus_lane_kernel + ") + kname, 3, n, 0, L);
+        note_variant(ctx, std::string(td_ring ? "bias_ring_kernel + " : "tau_surplus_lane_kernel + ") + kname, 3, n,
+                     0, L);
       else
         note_variant(ctx, kname, 9, cs.lpt > 1 ? cs.lpt : 0, ceil_log2_host(cs.groups), L);
       break;

@@ -154,7 +154,7 @@ def test_c5_shape_device_generated(oracle, gpu_ctx, algo):
     qdd, st = device_solve(gpu_ctx, pd.FdAlgo[algo], q, qd, tau)
     variant = gpu_ctx.last_variant()
     assert {"abia": "abia_ring_kernel<224>", "jsiia": "jsiia_dmma_kernel",
-            "cfa": "tau_surplus_lane_kernel + cfa_row_kernel"}[algo] in variant, variant
+            "cfa": "bias_ring_kernel + cfa_row_kernel"}[algo] in variant, variant
     assert (st == 0).all()
     idx = boundary_sample(B, 224, 16384, 1500 if algo != "jsiia" else 1300, 5)
     assert len(idx) >= 2048

@@ -222,18 +222,24 @@ def test_grid_wide_long_chain_paths(oracle, gpu_ctx, algo, n, B):
 
 
 @pytest.mark.parametrize("n", [7, 33, 64])
-def test_cfa_large_batch_with_lane_bias_pass(oracle, gpu_ctx, n):
-    """Batches of >= 128 x SMs chains: tau_delta comes from the lane-per-chain
-    pre-pass (tau_surplus_lane_kernel) instead of the CTA scans; same results."""
+@pytest.mark.parametrize("shared", [False, True])
+def test_cfa_large_batch_with_bias_pre_pass(oracle, gpu_ctx, n, shared):
+    """Batches of >= 128 x SMs chains: tau_delta comes from a pre-pass instead
+    of the CTA scans -- the ABIA ring kernel's passes A and B
+    (bias_ring_kernel, TMA) for independent models, the lane-per-chain
+    recurrence (tau_surplus_lane_kernel) for a shared model; same results."""
     B = 20000
     cell = oracle.workload_seed(42, n, B)
-    links = oracle.workload_chains(cell, n, B)
+    links = oracle.workload_chains(cell, n, 1 if shared else B)
     q, qd, tau = oracle.workload_inputs(cell, n, B, 0)
     gpu_ctx.set_models(links, None)
     qdd, st, _, _ = gpu_ctx.solve(pd.FdAlgo.cfa, q, qd, tau)
     assert (st == 0).all()
+    pre = "tau_surplus_lane_kernel" if shared else "bias_ring_kernel"
+    assert gpu_ctx.last_variant().startswith(pre), gpu_ctx.last_variant()
     idx = np.arange(0, B, 613)
-    ref, _ = oracle.batch_forward_dynamics("cfa", links[idx], [0, 0, -9.81], q[idx], qd[idx], tau[idx])
+    lk = links if shared else links[idx]
+    ref, _ = oracle.batch_forward_dynamics("cfa", lk, [0, 0, -9.81], q[idx], qd[idx], tau[idx])
     for k, b in enumerate(idx):
         assert rel_gap(qdd[b], ref[k]) <= TOL
 
