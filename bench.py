@@ -431,8 +431,9 @@ def measure_workload(ctx, name, wl, steps, warmup, rank, local, stream, want_e2e
 
 # ncu --set full captures of the dominant kernel per workload (profiles/, same
 # kernel and config as the bench command): DRAM bytes per launch
-NCU_TRAFFIC = {"c2": "profiles/ncu_c2_r1_s3g.txt", "c3": "profiles/ncu_c3_r1_s3g.txt",
-               "c2j": "profiles/ncu_c2j_r1_s3g.txt", "c5j": "profiles/ncu_c5j_r1_s3c.txt"}
+NCU_TRAFFIC = {"c2": "profiles/ncu_c2_r2d.txt", "c3": "profiles/ncu_c3_r2f.txt",
+               "c2j": "profiles/ncu_c2j_r2c.txt", "c5j": "profiles/ncu_c5j_r2b.txt",
+               "c5c": "profiles/ncu_c5c_r2e.txt"}
 
 
 def dropin_api_timings():
@@ -475,14 +476,12 @@ def ncu_traffic(workload: str):
     if workload not in NCU_TRAFFIC or not os.path.exists(path):
         return None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    total = 0.0
-    found = 0
-    for line in open(path):
+    got = {}
+    for line in open(path):  # first occurrence of each (summaries may repeat a metric in a later section)
         parts = line.split()
-        if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            total += float(parts[1]) * scale.get(parts[2], 1.0)
-            found += 1
-    return {"bytes_per_launch": total, "source": NCU_TRAFFIC[workload]} if found == 2 else None
+        if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum") and parts[0] not in got:
+            got[parts[0]] = float(parts[1]) * scale.get(parts[2], 1.0)
+    return {"bytes_per_launch": sum(got.values()), "source": NCU_TRAFFIC[workload]} if len(got) == 2 else None
 
 
 def _executed_fp64():
