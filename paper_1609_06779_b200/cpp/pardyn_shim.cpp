@@ -22,25 +22,27 @@ namespace {
 thread_local int t_device = 0;
 thread_local std::vector<int> t_devices;  // empty: {t_device}
 
-// One pd_ctx per (thread, device) -- contexts are single-threaded objects.
-// A sharded batch call opens one per worker thread as well.
+// pd_ctx objects of the calling thread, per (device, slot) -- contexts are
+// single-threaded objects. Slot 0 serves the thread's own calls; a batch call
+// lends slots 0.. to its worker threads (one each), so the contexts and their
+// device buffers outlive the workers and are reused call to call.
 struct CtxHolder {
-  std::map<int, pd_ctx*> by_dev;
+  std::map<std::pair<int, int>, pd_ctx*> by_dev;
   ~CtxHolder() {
     for (auto& kv : by_dev) pd_destroy(kv.second);
   }
 };
 thread_local CtxHolder t_ctx;
 
-pd_ctx* ctx_on(int device) {
-  auto it = t_ctx.by_dev.find(device);
+pd_ctx* ctx_on(int device, int slot = 0) {
+  auto it = t_ctx.by_dev.find({device, slot});
   if (it != t_ctx.by_dev.end()) return it->second;
   pd_ctx* c = nullptr;
   const pd_status st = pd_create(&c, device);
   if (st != PD_OK)
     throw DeviceError(std::string("pardyn: cannot open CUDA device ") + std::to_string(device) + ": " +
                       pd_status_string(st));
-  t_ctx.by_dev[device] = c;
+  t_ctx.by_dev[{device, slot}] = c;
   return c;
 }
 pd_ctx* ctx() { return ctx_on(t_device); }
@@ -476,7 +478,7 @@ struct Bucket {
   double *links = nullptr, *grav = nullptr, *q = nullptr, *qd = nullptr, *tau = nullptr, *qdd = nullptr;
   int32_t *st = nullptr, *rd = nullptr, *ix = nullptr;
 
-  void pack(std::span<const FdProblem> problems, double* base) {
+  void layout(double* base) {
     const std::size_t B = idx.size(), nn = static_cast<std::size_t>(n);
     links = base;
     grav = links + B * nn * PD_LINK_FIELDS;
@@ -487,8 +489,12 @@ struct Bucket {
     st = reinterpret_cast<int32_t*>(qdd + B * nn);
     rd = st + B;
     ix = rd + B;
-    parallel_ranges(B, 1024, [&](std::size_t lo, std::size_t hi) {
-      for (std::size_t j = lo; j < hi; ++j) {
+  }
+  // problems [lo, hi) of the bucket into the staging (host threads)
+  void pack(std::span<const FdProblem> problems, std::size_t lo, std::size_t hi) {
+    const std::size_t nn = static_cast<std::size_t>(n);
+    parallel_ranges(hi - lo, 1024, [&](std::size_t a, std::size_t b) {
+      for (std::size_t j = lo + a; j < lo + b; ++j) {
         const FdProblem& p = problems[idx[j]];
         double* rec = links + j * nn * PD_LINK_FIELDS;
         for (std::size_t i = 0; i < nn; ++i) detail::to_record(p.chain.links[i], rec + i * PD_LINK_FIELDS);
@@ -524,7 +530,11 @@ void solve_slice(pd_ctx* c, pd_algo a, Bucket& b, std::size_t lo, std::size_t hi
 // forward_dynamics.cpp:466-481: never throws per problem. Problems are
 // bucketed by link count; a bucket is packed (in parallel host threads) into
 // page-locked staging and split into contiguous slices over gpu::devices(),
-// one host thread and one context per device.
+// one worker thread per device on a context the calling thread lends it (so
+// the contexts and their device buffers are reused call to call). Packing the
+// whole bucket before the first upload is deliberate: both are bound by host
+// memory bandwidth, and overlapping them per slice measured slower
+// (profiles/dropin_batch_r2.txt).
 std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems, FdAlgo algo) {
   const pd_algo a = to_c(algo);
   std::vector<FdResult> out(problems.size());
@@ -542,10 +552,14 @@ std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems
   for (auto& [n, b] : buckets) {
     b.n = n;
     const std::size_t B = b.idx.size();
-    b.pack(problems, t_stage.get(Bucket::doubles(B, n)));
+    b.layout(t_stage.get(Bucket::doubles(B, n)));
+    b.pack(problems, 0, B);
     const std::size_t G = std::min<std::size_t>(devs.size(), B);
+    std::vector<pd_ctx*> ctxs;
+    std::map<int, int> slots;  // a device listed twice gets distinct contexts
+    for (std::size_t g = 0; g < G; ++g) ctxs.push_back(ctx_on(devs[g], slots[devs[g]]++));
     if (G <= 1) {
-      solve_slice(ctx_on(devs[0]), a, b, 0, B);
+      solve_slice(ctxs[0], a, b, 0, B);
     } else {
       std::vector<std::thread> workers;
       std::vector<std::string> errors(G);
@@ -553,7 +567,7 @@ std::vector<FdResult> batch_forward_dynamics(std::span<const FdProblem> problems
       for (std::size_t g = 0; g < G; ++g)
         workers.emplace_back([&, g] {
           try {
-            solve_slice(ctx_on(devs[g]), a, b, B * g / G, B * (g + 1) / G);
+            solve_slice(ctxs[g], a, b, B * g / G, B * (g + 1) / G);
           } catch (const std::invalid_argument& e) {
             errors[g] = e.what();
             kinds[g] = 1;

@@ -715,7 +715,10 @@ pd_status pd_set_models(pd_ctx* ctx, int64_t n_models, int32_t n_links, const do
   ctx->n_models = n_models;
   ctx->model_ld = model_ld;
   ctx->model_cl_valid = false;
-  if (raw_bytes <= ((size_t)64 << 20)) {
+  // keep a copy for the identical-model check only for small model sets (a
+  // chain re-sent with every single-problem call); a batch's slices are not
+  // worth a host copy
+  if (n_models <= 1024 && raw_bytes <= ((size_t)64 << 20)) {
     ctx->last_links.assign(links, links + raw_bytes / sizeof(double));
     ctx->last_grav = g;
     ctx->models_cached = true;

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstdio>
 #include <random>
 #include <string>
@@ -423,6 +424,37 @@ int main() {
     bool same = one.size() == three.size();
     for (std::size_t k = 0; same && k < one.size(); ++k) same = one[k].ok() && one[k].qddot == three[k].qddot;
     check(same, "batch sharded over a device list is bit-identical to one device");
+  }
+
+  // a large bucket over one device and over a device list (two slices on two
+  // contexts): the same bits, per-slot errors in their slots, slots matching
+  // the single-problem call
+  {
+    std::vector<FdProblem> probs;
+    for (int k = 0; k < 40000; ++k) {
+      Sample s = make_sample(4, 5000 + k);
+      probs.push_back({s.chain, s.q, s.qdot, s.tau});
+    }
+    probs[3].tau = JointVector::Zero(3);                        // rejected on the host (sizes)
+    probs[17001].q[1] = std::numeric_limits<double>::quiet_NaN();  // rejected by the kernel, second slice
+    const auto one = batch_forward_dynamics(probs, FdAlgo::abia);
+    gpu::set_devices({gpu::device(), gpu::device()});
+    const auto two = batch_forward_dynamics(probs, FdAlgo::abia);
+    gpu::set_devices({});
+    bool same = one.size() == probs.size() && two.size() == probs.size();
+    for (std::size_t k = 0; same && k < one.size(); ++k)
+      same = one[k].ok() == two[k].ok() && one[k].qddot == two[k].qddot && one[k].error == two[k].error;
+    check(same, "large batch: a device list gives the same bits");
+    check(!one[3].ok() && one[3].error.find("forward dynamics") != std::string::npos && !one[17001].ok() &&
+              !one[17001].error.empty() && one[17000].ok() && one[17002].ok(),
+          "large batch: per-slot errors stay in their slots");
+    double worst = 0.0;
+    for (std::size_t k = 0; k < probs.size(); k += 997) {
+      if (k == 3 || k == 17001) continue;
+      const JointVector ref = forward_dynamics(probs[k].chain, probs[k].q, probs[k].qdot, probs[k].tau, FdAlgo::abia);
+      worst = std::max(worst, (one[k].qddot - ref).norm() / std::max(1.0, ref.norm()));
+    }
+    check(worst < 1e-12, "large batch: slots match the single-problem call");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
