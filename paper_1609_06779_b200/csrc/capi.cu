@@ -604,7 +604,7 @@ void pd_destroy(pd_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->model, &ctx->gravity, &ctx->mstatus, &ctx->mrule, &ctx->raw, &ctx->abia_scratch, &ctx->cta_ws,
                     &ctx->slots, &ctx->io_q, &ctx->io_qd, &ctx->io_tau, &ctx->io_qdd, &ctx->io_status, &ctx->model_cl,
-                    &ctx->states, &ctx->cfa_td})
+                    &ctx->states, &ctx->cfa_td, &ctx->d_flag})
     b->release();
   if (ctx->cp_in) {
     cudaStreamSynchronize(ctx->cp_in);
