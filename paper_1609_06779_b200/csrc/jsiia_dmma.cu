@@ -321,8 +321,30 @@ __global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 5 : 3) jsiia_dmma_kern
 #pragma unroll
       for (int k = 0; k < 6; ++k) Ic[e].v[4 + k] = Js.A[k];
     }
-    link_scan<6, LPL, true, true>(Fw, lane);
-    link_scan<10, LPL, true, true>(Ic, lane);
+    // the wrench and composite-inertia suffix sums: one 16-wide scan for a link
+    // per lane (more shuffles in flight per round: c2j -0.7 %); two scans for
+    // NB > 4, where the wider live set spills (c5j +0.5 %)
+    if constexpr (LPL > 1) {
+      link_scan<6, LPL, true, true>(Fw, lane);
+      link_scan<10, LPL, true, true>(Ic, lane);
+    } else {
+      Vk<16> FI[LPL];
+#pragma unroll
+      for (int e = 0; e < LPL; ++e) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) FI[e].v[k] = Fw[e].v[k];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) FI[e].v[6 + k] = Ic[e].v[k];
+      }
+      link_scan<16, LPL, true, true>(FI, lane);
+#pragma unroll
+      for (int e = 0; e < LPL; ++e) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) Fw[e].v[k] = FI[e].v[k];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) Ic[e].v[k] = FI[e].v[6 + k];
+      }
+    }
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
       td[e] = tau[e] - dot(S0[e], un6(Fw[e]));
@@ -492,6 +514,7 @@ __global__ void __launch_bounds__(32 * kDWarps, NB <= 4 ? 5 : 3) jsiia_dmma_kern
       P[e] = sv6(x[e] * s0l[e]);
       Q[e] = sv6(x[e] * fbl[e]);
     }
+    // (one fused round loop for P and Q spills at NB = 4: c2j +1.4 %)
     link_scan<6, LPL, false, true>(P, lane);
     link_scan<6, LPL, true, false>(Q, lane);
     double rs = 0.0;
