@@ -189,9 +189,15 @@ __device__ __forceinline__ void abia_ring_body(const Maps& maps, const ModelView
           uint64_t* bar = &full[gk % kSlots];
           if (k < (uint32_t)n) {  // pass A: kinematic rows 0..F_NKIN-1, q, qd
             mbar_expect_tx(bar, kRowsA * KT * 8);
-            tma_3d(dst, &maps.model_kin, c0, (int)k, F_KIN, bar);
-            tma_2d(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar);
-            tma_2d(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar);
+            if constexpr (SPLIT) {  // 256-chain tiles (the largest batches): the rows would not survive to pass B
+              tma_3d_hint(dst, &maps.model_kin, c0, (int)k, F_KIN, bar, pol_first);
+              tma_2d_hint(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar, pol_first);
+              tma_2d_hint(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar, pol_first);
+            } else {
+              tma_3d(dst, &maps.model_kin, c0, (int)k, F_KIN, bar);
+              tma_2d(dst + F_NKIN * KT, &maps.q, c0, (int)k, bar);
+              tma_2d(dst + (F_NKIN + 1) * KT, &maps.qd, c0, (int)k, bar);
+            }
           } else if (k < 2u * n) {  // pass B: model rows 0..F_COUNT-1, q, qd, tau (last use)
             const int i = 2 * n - 1 - (int)k;
             mbar_expect_tx(bar, kRowsB * KT * 8);
